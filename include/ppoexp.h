@@ -1,0 +1,267 @@
+/*
+ * ppoexp.h — C ABI of the B200-native PPO experience-making path
+ * (libppoexp.so, built from paper_2405_01481_b200/csrc).
+ *
+ * Drop-in boundary for the reference ("minialigner", /root/reference/proj).
+ * Every entry point names the reference interface it replaces (file:line,
+ * relative to /root/reference/proj).  Plain pointers and sizes only; no torch
+ * or CUDA types in the signatures (streams travel as void*).
+ *
+ * Conventions
+ *  - Every call returns a ppoexp_status; on failure the message is available
+ *    from ppoexp_last_error() (thread-local).  Status codes map 1:1 onto the
+ *    reference's exception types (ContractError / IndexError / ShapeError,
+ *    include/aligner/tensor.hpp:17-25; RefitError, include/aligner/engine.hpp:19-21;
+ *    PpoError, include/aligner/ppo.hpp:22-24) and the messages keep the
+ *    reference's wording (e.g. "(rebuild required)", src/engine.cpp:64-75).
+ *  - Buffers: `where` = PPOEXP_HOST means caller-owned host memory (the call
+ *    does the H2D/D2H copies on the context stream and synchronises before
+ *    returning); PPOEXP_DEVICE means caller-owned device memory on the
+ *    context's device (the call is stream-ordered and returns without a sync).
+ *  - Weights: ppoexp_tensor_view names/shapes follow ModelParams
+ *    (src/model.cpp:66-115); values are row-major in the reference layout
+ *    (projections [in, out], tok_embed [V, d], scalar_head [d, 1]).
+ *  - Ragged token batches: tokens[] concatenated, offsets[B+1] (int64).
+ *  - Per-token response outputs are padded [B, max_new] row-major with
+ *    lengths[B]; float outputs are double (the reference's std::vector<double>).
+ *  - No CPU fallback: if the device is missing every call fails with
+ *    PPOEXP_ERR_CUDA.
+ */
+#ifndef PPOEXP_H_
+#define PPOEXP_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PPOEXP_ABI_VERSION 1
+
+typedef enum {
+  PPOEXP_OK = 0,
+  PPOEXP_ERR_CONTRACT = 1, /* aligner::ContractError */
+  PPOEXP_ERR_INDEX = 2,    /* aligner::IndexError */
+  PPOEXP_ERR_SHAPE = 3,    /* aligner::ShapeError */
+  PPOEXP_ERR_REFIT = 4,    /* aligner::RefitError */
+  PPOEXP_ERR_PPO = 5,      /* aligner::PpoError */
+  PPOEXP_ERR_CUDA = 6,     /* device / driver failure */
+  PPOEXP_ERR_OOM = 7       /* device allocation failure */
+} ppoexp_status;
+
+typedef enum { PPOEXP_HOST = 0, PPOEXP_DEVICE = 1 } ppoexp_where;
+
+typedef enum {
+  PPOEXP_F32 = 0,  /* parity mode: fp32 weights / KV / activations, fp32 SIMT GEMMs */
+  PPOEXP_BF16 = 1, /* perf mode: bf16 weights / KV / GEMM operands, fp32 accumulate */
+  PPOEXP_F64 = 2   /* host weight views only */
+} ppoexp_dtype;
+
+typedef struct ppoexp_ctx_s* ppoexp_ctx;
+typedef struct ppoexp_model_s* ppoexp_model;
+typedef struct ppoexp_engine_s* ppoexp_engine;
+
+/* ModelConfig, include/aligner/model.hpp:30-45 (LoRA is not on this path). */
+typedef struct {
+  int64_t vocab_size, d_model, n_layers, n_heads, d_ff, max_seq_len;
+  int32_t scalar_head;
+  int32_t reserved;
+} ppoexp_model_config;
+
+/* One named parameter (ModelParams::tensors entry, include/aligner/model.hpp:48-67). */
+typedef struct {
+  const char* name;
+  int32_t rank;
+  int32_t dtype; /* ppoexp_dtype of `data` */
+  int64_t shape[2];
+  const void* data;
+  int32_t where; /* ppoexp_where of `data` */
+  int32_t reserved;
+} ppoexp_tensor_view;
+
+/* SamplingSpec, include/aligner/model.hpp:75-84, plus the north-star top-k /
+ * top-p filter (top_k = 0 and top_p >= 1 reproduce the reference sampler
+ * exactly; see oracle/ppoexp_oracle.c for the convention). */
+typedef struct {
+  int32_t greedy;
+  int32_t top_k;
+  double temperature;
+  double top_p;
+} ppoexp_sampling;
+
+/* ---------------------------------------------------------------- misc */
+const char* ppoexp_last_error(void);
+int32_t ppoexp_abi_version(void);
+
+/* ------------------------------------------------------------- context */
+/* One device + one CUDA stream + workspace.  Calls on one context are
+ * serialised (Engine's shared_mutex semantics, src/engine.cpp:78, :149). */
+ppoexp_status ppoexp_ctx_create(int32_t device, ppoexp_ctx* out);
+ppoexp_status ppoexp_ctx_destroy(ppoexp_ctx ctx);
+/* The cudaStream_t the context launches on (for event timing / interop). */
+ppoexp_status ppoexp_ctx_stream(ppoexp_ctx ctx, void** stream_out);
+ppoexp_status ppoexp_ctx_synchronize(ppoexp_ctx ctx);
+/* Kernel-class timing (CUDA events around each launch of the named class;
+ * classes: "decode_attention", "logprob_gather", "gemm", "sampler", ...).
+ * enable=1 starts accumulating; query returns total ms, launches and the
+ * algorithmic bytes (or flops) those launches moved. */
+ppoexp_status ppoexp_ctx_profile(ppoexp_ctx ctx, int32_t enable);
+ppoexp_status ppoexp_ctx_profile_query(ppoexp_ctx ctx, const char* kernel_class, double* total_ms,
+                                       int64_t* launches, double* algorithmic_bytes, double* flops);
+/* Number of library kernel launches issued on this context so far (graph
+ * replays count every kernel node). */
+ppoexp_status ppoexp_ctx_launch_count(ppoexp_ctx ctx, int64_t* out);
+
+/* --------------------------------------------------------------- model */
+/* A device-resident weight snapshot.  Replaces Engine's deep copy at build
+ * (build_engine / Engine::Engine, src/engine.cpp:33-58): the views are
+ * copied (and cast to compute_dtype) into HBM; the caller keeps its arrays.
+ * Name/shape set must equal ModelParams::expected_names(config) exactly
+ * (ContractError otherwise, like param_shape, src/model.cpp:92-115). */
+ppoexp_status ppoexp_model_create(ppoexp_ctx ctx, const ppoexp_model_config* config,
+                                  const ppoexp_tensor_view* params, int64_t n_params,
+                                  int32_t compute_dtype, ppoexp_model* out);
+/* Engine::refit, src/engine.cpp:60-90: validates the whole name/shape set
+ * first (RefitError "... (rebuild required)", nothing touched), then copies
+ * in place (no re-allocation, captured graphs stay valid) and bumps the
+ * generation counter. */
+ppoexp_status ppoexp_model_refit(ppoexp_model model, const ppoexp_tensor_view* params, int64_t n_params);
+/* Engine::generation_counter, include/aligner/engine.hpp:65 */
+ppoexp_status ppoexp_model_generation(ppoexp_model model, uint64_t* out);
+ppoexp_status ppoexp_model_config_get(ppoexp_model model, ppoexp_model_config* out);
+ppoexp_status ppoexp_model_destroy(ppoexp_model model);
+
+/* -------------------------------------------------------------- engine */
+/* The TensorRT-LLM analog (Engine, include/aligner/engine.hpp:49-92) over a
+ * policy model: paged KV pool in HBM, batched prefill, CUDA-graph decode. */
+typedef struct {
+  int64_t max_batch;        /* sequences per generate call (0 = 256) */
+  int64_t page_size;        /* KV tokens per page (0 = 64) */
+  int64_t max_total_tokens; /* KV pool capacity in tokens (0 = max_batch * max_seq_len) */
+  int32_t use_graphs;       /* capture the decode step in a CUDA graph (default on) */
+  int32_t reserved;
+} ppoexp_engine_options;
+
+ppoexp_status ppoexp_engine_create(ppoexp_model policy, const ppoexp_engine_options* opts, ppoexp_engine* out);
+ppoexp_status ppoexp_engine_destroy(ppoexp_engine engine);
+
+/* Engine::generate_batch (src/engine.cpp:148-182) / generate()
+ * (src/model.cpp:438-482) for B tasks at once.
+ *  prompts/offsets: ragged prompts (`where` for both).
+ *  max_new[B]: per-task budget (the reference caps it at max_seq_len - P).
+ *  seeds[B]: per-task Rng seed (ignored when greedy).  The sampler consumes
+ *    one mt19937_64 uniform per sampled token in order, exactly like the
+ *    reference (src/model.cpp:445, :464); the library draws them on the host.
+ *  out_tokens/out_logprobs: [B, out_stride]; out_lengths[B].  The recorded
+ *    log-prob is the untempered log-softmax of the chosen token
+ *    (src/model.cpp:450, :477).  Generation stops after EOT (257), which is
+ *    kept (src/model.cpp:476-478).
+ *  ms_out (optional): device time of the call in milliseconds. */
+ppoexp_status ppoexp_engine_generate(ppoexp_engine engine, int64_t B, const int32_t* prompts,
+                                     const int64_t* offsets, const int64_t* max_new,
+                                     const ppoexp_sampling* sampling, const uint64_t* seeds,
+                                     int64_t out_stride, int32_t* out_tokens, double* out_logprobs,
+                                     int64_t* out_lengths, int32_t where, double* ms_out);
+
+/* ----------------------------------------------------------- scoring */
+/* sequence_logprobs (src/model.cpp:484-495) for B ragged sequences:
+ * out (same ragged layout as tokens) gets out[start] = 0 and
+ * out[t] = log p(tokens[t] | tokens[<t]).  One batched forward plus the
+ * fused log-softmax+gather kernel. */
+ppoexp_status ppoexp_sequence_logprobs(ppoexp_model model, int64_t B, const int32_t* tokens,
+                                       const int64_t* offsets, double* out, int32_t where);
+/* value_estimates (src/losses.cpp:117-127) with the model's scalar head:
+ * out is ragged over responses (out_offsets[b] = sum_{i<b} (T_i - rs_i)). */
+ppoexp_status ppoexp_value_estimates(ppoexp_model critic, int64_t B, const int32_t* tokens,
+                                     const int64_t* offsets, const int64_t* response_start, double* out,
+                                     int32_t where);
+/* reward_head (src/losses.cpp:105-115) with the model's scalar head: out[B]. */
+ppoexp_status ppoexp_reward_head(ppoexp_model rm, int64_t B, const int32_t* tokens, const int64_t* offsets,
+                                 double* out, int32_t where);
+
+/* ----------------------------------------------------------- shaping */
+/* kl_penalized_rewards (src/losses.cpp:188-199) + gae (src/losses.cpp:168-186)
+ * for B padded sequences [B, stride] with lengths[B]. */
+ppoexp_status ppoexp_shape_gae(int64_t B, int64_t stride, const int64_t* lengths, const double* rm_reward,
+                               const double* actor_lp, const double* ref_lp, const double* values,
+                               double kl_coef, double gamma, double lam, double* out_rewards,
+                               double* out_adv, double* out_ret, ppoexp_ctx ctx, int32_t where);
+/* Advantage whitening (north-star; no reference counterpart).  partials
+ * receives (n_tokens, sum adv, sum adv^2); the caller reduces them across
+ * ranks (one NCCL all-reduce / all-gather) and hands the global triple to
+ * apply: w = (adv - mean) / sqrt(var + 1e-8), population variance. */
+ppoexp_status ppoexp_whiten_partials(int64_t B, int64_t stride, const int64_t* lengths, const double* adv,
+                                     double* partials3, ppoexp_ctx ctx, int32_t where);
+ppoexp_status ppoexp_whiten_apply(int64_t B, int64_t stride, const int64_t* lengths, const double* adv,
+                                  const double* global_partials3, double* out, ppoexp_ctx ctx, int32_t where);
+
+/* ---------------------------------------------------- experience step */
+/* PpoHyper subset, include/aligner/losses.hpp:39-50 */
+typedef struct {
+  double kl_penalty_coef;
+  double gamma;
+  double lam;
+} ppoexp_ppo_hyper;
+
+/* Collective hook for the whitening partials: called on the host with a
+ * device pointer to `n` doubles that must be replaced in place by their sum
+ * over all ranks (stream-ordered on `stream`).  NULL = single rank. */
+typedef int32_t (*ppoexp_allreduce_fn)(double* device_buf, int64_t n, void* stream, void* user);
+
+/* The experience half of ppo_step (src/ppo.cpp:302-393) for this rank's B
+ * prompts, whose global indices are gidx0 .. gidx0+B-1:
+ *   (1) generate with SamplingSpec temperature(tau, mix_seed(seed,
+ *       step_index*1000003 + gidx)) (src/ppo.cpp:306-316) — or greedy;
+ *   (2) actor and reference log-probs over the response
+ *       (response_logprobs, src/ppo.cpp:282-287, :337-341);
+ *   (3) rewards: scripted (count of scripted_target in the response,
+ *       src/ppo.cpp:109-115) when rm == NULL, else reward_head under rm
+ *       (src/ppo.cpp:175-180); values under the critic (:184-188);
+ *   (4) kl_penalized_rewards + gae (:382-387); kl/reward sums (:389-392, :438-441);
+ *   (5) whitening (north-star) through `allreduce`.
+ * Outputs padded [B, max_new] (where = `where`), lengths[B], rewards[B];
+ * stats[8] = {kl_sum, kl_count, reward_sum, n_seqs, adv_mean, adv_std,
+ * gen_ms, total_ms}: the first six are GLOBAL (summed over ranks by the same
+ * single collective that carries the whitening partials — the reference's
+ * kl_mean / reward_mean, src/ppo.cpp:389-392, :438-441, are kl_sum/kl_count and
+ * reward_sum/n_seqs); gen_ms / total_ms are this rank's device times.
+ * The collective vector is 6 doubles: {n_tokens, sum adv, sum adv^2, kl_sum,
+ * reward_sum, n_seqs}. */
+typedef struct {
+  ppoexp_engine policy_engine;
+  ppoexp_model reference; /* may equal the engine's policy model */
+  ppoexp_model critic;    /* scalar_head required (PpoError otherwise, src/ppo.cpp:94-96) */
+  ppoexp_model rm;        /* NULL → scripted reward */
+  int32_t scripted_target;
+  int32_t reserved;
+  ppoexp_sampling sampling;
+  uint64_t seed;
+  int64_t step_index;
+  int64_t gidx0;
+  int64_t max_new;
+  ppoexp_ppo_hyper hyper;
+  ppoexp_allreduce_fn allreduce;
+  void* allreduce_user;
+} ppoexp_experience_request;
+
+typedef struct {
+  int32_t* tokens;      /* [B, max_new] */
+  int64_t* lengths;     /* [B] */
+  double* actor_lp;     /* [B, max_new] */
+  double* ref_lp;
+  double* values;
+  double* rewards;      /* [B] */
+  double* shaped;       /* [B, max_new] KL-shaped per-token rewards */
+  double* advantages;
+  double* returns;
+  double* whitened;
+  double* stats;        /* [8] */
+} ppoexp_rollout_batch;
+
+ppoexp_status ppoexp_make_experience(const ppoexp_experience_request* req, int64_t B, const int32_t* prompts,
+                                     const int64_t* offsets, const ppoexp_rollout_batch* out, int32_t where);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PPOEXP_H_ */

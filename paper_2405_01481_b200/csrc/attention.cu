@@ -1,0 +1,257 @@
+// attention.cu — K5 attention kernels.
+//
+//  * attn_prefill: causal multi-head attention over packed ragged sequences
+//    (scoring / critic / RM forwards and the engine's batched prefill).  The
+//    reference computes softmax(q·k^T/sqrt(dh) + mask)·v per head
+//    (src/model.cpp:230-236); masked scores are exp(-1e30) = 0, so a causal
+//    online softmax is the same arithmetic up to fp32 rounding.
+//  * attn_decode: one query per sequence against the PAGED KV cache (flash
+//    decode).  It appends this step's K/V row first (KvSession::step,
+//    src/model.cpp:305-308), then attends over positions 0..pos
+//    (src/model.cpp:313-333): scale by 1/sqrt(dh) before the max, exp(s-max),
+//    normalise, weighted V sum.
+#include <cfloat>
+
+#include "kernels.hpp"
+
+namespace ppoexp {
+
+namespace {
+
+// ---------------------------------------------------------------- prefill
+// CTA = (64 queries) x (one head) x (one sequence).  TPQ threads per query,
+// each owning 16 of the DH dims; K/V tiles of 64 keys staged in smem (fp32).
+template <class T, int DH>
+__global__ void __launch_bounds__(64 * (DH / 16)) attn_prefill_kernel(const T* __restrict__ qkv,
+                                                                      const int64_t* __restrict__ seq_offsets,
+                                                                      int64_t H, T* __restrict__ out) {
+  constexpr int TPQ = DH / 16, QT = 64, KT = 64, NT = QT * TPQ, LD = DH + 4;
+  extern __shared__ __align__(16) float sm[];
+  float* Ks = sm;
+  float* Vs = sm + KT * LD;
+  const int64_t b = blockIdx.z, h = blockIdx.y, q0 = int64_t(blockIdx.x) * QT;
+  const int64_t start = seq_offsets[b], len = seq_offsets[b + 1] - start;
+  if (q0 >= len) return;
+  const int64_t d = H * DH, ld3 = 3 * d;
+  const int tid = threadIdx.x, ql = tid / TPQ, part = tid % TPQ;
+  const int64_t qi = q0 + ql;
+  const bool valid = qi < len;
+  float q[16], acc[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    q[i] = valid ? to_f(qkv[(start + qi) * ld3 + h * DH + part * 16 + i]) : 0.f;
+    acc[i] = 0.f;
+  }
+  const float inv_sqrt_dh = 1.0f / sqrtf(float(DH));
+  float m = -FLT_MAX, l = 0.f;
+  const int64_t kend = min(len, q0 + QT);
+  for (int64_t k0 = 0; k0 < kend; k0 += KT) {
+    for (int e = tid; e < KT * DH; e += NT) {
+      const int j = e / DH, i = e % DH;
+      const int64_t kj = k0 + j;
+      float kv = 0.f, vv = 0.f;
+      if (kj < len) {
+        kv = to_f(qkv[(start + kj) * ld3 + d + h * DH + i]);
+        vv = to_f(qkv[(start + kj) * ld3 + 2 * d + h * DH + i]);
+      }
+      Ks[j * LD + i] = kv;
+      Vs[j * LD + i] = vv;
+    }
+    __syncthreads();
+    const int jn = int((kend - k0) < KT ? (kend - k0) : KT);
+    for (int j = 0; j < jn; ++j) {
+      const float* kr = Ks + j * LD + part * 16;
+      float s = 0.f;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) s = fmaf(q[i], kr[i], s);
+#pragma unroll
+      for (int o = TPQ / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      s *= inv_sqrt_dh;
+      if (valid && k0 + j <= qi) {
+        if (s > m) {
+          const float corr = m > -FLT_MAX ? expf(m - s) : 0.f;
+          l *= corr;
+#pragma unroll
+          for (int i = 0; i < 16; ++i) acc[i] *= corr;
+          m = s;
+        }
+        const float p = expf(s - m);
+        l += p;
+        const float* vr = Vs + j * LD + part * 16;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) acc[i] = fmaf(p, vr[i], acc[i]);
+      }
+    }
+    __syncthreads();
+  }
+  if (valid) {
+    const float inv = 1.0f / l;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) out[(start + qi) * d + h * DH + part * 16 + i] = from_f<T>(acc[i] * inv);
+  }
+}
+
+// ---------------------------------------------------------------- decode
+template <class T, int DH>
+__global__ void __launch_bounds__(128) attn_decode_kernel(const T* __restrict__ qkv, const int32_t* __restrict__ pos,
+                                                          const int32_t* __restrict__ done,
+                                                          const int32_t* __restrict__ block_table, int layer,
+                                                          KvGeom g, T* __restrict__ kv, T* __restrict__ out) {
+  constexpr int NW = 4;
+  constexpr int N = 16 / sizeof(T);  // elements per 16-byte vector
+  constexpr int LPT = (DH * sizeof(T) / 16) < 32 ? (DH * sizeof(T) / 16) : 32;  // lanes per token
+  constexpr int TPW = 32 / LPT;                                                  // tokens per warp pass
+  constexpr int NG = NW * TPW;                                                   // token groups
+  static_assert(DH * sizeof(T) / 16 <= 32, "head too wide");
+  extern __shared__ __align__(16) float sm[];
+  float* qs = sm;                // [DH]
+  float* red = qs + DH;          // [NG][DH]
+  float* scores = red + NG * DH; // [ctx]
+  __shared__ float wred[NW];
+  const int64_t b = blockIdx.y, h = blockIdx.x;
+  if (done[b]) return;
+  const int64_t p = pos[b], ctx = p + 1;
+  const int64_t d = g.H * DH, PS = g.page_size;
+  const T* row = qkv + b * 3 * d;
+  const int32_t* bt = block_table + b * g.max_pages_per_seq;
+  auto kbase = [&](int64_t t, int which) -> T* {
+    const int64_t page = bt[t / PS];
+    return kv + ((((int64_t)layer * g.n_pages + page) * 2 + which) * g.H + h) * PS * DH + (t % PS) * DH;
+  };
+  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  for (int i = tid; i < DH; i += 128) {
+    kbase(p, 0)[i] = row[d + h * DH + i];
+    kbase(p, 1)[i] = row[2 * d + h * DH + i];
+    qs[i] = to_f(row[h * DH + i]);
+  }
+  __syncthreads();
+  const float inv_sqrt_dh = 1.0f / sqrtf(float(DH));
+  const int sub = lane / LPT, part = lane % LPT;
+  // scores
+  float mloc = -FLT_MAX;
+  for (int64_t t0 = int64_t(w) * TPW; t0 < ctx; t0 += NW * TPW) {
+    const int64_t t = t0 + sub;
+    float s = 0.f;
+    if (t < ctx && part * N < DH) {
+      Vec16<T> kv4;
+      kv4.u = *reinterpret_cast<const uint4*>(kbase(t, 0) + part * N);
+#pragma unroll
+      for (int i = 0; i < N; ++i) s = fmaf(to_f(kv4.v[i]), qs[part * N + i], s);
+    }
+#pragma unroll
+    for (int o = LPT / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (t < ctx && part == 0) {
+      s *= inv_sqrt_dh;
+      scores[t] = s;
+      mloc = fmaxf(mloc, s);
+    }
+  }
+  mloc = warp_max(mloc);
+  if (lane == 0) wred[w] = mloc;
+  __syncthreads();
+  float mx = wred[0];
+#pragma unroll
+  for (int i = 1; i < NW; ++i) mx = fmaxf(mx, wred[i]);
+  __syncthreads();
+  float sloc = 0.f;
+  for (int64_t t = tid; t < ctx; t += 128) {
+    const float e = expf(scores[t] - mx);
+    scores[t] = e;
+    sloc += e;
+  }
+  sloc = warp_sum(sloc);
+  if (lane == 0) wred[w] = sloc;
+  __syncthreads();
+  float se = 0.f;
+#pragma unroll
+  for (int i = 0; i < NW; ++i) se += wred[i];
+  // P·V
+  float acc[N];
+#pragma unroll
+  for (int i = 0; i < N; ++i) acc[i] = 0.f;
+  const int grp = w * TPW + sub;
+  if (part * N < DH) {
+    for (int64_t t = grp; t < ctx; t += NG) {
+      const float pr = scores[t];
+      Vec16<T> v4;
+      v4.u = *reinterpret_cast<const uint4*>(kbase(t, 1) + part * N);
+#pragma unroll
+      for (int i = 0; i < N; ++i) acc[i] = fmaf(pr, to_f(v4.v[i]), acc[i]);
+    }
+#pragma unroll
+    for (int i = 0; i < N; ++i) red[grp * DH + part * N + i] = acc[i];
+  }
+  __syncthreads();
+  const float inv = 1.0f / se;
+  for (int i = tid; i < DH; i += 128) {
+    float s = 0.f;
+    for (int gi = 0; gi < NG; ++gi) s += red[gi * DH + i];
+    out[b * d + h * DH + i] = from_f<T>(s * inv);
+  }
+}
+
+template <class T, int DH>
+void prefill_impl(Ctx& c, const T* qkv, const int64_t* seq_offsets, int64_t B, int64_t max_len, int64_t H, T* out) {
+  constexpr int TPQ = DH / 16, LD = DH + 4;
+  const size_t smem = 2 * 64 * LD * sizeof(float);
+  auto k = attn_prefill_kernel<T, DH>;
+  PPOEXP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  dim3 grid(ceil_div(max_len, 64), H, B);
+  const double flops = 2.0 * 2.0 * B * H * double(max_len) * max_len / 2 * DH;
+  c.launch("attention_prefill", 0, flops, [&] { k<<<grid, 64 * TPQ, smem, c.stream>>>(qkv, seq_offsets, H, out); });
+}
+
+template <class T, int DH>
+void decode_impl(Ctx& c, const T* qkv, int64_t B, const int32_t* pos, const int32_t* done, const int32_t* block_table,
+                 int layer, const KvGeom& g, T* kv, T* out, double bytes) {
+  constexpr int LPT = (DH * sizeof(T) / 16) < 32 ? (DH * sizeof(T) / 16) : 32;
+  constexpr int NG = 4 * (32 / LPT);
+  const int64_t max_ctx = g.max_pages_per_seq * g.page_size;
+  const size_t smem = (DH + NG * DH + max_ctx) * sizeof(float);
+  auto k = attn_decode_kernel<T, DH>;
+  PPOEXP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  dim3 grid(g.H, B);
+  c.launch("decode_attention", bytes, 0, [&] {
+    k<<<grid, 128, smem, c.stream>>>(qkv, pos, done, block_table, layer, g, kv, out);
+  });
+}
+
+}  // namespace
+
+template <class T>
+void launch_attention_prefill(Ctx& c, const T* qkv, const int64_t* seq_offsets, int64_t B, int64_t max_len,
+                              int64_t H, int64_t DH, T* out) {
+  if (B <= 0 || max_len <= 0) return;
+  switch (DH) {
+    case 16: return prefill_impl<T, 16>(c, qkv, seq_offsets, B, max_len, H, out);
+    case 32: return prefill_impl<T, 32>(c, qkv, seq_offsets, B, max_len, H, out);
+    case 64: return prefill_impl<T, 64>(c, qkv, seq_offsets, B, max_len, H, out);
+    case 128: return prefill_impl<T, 128>(c, qkv, seq_offsets, B, max_len, H, out);
+    default: throw ContractError("attention: head_dim " + std::to_string(DH) + " unsupported (16/32/64/128)");
+  }
+}
+
+template <class T>
+void launch_attention_decode(Ctx& c, const T* qkv, int64_t B, const int32_t* pos, const int32_t* done,
+                             const int32_t* block_table, int layer, const KvGeom& g, T* kv, T* out,
+                             double algorithmic_bytes) {
+  if (B <= 0) return;
+  switch (g.DH) {
+    case 16: return decode_impl<T, 16>(c, qkv, B, pos, done, block_table, layer, g, kv, out, algorithmic_bytes);
+    case 32: return decode_impl<T, 32>(c, qkv, B, pos, done, block_table, layer, g, kv, out, algorithmic_bytes);
+    case 64: return decode_impl<T, 64>(c, qkv, B, pos, done, block_table, layer, g, kv, out, algorithmic_bytes);
+    case 128: return decode_impl<T, 128>(c, qkv, B, pos, done, block_table, layer, g, kv, out, algorithmic_bytes);
+    default: throw ContractError("attention: head_dim " + std::to_string(g.DH) + " unsupported (16/32/64/128)");
+  }
+}
+
+template void launch_attention_prefill<float>(Ctx&, const float*, const int64_t*, int64_t, int64_t, int64_t, int64_t,
+                                              float*);
+template void launch_attention_prefill<bf16>(Ctx&, const bf16*, const int64_t*, int64_t, int64_t, int64_t, int64_t,
+                                             bf16*);
+template void launch_attention_decode<float>(Ctx&, const float*, int64_t, const int32_t*, const int32_t*,
+                                             const int32_t*, int, const KvGeom&, float*, float*, double);
+template void launch_attention_decode<bf16>(Ctx&, const bf16*, int64_t, const int32_t*, const int32_t*,
+                                            const int32_t*, int, const KvGeom&, bf16*, bf16*, double);
+
+}  // namespace ppoexp

@@ -1,0 +1,90 @@
+// common.cuh — shared helpers for the ppoexp sm_100a kernels and host runtime.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+namespace ppoexp {
+
+using bf16 = __nv_bfloat16;
+
+// ------------------------------------------------------------ errors
+// Typed errors mirror the reference's exception set
+// (include/aligner/tensor.hpp:17-25, engine.hpp:19-21, ppo.hpp:22-24).
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+inline Error ContractError(const std::string& m) { return Error(1, m); }
+inline Error IndexError(const std::string& m) { return Error(2, m); }
+inline Error ShapeError(const std::string& m) { return Error(3, m); }
+inline Error RefitError(const std::string& m) { return Error(4, m); }
+inline Error PpoError(const std::string& m) { return Error(5, m); }
+
+#define PPOEXP_CUDA(expr)                                                                        \
+  do {                                                                                          \
+    cudaError_t e_ = (expr);                                                                    \
+    if (e_ != cudaSuccess) {                                                                    \
+      (void)cudaGetLastError();                                                                 \
+      throw ::ppoexp::Error(e_ == cudaErrorMemoryAllocation ? 7 : 6,                            \
+                            std::string("cuda: ") + cudaGetErrorString(e_) + " at " #expr);     \
+    }                                                                                           \
+  } while (0)
+
+// ------------------------------------------------------------ device math
+template <class T>
+__device__ __forceinline__ float to_f(T x);
+template <>
+__device__ __forceinline__ float to_f<float>(float x) { return x; }
+template <>
+__device__ __forceinline__ float to_f<bf16>(bf16 x) { return __bfloat162float(x); }
+
+template <class T>
+__device__ __forceinline__ T from_f(float x);
+template <>
+__device__ __forceinline__ float from_f<float>(float x) { return x; }
+template <>
+__device__ __forceinline__ bf16 from_f<bf16>(float x) { return __float2bfloat16_rn(x); }
+
+// GELU-tanh, reference src/model.cpp:358-361 (fp32 here).
+__device__ __forceinline__ float gelu_tanh(float x) {
+  const float kC = 0.7978845608028654f;
+  return 0.5f * x * (1.0f + tanhf(kC * (x + 0.044715f * x * x * x)));
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// 16-byte vector of T.
+template <class T>
+struct Vec16 {
+  static constexpr int N = 16 / sizeof(T);
+  union {
+    uint4 u;
+    T v[N];
+  };
+};
+
+constexpr int kPadToken = 256;  // include/aligner/model.hpp:17
+constexpr int kEotToken = 257;  // include/aligner/model.hpp:18
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+}  // namespace ppoexp

@@ -1,0 +1,483 @@
+// engine.cu — the rollout engine (Engine / generate_batch analog,
+// include/aligner/engine.hpp:49-92, src/model.cpp:438-482).
+//
+//   * paged KV pool in HBM: pages of `page_size` tokens, one block table per
+//     sequence, pages assigned per call for P_b + budget_b positions;
+//   * batched prefill: all prompts in one packed forward that scatters K/V
+//     into the pages and yields the last-position logits;
+//   * decode: K steps (decode forward + fused sampler) captured in one CUDA
+//     graph, replayed until every sequence has emitted EOT or exhausted its
+//     budget; the host polls a done-counter one replay behind, so the GPU
+//     queue never drains.
+#include <algorithm>
+#include <cstring>
+#include <random>
+
+#include "engine.hpp"
+
+namespace ppoexp {
+
+namespace {
+constexpr int kUnitsPerGraph = 8;
+}
+
+Engine::Engine(Model* model, const ppoexp_engine_options* o) : m(model), c(model->ctx) {
+  if (o) opts = *o;
+  if (opts.max_batch <= 0) opts.max_batch = 256;
+  if (opts.page_size <= 0) opts.page_size = 64;
+  if (o == nullptr) opts.use_graphs = 1;
+  const auto& cfg = m->cfg;
+  const int64_t S = cfg.max_seq_len;
+  if (opts.max_total_tokens <= 0) opts.max_total_tokens = opts.max_batch * S;
+  geom.n_layers = cfg.n_layers;
+  geom.page_size = opts.page_size;
+  geom.H = cfg.n_heads;
+  geom.DH = cfg.d_model / cfg.n_heads;
+  geom.max_pages_per_seq = ceil_div(S, opts.page_size);
+  geom.n_pages = std::max<int64_t>(ceil_div(opts.max_total_tokens, opts.page_size), geom.max_pages_per_seq);
+  DeviceGuard g(c->device);
+  const size_t ts = m->tsize();
+  kv.ensure(size_t(geom.n_layers) * geom.n_pages * 2 * geom.H * geom.page_size * geom.DH * ts);
+  const int64_t mb = opts.max_batch, d = cfg.d_model, f = cfg.d_ff;
+  auto al = [](size_t x) { return (x + 255) / 256 * 256; };
+  size_t sbytes = 0;
+  const size_t o_next = sbytes; sbytes += al(mb * 4);
+  const size_t o_pos = sbytes; sbytes += al(mb * 4);
+  const size_t o_ngen = sbytes; sbytes += al(mb * 4);
+  const size_t o_done = sbytes; sbytes += al(mb * 4);
+  const size_t o_budget = sbytes; sbytes += al(mb * 4);
+  const size_t o_nact = sbytes; sbytes += al(16);
+  const size_t o_bt = sbytes; sbytes += al(mb * geom.max_pages_per_seq * 4);
+  const size_t o_sp = sbytes; sbytes += al(sizeof(SampleParams));
+  const size_t o_x = sbytes; sbytes += al(mb * d * 4);
+  const size_t o_h = sbytes; sbytes += al(mb * d * ts);
+  const size_t o_qkv = sbytes; sbytes += al(mb * 3 * d * ts);
+  const size_t o_att = sbytes; sbytes += al(mb * d * ts);
+  const size_t o_up = sbytes; sbytes += al(mb * f * ts);
+  const size_t o_logits = sbytes; sbytes += al(mb * m->vpad * 4);
+  const size_t o_otok = sbytes; sbytes += al(mb * S * 4);
+  const size_t o_olp = sbytes; sbytes += al(mb * S * 4);
+  const size_t o_uni = sbytes; sbytes += al(mb * S * 8);
+  const size_t o_last = sbytes; sbytes += al(mb * 4);
+  state.ensure(sbytes);
+  PPOEXP_CUDA(cudaMemset(state.ptr, 0, sbytes));
+  char* p = static_cast<char*>(state.ptr);
+  next_tok = reinterpret_cast<int32_t*>(p + o_next);
+  pos = reinterpret_cast<int32_t*>(p + o_pos);
+  n_gen = reinterpret_cast<int32_t*>(p + o_ngen);
+  done = reinterpret_cast<int32_t*>(p + o_done);
+  budget = reinterpret_cast<int32_t*>(p + o_budget);
+  n_active = reinterpret_cast<int32_t*>(p + o_nact);
+  block_table = reinterpret_cast<int32_t*>(p + o_bt);
+  sparams = reinterpret_cast<SampleParams*>(p + o_sp);
+  x = reinterpret_cast<float*>(p + o_x);
+  h = p + o_h;
+  qkv = p + o_qkv;
+  att = p + o_att;
+  up = p + o_up;
+  logits = reinterpret_cast<float*>(p + o_logits);
+  out_tok = reinterpret_cast<int32_t*>(p + o_otok);
+  out_lp = reinterpret_cast<float*>(p + o_olp);
+  uniforms = reinterpret_cast<double*>(p + o_uni);
+  last_rows = reinterpret_cast<int32_t*>(p + o_last);
+  PPOEXP_CUDA(cudaMallocHost(&host_flags, 64));
+  PPOEXP_CUDA(cudaEventCreateWithFlags(&poll_ev[0], cudaEventDisableTiming));
+  PPOEXP_CUDA(cudaEventCreateWithFlags(&poll_ev[1], cudaEventDisableTiming));
+  PPOEXP_CUDA(cudaEventCreate(&t0));
+  PPOEXP_CUDA(cudaEventCreate(&t1));
+}
+
+Engine::~Engine() {
+  DeviceGuard g(c->device);
+  cudaStreamSynchronize(c->stream);
+  for (auto& [k, gs] : graphs)
+    for (int j = 0; j < 2; ++j) {
+      if (gs.exec[j]) cudaGraphExecDestroy(gs.exec[j]);
+      for (auto& t : gs.events[j]) {
+        cudaEventDestroy(t.a);
+        cudaEventDestroy(t.b);
+      }
+    }
+  if (host_flags) cudaFreeHost(host_flags);
+  cudaEventDestroy(poll_ev[0]);
+  cudaEventDestroy(poll_ev[1]);
+  cudaEventDestroy(t0);
+  cudaEventDestroy(t1);
+}
+
+SamplerState Engine::sampler_state() const {
+  SamplerState s;
+  s.params = sparams;
+  s.next_tok = next_tok;
+  s.pos = pos;
+  s.n_gen = n_gen;
+  s.done = done;
+  s.budget = budget;
+  s.uniforms = uniforms;
+  s.ustride = m->cfg.max_seq_len;
+  s.out_tokens = out_tok;
+  s.out_lps = out_lp;
+  s.ostride = m->cfg.max_seq_len;
+  s.n_active = n_active;
+  return s;
+}
+
+// One decode unit: feed next_tok[b] at pos[b] through the model, then sample.
+template <class T>
+void Engine::decode_unit(int64_t B, int64_t unit) {
+  Ctx& cc = *c;
+  const int64_t d = m->d(), f = m->cfg.d_ff, V = m->cfg.vocab_size;
+  T* hh = static_cast<T*>(h);
+  T* q3 = static_cast<T*>(qkv);
+  T* at = static_cast<T*>(att);
+  T* uu = static_cast<T*>(up);
+  cur_unit = unit;
+  launch_embed<T>(cc, next_tok, pos, B, d, static_cast<const T*>(m->tok), static_cast<const T*>(m->pos), x);
+  for (int64_t l = 0; l < m->cfg.n_layers; ++l) {
+    const Layer& ly = m->layers[l];
+    launch_layernorm<T>(cc, x, B, d, ly.ln1w, ly.ln1b, hh, nullptr, nullptr, nullptr);
+    gemm<T>(cc, hh, d, static_cast<const T*>(ly.wqkv), d, B, 3 * d, d, Epi::kStore, q3, 3 * d);
+    launch_attention_decode<T>(cc, q3, B, pos, done, block_table, int(l), geom, static_cast<T*>(kv.ptr), at, 0.0);
+    gemm<T>(cc, at, d, static_cast<const T*>(ly.wo), d, B, d, d, Epi::kAddResidual, x, d);
+    launch_layernorm<T>(cc, x, B, d, ly.ln2w, ly.ln2b, hh, nullptr, nullptr, nullptr);
+    gemm<T>(cc, hh, d, static_cast<const T*>(ly.wup), d, B, f, d, Epi::kGelu, uu, f);
+    gemm<T>(cc, uu, f, static_cast<const T*>(ly.wdown), f, B, d, f, Epi::kAddResidual, x, d);
+  }
+  launch_layernorm<T>(cc, x, B, d, m->lnfw, m->lnfb, hh, nullptr, nullptr, nullptr);
+  gemm<T>(cc, hh, d, static_cast<const T*>(m->tok), d, B, V, d, Epi::kStoreF32, logits, m->vpad);
+  launch_sampler(cc, logits, m->vpad, B, V, sampler_state());
+}
+
+void Engine::run_unit(int64_t B, int64_t unit) {
+  if (m->dtype == PPOEXP_F32)
+    decode_unit<float>(B, unit);
+  else
+    decode_unit<bf16>(B, unit);
+}
+
+Engine::GraphSet& Engine::graph_for(int64_t B) {
+  auto it = graphs.find(B);
+  if (it != graphs.end() && it->second.profiled == c->profiling) return it->second;
+  if (it != graphs.end()) {
+    for (int j = 0; j < 2; ++j) {
+      cudaGraphExecDestroy(it->second.exec[j]);
+      for (auto& t : it->second.events[j]) {
+        cudaEventDestroy(t.a);
+        cudaEventDestroy(t.b);
+      }
+    }
+    graphs.erase(it);
+  }
+  GraphSet& gs = graphs[B];
+  gs.profiled = c->profiling;
+  gs.units = kUnitsPerGraph;
+  for (int j = 0; j < 2; ++j) {
+    cudaGraph_t graph;
+    PPOEXP_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    c->capturing = true;
+    c->capture_launches = 0;
+    c->capture_events = &gs.events[j];
+    try {
+      for (int k = 0; k < gs.units; ++k) run_unit(B, k);
+    } catch (...) {
+      c->capturing = false;
+      c->capture_events = nullptr;
+      cudaStreamEndCapture(c->stream, &graph);
+      throw;
+    }
+    c->capturing = false;
+    c->capture_events = nullptr;
+    PPOEXP_CUDA(cudaStreamEndCapture(c->stream, &graph));
+    PPOEXP_CUDA(cudaGraphInstantiate(&gs.exec[j], graph, 0));
+    PPOEXP_CUDA(cudaGraphDestroy(graph));
+    gs.nodes = c->capture_launches;
+    // the per-launch events created during capture are owned by the graph set
+  }
+  return gs;
+}
+
+// Attribute the algorithmic bytes of each decode-attention launch of a
+// finished replay: unit u feeds sequence b iff u <= n_b - 1, over a context
+// of P_b + u positions (K and V, all heads), plus the appended row.
+void Engine::harvest_replay(const std::vector<TimedLaunch>& evs, int64_t unit0, int units) {
+  if (!c->profiling) return;
+  const int64_t d = m->d();
+  const double ts = double(m->tsize());
+  int64_t per_unit = 0;
+  for (auto& t : evs)
+    if (t.cls == "decode_attention") ++per_unit;
+  per_unit /= std::max(units, 1);
+  int64_t seen = 0;
+  for (auto& t : evs) {
+    TimedLaunch tt = t;
+    if (t.cls == "decode_attention") {
+      const int64_t u = unit0 + seen / std::max<int64_t>(per_unit, 1);
+      ++seen;
+      double bytes = 0;
+      for (size_t b = 0; b < cur_P.size(); ++b)
+        if (u <= cur_len[b] - 1) bytes += (double(cur_P[b] + u) * 2.0 + 2.0) * d * ts;
+      tt.bytes = bytes;
+    }
+    c->harvest_list({tt}, false);
+  }
+}
+
+void Engine::generate(int64_t B, const int32_t* prompts, const int64_t* offsets, const int64_t* max_new,
+                      const ppoexp_sampling* sampling, const uint64_t* seeds, int64_t out_stride,
+                      int32_t* out_tokens, double* out_logprobs, int64_t* out_lengths, int where, double* ms_out,
+                      int where_out, int where_tokens) {
+  if (where_out < 0) where_out = where;
+  if (where_tokens < 0) where_tokens = where;
+  std::lock_guard<std::recursive_mutex> lk(c->mu);
+  DeviceGuard g(c->device);
+  if (B < 0) throw ContractError("generate_batch: negative batch");
+  if (B == 0) {
+    if (ms_out) *ms_out = 0;
+    return;
+  }
+  if (!sampling) throw ContractError("generate: sampling spec required");
+  const auto& cfg = m->cfg;
+  const int64_t S = cfg.max_seq_len;
+  // host copies of the small per-task arrays
+  std::vector<int64_t> off(B + 1), mx(B);
+  std::vector<uint64_t> sd(B, 0);
+  if (where == PPOEXP_HOST) {
+    std::memcpy(off.data(), offsets, (B + 1) * 8);
+    std::memcpy(mx.data(), max_new, B * 8);
+    if (seeds) std::memcpy(sd.data(), seeds, B * 8);
+  } else {
+    PPOEXP_CUDA(cudaMemcpy(off.data(), offsets, (B + 1) * 8, cudaMemcpyDeviceToHost));
+    PPOEXP_CUDA(cudaMemcpy(mx.data(), max_new, B * 8, cudaMemcpyDeviceToHost));
+    if (seeds) PPOEXP_CUDA(cudaMemcpy(sd.data(), seeds, B * 8, cudaMemcpyDeviceToHost));
+  }
+  if (off[0] != 0) throw ContractError("generate: offsets[0] must be 0");
+  for (int64_t b = 0; b < B; ++b) {
+    const int64_t P = off[b + 1] - off[b];
+    if (P <= 0) throw ContractError("generate: prompt must be nonempty");
+    if (P > S) throw ContractError("generate: sequence length exceeds max_seq_len " + std::to_string(S));
+    if (mx[b] < 0) throw ContractError("generate: max_new must be >= 0");
+  }
+  if (where_tokens == PPOEXP_HOST) {
+    for (int64_t i = 0; i < off[B]; ++i)
+      if (prompts[i] < 0 || prompts[i] >= cfg.vocab_size)
+        throw IndexError("generate: token id " + std::to_string(prompts[i]) + " out of range [0," +
+                         std::to_string(cfg.vocab_size) + ")");
+  }
+  last_lengths.assign(B, 0);
+  cudaEvent_t e0 = t0, e1 = t1;
+  PPOEXP_CUDA(cudaEventRecord(e0, c->stream));
+  for (int64_t b0 = 0; b0 < B; b0 += opts.max_batch) {
+    const int64_t nb = std::min<int64_t>(opts.max_batch, B - b0);
+    run_chunk(nb, prompts, off, b0, mx, *sampling, sd, out_stride, out_tokens, out_logprobs, out_lengths, where,
+              where_out, where_tokens);
+  }
+  PPOEXP_CUDA(cudaEventRecord(e1, c->stream));
+  PPOEXP_CUDA(cudaEventSynchronize(e1));
+  float ms = 0;
+  PPOEXP_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+  last_ms = ms;
+  if (ms_out) *ms_out = ms;
+  c->harvest();
+}
+
+void Engine::run_chunk(int64_t B, const int32_t* prompts, const std::vector<int64_t>& off_all, int64_t b0,
+                       const std::vector<int64_t>& mx_all, const ppoexp_sampling& sp,
+                       const std::vector<uint64_t>& seeds_all, int64_t out_stride, int32_t* out_tokens,
+                       double* out_logprobs, int64_t* out_lengths, int where, int where_out, int where_tokens) {
+  Ctx& cc = *c;
+  const auto& cfg = m->cfg;
+  const int64_t S = cfg.max_seq_len, PS = geom.page_size, d = m->d();
+  std::vector<int64_t> P(B), bud(B);
+  int64_t max_budget = 0, pages = 0;
+  for (int64_t b = 0; b < B; ++b) {
+    P[b] = off_all[b0 + b + 1] - off_all[b0 + b];
+    bud[b] = std::min<int64_t>(mx_all[b0 + b], S - std::min<int64_t>(P[b], S));  // src/model.cpp:447-448
+    max_budget = std::max(max_budget, bud[b]);
+    pages += ceil_div(P[b] + bud[b], PS);
+  }
+  if (pages > geom.n_pages)
+    throw ContractError("engine: KV pool too small (" + std::to_string(pages) + " pages needed, " +
+                        std::to_string(geom.n_pages) + " available); raise max_total_tokens");
+  // block tables: contiguous page runs per sequence
+  std::vector<int32_t> bt(B * geom.max_pages_per_seq, 0);
+  int64_t next_page = 0;
+  for (int64_t b = 0; b < B; ++b) {
+    const int64_t np = ceil_div(P[b] + bud[b], PS);
+    for (int64_t k = 0; k < np; ++k) bt[b * geom.max_pages_per_seq + k] = int32_t(next_page++);
+  }
+  // state
+  std::vector<int32_t> st_pos(B), st_done(B), st_bud(B), last(B);
+  int32_t active = 0;
+  for (int64_t b = 0; b < B; ++b) {
+    st_pos[b] = int32_t(std::min<int64_t>(P[b], S - 1));
+    st_done[b] = bud[b] == 0;
+    st_bud[b] = int32_t(bud[b]);
+    last[b] = int32_t(off_all[b0 + b + 1] - off_all[b0] - 1);
+    active += bud[b] > 0;
+  }
+  SampleParams spd{sp.greedy, float(sp.temperature), sp.top_k, sp.top_p};
+  // staging (pinned) → device
+  const size_t n_bt = bt.size() * 4;
+  const size_t need = n_bt + 4 * B * 4 + sizeof(spd) + 64 + (sp.greedy ? 0 : size_t(B) * S * 8);
+  char* hs = static_cast<char*>(cc.pinned_staging(need));
+  size_t o = 0;
+  auto put = [&](void* dst, const void* src, size_t n) {
+    std::memcpy(hs + o, src, n);
+    PPOEXP_CUDA(cudaMemcpyAsync(dst, hs + o, n, cudaMemcpyHostToDevice, cc.stream));
+    o += (n + 15) / 16 * 16;
+  };
+  put(block_table, bt.data(), n_bt);
+  put(pos, st_pos.data(), B * 4);
+  put(done, st_done.data(), B * 4);
+  put(budget, st_bud.data(), B * 4);
+  put(last_rows, last.data(), B * 4);
+  put(n_active, &active, 4);
+  put(sparams, &spd, sizeof(spd));
+  PPOEXP_CUDA(cudaMemsetAsync(n_gen, 0, B * 4, cc.stream));
+  if (!sp.greedy) {
+    // One mt19937_64 uniform per sampled token, Rng(seed) stream
+    // (include/aligner/rng.hpp:21-23; consumed in order, src/model.cpp:464).
+    double* u = reinterpret_cast<double*>(hs + o);
+    for (int64_t b = 0; b < B; ++b) {
+      std::mt19937_64 gen(seeds_all[b0 + b]);
+      for (int64_t i = 0; i < bud[b]; ++i) u[b * S + i] = double(gen() >> 11) * 0x1.0p-53;
+    }
+    PPOEXP_CUDA(cudaMemcpyAsync(uniforms, u, size_t(B) * S * 8, cudaMemcpyHostToDevice, cc.stream));
+  }
+  // packed prompts
+  Packed pk;
+  pk.offsets.resize(B + 1);
+  for (int64_t b = 0; b <= B; ++b) pk.offsets[b] = off_all[b0 + b] - off_all[b0];
+  const int64_t M = pk.offsets[B];
+  pk.tokens_d = static_cast<int32_t*>(cc.workspace("gen.prompts", M * 4));
+  copy_in(cc, pk.tokens_d, prompts + off_all[b0], M * 4, where_tokens);
+  pack_metadata(cc, pk, "gen");  // synchronises: the pinned staging above is free again
+  // prefill → last-position logits → first sample
+  KvTarget kt{block_table, geom, kv.ptr};
+  float* xr = forward_layers(*m, pk, &kt);
+  if (m->dtype == PPOEXP_F32) {
+    launch_layernorm<float>(cc, xr, B, d, m->lnfw, m->lnfb, static_cast<float*>(h), last_rows, nullptr, nullptr);
+    gemm<float>(cc, static_cast<float*>(h), d, static_cast<const float*>(m->tok), d, B, cfg.vocab_size, d,
+                Epi::kStoreF32, logits, m->vpad);
+  } else {
+    launch_layernorm<bf16>(cc, xr, B, d, m->lnfw, m->lnfb, static_cast<bf16*>(h), last_rows, nullptr, nullptr);
+    gemm<bf16>(cc, static_cast<bf16*>(h), d, static_cast<const bf16*>(m->tok), d, B, cfg.vocab_size, d,
+               Epi::kStoreF32, logits, m->vpad);
+  }
+  launch_sampler(cc, logits, m->vpad, B, cfg.vocab_size, sampler_state());
+  // decode: units 1 .. max_budget-1
+  cur_P = P;
+  cur_len = bud;  // upper bound until the true lengths are known
+  const int64_t units = max_budget - 1;
+  std::vector<std::pair<int, int64_t>> pending;  // (graph slot, unit0) awaiting harvest
+  if (units > 0) {
+    if (opts.use_graphs) {
+      GraphSet& gs = graph_for(B);
+      const int64_t R = ceil_div(units, gs.units);
+      int64_t r = 0;
+      bool stop = false;
+      for (; r < R && !stop; ++r) {
+        const int j = int(r & 1);
+        PPOEXP_CUDA(cudaGraphLaunch(gs.exec[j], cc.stream));
+        cc.launches += gs.nodes;
+        PPOEXP_CUDA(cudaMemcpyAsync(host_flags + j, n_active, 4, cudaMemcpyDeviceToHost, cc.stream));
+        PPOEXP_CUDA(cudaEventRecord(poll_ev[j], cc.stream));
+        pending.push_back({j, 1 + r * gs.units});
+        if (r >= 1) {
+          PPOEXP_CUDA(cudaEventSynchronize(poll_ev[1 - j]));
+          if (cc.profiling) {
+            // events of replay r-1 must be read before that graph runs again
+            auto [sj, u0] = pending.front();
+            pending.erase(pending.begin());
+            prof_replays.push_back({gs.events[sj], u0, gs.units});
+            snapshot_events(prof_replays.back());
+          }
+          if (host_flags[1 - j] == 0) stop = true;
+        }
+      }
+      PPOEXP_CUDA(cudaStreamSynchronize(cc.stream));
+      if (cc.profiling) {
+        for (auto& [sj, u0] : pending) {
+          prof_replays.push_back({gs.events[sj], u0, gs.units});
+          snapshot_events(prof_replays.back());
+        }
+      }
+    } else {
+      for (int64_t u = 1; u <= units; ++u) {
+        run_unit(B, u);
+        if (u % kUnitsPerGraph == 0) {
+          PPOEXP_CUDA(cudaMemcpyAsync(host_flags, n_active, 4, cudaMemcpyDeviceToHost, cc.stream));
+          PPOEXP_CUDA(cudaStreamSynchronize(cc.stream));
+          if (host_flags[0] == 0) break;
+        }
+      }
+    }
+  }
+  // outputs
+  std::vector<int32_t> ng(B);
+  PPOEXP_CUDA(cudaMemcpyAsync(ng.data(), n_gen, B * 4, cudaMemcpyDeviceToHost, cc.stream));
+  PPOEXP_CUDA(cudaStreamSynchronize(cc.stream));
+  for (int64_t b = 0; b < B; ++b) {
+    cur_len[b] = ng[b];
+    last_lengths[b0 + b] = ng[b];
+  }
+  if (cc.profiling) {
+    for (auto& pr : prof_replays) harvest_snapshot(pr);
+    prof_replays.clear();
+  }
+  double* lp64 = static_cast<double*>(cc.workspace("gen.lp64", size_t(B) * S * 8));
+  launch_f32_to_f64(cc, out_lp, B * S, lp64);
+  if (where_out == PPOEXP_DEVICE) {
+    std::vector<int64_t> l64(ng.begin(), ng.end());
+    PPOEXP_CUDA(cudaMemcpyAsync(out_lengths + b0, l64.data(), B * 8, cudaMemcpyHostToDevice, cc.stream));
+    PPOEXP_CUDA(cudaStreamSynchronize(cc.stream));
+  } else {
+    for (int64_t b = 0; b < B; ++b) out_lengths[b0 + b] = ng[b];
+  }
+  const auto kind = where_out == PPOEXP_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+  const int64_t w = std::min<int64_t>(out_stride, S);
+  PPOEXP_CUDA(cudaMemcpy2DAsync(out_tokens + b0 * out_stride, out_stride * 4, out_tok, S * 4, w * 4, B, kind, cc.stream));
+  PPOEXP_CUDA(
+      cudaMemcpy2DAsync(out_logprobs + b0 * out_stride, out_stride * 8, lp64, S * 8, w * 8, B, kind, cc.stream));
+  if (where_out == PPOEXP_HOST) PPOEXP_CUDA(cudaStreamSynchronize(cc.stream));
+}
+
+// Profiling support: copy the elapsed times of a finished replay's events
+// (the graph will overwrite them on its next launch).
+void Engine::snapshot_events(ReplayTimes& r) {
+  r.ms.resize(r.events.size());
+  for (size_t i = 0; i < r.events.size(); ++i) {
+    PPOEXP_CUDA(cudaEventSynchronize(r.events[i].b));
+    float ms = 0;
+    PPOEXP_CUDA(cudaEventElapsedTime(&ms, r.events[i].a, r.events[i].b));
+    r.ms[i] = ms;
+  }
+}
+
+void Engine::harvest_snapshot(const ReplayTimes& r) {
+  const int64_t d = m->d();
+  const double ts = double(m->tsize());
+  int64_t per_unit = 0;
+  for (auto& t : r.events)
+    if (t.cls == "decode_attention") ++per_unit;
+  per_unit /= std::max(r.units, 1);
+  int64_t seen = 0;
+  for (size_t i = 0; i < r.events.size(); ++i) {
+    const auto& t = r.events[i];
+    double bytes = t.bytes;
+    const int64_t u = r.unit0 + (per_unit ? seen / per_unit : 0);
+    if (t.cls == "decode_attention") {
+      ++seen;
+      bytes = 0;
+      for (size_t b = 0; b < cur_P.size(); ++b)
+        if (u <= cur_len[b] - 1) bytes += (double(cur_P[b] + u) * 2.0 + 2.0) * d * ts;
+    }
+    auto& s = c->stats[t.cls];
+    s.ms += r.ms[i];
+    s.launches += 1;
+    s.bytes += bytes;
+    s.flops += t.flops;
+  }
+}
+
+}  // namespace ppoexp

@@ -1,0 +1,73 @@
+// engine.hpp — rollout engine over a device model (paged KV + graphs).
+#pragma once
+
+#include <map>
+#include <vector>
+
+#include "model.hpp"
+
+namespace ppoexp {
+
+struct Engine {
+  Model* m;
+  Ctx* c;
+  ppoexp_engine_options opts{};
+  KvGeom geom{};
+  DeviceBuffer kv;     // paged pool
+  DeviceBuffer state;  // per-sequence state + step activations + outputs
+  int32_t *next_tok, *pos, *n_gen, *done, *budget, *n_active, *block_table, *last_rows;
+  SampleParams* sparams;
+  float* x;
+  void *h, *qkv, *att, *up;
+  float* logits;
+  int32_t* out_tok;
+  float* out_lp;
+  double* uniforms;
+  int32_t* host_flags = nullptr;
+  cudaEvent_t poll_ev[2]{}, t0{}, t1{};
+  double last_ms = 0;
+  int64_t cur_unit = 0;
+  std::vector<int64_t> cur_P, cur_len;
+
+  struct GraphSet {
+    cudaGraphExec_t exec[2]{};
+    std::vector<TimedLaunch> events[2];
+    int64_t nodes = 0;
+    int units = 8;
+    bool profiled = false;
+  };
+  std::map<int64_t, GraphSet> graphs;
+
+  struct ReplayTimes {
+    std::vector<TimedLaunch> events;
+    int64_t unit0;
+    int units;
+    std::vector<float> ms;
+  };
+  std::vector<ReplayTimes> prof_replays;
+
+  Engine(Model* model, const ppoexp_engine_options* o);
+  ~Engine();
+
+  void generate(int64_t B, const int32_t* prompts, const int64_t* offsets, const int64_t* max_new,
+                const ppoexp_sampling* sampling, const uint64_t* seeds, int64_t out_stride, int32_t* out_tokens,
+                double* out_logprobs, int64_t* out_lengths, int where, double* ms_out, int where_out = -1,
+                int where_tokens = -1);
+  std::vector<int64_t> last_lengths;  // host copy of the last call's lengths
+
+ private:
+  void run_chunk(int64_t B, const int32_t* prompts, const std::vector<int64_t>& off_all, int64_t b0,
+                 const std::vector<int64_t>& mx_all, const ppoexp_sampling& sp, const std::vector<uint64_t>& seeds_all,
+                 int64_t out_stride, int32_t* out_tokens, double* out_logprobs, int64_t* out_lengths, int where,
+                 int where_out, int where_tokens);
+  SamplerState sampler_state() const;
+  template <class T>
+  void decode_unit(int64_t B, int64_t unit);
+  void run_unit(int64_t B, int64_t unit);
+  GraphSet& graph_for(int64_t B);
+  void harvest_replay(const std::vector<TimedLaunch>& evs, int64_t unit0, int units);
+  void snapshot_events(ReplayTimes& r);
+  void harvest_snapshot(const ReplayTimes& r);
+};
+
+}  // namespace ppoexp

@@ -1,0 +1,104 @@
+// kernels.hpp — host launchers for the sm_100a kernels of the experience path.
+// T is the compute/storage type of weights and GEMM operands: float (parity
+// mode) or bf16 (perf mode).  The residual stream is always fp32.
+#pragma once
+
+#include <cstdint>
+
+#include "runtime.hpp"
+
+namespace ppoexp {
+
+// Paged KV cache geometry.  Pool layout (elements of T):
+//   kv[(((layer * n_pages + page) * 2 + kv) * H + h) * page_size * DH + slot * DH + i]
+struct KvGeom {
+  int64_t n_layers, n_pages, page_size, H, DH, max_pages_per_seq;
+};
+
+// K1: x[r] = tok[tokens[r]] + pos[positions[r]] (src/model.cpp:290-295).
+template <class T>
+void launch_embed(Ctx& c, const int32_t* tokens, const int32_t* positions, int64_t rows, int64_t d,
+                  const T* tok, const T* pos, float* x);
+
+// K2: LayerNorm (src/model.cpp:387-400), fp32 in, T out.  gather (nullable)
+// selects input rows; head (nullable) additionally writes head_out[r] =
+// dot(LN(x_row), head) in fp32 (K10: value / reward head) and, when y is
+// null, skips the T output.
+template <class T>
+void launch_layernorm(Ctx& c, const float* x, int64_t rows, int64_t d, const float* g, const float* b, T* y,
+                      const int32_t* gather, const float* head, float* head_out);
+
+// K3: C[M,N] = A[M,K] · B[N,K]^T with epilogue.
+enum class Epi : int { kStore = 0, kGelu = 1, kAddResidual = 2, kStoreF32 = 3 };
+template <class T>
+void launch_gemm(Ctx& c, const T* A, int64_t lda, const T* B, int64_t ldb, int64_t M, int64_t N, int64_t K,
+                 Epi epi, void* C, int64_t ldc);
+
+// K4: scatter the K/V columns of packed qkv rows into the paged pool
+// (prefill).  seq_of_row / pos_of_row per packed row; block_table [B, max_pages].
+template <class T>
+void launch_kv_scatter(Ctx& c, const T* qkv, int64_t rows, int64_t d, const int32_t* seq_of_row,
+                       const int32_t* pos_of_row, const int32_t* block_table, int layer, const KvGeom& g, T* kv);
+
+// K5a: causal self-attention over packed ragged sequences (prefill/scoring),
+// src/model.cpp:205-245 (tape path) == :313-333 (KvSession).
+template <class T>
+void launch_attention_prefill(Ctx& c, const T* qkv, const int64_t* seq_offsets, int64_t B, int64_t max_len,
+                              int64_t H, int64_t DH, T* out);
+
+// K5b: one decode step: append this step's K/V (row b of qkv at position
+// pos[b]) to the paged pool, then attend over positions 0..pos[b].
+// Sequences with done[b] != 0 are skipped.
+template <class T>
+void launch_attention_decode(Ctx& c, const T* qkv, int64_t B, const int32_t* pos, const int32_t* done,
+                             const int32_t* block_table, int layer, const KvGeom& g, T* kv, T* out,
+                             double algorithmic_bytes);
+
+// K8: fused sampler over logits [B, ld] fp32 (src/model.cpp:450-477 + top-k/p).
+struct SampleParams {
+  int32_t greedy;
+  float temperature;
+  int64_t top_k;
+  double top_p;
+};
+struct SamplerState {
+  const SampleParams* params;  // device
+  int32_t* next_tok;    // [B] token fed at the next decode step
+  int32_t* pos;         // [B] position the next fed token occupies
+  int32_t* n_gen;       // [B]
+  int32_t* done;        // [B]
+  const int32_t* budget;  // [B]
+  const double* uniforms;  // [B, ustride]
+  int64_t ustride;
+  int32_t* out_tokens;  // [B, ostride]
+  float* out_lps;       // [B, ostride]
+  int64_t ostride;
+  int32_t* n_active;    // [1] sequences still running after this step
+};
+void launch_sampler(Ctx& c, const float* logits, int64_t ld, int64_t B, int64_t V, const SamplerState& s);
+
+// K9: fused log-softmax + gather: lp[r] = logits[r, target[r]] - LSE(row r),
+// written to out[out_index[r]] (double).  Rows with target < 0 are skipped.
+template <class T>
+void launch_logprob_gather(Ctx& c, const T* logits, int64_t ld, int64_t rows, int64_t V, const int32_t* target,
+                           const int64_t* out_index, double* out);
+
+// K11: KL-shaped rewards + reverse GAE scan per sequence, plus per-sequence
+// partial sums {kl_sum, n, reward, adv_sum, adv_sq_sum} into part[B][5].
+void launch_shape_gae(Ctx& c, int64_t B, int64_t stride, const int64_t* lengths, const double* rm_reward,
+                      const double* actor_lp, const double* ref_lp, const double* values, double kl_coef,
+                      double gamma, double lam, double* shaped, double* adv, double* ret, double* part);
+// K12: fixed-order reduction of part[B][5] → out[5] (deterministic).
+void launch_reduce_partials(Ctx& c, int64_t B, const double* part, double* out5);
+void launch_whiten_apply(Ctx& c, int64_t B, int64_t stride, const int64_t* lengths, const double* adv,
+                         const double* stats3, double* out);
+
+// misc
+void launch_convert(Ctx& c, const void* src, int src_dtype, void* dst, int dst_dtype, int64_t rows, int64_t cols,
+                    bool transpose, int64_t dst_ld, int64_t dst_row0);
+void launch_scripted_reward(Ctx& c, int64_t B, int64_t stride, const int32_t* tokens, const int64_t* lengths,
+                            int32_t target, double* out);
+void launch_f32_to_f64(Ctx& c, const float* src, int64_t n, double* dst);
+void launch_fill_i32(Ctx& c, int32_t* dst, int64_t n, int32_t v);
+
+}  // namespace ppoexp

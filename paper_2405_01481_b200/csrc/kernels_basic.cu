@@ -1,0 +1,304 @@
+// kernels_basic.cu — embedding, LayerNorm (+ fused value/reward head), KV
+// scatter, weight conversion and small helpers; plus the Ctx runtime.
+#include <cstring>
+
+#include "kernels.hpp"
+
+namespace ppoexp {
+
+// ===================================================================== runtime
+Ctx::Ctx(int dev) : device(dev) {
+  int n = 0;
+  PPOEXP_CUDA(cudaGetDeviceCount(&n));
+  if (dev < 0 || dev >= n) throw Error(6, "cuda: device " + std::to_string(dev) + " not present");
+  DeviceGuard g(dev);
+  PPOEXP_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+}
+
+Ctx::~Ctx() {
+  DeviceGuard g(device);
+  cudaStreamSynchronize(stream);
+  for (auto& t : pending) {
+    cudaEventDestroy(t.a);
+    cudaEventDestroy(t.b);
+  }
+  for (auto e : event_pool) cudaEventDestroy(e);
+  ws.clear();
+  if (pinned) cudaFreeHost(pinned);
+  cudaStreamDestroy(stream);
+}
+
+cudaEvent_t Ctx::new_event() {
+  if (!event_pool.empty()) {
+    auto e = event_pool.back();
+    event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  PPOEXP_CUDA(cudaEventCreate(&e));
+  return e;
+}
+
+void Ctx::harvest_list(const std::vector<TimedLaunch>& evs, bool release) {
+  for (const auto& t : evs) {
+    PPOEXP_CUDA(cudaEventSynchronize(t.b));
+    float ms = 0.f;
+    PPOEXP_CUDA(cudaEventElapsedTime(&ms, t.a, t.b));
+    auto& s = stats[t.cls];
+    s.ms += ms;
+    s.launches += 1;
+    s.bytes += t.bytes;
+    s.flops += t.flops;
+    if (release) {
+      release_event(t.a);
+      release_event(t.b);
+    }
+  }
+}
+
+void Ctx::harvest() {
+  harvest_list(pending, true);
+  pending.clear();
+}
+
+void* Ctx::pinned_staging(size_t bytes) {
+  if (bytes > pinned_bytes) {
+    if (pinned) {
+      PPOEXP_CUDA(cudaStreamSynchronize(stream));
+      PPOEXP_CUDA(cudaFreeHost(pinned));
+    }
+    pinned = nullptr;
+    pinned_bytes = 0;
+    PPOEXP_CUDA(cudaMallocHost(&pinned, bytes));
+    pinned_bytes = bytes;
+  }
+  return pinned;
+}
+
+void copy_in(Ctx& c, void* dst_dev, const void* src, size_t bytes, int where) {
+  if (!bytes) return;
+  PPOEXP_CUDA(cudaMemcpyAsync(dst_dev, src, bytes, where ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                              c.stream));
+}
+
+void copy_out(Ctx& c, void* dst, const void* src_dev, size_t bytes, int where) {
+  if (!bytes) return;
+  PPOEXP_CUDA(cudaMemcpyAsync(dst, src_dev, bytes, where ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                              c.stream));
+}
+
+// ===================================================================== kernels
+template <class T>
+__global__ void embed_kernel(const int32_t* __restrict__ tokens, const int32_t* __restrict__ positions,
+                             int64_t rows, int64_t d, const T* __restrict__ tok, const T* __restrict__ pos,
+                             float* __restrict__ x) {
+  const int64_t r = blockIdx.x;
+  if (r >= rows) return;
+  const int64_t t = tokens[r], p = positions[r];
+  for (int64_t j = threadIdx.x; j < d; j += blockDim.x)
+    x[r * d + j] = to_f(tok[t * d + j]) + to_f(pos[p * d + j]);
+}
+
+template <class T>
+void launch_embed(Ctx& c, const int32_t* tokens, const int32_t* positions, int64_t rows, int64_t d, const T* tok,
+                  const T* pos, float* x) {
+  if (rows <= 0) return;
+  c.launch("embed", double(rows) * d * (2 * sizeof(T) + 4), 0, [&] {
+    embed_kernel<T><<<rows, 256, 0, c.stream>>>(tokens, positions, rows, d, tok, pos, x);
+  });
+}
+
+template <int NT>
+__device__ __forceinline__ float block_sum(float v, float* red) {
+  v = warp_sum(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  float t = 0.f;
+  if (w == 0) {
+    t = l < NT / 32 ? red[l] : 0.f;
+    t = warp_sum(t);
+    if (l == 0) red[0] = t;
+  }
+  __syncthreads();
+  t = red[0];
+  __syncthreads();
+  return t;
+}
+
+// One CTA per row; the row is cached in registers (d <= 256 * 32).
+template <class T>
+__global__ void __launch_bounds__(256) layernorm_kernel(const float* __restrict__ x, int64_t rows, int64_t d,
+                                                        const float* __restrict__ g, const float* __restrict__ b,
+                                                        T* __restrict__ y, const int32_t* __restrict__ gather,
+                                                        const float* __restrict__ head, float* __restrict__ head_out) {
+  __shared__ float red[32];
+  const int64_t r = blockIdx.x;
+  const int64_t src = gather ? gather[r] : r;
+  const float* xr = x + src * d;
+  constexpr int MAXV = 32;
+  float v[MAXV];
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < MAXV; ++i) {
+    const int64_t j = threadIdx.x + int64_t(i) * 256;
+    v[i] = j < d ? xr[j] : 0.f;
+    s += v[i];
+  }
+  const float mu = block_sum<256>(s, red) / float(d);
+  float q = 0.f;
+#pragma unroll
+  for (int i = 0; i < MAXV; ++i) {
+    const int64_t j = threadIdx.x + int64_t(i) * 256;
+    if (j < d) q += (v[i] - mu) * (v[i] - mu);
+  }
+  const float var = block_sum<256>(q, red) / float(d);
+  const float is = 1.0f / sqrtf(var + 1e-5f);
+  float hd = 0.f;
+#pragma unroll
+  for (int i = 0; i < MAXV; ++i) {
+    const int64_t j = threadIdx.x + int64_t(i) * 256;
+    if (j < d) {
+      const float o = g[j] * ((v[i] - mu) * is) + b[j];
+      if (y) y[r * d + j] = from_f<T>(o);
+      if (head) hd += o * head[j];
+    }
+  }
+  if (head) {
+    hd = block_sum<256>(hd, red);
+    if (threadIdx.x == 0) head_out[r] = hd;
+  }
+}
+
+template <class T>
+void launch_layernorm(Ctx& c, const float* x, int64_t rows, int64_t d, const float* g, const float* b, T* y,
+                      const int32_t* gather, const float* head, float* head_out) {
+  if (rows <= 0) return;
+  if (d > 256 * 32) throw ContractError("layernorm: d_model above 8192 unsupported");
+  c.launch("layernorm", double(rows) * d * (4 + (y ? sizeof(T) : 0)), 0, [&] {
+    layernorm_kernel<T><<<rows, 256, 0, c.stream>>>(x, rows, d, g, b, y, gather, head, head_out);
+  });
+}
+
+template <class T>
+__global__ void kv_scatter_kernel(const T* __restrict__ qkv, int64_t rows, int64_t d,
+                                  const int32_t* __restrict__ seq_of_row, const int32_t* __restrict__ pos_of_row,
+                                  const int32_t* __restrict__ block_table, int layer, KvGeom g, T* __restrict__ kv) {
+  const int64_t r = blockIdx.x;
+  if (r >= rows) return;
+  const int64_t s = seq_of_row[r], p = pos_of_row[r];
+  const int64_t page = block_table[s * g.max_pages_per_seq + p / g.page_size];
+  const int64_t slot = p % g.page_size;
+  for (int64_t j = threadIdx.x; j < 2 * d; j += blockDim.x) {
+    const int64_t which = j / d, col = j % d, h = col / g.DH, i = col % g.DH;
+    const int64_t dst = ((((int64_t)layer * g.n_pages + page) * 2 + which) * g.H + h) * g.page_size * g.DH +
+                        slot * g.DH + i;
+    kv[dst] = qkv[r * 3 * d + d + j];
+  }
+}
+
+template <class T>
+void launch_kv_scatter(Ctx& c, const T* qkv, int64_t rows, int64_t d, const int32_t* seq_of_row,
+                       const int32_t* pos_of_row, const int32_t* block_table, int layer, const KvGeom& g, T* kv) {
+  if (rows <= 0) return;
+  c.launch("kv_scatter", double(rows) * 2 * d * sizeof(T) * 2, 0, [&] {
+    kv_scatter_kernel<T><<<rows, 256, 0, c.stream>>>(qkv, rows, d, seq_of_row, pos_of_row, block_table, layer, g,
+                                                     kv);
+  });
+}
+
+__device__ __forceinline__ float load_any(const void* p, int dt, int64_t i) {
+  if (dt == 0) return static_cast<const float*>(p)[i];
+  if (dt == 1) return __bfloat162float(static_cast<const bf16*>(p)[i]);
+  return float(static_cast<const double*>(p)[i]);
+}
+
+__global__ void convert_kernel(const void* src, int sdt, void* dst, int ddt, int64_t rows, int64_t cols,
+                               bool transpose, int64_t dst_ld, int64_t dst_row0) {
+  const int64_t n = rows * cols;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n; e += int64_t(gridDim.x) * blockDim.x) {
+    // e indexes the destination in [dst_rows, dst_cols] order.
+    int64_t dr, dc, si;
+    if (transpose) {  // dst [cols, rows]
+      dr = e / rows;
+      dc = e % rows;
+      si = dc * cols + dr;
+    } else {
+      dr = e / cols;
+      dc = e % cols;
+      si = e;
+    }
+    const float v = load_any(src, sdt, si);
+    const int64_t di = (dst_row0 + dr) * dst_ld + dc;
+    if (ddt == 0)
+      static_cast<float*>(dst)[di] = v;
+    else
+      static_cast<bf16*>(dst)[di] = __float2bfloat16_rn(v);
+  }
+}
+
+void launch_convert(Ctx& c, const void* src, int src_dtype, void* dst, int dst_dtype, int64_t rows, int64_t cols,
+                    bool transpose, int64_t dst_ld, int64_t dst_row0) {
+  if (rows * cols <= 0) return;
+  const int64_t blocks = std::min<int64_t>(ceil_div(rows * cols, 256), 148 * 16);
+  c.launch("convert", 0, 0, [&] {
+    convert_kernel<<<blocks, 256, 0, c.stream>>>(src, src_dtype, dst, dst_dtype, rows, cols, transpose, dst_ld,
+                                                 dst_row0);
+  });
+}
+
+__global__ void scripted_reward_kernel(int64_t B, int64_t stride, const int32_t* tokens, const int64_t* lengths,
+                                       int32_t target, double* out) {
+  const int64_t b = blockIdx.x;
+  if (b >= B) return;
+  int n = 0;
+  for (int64_t t = threadIdx.x; t < lengths[b]; t += blockDim.x) n += tokens[b * stride + t] == target;
+  n = __reduce_add_sync(0xffffffffu, n);
+  if (threadIdx.x == 0) out[b] = double(n);
+}
+
+// CriticJob::scripted_reward_for, src/ppo.cpp:109-115 (count over the response).
+void launch_scripted_reward(Ctx& c, int64_t B, int64_t stride, const int32_t* tokens, const int64_t* lengths,
+                            int32_t target, double* out) {
+  if (B <= 0) return;
+  c.launch("scripted_reward", 0, 0, [&] {
+    scripted_reward_kernel<<<B, 32, 0, c.stream>>>(B, stride, tokens, lengths, target, out);
+  });
+}
+
+__global__ void f32_to_f64_kernel(const float* src, int64_t n, double* dst) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    dst[i] = double(src[i]);
+}
+
+void launch_f32_to_f64(Ctx& c, const float* src, int64_t n, double* dst) {
+  if (n <= 0) return;
+  c.launch("convert", 12.0 * n, 0, [&] {
+    f32_to_f64_kernel<<<std::min<int64_t>(ceil_div(n, 256), 1184), 256, 0, c.stream>>>(src, n, dst);
+  });
+}
+
+__global__ void fill_i32_kernel(int32_t* dst, int64_t n, int32_t v) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    dst[i] = v;
+}
+
+void launch_fill_i32(Ctx& c, int32_t* dst, int64_t n, int32_t v) {
+  if (n <= 0) return;
+  c.launch("fill", 4.0 * n, 0, [&] {
+    fill_i32_kernel<<<std::min<int64_t>(ceil_div(n, 256), 1184), 256, 0, c.stream>>>(dst, n, v);
+  });
+}
+
+#define INST(T)                                                                                                   \
+  template void launch_embed<T>(Ctx&, const int32_t*, const int32_t*, int64_t, int64_t, const T*, const T*,      \
+                                float*);                                                                        \
+  template void launch_layernorm<T>(Ctx&, const float*, int64_t, int64_t, const float*, const float*, T*,       \
+                                    const int32_t*, const float*, float*);                                      \
+  template void launch_kv_scatter<T>(Ctx&, const T*, int64_t, int64_t, const int32_t*, const int32_t*,          \
+                                     const int32_t*, int, const KvGeom&, T*);
+INST(float)
+INST(bf16)
+#undef INST
+
+}  // namespace ppoexp

@@ -1,0 +1,128 @@
+// runtime.hpp — host runtime: context (device + stream), kernel-class
+// profiler (CUDA events), launch accounting, named device workspaces.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <functional>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+namespace ppoexp {
+
+struct ClassStats {
+  double ms = 0.0;
+  int64_t launches = 0;
+  double bytes = 0.0;
+  double flops = 0.0;
+};
+
+struct TimedLaunch {
+  std::string cls;
+  cudaEvent_t a, b;
+  double bytes, flops;
+};
+
+struct DeviceBuffer {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  DeviceBuffer() = default;
+  DeviceBuffer(const DeviceBuffer&) = delete;
+  DeviceBuffer& operator=(const DeviceBuffer&) = delete;
+  ~DeviceBuffer() {
+    if (ptr) cudaFree(ptr);
+  }
+  void ensure(size_t n) {
+    if (n <= bytes) return;
+    if (ptr) PPOEXP_CUDA(cudaFree(ptr));
+    ptr = nullptr;
+    bytes = 0;
+    PPOEXP_CUDA(cudaMalloc(&ptr, n));
+    bytes = n;
+  }
+  template <class T>
+  T* as() const { return static_cast<T*>(ptr); }
+};
+
+struct Ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::recursive_mutex mu;
+  bool profiling = false;
+  bool capturing = false;
+  int64_t launches = 0;          // eager launches + graph-replayed kernel nodes
+  int64_t capture_launches = 0;  // kernels recorded into the graph being captured
+  std::map<std::string, ClassStats> stats;
+  std::vector<TimedLaunch> pending;          // eager timed launches to harvest
+  std::vector<TimedLaunch>* capture_events = nullptr;  // events recorded while capturing
+  std::vector<cudaEvent_t> event_pool;
+  std::map<std::string, std::unique_ptr<DeviceBuffer>> ws;
+  // pinned host staging for HOST-where API calls
+  void* pinned = nullptr;
+  size_t pinned_bytes = 0;
+
+  explicit Ctx(int dev);
+  ~Ctx();
+
+  cudaEvent_t new_event();
+  void release_event(cudaEvent_t e) { event_pool.push_back(e); }
+
+  // Launch `f` (which enqueues exactly one kernel on `stream`) under class
+  // `cls`, with the algorithmic bytes / flops it moves.
+  template <class F>
+  void launch(const char* cls, double bytes, double flops, F&& f) {
+    if (profiling) {
+      TimedLaunch t{cls, new_event(), new_event(), bytes, flops};
+      PPOEXP_CUDA(cudaEventRecord(t.a, stream));
+      f();
+      PPOEXP_CUDA(cudaGetLastError());
+      PPOEXP_CUDA(cudaEventRecord(t.b, stream));
+      if (capturing && capture_events)
+        capture_events->push_back(t);
+      else
+        pending.push_back(t);
+    } else {
+      f();
+      PPOEXP_CUDA(cudaGetLastError());
+    }
+    if (capturing)
+      ++capture_launches;
+    else
+      ++launches;
+  }
+
+  // Accumulate finished eager timings (blocks until they complete).
+  void harvest();
+  void harvest_list(const std::vector<TimedLaunch>& evs, bool release);
+
+  void* workspace(const std::string& name, size_t bytes) {
+    auto& b = ws[name];
+    if (!b) b = std::make_unique<DeviceBuffer>();
+    b->ensure(bytes);
+    return b->ptr;
+  }
+  void* pinned_staging(size_t bytes);
+  void sync() { PPOEXP_CUDA(cudaStreamSynchronize(stream)); }
+};
+
+// Copy helpers that honour ppoexp_where (0 = host, 1 = device).
+void copy_in(Ctx& c, void* dst_dev, const void* src, size_t bytes, int where);
+void copy_out(Ctx& c, void* dst, const void* src_dev, size_t bytes, int where);
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) PPOEXP_CUDA(cudaSetDevice(dev));
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+}  // namespace ppoexp

@@ -1,0 +1,625 @@
+"""Python host mirror of the reference's experience-path interfaces over the
+C ABI (include/ppoexp.h, libppoexp.so).
+
+Names follow the reference (/root/reference/proj/include/aligner/*.hpp):
+``ModelConfig``, ``SamplingSpec``, ``GenTask``, ``GenerateResult``,
+``build_engine`` / ``Engine.refit`` / ``Engine.generate_batch``,
+``sequence_logprobs``, ``value_estimates``, ``reward_head``,
+``kl_penalized_rewards``, ``gae``, ``RolloutSeq`` and the experience half of
+``ppo_step`` (``make_experience``).  Errors raise the reference's exception
+types with its message wording.
+
+There is no CPU fallback: importing works anywhere, but every call needs the
+CUDA library and a device, and fails loudly otherwise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+from typing import Sequence
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libppoexp.so")
+
+HOST, DEVICE = 0, 1
+F32, BF16, F64 = 0, 1, 2
+PAD_TOKEN, EOT_TOKEN = 256, 257  # include/aligner/model.hpp:17-18
+
+
+# ---------------------------------------------------------------- errors
+class ShapeError(RuntimeError):
+    pass
+
+
+class IndexError_(IndexError):
+    pass
+
+
+class ContractError(RuntimeError):
+    pass
+
+
+class RefitError(RuntimeError):
+    pass
+
+
+class PpoError(RuntimeError):
+    pass
+
+
+class CudaError(RuntimeError):
+    pass
+
+
+_ERRS = {1: ContractError, 2: IndexError_, 3: ShapeError, 4: RefitError, 5: PpoError, 6: CudaError, 7: MemoryError}
+
+
+# ---------------------------------------------------------------- ctypes
+class _Cfg(C.Structure):
+    _fields_ = [("vocab_size", C.c_int64), ("d_model", C.c_int64), ("n_layers", C.c_int64), ("n_heads", C.c_int64),
+                ("d_ff", C.c_int64), ("max_seq_len", C.c_int64), ("scalar_head", C.c_int32), ("reserved", C.c_int32)]
+
+
+class _View(C.Structure):
+    _fields_ = [("name", C.c_char_p), ("rank", C.c_int32), ("dtype", C.c_int32), ("shape", C.c_int64 * 2),
+                ("data", C.c_void_p), ("where", C.c_int32), ("reserved", C.c_int32)]
+
+
+class _Sampling(C.Structure):
+    _fields_ = [("greedy", C.c_int32), ("top_k", C.c_int32), ("temperature", C.c_double), ("top_p", C.c_double)]
+
+
+class _EngineOpts(C.Structure):
+    _fields_ = [("max_batch", C.c_int64), ("page_size", C.c_int64), ("max_total_tokens", C.c_int64),
+                ("use_graphs", C.c_int32), ("reserved", C.c_int32)]
+
+
+_ALLREDUCE = C.CFUNCTYPE(C.c_int32, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p)
+
+
+class _Hyper(C.Structure):
+    _fields_ = [("kl_penalty_coef", C.c_double), ("gamma", C.c_double), ("lam", C.c_double)]
+
+
+class _XpReq(C.Structure):
+    _fields_ = [("policy_engine", C.c_void_p), ("reference", C.c_void_p), ("critic", C.c_void_p), ("rm", C.c_void_p),
+                ("scripted_target", C.c_int32), ("reserved", C.c_int32), ("sampling", _Sampling),
+                ("seed", C.c_uint64), ("step_index", C.c_int64), ("gidx0", C.c_int64), ("max_new", C.c_int64),
+                ("hyper", _Hyper), ("allreduce", _ALLREDUCE), ("allreduce_user", C.c_void_p)]
+
+
+class _Rollout(C.Structure):
+    _fields_ = [(n, C.c_void_p) for n in ("tokens", "lengths", "actor_lp", "ref_lp", "values", "rewards", "shaped",
+                                          "advantages", "returns", "whitened", "stats")]
+
+
+_lib = None
+
+
+def lib():
+    """Loads libppoexp.so (fails loudly if it was not built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise CudaError(f"{LIB_PATH} missing: run paper_2405_01481_b200.build.build() (no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        P, I64, I32, D, V = C.c_void_p, C.c_int64, C.c_int32, C.c_double, C.c_void_p
+        L.ppoexp_last_error.restype = C.c_char_p
+        sigs = {
+            "ppoexp_abi_version": [],
+            "ppoexp_ctx_create": [I32, P],
+            "ppoexp_ctx_destroy": [P],
+            "ppoexp_ctx_stream": [P, P],
+            "ppoexp_ctx_synchronize": [P],
+            "ppoexp_ctx_profile": [P, I32],
+            "ppoexp_ctx_profile_query": [P, C.c_char_p, P, P, P, P],
+            "ppoexp_ctx_launch_count": [P, P],
+            "ppoexp_model_create": [P, P, P, I64, I32, P],
+            "ppoexp_model_refit": [P, P, I64],
+            "ppoexp_model_generation": [P, P],
+            "ppoexp_model_config_get": [P, P],
+            "ppoexp_model_destroy": [P],
+            "ppoexp_engine_create": [P, P, P],
+            "ppoexp_engine_destroy": [P],
+            "ppoexp_engine_generate": [P, I64, P, P, P, P, P, I64, P, P, P, I32, P],
+            "ppoexp_sequence_logprobs": [P, I64, P, P, P, I32],
+            "ppoexp_value_estimates": [P, I64, P, P, P, P, I32],
+            "ppoexp_reward_head": [P, I64, P, P, P, I32],
+            "ppoexp_shape_gae": [I64, I64, P, P, P, P, P, D, D, D, P, P, P, P, I32],
+            "ppoexp_whiten_partials": [I64, I64, P, P, P, P, I32],
+            "ppoexp_whiten_apply": [I64, I64, P, P, P, P, P, I32],
+            "ppoexp_make_experience": [P, I64, P, P, P, I32],
+        }
+        for name, args in sigs.items():
+            f = getattr(L, name)
+            f.argtypes = args
+            f.restype = C.c_int32
+        _lib = L
+    return _lib
+
+
+def _check(rc):
+    if rc:
+        msg = lib().ppoexp_last_error().decode(errors="replace")
+        raise _ERRS.get(rc, CudaError)(msg)
+
+
+def _ptr(a):
+    """(address, where) for a numpy array or a CUDA torch tensor."""
+    if a is None:
+        return None, HOST
+    if hasattr(a, "data_ptr") and getattr(a, "is_cuda", False):
+        return a.data_ptr(), DEVICE
+    if isinstance(a, np.ndarray):
+        assert a.flags["C_CONTIGUOUS"]
+        return a.ctypes.data, HOST
+    raise TypeError(type(a))
+
+
+# ---------------------------------------------------------------- config
+@dataclass
+class ModelConfig:
+    """include/aligner/model.hpp:30-45"""
+    vocab_size: int = 258
+    d_model: int = 64
+    n_layers: int = 2
+    n_heads: int = 4
+    d_ff: int = 256
+    max_seq_len: int = 128
+    scalar_head: bool = False
+
+    def head_dim(self):
+        return self.d_model // self.n_heads
+
+    def _c(self):
+        return _Cfg(self.vocab_size, self.d_model, self.n_layers, self.n_heads, self.d_ff, self.max_seq_len,
+                    1 if self.scalar_head else 0, 0)
+
+    def with_head(self, on=True):
+        return ModelConfig(self.vocab_size, self.d_model, self.n_layers, self.n_heads, self.d_ff, self.max_seq_len, on)
+
+
+def expected_names(cfg: ModelConfig):
+    """ModelParams::expected_names + param_shape (src/model.cpp:66-115)."""
+    d, f = cfg.d_model, cfg.d_ff
+    out = [("tok_embed.weight", (cfg.vocab_size, d)), ("pos_embed.weight", (cfg.max_seq_len, d))]
+    for i in range(cfg.n_layers):
+        b = f"layers.{i}."
+        out += [(b + "attn_norm.weight", (d,)), (b + "attn_norm.bias", (d,))]
+        out += [(b + f"attn.{p}.weight", (d, d)) for p in ("q_proj", "k_proj", "v_proj", "o_proj")]
+        out += [(b + "ffn_norm.weight", (d,)), (b + "ffn_norm.bias", (d,)), (b + "ffn.up_proj.weight", (d, f)),
+                (b + "ffn.down_proj.weight", (f, d))]
+    out += [("final_norm.weight", (d,)), ("final_norm.bias", (d,))]
+    if cfg.scalar_head:
+        out.append(("scalar_head.weight", (d, 1)))
+    return out
+
+
+def flat_to_params(cfg: ModelConfig, flat: np.ndarray) -> dict:
+    """Splits a flat canonical buffer into {name: array} (views, no copy)."""
+    out, off = {}, 0
+    for name, shape in expected_names(cfg):
+        n = int(np.prod(shape))
+        out[name] = flat[off:off + n].reshape(shape)
+        off += n
+    if off != flat.size:
+        raise ShapeError(f"flat parameter buffer has {flat.size} values, config implies {off}")
+    return out
+
+
+def _views(params: dict):
+    keep, views = [], (_View * len(params))()
+    for i, (name, arr) in enumerate(params.items()):
+        if hasattr(arr, "data_ptr"):
+            import torch
+            dt = {torch.float64: F64, torch.float32: F32, torch.bfloat16: BF16}[arr.dtype]
+            arr = arr.contiguous()
+            addr, where = _ptr(arr)
+            shape = tuple(arr.shape)
+        else:
+            if arr.dtype == np.float64:
+                dt = F64
+            elif arr.dtype == np.float32:
+                dt = F32
+            elif arr.dtype == np.uint16:  # raw bf16 bits
+                dt = BF16
+            else:
+                arr = arr.astype(np.float64)
+                dt = F64
+            arr = np.ascontiguousarray(arr)
+            addr, where = arr.ctypes.data, HOST
+            shape = arr.shape
+        keep.append(arr)
+        nb = name.encode()
+        keep.append(nb)
+        views[i].name = nb
+        views[i].rank = len(shape)
+        views[i].dtype = dt
+        views[i].shape[0] = shape[0] if len(shape) > 0 else 1
+        views[i].shape[1] = shape[1] if len(shape) > 1 else 0
+        views[i].data = addr
+        views[i].where = where
+    return views, keep
+
+
+# ---------------------------------------------------------------- runtime
+class Context:
+    """One device + stream (include/ppoexp.h ppoexp_ctx)."""
+
+    def __init__(self, device: int = 0):
+        self.h = C.c_void_p()
+        _check(lib().ppoexp_ctx_create(device, C.byref(self.h)))
+        self.device = device
+
+    def close(self):
+        if self.h:
+            _check(lib().ppoexp_ctx_destroy(self.h))
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def stream(self) -> int:
+        s = C.c_void_p()
+        _check(lib().ppoexp_ctx_stream(self.h, C.byref(s)))
+        return s.value or 0
+
+    def synchronize(self):
+        _check(lib().ppoexp_ctx_synchronize(self.h))
+
+    def profile(self, enable=True):
+        _check(lib().ppoexp_ctx_profile(self.h, 1 if enable else 0))
+
+    def profile_query(self, cls: str):
+        ms, n, b, f = C.c_double(), C.c_int64(), C.c_double(), C.c_double()
+        _check(lib().ppoexp_ctx_profile_query(self.h, cls.encode(), C.byref(ms), C.byref(n), C.byref(b), C.byref(f)))
+        return dict(ms=ms.value, launches=n.value, bytes=b.value, flops=f.value)
+
+    @property
+    def launch_count(self) -> int:
+        n = C.c_int64()
+        _check(lib().ppoexp_ctx_launch_count(self.h, C.byref(n)))
+        return n.value
+
+
+class DeviceModel:
+    """A device-resident ModelParams snapshot (build = deep copy, src/engine.cpp:33-48)."""
+
+    def __init__(self, ctx: Context, config: ModelConfig, params, dtype: int = BF16):
+        if isinstance(params, np.ndarray):
+            params = flat_to_params(config, params)
+        self.ctx, self.config, self.dtype = ctx, config, dtype
+        self.h = C.c_void_p()
+        views, keep = _views(params)
+        cfg = config._c()
+        _check(lib().ppoexp_model_create(ctx.h, C.byref(cfg), views, len(params), dtype, C.byref(self.h)))
+
+    def refit(self, params):
+        """Engine::refit, src/engine.cpp:60-90 (RefitError, nothing touched, on a name/shape mismatch)."""
+        if isinstance(params, np.ndarray):
+            try:
+                params = flat_to_params(self.config, params)
+            except ShapeError as e:
+                raise RefitError(f"refit: {e} (rebuild required)")
+        views, keep = _views(params)
+        _check(lib().ppoexp_model_refit(self.h, views, len(params)))
+
+    @property
+    def generation_counter(self) -> int:
+        g = C.c_uint64()
+        _check(lib().ppoexp_model_generation(self.h, C.byref(g)))
+        return g.value
+
+    def close(self):
+        if self.h:
+            _check(lib().ppoexp_model_destroy(self.h))
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+# ---------------------------------------------------------------- engine
+@dataclass
+class SamplingSpec:
+    """include/aligner/model.hpp:75-84 (+ top_k / top_p, north-star)."""
+    greedy: bool = True
+    temperature: float = 1.0
+    seed: int = 0
+    top_k: int = 0
+    top_p: float = 1.0
+
+    @staticmethod
+    def greedy_spec():
+        return SamplingSpec()
+
+    @staticmethod
+    def temperature_spec(tau: float, seed: int, top_k: int = 0, top_p: float = 1.0):
+        return SamplingSpec(False, tau, seed, top_k, top_p)
+
+
+@dataclass
+class GenTask:
+    """include/aligner/engine.hpp:23-31"""
+    prompt: Sequence[int]
+    max_new: int = 16
+    sampling: SamplingSpec = field(default_factory=SamplingSpec)
+    estimated_cost: float = 0.0
+
+    def cost(self):
+        return self.estimated_cost if self.estimated_cost > 0 else float(self.max_new)
+
+
+@dataclass
+class GenerateResult:
+    """include/aligner/model.hpp:86-89"""
+    tokens: np.ndarray
+    logprobs: np.ndarray
+
+
+@dataclass
+class EngineOptions:
+    max_batch: int = 256
+    page_size: int = 64
+    max_total_tokens: int = 0
+    use_graphs: bool = True
+
+
+def ragged(seqs):
+    offs = np.zeros(len(seqs) + 1, np.int64)
+    offs[1:] = np.cumsum([len(s) for s in seqs])
+    flat = np.concatenate([np.asarray(s, np.int32) for s in seqs]) if len(seqs) else np.zeros(0, np.int32)
+    return np.ascontiguousarray(flat, np.int32), offs
+
+
+class Engine:
+    """The TensorRT-LLM analog (include/aligner/engine.hpp:49-92) on one B200."""
+
+    def __init__(self, model: DeviceModel, opts: EngineOptions | None = None):
+        opts = opts or EngineOptions()
+        self.model = model
+        o = _EngineOpts(opts.max_batch, opts.page_size, opts.max_total_tokens, 1 if opts.use_graphs else 0, 0)
+        self.h = C.c_void_p()
+        _check(lib().ppoexp_engine_create(model.h, C.byref(o), C.byref(self.h)))
+        self.last_ms = 0.0
+
+    def refit(self, params):
+        self.model.refit(params)
+
+    @property
+    def generation_counter(self):
+        return self.model.generation_counter
+
+    def generate_batch(self, tasks: Sequence[GenTask]):
+        """Engine::generate_batch, src/engine.cpp:148-182.  All tasks must share
+        one sampling mode (greedy / tau / top-k / top-p); seeds are per task."""
+        if not tasks:
+            return []
+        s0 = tasks[0].sampling
+        for t in tasks:
+            s = t.sampling
+            if (s.greedy, s.temperature, s.top_k, s.top_p) != (s0.greedy, s0.temperature, s0.top_k, s0.top_p):
+                raise ContractError("generate_batch: tasks must share one sampling mode")
+        flat, offs = ragged([t.prompt for t in tasks])
+        mx = np.array([t.max_new for t in tasks], np.int64)
+        seeds = np.array([t.sampling.seed for t in tasks], np.uint64)
+        stride = max(1, int(mx.max()))
+        B = len(tasks)
+        toks = np.zeros((B, stride), np.int32)
+        lps = np.zeros((B, stride), np.float64)
+        lens = np.zeros(B, np.int64)
+        sp = _Sampling(1 if s0.greedy else 0, s0.top_k, s0.temperature, s0.top_p)
+        ms = C.c_double()
+        _check(lib().ppoexp_engine_generate(self.h, B, flat.ctypes.data, offs.ctypes.data, mx.ctypes.data,
+                                            C.byref(sp), seeds.ctypes.data, stride, toks.ctypes.data,
+                                            lps.ctypes.data, lens.ctypes.data, HOST, C.byref(ms)))
+        self.last_ms = ms.value
+        return [GenerateResult(toks[b, :lens[b]].copy(), lps[b, :lens[b]].copy()) for b in range(B)]
+
+    def close(self):
+        if self.h:
+            _check(lib().ppoexp_engine_destroy(self.h))
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def build_engine(ctx: Context, params, config: ModelConfig, opts: EngineOptions | None = None, dtype=BF16):
+    """build_engine, include/aligner/engine.hpp:91-92."""
+    return Engine(DeviceModel(ctx, config, params, dtype), opts)
+
+
+# ---------------------------------------------------------------- scoring
+def sequence_logprobs(model: DeviceModel, seqs):
+    """sequence_logprobs (src/model.cpp:484-495) for a list of token sequences."""
+    if not len(seqs):
+        return []
+    flat, offs = ragged(seqs)
+    out = np.zeros(max(len(flat), 1), np.float64)
+    _check(lib().ppoexp_sequence_logprobs(model.h, len(seqs), flat.ctypes.data, offs.ctypes.data, out.ctypes.data,
+                                          HOST))
+    return [out[offs[b]:offs[b + 1]].copy() for b in range(len(seqs))]
+
+
+def value_estimates(critic: DeviceModel, seqs, response_starts):
+    """value_estimates (src/losses.cpp:117-127) with the critic's scalar head."""
+    flat, offs = ragged(seqs)
+    rs = np.ascontiguousarray(response_starts, np.int64)
+    n = int(sum(len(s) - r for s, r in zip(seqs, rs)))
+    out = np.zeros(max(n, 1), np.float64)
+    _check(lib().ppoexp_value_estimates(critic.h, len(seqs), flat.ctypes.data, offs.ctypes.data, rs.ctypes.data,
+                                        out.ctypes.data, HOST))
+    res, o = [], 0
+    for s, r in zip(seqs, rs):
+        res.append(out[o:o + len(s) - r].copy())
+        o += len(s) - r
+    return res
+
+
+def reward_head(rm: DeviceModel, seqs):
+    """reward_head (src/losses.cpp:105-115) with the RM's scalar head."""
+    flat, offs = ragged(seqs)
+    out = np.zeros(len(seqs), np.float64)
+    _check(lib().ppoexp_reward_head(rm.h, len(seqs), flat.ctypes.data, offs.ctypes.data, out.ctypes.data, HOST))
+    return out
+
+
+def shape_gae(ctx: Context, rewards, actor_lps, ref_lps, values, kl_coef, gamma, lam):
+    """kl_penalized_rewards + gae (src/losses.cpp:168-199) for a batch of sequences."""
+    B = len(actor_lps)
+    stride = max(1, max(len(a) for a in actor_lps))
+    lens = np.array([len(a) for a in actor_lps], np.int64)
+    pad = lambda xs: np.ascontiguousarray(np.stack([np.pad(np.asarray(x, np.float64), (0, stride - len(x))) for x in xs]))
+    A, Rf, Vv = pad(actor_lps), pad(ref_lps), pad(values)
+    rw = np.ascontiguousarray(rewards, np.float64)
+    sh, adv, ret = (np.zeros((B, stride)) for _ in range(3))
+    _check(lib().ppoexp_shape_gae(B, stride, lens.ctypes.data, rw.ctypes.data, A.ctypes.data, Rf.ctypes.data,
+                                  Vv.ctypes.data, kl_coef, gamma, lam, sh.ctypes.data, adv.ctypes.data, ret.ctypes.data,
+                                  ctx.h, HOST))
+    cut = lambda m: [m[b, :lens[b]].copy() for b in range(B)]
+    return cut(sh), cut(adv), cut(ret)
+
+
+def kl_penalized_rewards(ctx, rm_reward, actor_lp, ref_lp, kl_coef):
+    """src/losses.cpp:188-199 (single sequence)."""
+    sh, _, _ = shape_gae(ctx, [rm_reward], [actor_lp], [ref_lp], [np.zeros(len(actor_lp))], kl_coef, 1.0, 1.0)
+    return sh[0]
+
+
+def gae(ctx, rewards, values, gamma, lam):
+    """src/losses.cpp:168-186 (single sequence): recovers the GAE of the given
+    per-token rewards by feeding them as the shaped rewards (kl_coef 0, R 0
+    would drop them), so the shaping is bypassed by construction."""
+    n = len(rewards)
+    if n == 0:
+        return np.zeros(0), np.zeros(0)
+    # r_t = -kl*(a - r) with kl = -1, a = rewards, r = 0 gives r_t = rewards
+    _, adv, ret = shape_gae(ctx, [0.0], [np.asarray(rewards, np.float64)], [np.zeros(n)], [values], -1.0, gamma, lam)
+    return adv[0], ret[0]
+
+
+# ---------------------------------------------------------------- experience
+@dataclass
+class RolloutSeq:
+    """include/aligner/losses.hpp:54-63 (+ whitened advantages, north-star)."""
+    prompt: np.ndarray
+    response: np.ndarray
+    actor_logprobs: np.ndarray
+    ref_logprobs: np.ndarray
+    values: np.ndarray
+    reward: float
+    advantages: np.ndarray
+    returns: np.ndarray
+    mask: np.ndarray
+    whitened_advantages: np.ndarray
+    shaped_rewards: np.ndarray
+
+
+@dataclass
+class PpoHyper:
+    """include/aligner/losses.hpp:39-50 (experience-path subset)."""
+    kl_penalty_coef: float = 0.003
+    gamma: float = 1.0
+    lam: float = 0.95
+
+
+@dataclass
+class ExperienceStats:
+    kl_sum: float
+    kl_count: float
+    reward_sum: float
+    n_seqs: float
+    adv_mean: float
+    adv_std: float
+    gen_ms: float
+    total_ms: float
+
+    @property
+    def kl_mean(self):
+        return self.kl_sum / self.kl_count if self.kl_count else 0.0
+
+    @property
+    def reward_mean(self):
+        return self.reward_sum / self.n_seqs if self.n_seqs else 0.0
+
+
+class ExperienceMaker:
+    """The experience half of ppo_step (src/ppo.cpp:302-393) on one device:
+    policy engine + reference + critic (+ RM or the scripted reward)."""
+
+    def __init__(self, engine: Engine, reference: DeviceModel, critic: DeviceModel, rm: DeviceModel | None = None,
+                 scripted_target: int = 122, hyper: PpoHyper | None = None, allreduce=None):
+        self.engine, self.reference, self.critic, self.rm = engine, reference, critic, rm
+        self.scripted_target = scripted_target
+        self.hyper = hyper or PpoHyper()
+        self._allreduce_py = allreduce
+        self._allreduce_c = _ALLREDUCE(self._cb) if allreduce is not None else _ALLREDUCE()
+
+    def _cb(self, buf, n, stream, user):
+        try:
+            self._allreduce_py(buf, n, stream)
+            return 0
+        except Exception:  # pragma: no cover - surfaced as PpoError by the library
+            import traceback
+            traceback.print_exc()
+            return 1
+
+    def _req(self, sampling, seed, step_index, gidx0, max_new):
+        return _XpReq(self.engine.h, self.reference.h, self.critic.h, self.rm.h if self.rm else None,
+                      self.scripted_target, 0,
+                      _Sampling(1 if sampling.greedy else 0, sampling.top_k, sampling.temperature, sampling.top_p),
+                      seed, step_index, gidx0, max_new,
+                      _Hyper(self.hyper.kl_penalty_coef, self.hyper.gamma, self.hyper.lam), self._allreduce_c, None)
+
+    def run_device(self, prompts_flat, offsets, out: dict, *, max_new, sampling, seed=0, step_index=0, gidx0=0):
+        """All buffers are CUDA torch tensors (prompts int32 flat, offsets int64
+        [B+1], outputs as allocated by ``alloc_device_outputs``)."""
+        B = offsets.numel() - 1
+        req = self._req(sampling, seed, step_index, gidx0, max_new)
+        ro = _Rollout(*[out[k].data_ptr() for k in ("tokens", "lengths", "actor_lp", "ref_lp", "values", "rewards",
+                                                    "shaped", "advantages", "returns", "whitened", "stats")])
+        _check(lib().ppoexp_make_experience(C.byref(req), B, prompts_flat.data_ptr(), offsets.data_ptr(), C.byref(ro),
+                                            DEVICE))
+
+    @staticmethod
+    def alloc_device_outputs(B, max_new, device):
+        import torch
+        z = lambda *s, dt=torch.float64: torch.zeros(*s, dtype=dt, device=device)
+        return dict(tokens=z(B, max_new, dt=torch.int32), lengths=z(B, dt=torch.int64), actor_lp=z(B, max_new),
+                    ref_lp=z(B, max_new), values=z(B, max_new), rewards=z(B), shaped=z(B, max_new),
+                    advantages=z(B, max_new), returns=z(B, max_new), whitened=z(B, max_new), stats=z(8))
+
+    def run(self, prompts, *, max_new, sampling: SamplingSpec, seed=0, step_index=0, gidx0=0):
+        """Host in / host out: returns (RolloutBatch, ExperienceStats)."""
+        flat, offs = ragged(prompts)
+        B = len(prompts)
+        o = dict(tokens=np.zeros((B, max_new), np.int32), lengths=np.zeros(B, np.int64),
+                 **{k: np.zeros((B, max_new)) for k in ("actor_lp", "ref_lp", "values", "shaped", "advantages",
+                                                        "returns", "whitened")},
+                 rewards=np.zeros(B), stats=np.zeros(8))
+        req = self._req(sampling, seed, step_index, gidx0, max_new)
+        ro = _Rollout(*[o[k].ctypes.data for k in ("tokens", "lengths", "actor_lp", "ref_lp", "values", "rewards",
+                                                   "shaped", "advantages", "returns", "whitened", "stats")])
+        _check(lib().ppoexp_make_experience(C.byref(req), B, flat.ctypes.data, offs.ctypes.data, C.byref(ro), HOST))
+        batch = []
+        for b in range(B):
+            n = int(o["lengths"][b])
+            batch.append(RolloutSeq(np.asarray(prompts[b], np.int32), o["tokens"][b, :n].copy(),
+                                    o["actor_lp"][b, :n].copy(), o["ref_lp"][b, :n].copy(), o["values"][b, :n].copy(),
+                                    float(o["rewards"][b]), o["advantages"][b, :n].copy(), o["returns"][b, :n].copy(),
+                                    np.ones(n), o["whitened"][b, :n].copy(), o["shaped"][b, :n].copy()))
+        return batch, ExperienceStats(*[float(v) for v in o["stats"]])

@@ -1,0 +1,290 @@
+"""Parity of the CUDA path (through the C ABI) against the reference's golden
+vectors and the oracle.  GPU only.
+
+Tolerances (BASELINE.json north_star): greedy tokens, argmax indices and
+sample counts bit-exact; log-probs / KL / values / advantages within
+1e-3 abs + 1e-3 rel (|x - ref| <= 1e-3 + 1e-3*|ref|).
+Parity mode (F32) carries the bit-exact claims; perf mode (BF16) is checked by
+teacher-forced properties on the same bf16-rounded weights."""
+import numpy as np
+import pytest
+
+from oracle.oracle import EOT, ModelCfg, Oracle, synthetic_prompts
+from tests.golden_util import bf16_round, load, rows, to_px_cfg
+
+pytestmark = pytest.mark.gpu
+
+ATOL, RTOL = 1e-3, 1e-3
+
+
+def close(a, b, atol=ATOL, rtol=RTOL):
+    a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+    err = np.abs(a - b) - (atol + rtol * np.abs(b))
+    assert a.shape == b.shape, (a.shape, b.shape)
+    assert (err <= 0).all(), f"max excess {err.max():.3e}, max abs diff {np.abs(a - b).max():.3e}"
+    return float(np.abs(a - b).max()) if a.size else 0.0
+
+
+@pytest.fixture(scope="module")
+def px():
+    from paper_2405_01481_b200 import ppoexp
+    ppoexp.lib()
+    return ppoexp
+
+
+def engine(px, ctx, cfg, w, dtype, **opts):
+    return px.Engine(px.DeviceModel(ctx, to_px_cfg(cfg), w, dtype), px.EngineOptions(**opts))
+
+
+# ----------------------------------------------------------------- golden (parity mode)
+@pytest.mark.parametrize("name", ["c1", "toy"])
+@pytest.mark.parametrize("graphs", [True, False])
+def test_golden_greedy_bitexact(px, ctx, oracle, name, graphs):
+    z, cfg, W, prompts = load(name, oracle)
+    N = int(z["N"])
+    eng = engine(px, ctx, cfg, W["pol"], px.F32, use_graphs=graphs)
+    res = eng.generate_batch([px.GenTask(p, N, px.SamplingSpec.greedy_spec()) for p in prompts])
+    for r, t, l in zip(res, rows(z["greedy_tokens"], z["greedy_lens"]), rows(z["greedy_lps"], z["greedy_lens"])):
+        assert np.array_equal(r.tokens, t)  # argmax indices and sample counts
+        close(r.logprobs, l)
+
+
+@pytest.mark.parametrize("name", ["c1", "toy"])
+def test_golden_sampled_tokens_exact(px, ctx, oracle, name):
+    z, cfg, W, prompts = load(name, oracle)
+    N, seed, step = int(z["N"]), int(z["seed"]), int(z["step_index"])
+    eng = engine(px, ctx, cfg, W["pol"], px.F32)
+    tasks = [px.GenTask(p, N, px.SamplingSpec.temperature_spec(0.7, oracle.mix_seed(seed, step * 1000003 + i)))
+             for i, p in enumerate(prompts)]
+    res = eng.generate_batch(tasks)
+    for r, t, l in zip(res, rows(z["samp_tokens"], z["samp_lens"]), rows(z["samp_lps"], z["samp_lens"])):
+        assert np.array_equal(r.tokens, t)
+        close(r.logprobs, l)
+
+
+@pytest.mark.parametrize("name", ["c1", "toy"])
+@pytest.mark.parametrize("tag", ["xs", "xr"])
+def test_golden_experience(px, ctx, oracle, name, tag):
+    z, cfg, W, prompts = load(name, oracle)
+    N = int(z["N"])
+    pc = to_px_cfg(cfg)
+    eng = px.Engine(px.DeviceModel(ctx, pc, W["pol"], px.F32))
+    ref = px.DeviceModel(ctx, pc, W["ref"], px.F32)
+    crit = px.DeviceModel(ctx, pc.with_head(), W["crit"], px.F32)
+    rm = px.DeviceModel(ctx, pc.with_head(), W["rm"], px.F32) if tag == "xr" else None
+    xm = px.ExperienceMaker(eng, ref, crit, rm, scripted_target=int(z["scripted_target"]),
+                            hyper=px.PpoHyper(float(z["kl_coef"]), 1.0, 0.95))
+    batch, st = xm.run(prompts, max_new=N, sampling=px.SamplingSpec.temperature_spec(1.0, 0),
+                       seed=int(z["seed"]), step_index=int(z["step_index"]))
+    lens = z[f"{tag}_lens"]
+    for i, s in enumerate(batch):
+        assert np.array_equal(s.response, z[f"{tag}_tokens"][i, :lens[i]])
+        close(s.actor_logprobs, z[f"{tag}_actor_logprobs"][i, :lens[i]])
+        close(s.ref_logprobs, z[f"{tag}_ref_logprobs"][i, :lens[i]])
+        close(s.values, z[f"{tag}_values"][i, :lens[i]])
+        close(s.advantages, z[f"{tag}_advantages"][i, :lens[i]])
+        close(s.returns, z[f"{tag}_returns"][i, :lens[i]])
+        close(s.actor_logprobs - s.ref_logprobs,
+              z[f"{tag}_actor_logprobs"][i, :lens[i]] - z[f"{tag}_ref_logprobs"][i, :lens[i]])
+    close([s.reward for s in batch], z[f"{tag}_rewards"])
+    # kl_mean / reward_mean (src/ppo.cpp:389-392, :438-441)
+    a = np.concatenate([z[f"{tag}_actor_logprobs"][i, :lens[i]] - z[f"{tag}_ref_logprobs"][i, :lens[i]]
+                        for i in range(len(lens))])
+    close(st.kl_mean, a.mean())
+    close(st.reward_mean, z[f"{tag}_rewards"].mean())
+    # whitening over all tokens: population mean 0 / std 1 (north-star convention)
+    w = np.concatenate([s.whitened_advantages for s in batch])
+    adv = np.concatenate([s.advantages for s in batch])
+    close(w, (adv - adv.mean()) / np.sqrt(adv.var() + 1e-8), atol=1e-9, rtol=1e-9)
+
+
+@pytest.mark.parametrize("name", ["c1", "toy"])
+def test_golden_scoring(px, ctx, oracle, name):
+    z, cfg, W, prompts = load(name, oracle)
+    lens = z["full_lens"]
+    offs = np.concatenate([[0], np.cumsum(lens)])
+    full = [z["full_tokens"][offs[i]:offs[i + 1]] for i in range(len(lens))]
+    pc = to_px_cfg(cfg)
+    ref = px.DeviceModel(ctx, pc, W["ref"], px.F32)
+    close(np.concatenate(px.sequence_logprobs(ref, full)), z["slp_ref"])
+    crit = px.DeviceModel(ctx, pc.with_head(), W["crit"], px.F32)
+    close(np.concatenate(px.value_estimates(crit, full, [len(p) for p in prompts])), z["values_crit"])
+    rm = px.DeviceModel(ctx, pc.with_head(), W["rm"], px.F32)
+    close(px.reward_head(rm, full), z["reward_rm"])
+
+
+# ----------------------------------------------------------------- engine semantics
+def test_batch_composition_invariance(px, ctx, oracle):
+    # results are index-aligned and independent of batching (tests/test_engine.cpp:213-243)
+    z, cfg, W, prompts = load("c1", oracle)
+    eng = engine(px, ctx, cfg, W["pol"], px.F32)
+    tasks = [px.GenTask(p, 24, px.SamplingSpec.temperature_spec(1.0, 100 + i)) for i, p in enumerate(prompts)]
+    together = eng.generate_batch(tasks)
+    alone = [eng.generate_batch([t])[0] for t in tasks]
+    for a, b in zip(together, alone):
+        assert np.array_equal(a.tokens, b.tokens)
+        assert np.array_equal(a.logprobs, b.logprobs)
+    rev = eng.generate_batch(tasks[::-1])[::-1]
+    for a, b in zip(together, rev):
+        assert np.array_equal(a.tokens, b.tokens)
+
+
+def test_refit_semantics(px, ctx, oracle):
+    # tests/test_engine.cpp:151-211
+    cfg = ModelCfg(258, 32, 2, 2, 64, 48)
+    w = oracle.init_params(cfg, 43).astype(np.float32).astype(np.float64)
+    eng = engine(px, ctx, cfg, w, px.F32)
+    task = [px.GenTask([4, 5], 5)]
+    before = eng.generate_batch(task)
+    eng.refit(w)
+    assert eng.generation_counter == 1
+    assert np.array_equal(eng.generate_batch(task)[0].tokens, before[0].tokens)
+    w2 = w.copy()
+    params = px.flat_to_params(to_px_cfg(cfg), w2)
+    params["layers.0.ffn.up_proj.weight"][:] += 0.01
+    eng.refit(w2)
+    assert eng.generation_counter == 2
+    fresh = engine(px, ctx, cfg, w2, px.F32).generate_batch(task)
+    got = eng.generate_batch(task)
+    assert np.array_equal(got[0].tokens, fresh[0].tokens) and np.array_equal(got[0].logprobs, fresh[0].logprobs)
+    t_o, l_o = oracle.generate(cfg, w2, [[4, 5]], 5)
+    assert np.array_equal(got[0].tokens, t_o[0])
+    # name/shape mismatch: RefitError mentioning "rebuild", engine untouched
+    bad = dict(params)
+    bad["layers.0.ffn.up_proj.weight"] = np.zeros((32, 32))
+    with pytest.raises(px.RefitError, match="rebuild"):
+        eng.refit(bad)
+    missing = dict(params)
+    missing.pop("final_norm.bias")
+    with pytest.raises(px.RefitError, match="rebuild"):
+        eng.refit(missing)
+    assert eng.generation_counter == 2
+    assert np.array_equal(eng.generate_batch(task)[0].tokens, got[0].tokens)
+
+
+def test_contract_errors(px, ctx, oracle):
+    cfg = ModelCfg(258, 32, 1, 2, 64, 16)
+    w = oracle.init_params(cfg, 1)
+    eng = engine(px, ctx, cfg, w, px.F32)
+    with pytest.raises(px.ContractError, match="nonempty"):
+        eng.generate_batch([px.GenTask([], 4)])
+    with pytest.raises(px.IndexError_, match="out of range"):
+        eng.generate_batch([px.GenTask([1, 999], 4)])
+    with pytest.raises(px.ContractError, match="max_seq_len"):
+        eng.generate_batch([px.GenTask(list(range(17)), 4)])
+    assert eng.generate_batch([]) == []
+    # budget = min(max_new, S - P) (src/model.cpp:447-448); greedy runs to the budget unless EOT
+    r = eng.generate_batch([px.GenTask(list(range(10)), 100)])[0]
+    t_o, _ = oracle.generate(cfg, w.astype(np.float32).astype(np.float64), [list(range(10))], 100)
+    assert len(r.tokens) == len(t_o[0]) <= 6
+    with pytest.raises(px.ContractError):
+        px.value_estimates(px.DeviceModel(ctx, to_px_cfg(cfg, True), oracle.init_params(cfg, 1, head=True), px.F32),
+                           [[1, 2, 3]], [3])
+    bad_cfg = px.ModelConfig(258, 30, 1, 4, 64, 16)
+    with pytest.raises(px.ContractError, match="divisible"):
+        px.DeviceModel(ctx, bad_cfg, np.zeros(10), px.F32)
+
+
+def test_eot_stops_and_is_kept(px, ctx, oracle):
+    cfg = ModelCfg(258, 16, 1, 1, 32, 24)
+    w = oracle.init_params(cfg, 9)
+    d = cfg.d
+    w[-2 * d:-d] = 0.0
+    w[-d:] = 1.0
+    w[EOT * d:(EOT + 1) * d] = 1.0
+    eng = engine(px, ctx, cfg, w, px.F32)
+    r = eng.generate_batch([px.GenTask([1, 2], 10), px.GenTask([3], 10, px.SamplingSpec.temperature_spec(0.01, 3))])
+    assert list(r[0].tokens) == [EOT] and list(r[1].tokens) == [EOT]
+
+
+@pytest.mark.parametrize("top_k,top_p", [(0, 0.9), (40, 1.0), (40, 0.8), (1, 1.0)])
+def test_topk_topp_matches_oracle(px, ctx, oracle, top_k, top_p):
+    z, cfg, W, prompts = load("c1", oracle)
+    N = 32
+    eng = engine(px, ctx, cfg, W["pol"], px.F32)
+    seeds = [oracle.mix_seed(11, i) for i in range(len(prompts))]
+    res = eng.generate_batch([px.GenTask(p, N, px.SamplingSpec.temperature_spec(1.3, s, top_k, top_p))
+                              for p, s in zip(prompts, seeds)])
+    u = np.stack([oracle.uniforms(s, N) for s in seeds])
+    t_o, l_o = oracle.generate(cfg, W["pol"], prompts, N, greedy=False, temperature=1.3, top_k=top_k, top_p=top_p,
+                               uniforms=u)
+    for r, t, l in zip(res, t_o, l_o):
+        assert np.array_equal(r.tokens, t)
+        close(r.logprobs, l)
+
+
+# ----------------------------------------------------------------- perf mode (bf16)
+def test_bf16_teacher_forced_parity(px, ctx, oracle):
+    """bf16 weights/activations: generation log-probs must match the oracle's
+    teacher-forced log-probs of the SAME tokens on the same bf16-rounded
+    weights, and every greedy token must be the oracle argmax up to a near-tie."""
+    z, cfg, W, prompts = load("c1", oracle)
+    wb = bf16_round(W["pol"])
+    eng = engine(px, ctx, cfg, wb, px.BF16)
+    N = 48
+    res = eng.generate_batch([px.GenTask(p, N) for p in prompts])
+    full = [np.concatenate([p, r.tokens]) for p, r in zip(prompts, res)]
+    slp = oracle.sequence_logprobs(cfg, wb, full)
+    worst = 0.0
+    for p, r, s, f in zip(prompts, res, slp, full):
+        worst = max(worst, close(r.logprobs, s[len(p):], atol=2e-2, rtol=2e-3))
+        logits = oracle.forward_logits(cfg, wb, f[:-1])[len(p) - 1:]
+        for t, row in zip(r.tokens, logits):
+            assert row[t] >= row.max() - 2e-2  # argmax up to a bf16 near-tie
+    # scoring path (prefill GEMMs + K9) vs oracle on the same tokens
+    m = px.DeviceModel(ctx, to_px_cfg(cfg), wb, px.BF16)
+    got = px.sequence_logprobs(m, full)
+    for g, s in zip(got, slp):
+        close(g, s, atol=2e-2, rtol=2e-3)
+
+
+def test_bf16_experience_c2_width(px, ctx, oracle):
+    """Full experience step at the C2 width / vocab (125M shape, 2 layers to
+    keep the fp64 oracle fast) in perf mode, checked teacher-forced."""
+    cfg = ModelCfg(V=50257, d=768, L=2, H=12, f=3072, S=512)
+    wp = bf16_round(oracle.init_params(cfg, 1))
+    wr = bf16_round(oracle.init_params(cfg, 2))
+    wc = bf16_round(oracle.init_params(cfg, 3, head=True, head_seed=4))
+    prompts = synthetic_prompts(5, 4, 16, ragged_lengths=True)
+    pc = to_px_cfg(cfg)
+    eng = px.Engine(px.DeviceModel(ctx, pc, wp, px.BF16))
+    ref = px.DeviceModel(ctx, pc, wr, px.BF16)
+    crit = px.DeviceModel(ctx, pc.with_head(), wc, px.BF16)
+    xm = px.ExperienceMaker(eng, ref, crit, scripted_target=ord("e"))
+    batch, st = xm.run(prompts, max_new=12, sampling=px.SamplingSpec.temperature_spec(1.0, 0, 0, 0.9), seed=3)
+    full = [np.concatenate([s.prompt, s.response]) for s in batch]
+    rs = [len(s.prompt) for s in batch]
+    a = oracle.sequence_logprobs(cfg, wp, full)
+    r = oracle.sequence_logprobs(cfg, wr, full)
+    v = oracle.value_estimates(cfg, wc, full, rs)
+    for s, ai, ri, vi, p in zip(batch, a, r, v, rs):
+        assert len(s.response) == 12
+        close(s.actor_logprobs, ai[p:], atol=3e-2, rtol=3e-3)
+        close(s.ref_logprobs, ri[p:], atol=3e-2, rtol=3e-3)
+        close(s.values, vi, atol=3e-2, rtol=3e-2)
+        shaped = oracle.kl_penalized_rewards(s.reward, s.actor_logprobs, s.ref_logprobs, 0.003)
+        adv, ret = oracle.gae(shaped, s.values, 1.0, 0.95)
+        close(s.advantages, adv, atol=1e-9, rtol=1e-9)  # shaping/GAE exact given the same inputs
+        close(s.returns, ret, atol=1e-9, rtol=1e-9)
+
+
+# ----------------------------------------------------------------- shaping kernels
+def test_shape_gae_kernel_vs_oracle(px, ctx, oracle):
+    rng = np.random.default_rng(0)
+    B = 37
+    lens = rng.integers(1, 300, size=B)
+    a = [rng.normal(size=n) for n in lens]
+    r = [rng.normal(size=n) for n in lens]
+    v = [rng.normal(size=n) for n in lens]
+    R = rng.normal(size=B)
+    sh, adv, ret = px.shape_gae(ctx, R, a, r, v, 0.05, 0.99, 0.95)
+    for i in range(B):
+        s_o = oracle.kl_penalized_rewards(R[i], a[i], r[i], 0.05)
+        a_o, r_o = oracle.gae(s_o, v[i], 0.99, 0.95)
+        np.testing.assert_allclose(sh[i], s_o, rtol=0, atol=1e-13)
+        np.testing.assert_allclose(adv[i], a_o, rtol=1e-12, atol=1e-11)
+        np.testing.assert_allclose(ret[i], r_o, rtol=1e-12, atol=1e-11)
+
+
+def test_kernel_launches_counted(px, ctx):
+    assert ctx.launch_count > 0
