@@ -149,6 +149,8 @@ ppoexp_status ppoexp_engine_destroy(ppoexp_engine engine);
  * (src/model.cpp:438-482) for B tasks at once.
  *  prompts/offsets: ragged prompts (`where` for both).
  *  max_new[B]: per-task budget (the reference caps it at max_seq_len - P).
+ *  sampling[B]: per-task SamplingSpec (each GenTask carries its own,
+ *    include/aligner/engine.hpp:23-31) — greedy and sampled tasks may mix.
  *  seeds[B]: per-task Rng seed (ignored when greedy).  The sampler consumes
  *    one mt19937_64 uniform per sampled token in order, exactly like the
  *    reference (src/model.cpp:445, :464); the library draws them on the host.

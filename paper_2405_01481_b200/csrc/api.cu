@@ -264,8 +264,8 @@ ppoexp_status ppoexp_model_destroy(ppoexp_model model) {
   return guard([&] {
     if (!model) return;
     std::lock_guard<std::recursive_mutex> lk(model->m.ctx->mu);
-    DeviceGuard g(model->m.ctx->device);
-    model->m.ctx->sync();
+    DeviceGuard g(model->m.ctx->device, true);
+    cudaStreamSynchronize(model->m.ctx->stream);
     delete model;
   });
 }
@@ -580,7 +580,8 @@ ppoexp_status ppoexp_make_experience(const ppoexp_experience_request* req, int64
     int64_t* poff_d = upload(c, "xp.poff", off);
     double gen_ms = 0;
     if (where == PPOEXP_HOST) check_tokens_host(prompts, off[B], pol.cfg.vocab_size);
-    E.generate(B, pd, off.data(), mx.data(), &req->sampling, seeds.data(), N, gtok, glp, glen, PPOEXP_HOST, &gen_ms,
+    const std::vector<ppoexp_sampling> sps(B, req->sampling);
+    E.generate(B, pd, off.data(), mx.data(), sps.data(), seeds.data(), N, gtok, glp, glen, PPOEXP_HOST, &gen_ms,
                PPOEXP_DEVICE, PPOEXP_DEVICE);
     const std::vector<int64_t> n = E.last_lengths;
     for (int64_t b = 0; b < B; ++b)

@@ -48,7 +48,7 @@ Engine::Engine(Model* model, const ppoexp_engine_options* o) : m(model), c(model
   const size_t o_budget = sbytes; sbytes += al(mb * 4);
   const size_t o_nact = sbytes; sbytes += al(16);
   const size_t o_bt = sbytes; sbytes += al(mb * geom.max_pages_per_seq * 4);
-  const size_t o_sp = sbytes; sbytes += al(sizeof(SampleParams));
+  const size_t o_sp = sbytes; sbytes += al(mb * sizeof(SampleParams));
   const size_t o_x = sbytes; sbytes += al(mb * d * 4);
   const size_t o_h = sbytes; sbytes += al(mb * d * ts);
   const size_t o_qkv = sbytes; sbytes += al(mb * 3 * d * ts);
@@ -88,7 +88,7 @@ Engine::Engine(Model* model, const ppoexp_engine_options* o) : m(model), c(model
 }
 
 Engine::~Engine() {
-  DeviceGuard g(c->device);
+  DeviceGuard g(c->device, true);
   cudaStreamSynchronize(c->stream);
   for (auto& [k, gs] : graphs)
     for (int j = 0; j < 2; ++j) {
@@ -235,7 +235,7 @@ void Engine::generate(int64_t B, const int32_t* prompts, const int64_t* offsets,
     if (ms_out) *ms_out = 0;
     return;
   }
-  if (!sampling) throw ContractError("generate: sampling spec required");
+  if (!sampling) throw ContractError("generate: sampling specs required");
   const auto& cfg = m->cfg;
   const int64_t S = cfg.max_seq_len;
   // host copies of the small per-task arrays
@@ -268,7 +268,7 @@ void Engine::generate(int64_t B, const int32_t* prompts, const int64_t* offsets,
   PPOEXP_CUDA(cudaEventRecord(e0, c->stream));
   for (int64_t b0 = 0; b0 < B; b0 += opts.max_batch) {
     const int64_t nb = std::min<int64_t>(opts.max_batch, B - b0);
-    run_chunk(nb, prompts, off, b0, mx, *sampling, sd, out_stride, out_tokens, out_logprobs, out_lengths, where,
+    run_chunk(nb, prompts, off, b0, mx, sampling, sd, out_stride, out_tokens, out_logprobs, out_lengths, where,
               where_out, where_tokens);
   }
   PPOEXP_CUDA(cudaEventRecord(e1, c->stream));
@@ -281,7 +281,7 @@ void Engine::generate(int64_t B, const int32_t* prompts, const int64_t* offsets,
 }
 
 void Engine::run_chunk(int64_t B, const int32_t* prompts, const std::vector<int64_t>& off_all, int64_t b0,
-                       const std::vector<int64_t>& mx_all, const ppoexp_sampling& sp,
+                       const std::vector<int64_t>& mx_all, const ppoexp_sampling* sp_all,
                        const std::vector<uint64_t>& seeds_all, int64_t out_stride, int32_t* out_tokens,
                        double* out_logprobs, int64_t* out_lengths, int where, int where_out, int where_tokens) {
   Ctx& cc = *c;
@@ -315,10 +315,16 @@ void Engine::run_chunk(int64_t B, const int32_t* prompts, const std::vector<int6
     last[b] = int32_t(off_all[b0 + b + 1] - off_all[b0] - 1);
     active += bud[b] > 0;
   }
-  SampleParams spd{sp.greedy, float(sp.temperature), sp.top_k, sp.top_p};
+  std::vector<SampleParams> spd(B);
+  bool any_sampled = false;
+  for (int64_t b = 0; b < B; ++b) {
+    const ppoexp_sampling& sp = sp_all[b0 + b];
+    spd[b] = SampleParams{sp.greedy, float(sp.temperature), sp.top_k, sp.top_p};
+    any_sampled |= !sp.greedy;
+  }
   // staging (pinned) → device
   const size_t n_bt = bt.size() * 4;
-  const size_t need = n_bt + 4 * B * 4 + sizeof(spd) + 64 + (sp.greedy ? 0 : size_t(B) * S * 8);
+  const size_t need = n_bt + 5 * B * 16 + B * sizeof(SampleParams) + 256 + (any_sampled ? size_t(B) * S * 8 : 0);
   char* hs = static_cast<char*>(cc.pinned_staging(need));
   size_t o = 0;
   auto put = [&](void* dst, const void* src, size_t n) {
@@ -332,13 +338,14 @@ void Engine::run_chunk(int64_t B, const int32_t* prompts, const std::vector<int6
   put(budget, st_bud.data(), B * 4);
   put(last_rows, last.data(), B * 4);
   put(n_active, &active, 4);
-  put(sparams, &spd, sizeof(spd));
+  put(sparams, spd.data(), B * sizeof(SampleParams));
   PPOEXP_CUDA(cudaMemsetAsync(n_gen, 0, B * 4, cc.stream));
-  if (!sp.greedy) {
+  if (any_sampled) {
     // One mt19937_64 uniform per sampled token, Rng(seed) stream
     // (include/aligner/rng.hpp:21-23; consumed in order, src/model.cpp:464).
     double* u = reinterpret_cast<double*>(hs + o);
     for (int64_t b = 0; b < B; ++b) {
+      if (spd[b].greedy) continue;
       std::mt19937_64 gen(seeds_all[b0 + b]);
       for (int64_t i = 0; i < bud[b]; ++i) u[b * S + i] = double(gen() >> 11) * 0x1.0p-53;
     }

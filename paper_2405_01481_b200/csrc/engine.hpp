@@ -57,7 +57,8 @@ struct Engine {
 
  private:
   void run_chunk(int64_t B, const int32_t* prompts, const std::vector<int64_t>& off_all, int64_t b0,
-                 const std::vector<int64_t>& mx_all, const ppoexp_sampling& sp, const std::vector<uint64_t>& seeds_all,
+                 const std::vector<int64_t>& mx_all, const ppoexp_sampling* sp_all,
+                 const std::vector<uint64_t>& seeds_all,
                  int64_t out_stride, int32_t* out_tokens, double* out_logprobs, int64_t* out_lengths, int where,
                  int where_out, int where_tokens);
   SamplerState sampler_state() const;

@@ -62,7 +62,7 @@ struct SampleParams {
   double top_p;
 };
 struct SamplerState {
-  const SampleParams* params;  // device
+  const SampleParams* params;  // device, [B] (one spec per task)
   int32_t* next_tok;    // [B] token fed at the next decode step
   int32_t* pos;         // [B] position the next fed token occupies
   int32_t* n_gen;       // [B]

@@ -16,7 +16,7 @@ Ctx::Ctx(int dev) : device(dev) {
 }
 
 Ctx::~Ctx() {
-  DeviceGuard g(device);
+  DeviceGuard g(device, true);
   cudaStreamSynchronize(stream);
   for (auto& t : pending) {
     cudaEventDestroy(t.a);
@@ -62,11 +62,9 @@ void Ctx::harvest() {
 }
 
 void* Ctx::pinned_staging(size_t bytes) {
+  PPOEXP_CUDA(cudaStreamSynchronize(stream));
   if (bytes > pinned_bytes) {
-    if (pinned) {
-      PPOEXP_CUDA(cudaStreamSynchronize(stream));
-      PPOEXP_CUDA(cudaFreeHost(pinned));
-    }
+    if (pinned) PPOEXP_CUDA(cudaFreeHost(pinned));
     pinned = nullptr;
     pinned_bytes = 0;
     PPOEXP_CUDA(cudaMallocHost(&pinned, bytes));

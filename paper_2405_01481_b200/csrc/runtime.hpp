@@ -78,10 +78,13 @@ struct Ctx {
   void launch(const char* cls, double bytes, double flops, F&& f) {
     if (profiling) {
       TimedLaunch t{cls, new_event(), new_event(), bytes, flops};
-      PPOEXP_CUDA(cudaEventRecord(t.a, stream));
+      // inside stream capture a plain record is only a dependency marker;
+      // cudaEventRecordExternal materialises a timing node in the graph
+      const unsigned fl = capturing ? cudaEventRecordExternal : cudaEventRecordDefault;
+      PPOEXP_CUDA(cudaEventRecordWithFlags(t.a, stream, fl));
       f();
       PPOEXP_CUDA(cudaGetLastError());
-      PPOEXP_CUDA(cudaEventRecord(t.b, stream));
+      PPOEXP_CUDA(cudaEventRecordWithFlags(t.b, stream, fl));
       if (capturing && capture_events)
         capture_events->push_back(t);
       else
@@ -106,6 +109,8 @@ struct Ctx {
     b->ensure(bytes);
     return b->ptr;
   }
+  // Pinned host staging for H2D/D2H copies.  Synchronises the stream first:
+  // earlier async copies may still be reading the previous contents.
   void* pinned_staging(size_t bytes);
   void sync() { PPOEXP_CUDA(cudaStreamSynchronize(stream)); }
 };
@@ -116,9 +121,19 @@ void copy_out(Ctx& c, void* dst, const void* src_dev, size_t bytes, int where);
 
 struct DeviceGuard {
   int prev = -1;
-  explicit DeviceGuard(int dev) {
-    cudaGetDevice(&prev);
-    if (prev != dev) PPOEXP_CUDA(cudaSetDevice(dev));
+  explicit DeviceGuard(int dev, bool nothrow = false) {
+    if (cudaGetDevice(&prev) != cudaSuccess) {
+      prev = -1;
+      (void)cudaGetLastError();
+      if (nothrow) return;
+    }
+    if (prev != dev) {
+      const cudaError_t e = cudaSetDevice(dev);
+      if (e != cudaSuccess) {
+        (void)cudaGetLastError();
+        if (!nothrow) PPOEXP_CUDA(e);
+      }
+    }
   }
   ~DeviceGuard() {
     if (prev >= 0) cudaSetDevice(prev);

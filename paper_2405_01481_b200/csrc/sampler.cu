@@ -111,11 +111,12 @@ __device__ void radix_select(const float* row, int64_t V, float M, float inv_tau
 __global__ void __launch_bounds__(NT) sampler_kernel(const float* __restrict__ logits, int64_t ld, int64_t V,
                                                      SamplerState s) {
   __shared__ Shared sh;
-  const int greedy = s.params->greedy;
-  const float temperature = s.params->temperature;
-  const int64_t top_k = s.params->top_k;
-  const double top_p = s.params->top_p;
   const int64_t b = blockIdx.x;
+  const SampleParams prm = s.params[b];
+  const int greedy = prm.greedy;
+  const float temperature = prm.temperature;
+  const int64_t top_k = prm.top_k;
+  const double top_p = prm.top_p;
   if (s.done[b]) return;
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
   const float* row = logits + b * ld;

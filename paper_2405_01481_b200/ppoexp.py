@@ -200,6 +200,9 @@ def expected_names(cfg: ModelConfig):
 
 def flat_to_params(cfg: ModelConfig, flat: np.ndarray) -> dict:
     """Splits a flat canonical buffer into {name: array} (views, no copy)."""
+    total = sum(int(np.prod(s)) for _, s in expected_names(cfg))
+    if total != flat.size:
+        raise ShapeError(f"flat parameter buffer has {flat.size} values, config implies {total}")
     out, off = {}, 0
     for name, shape in expected_names(cfg):
         n = int(np.prod(shape))
@@ -294,7 +297,10 @@ class DeviceModel:
 
     def __init__(self, ctx: Context, config: ModelConfig, params, dtype: int = BF16):
         if isinstance(params, np.ndarray):
-            params = flat_to_params(config, params)
+            try:
+                params = flat_to_params(config, params)
+            except (ShapeError, ValueError):
+                params = {}  # the library reports the config / name-set error
         self.ctx, self.config, self.dtype = ctx, config, dtype
         self.h = C.c_void_p()
         views, keep = _views(params)
@@ -401,15 +407,9 @@ class Engine:
         return self.model.generation_counter
 
     def generate_batch(self, tasks: Sequence[GenTask]):
-        """Engine::generate_batch, src/engine.cpp:148-182.  All tasks must share
-        one sampling mode (greedy / tau / top-k / top-p); seeds are per task."""
+        """Engine::generate_batch, src/engine.cpp:148-182 (per-task SamplingSpec)."""
         if not tasks:
             return []
-        s0 = tasks[0].sampling
-        for t in tasks:
-            s = t.sampling
-            if (s.greedy, s.temperature, s.top_k, s.top_p) != (s0.greedy, s0.temperature, s0.top_k, s0.top_p):
-                raise ContractError("generate_batch: tasks must share one sampling mode")
         flat, offs = ragged([t.prompt for t in tasks])
         mx = np.array([t.max_new for t in tasks], np.int64)
         seeds = np.array([t.sampling.seed for t in tasks], np.uint64)
@@ -418,10 +418,11 @@ class Engine:
         toks = np.zeros((B, stride), np.int32)
         lps = np.zeros((B, stride), np.float64)
         lens = np.zeros(B, np.int64)
-        sp = _Sampling(1 if s0.greedy else 0, s0.top_k, s0.temperature, s0.top_p)
+        sp = (_Sampling * B)(*[_Sampling(1 if t.sampling.greedy else 0, t.sampling.top_k, t.sampling.temperature,
+                                          t.sampling.top_p) for t in tasks])
         ms = C.c_double()
         _check(lib().ppoexp_engine_generate(self.h, B, flat.ctypes.data, offs.ctypes.data, mx.ctypes.data,
-                                            C.byref(sp), seeds.ctypes.data, stride, toks.ctypes.data,
+                                            sp, seeds.ctypes.data, stride, toks.ctypes.data,
                                             lps.ctypes.data, lens.ctypes.data, HOST, C.byref(ms)))
         self.last_ms = ms.value
         return [GenerateResult(toks[b, :lens[b]].copy(), lps[b, :lens[b]].copy()) for b in range(B)]
