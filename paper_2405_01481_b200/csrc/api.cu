@@ -8,6 +8,7 @@
 #include <string>
 #include <vector>
 
+#include "../../include/ppoexp_testing.h"
 #include "engine.hpp"
 
 using namespace ppoexp;
@@ -97,6 +98,7 @@ Packed pack_tokens(Ctx& c, const int32_t* tokens, const std::vector<int64_t>& of
 
 __global__ void seq_meta_kernel(int64_t B, const int64_t* offs, const int32_t* tokens, int32_t* gather,
                                 int32_t* target, int64_t* out_index) {
+  PDL_ENTRY();
   const int64_t b = blockIdx.x;
   const int64_t o = offs[b], n = offs[b + 1] - o, co = o - b;  // compact rows skip each sequence's last row
   for (int64_t t = threadIdx.x; t + 1 < n; t += blockDim.x) {
@@ -108,6 +110,7 @@ __global__ void seq_meta_kernel(int64_t B, const int64_t* offs, const int32_t* t
 
 __global__ void last_content_kernel(int64_t B, const int64_t* offs, const int32_t* tokens, int32_t* gather,
                                     int64_t* out_index) {
+  PDL_ENTRY();
   const int64_t b = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   if (b >= B) return;
   int64_t last = -1;
@@ -330,7 +333,7 @@ ppoexp_status ppoexp_sequence_logprobs(ppoexp_model model, int64_t B, const int3
     int32_t* gather = static_cast<int32_t*>(c.workspace("lp.gather", std::max<int64_t>(R, 1) * 4));
     int32_t* target = static_cast<int32_t*>(c.workspace("lp.target", std::max<int64_t>(R, 1) * 4));
     int64_t* oidx = static_cast<int64_t*>(c.workspace("lp.oidx", std::max<int64_t>(R, 1) * 8));
-    c.launch("meta", 0, 0, [&] { seq_meta_kernel<<<B, 128, 0, c.stream>>>(B, p.offsets_d, p.tokens_d, gather, target, oidx); });
+    c.launch("meta", 0, 0, [&] { launch_kernel(c, seq_meta_kernel, dim3(B), dim3(128), 0, 1, B, p.offsets_d, p.tokens_d, gather, target, oidx); });
     // empty sequences contribute nothing (the reference returns {}, src/model.cpp:485)
     Packed q = p;
     if (R > 0) {
@@ -399,7 +402,7 @@ ppoexp_status ppoexp_reward_head(ppoexp_model rm, int64_t B, const int32_t* toke
     int32_t* gd = static_cast<int32_t*>(c.workspace("rw.gather", B * 4));
     int64_t* od = static_cast<int64_t*>(c.workspace("rw.oidx", B * 8));
     c.launch("meta", 0, 0, [&] {
-      last_content_kernel<<<ceil_div(B, 128), 128, 0, c.stream>>>(B, p.offsets_d, p.tokens_d, gd, od);
+      launch_kernel(c, last_content_kernel, dim3(ceil_div(B, 128)), dim3(128), 0, 1, B, p.offsets_d, p.tokens_d, gd, od);
     });
     std::vector<int32_t> chk(B);
     PPOEXP_CUDA(cudaMemcpyAsync(chk.data(), gd, B * 4, cudaMemcpyDeviceToHost, c.stream));
@@ -626,7 +629,7 @@ ppoexp_status ppoexp_make_experience(const ppoexp_experience_request* req, int64
       int32_t* lg = static_cast<int32_t*>(c.workspace("xp.lastg", B * 4));
       int64_t* lo = static_cast<int64_t*>(c.workspace("xp.lasto", B * 8));
       c.launch("meta", 0, 0, [&] {
-        last_content_kernel<<<ceil_div(B, 128), 128, 0, c.stream>>>(B, pk.offsets_d, pk.tokens_d, lg, lo);
+        launch_kernel(c, last_content_kernel, dim3(ceil_div(B, 128)), dim3(128), 0, 1, B, pk.offsets_d, pk.tokens_d, lg, lo);
       });
       float* x = forward_layers(*rm, pk, nullptr);
       score_head(*rm, x, lg, lo, B, rew);
@@ -717,3 +720,29 @@ ppoexp_status ppoexp_make_experience(const ppoexp_experience_request* req, int64
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------------------ testing
+namespace ppoexp {
+template <class T>
+void launch_gemm_simt(Ctx& c, const T* A, int64_t lda, const T* B, int64_t ldb, int64_t M, int64_t N, int64_t K,
+                      Epi epi, void* C, int64_t ldc);
+}
+
+extern "C" ppoexp_status ppoexp_testing_gemm_bf16(ppoexp_ctx ctx, const void* A, int64_t lda, const void* B,
+                                                  int64_t ldb, int64_t M, int64_t N, int64_t K, int32_t epi, void* C,
+                                                  int64_t ldc, int32_t path) {
+  return guard([&] {
+    need(ctx, "ctx");
+    Ctx& c = *ctx->c;
+    std::lock_guard<std::recursive_mutex> lk(c.mu);
+    DeviceGuard g(c.device);
+    if (epi < 0 || epi > 3) throw ContractError("epi must be 0..3");
+    const auto* a = static_cast<const bf16*>(A);
+    const auto* b = static_cast<const bf16*>(B);
+    if (path == 1)
+      launch_gemm_simt<bf16>(c, a, lda, b, ldb, M, N, K, static_cast<Epi>(epi), C, ldc);
+    else
+      gemm<bf16>(c, a, lda, b, ldb, M, N, K, static_cast<Epi>(epi), C, ldc);
+    c.sync();
+  });
+}

@@ -25,6 +25,7 @@ template <class T, int DH>
 __global__ void __launch_bounds__(64 * (DH / 16)) attn_prefill_kernel(const T* __restrict__ qkv,
                                                                       const int64_t* __restrict__ seq_offsets,
                                                                       int64_t H, T* __restrict__ out) {
+  PDL_ENTRY();
   constexpr int TPQ = DH / 16, QT = 64, KT = 64, NT = QT * TPQ, LD = DH + 4;
   extern __shared__ __align__(16) float sm[];
   float* Ks = sm;
@@ -92,101 +93,135 @@ __global__ void __launch_bounds__(64 * (DH / 16)) attn_prefill_kernel(const T* _
 }
 
 // ---------------------------------------------------------------- decode
+// CTA per (sequence, head), 4 warps splitting the context into 32-token
+// tiles.  Q·K: lane-per-token (each lane streams whole K rows of its token
+// with 16-byte loads; LPT lanes per token when a row exceeds 128 bytes), no
+// per-token shuffles.  Online softmax per tile.  P·V: lane-per-dim with
+// coalesced V-row loads and the tile's probabilities broadcast by shuffle.
+// The four warps' (max, sum, acc) are merged through shared memory.
 template <class T, int DH>
 __global__ void __launch_bounds__(128) attn_decode_kernel(const T* __restrict__ qkv, const int32_t* __restrict__ pos,
                                                           const int32_t* __restrict__ done,
                                                           const int32_t* __restrict__ block_table, int layer,
                                                           KvGeom g, T* __restrict__ kv, T* __restrict__ out) {
+  PDL_ENTRY();
   constexpr int NW = 4;
-  constexpr int N = 16 / sizeof(T);  // elements per 16-byte vector
-  constexpr int LPT = (DH * sizeof(T) / 16) < 32 ? (DH * sizeof(T) / 16) : 32;  // lanes per token
-  constexpr int TPW = 32 / LPT;                                                  // tokens per warp pass
-  constexpr int NG = NW * TPW;                                                   // token groups
-  static_assert(DH * sizeof(T) / 16 <= 32, "head too wide");
-  extern __shared__ __align__(16) float sm[];
-  float* qs = sm;                // [DH]
-  float* red = qs + DH;          // [NG][DH]
-  float* scores = red + NG * DH; // [ctx]
-  __shared__ float wred[NW];
+  constexpr int ROWB = DH * int(sizeof(T));          // bytes per K/V row
+  constexpr int LPT = ROWB > 128 ? ROWB / 128 : 1;   // lanes per token (Q·K)
+  constexpr int EPL = DH / LPT;                      // elements per lane (Q·K)
+  constexpr int TT = 32 / LPT;                       // tokens per tile
+  constexpr int NV = EPL * int(sizeof(T)) / 16;      // 16-byte vectors per lane
+  constexpr int VE = 16 / int(sizeof(T));            // elements per vector
+  constexpr int DPL = DH >= 32 ? DH / 32 : 1;        // dims per lane (P·V)
+  constexpr int DLANES = DH / DPL;                   // lanes holding dims
+  __shared__ float sm_m[NW], sm_l[NW];
+  __shared__ float sm_acc[NW][DH];
   const int64_t b = blockIdx.y, h = blockIdx.x;
   if (done[b]) return;
   const int64_t p = pos[b], ctx = p + 1;
   const int64_t d = g.H * DH, PS = g.page_size;
   const T* row = qkv + b * 3 * d;
   const int32_t* bt = block_table + b * g.max_pages_per_seq;
-  auto kbase = [&](int64_t t, int which) -> T* {
+  const int64_t head_stride = PS * DH;
+  auto base = [&](int64_t t, int which) -> T* {
     const int64_t page = bt[t / PS];
-    return kv + ((((int64_t)layer * g.n_pages + page) * 2 + which) * g.H + h) * PS * DH + (t % PS) * DH;
+    return kv + ((((int64_t)layer * g.n_pages + page) * 2 + which) * g.H + h) * head_stride + (t % PS) * DH;
   };
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  // append this step's K/V row (KvSession::step, src/model.cpp:305-308)
   for (int i = tid; i < DH; i += 128) {
-    kbase(p, 0)[i] = row[d + h * DH + i];
-    kbase(p, 1)[i] = row[2 * d + h * DH + i];
-    qs[i] = to_f(row[h * DH + i]);
+    base(p, 0)[i] = row[d + h * DH + i];
+    base(p, 1)[i] = row[2 * d + h * DH + i];
   }
-  __syncthreads();
+  __syncthreads();  // the appended row is visible to the whole CTA
+  const int part = lane % LPT, tok = lane / LPT;
+  float q[EPL];
+#pragma unroll
+  for (int i = 0; i < EPL; ++i) q[i] = to_f(row[h * DH + part * EPL + i]);
   const float inv_sqrt_dh = 1.0f / sqrtf(float(DH));
-  const int sub = lane / LPT, part = lane % LPT;
-  // scores
-  float mloc = -FLT_MAX;
-  for (int64_t t0 = int64_t(w) * TPW; t0 < ctx; t0 += NW * TPW) {
-    const int64_t t = t0 + sub;
-    float s = 0.f;
-    if (t < ctx && part * N < DH) {
-      Vec16<T> kv4;
-      kv4.u = *reinterpret_cast<const uint4*>(kbase(t, 0) + part * N);
+  float m = -FLT_MAX, l = 0.f, acc[DPL];
 #pragma unroll
-      for (int i = 0; i < N; ++i) s = fmaf(to_f(kv4.v[i]), qs[part * N + i], s);
+  for (int i = 0; i < DPL; ++i) acc[i] = 0.f;
+  const int dl = lane < DLANES ? lane : 0;
+  for (int64_t t0 = int64_t(w) * TT; t0 < ctx; t0 += int64_t(NW) * TT) {
+    // ---- scores for the tile
+    const int64_t t = t0 + tok;
+    float s = -FLT_MAX;
+    {
+      float dot = 0.f;
+      if (t < ctx) {
+        const uint4* kr = reinterpret_cast<const uint4*>(base(t, 0) + part * EPL);
+        Vec16<T> kv4[NV];
+#pragma unroll
+        for (int v = 0; v < NV; ++v) kv4[v].u = kr[v];
+#pragma unroll
+        for (int v = 0; v < NV; ++v)
+#pragma unroll
+          for (int e = 0; e < VE; ++e) dot = fmaf(to_f(kv4[v].v[e]), q[v * VE + e], dot);
+      }
+#pragma unroll
+      for (int o = LPT / 2; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+      if (t < ctx) s = dot * inv_sqrt_dh;
     }
+    // ---- online softmax over the tile
+    float tm = s;
 #pragma unroll
-    for (int o = LPT / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (t < ctx && part == 0) {
-      s *= inv_sqrt_dh;
-      scores[t] = s;
-      mloc = fmaxf(mloc, s);
+    for (int o = 16; o > 0; o >>= 1) tm = fmaxf(tm, __shfl_xor_sync(0xffffffffu, tm, o));
+    const float mnew = fmaxf(m, tm);
+    const float corr = m == -FLT_MAX ? 0.f : expf(m - mnew);
+    const float pr = t < ctx && part == 0 ? expf(s - mnew) : 0.f;
+    float ps = pr;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ps += __shfl_xor_sync(0xffffffffu, ps, o);
+    l = l * corr + ps;
+    m = mnew;
+#pragma unroll
+    for (int i = 0; i < DPL; ++i) acc[i] *= corr;
+    // ---- P·V over the tile
+    const int nt = int((ctx - t0) < TT ? (ctx - t0) : TT);
+    constexpr int U = 8;
+    for (int j0 = 0; j0 < nt; j0 += U) {
+      T vv[U][DPL];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (j0 + u < nt) {
+          const T* vr = base(t0 + j0 + u, 1) + dl * DPL;
+#pragma unroll
+          for (int i = 0; i < DPL; ++i) vv[u][i] = vr[i];
+        }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const float pj = __shfl_sync(0xffffffffu, pr, ((j0 + u) & (TT - 1)) * LPT);
+        if (j0 + u < nt)
+#pragma unroll
+          for (int i = 0; i < DPL; ++i) acc[i] = fmaf(pj, to_f(vv[u][i]), acc[i]);
+      }
     }
   }
-  mloc = warp_max(mloc);
-  if (lane == 0) wred[w] = mloc;
-  __syncthreads();
-  float mx = wred[0];
-#pragma unroll
-  for (int i = 1; i < NW; ++i) mx = fmaxf(mx, wred[i]);
-  __syncthreads();
-  float sloc = 0.f;
-  for (int64_t t = tid; t < ctx; t += 128) {
-    const float e = expf(scores[t] - mx);
-    scores[t] = e;
-    sloc += e;
+  // ---- merge the warps
+  if (lane == 0) {
+    sm_m[w] = m;
+    sm_l[w] = l;
   }
-  sloc = warp_sum(sloc);
-  if (lane == 0) wred[w] = sloc;
+  if (lane < DLANES)
+#pragma unroll
+    for (int i = 0; i < DPL; ++i) sm_acc[w][lane * DPL + i] = acc[i];
   __syncthreads();
-  float se = 0.f;
+  float M = sm_m[0];
 #pragma unroll
-  for (int i = 0; i < NW; ++i) se += wred[i];
-  // P·V
-  float acc[N];
+  for (int k = 1; k < NW; ++k) M = fmaxf(M, sm_m[k]);
+  float L = 0.f, sc[NW];
 #pragma unroll
-  for (int i = 0; i < N; ++i) acc[i] = 0.f;
-  const int grp = w * TPW + sub;
-  if (part * N < DH) {
-    for (int64_t t = grp; t < ctx; t += NG) {
-      const float pr = scores[t];
-      Vec16<T> v4;
-      v4.u = *reinterpret_cast<const uint4*>(kbase(t, 1) + part * N);
-#pragma unroll
-      for (int i = 0; i < N; ++i) acc[i] = fmaf(pr, to_f(v4.v[i]), acc[i]);
-    }
-#pragma unroll
-    for (int i = 0; i < N; ++i) red[grp * DH + part * N + i] = acc[i];
+  for (int k = 0; k < NW; ++k) {
+    sc[k] = sm_m[k] == -FLT_MAX ? 0.f : expf(sm_m[k] - M);
+    L += sm_l[k] * sc[k];
   }
-  __syncthreads();
-  const float inv = 1.0f / se;
+  const float inv = 1.0f / L;
   for (int i = tid; i < DH; i += 128) {
-    float s = 0.f;
-    for (int gi = 0; gi < NG; ++gi) s += red[gi * DH + i];
-    out[b * d + h * DH + i] = from_f<T>(s * inv);
+    float o = 0.f;
+#pragma unroll
+    for (int k = 0; k < NW; ++k) o += sm_acc[k][i] * sc[k];
+    out[b * d + h * DH + i] = from_f<T>(o * inv);
   }
 }
 
@@ -198,21 +233,16 @@ void prefill_impl(Ctx& c, const T* qkv, const int64_t* seq_offsets, int64_t B, i
   PPOEXP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   dim3 grid(ceil_div(max_len, 64), H, B);
   const double flops = 2.0 * 2.0 * B * H * double(max_len) * max_len / 2 * DH;
-  c.launch("attention_prefill", 0, flops, [&] { k<<<grid, 64 * TPQ, smem, c.stream>>>(qkv, seq_offsets, H, out); });
+  c.launch("attention_prefill", 0, flops, [&] { launch_kernel(c, k, dim3(grid), dim3(64 * TPQ), smem, 1, qkv, seq_offsets, H, out); });
 }
 
 template <class T, int DH>
 void decode_impl(Ctx& c, const T* qkv, int64_t B, const int32_t* pos, const int32_t* done, const int32_t* block_table,
                  int layer, const KvGeom& g, T* kv, T* out, double bytes) {
-  constexpr int LPT = (DH * sizeof(T) / 16) < 32 ? (DH * sizeof(T) / 16) : 32;
-  constexpr int NG = 4 * (32 / LPT);
-  const int64_t max_ctx = g.max_pages_per_seq * g.page_size;
-  const size_t smem = (DH + NG * DH + max_ctx) * sizeof(float);
   auto k = attn_decode_kernel<T, DH>;
-  PPOEXP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   dim3 grid(g.H, B);
   c.launch("decode_attention", bytes, 0, [&] {
-    k<<<grid, 128, smem, c.stream>>>(qkv, pos, done, block_table, layer, g, kv, out);
+    launch_kernel(c, k, dim3(grid), dim3(128), 0, 1, qkv, pos, done, block_table, layer, g, kv, out);
   });
 }
 

@@ -82,6 +82,19 @@ struct Vec16 {
   };
 };
 
+// Programmatic dependent launch (PDL): every kernel is launched with
+// programmatic stream serialization, so it may start while its predecessor
+// drains.  pdl_wait() blocks until the predecessor grid has completed and its
+// writes are visible; nothing produced upstream may be touched before it.
+// pdl_trigger() lets the successor grid begin its own prologue early.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+#define PDL_ENTRY() \
+  do {              \
+    pdl_wait();     \
+    pdl_trigger();  \
+  } while (0)
+
 constexpr int kPadToken = 256;  // include/aligner/model.hpp:17
 constexpr int kEotToken = 257;  // include/aligner/model.hpp:18
 

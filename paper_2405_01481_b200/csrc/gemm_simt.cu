@@ -14,6 +14,7 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(const T* __restrict__ A,
                                                          const T* __restrict__ B, int64_t ldb, int64_t M,
                                                          int64_t N, int64_t K, void* __restrict__ Cv,
                                                          int64_t ldc) {
+  PDL_ENTRY();
   __shared__ __align__(16) float As[BK][BM + 4];
   __shared__ __align__(16) float Bs[BK][BN + 4];
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
@@ -80,16 +81,16 @@ void launch_gemm_simt(Ctx& c, const T* A, int64_t lda, const T* B, int64_t ldb, 
   c.launch("gemm_simt", bytes, flops, [&] {
     switch (epi) {
       case Epi::kStore:
-        gemm_simt_kernel<T, 0><<<grid, 256, 0, c.stream>>>(A, lda, B, ldb, M, N, K, C, ldc);
+        launch_kernel(c, gemm_simt_kernel<T, 0>, dim3(grid), dim3(256), 0, 1, A, lda, B, ldb, M, N, K, C, ldc);
         break;
       case Epi::kGelu:
-        gemm_simt_kernel<T, 1><<<grid, 256, 0, c.stream>>>(A, lda, B, ldb, M, N, K, C, ldc);
+        launch_kernel(c, gemm_simt_kernel<T, 1>, dim3(grid), dim3(256), 0, 1, A, lda, B, ldb, M, N, K, C, ldc);
         break;
       case Epi::kAddResidual:
-        gemm_simt_kernel<T, 2><<<grid, 256, 0, c.stream>>>(A, lda, B, ldb, M, N, K, C, ldc);
+        launch_kernel(c, gemm_simt_kernel<T, 2>, dim3(grid), dim3(256), 0, 1, A, lda, B, ldb, M, N, K, C, ldc);
         break;
       case Epi::kStoreF32:
-        gemm_simt_kernel<T, 3><<<grid, 256, 0, c.stream>>>(A, lda, B, ldb, M, N, K, C, ldc);
+        launch_kernel(c, gemm_simt_kernel<T, 3>, dim3(grid), dim3(256), 0, 1, A, lda, B, ldb, M, N, K, C, ldc);
         break;
     }
   });

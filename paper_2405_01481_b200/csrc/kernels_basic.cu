@@ -90,6 +90,7 @@ template <class T>
 __global__ void embed_kernel(const int32_t* __restrict__ tokens, const int32_t* __restrict__ positions,
                              int64_t rows, int64_t d, const T* __restrict__ tok, const T* __restrict__ pos,
                              float* __restrict__ x) {
+  PDL_ENTRY();
   const int64_t r = blockIdx.x;
   if (r >= rows) return;
   const int64_t t = tokens[r], p = positions[r];
@@ -102,7 +103,7 @@ void launch_embed(Ctx& c, const int32_t* tokens, const int32_t* positions, int64
                   const T* pos, float* x) {
   if (rows <= 0) return;
   c.launch("embed", double(rows) * d * (2 * sizeof(T) + 4), 0, [&] {
-    embed_kernel<T><<<rows, 256, 0, c.stream>>>(tokens, positions, rows, d, tok, pos, x);
+    launch_kernel(c, embed_kernel<T>, dim3(rows), dim3(256), 0, 1, tokens, positions, rows, d, tok, pos, x);
   });
 }
 
@@ -130,6 +131,7 @@ __global__ void __launch_bounds__(256) layernorm_kernel(const float* __restrict_
                                                         const float* __restrict__ g, const float* __restrict__ b,
                                                         T* __restrict__ y, const int32_t* __restrict__ gather,
                                                         const float* __restrict__ head, float* __restrict__ head_out) {
+  PDL_ENTRY();
   __shared__ float red[32];
   const int64_t r = blockIdx.x;
   const int64_t src = gather ? gather[r] : r;
@@ -168,13 +170,128 @@ __global__ void __launch_bounds__(256) layernorm_kernel(const float* __restrict_
   }
 }
 
+// Warp-per-row variant for d <= 1024 (8 rows per 256-thread CTA): the
+// decode step's LayerNorms are 64-row launches where a CTA per row wastes
+// three block barriers per row.
+template <class T>
+__global__ void __launch_bounds__(256) layernorm_warp_kernel(const float* __restrict__ x, int64_t rows, int64_t d,
+                                                             const float* __restrict__ g, const float* __restrict__ b,
+                                                             T* __restrict__ y, const int32_t* __restrict__ gather,
+                                                             const float* __restrict__ head,
+                                                             float* __restrict__ head_out) {
+  PDL_ENTRY();
+  const int lane = threadIdx.x & 31;
+  const int64_t r = int64_t(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  if (r >= rows) return;
+  const int64_t src = gather ? gather[r] : r;
+  const float* xr = x + src * d;
+  constexpr int MAXV = 32;
+  float v[MAXV];
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < MAXV; ++i) {
+    const int64_t j = lane + int64_t(i) * 32;
+    v[i] = j < d ? xr[j] : 0.f;
+    s += v[i];
+  }
+  const float mu = warp_sum(s) / float(d);
+  float q = 0.f;
+#pragma unroll
+  for (int i = 0; i < MAXV; ++i) {
+    const int64_t j = lane + int64_t(i) * 32;
+    if (j < d) q += (v[i] - mu) * (v[i] - mu);
+  }
+  const float var = warp_sum(q) / float(d);
+  const float is = 1.0f / sqrtf(var + 1e-5f);
+  float hd = 0.f;
+#pragma unroll
+  for (int i = 0; i < MAXV; ++i) {
+    const int64_t j = lane + int64_t(i) * 32;
+    if (j < d) {
+      const float o = g[j] * ((v[i] - mu) * is) + b[j];
+      if (y) y[r * d + j] = from_f<T>(o);
+      if (head) hd += o * head[j];
+    }
+  }
+  if (head) {
+    hd = warp_sum(hd);
+    if (lane == 0) head_out[r] = hd;
+  }
+}
+
+// CTA-per-row float4 variant for few rows (decode): one float4 per thread,
+// two barrier-reductions — short dependency chains on many SMs.
+template <class T>
+__global__ void layernorm_vec_kernel(const float* __restrict__ x, int64_t d, const float* __restrict__ g,
+                                     const float* __restrict__ b, T* __restrict__ y,
+                                     const int32_t* __restrict__ gather, const float* __restrict__ head,
+                                     float* __restrict__ head_out) {
+  PDL_ENTRY();
+  __shared__ float red[2][32];
+  const int64_t r = blockIdx.x;
+  const int64_t src = gather ? gather[r] : r;
+  const int j = threadIdx.x * 4;
+  const bool act = j < d;
+  float4 v = act ? *reinterpret_cast<const float4*>(x + src * d + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = (blockDim.x + 31) >> 5;
+  float s = warp_sum(v.x + v.y + v.z + v.w);
+  if (lane == 0) red[0][w] = s;
+  __syncthreads();
+  float mu = 0.f;
+  for (int k = 0; k < nw; ++k) mu += red[0][k];
+  mu /= float(d);
+  const float4 c = make_float4(v.x - mu, v.y - mu, v.z - mu, v.w - mu);
+  float q = act ? c.x * c.x + c.y * c.y + c.z * c.z + c.w * c.w : 0.f;
+  q = warp_sum(q);
+  if (lane == 0) red[1][w] = q;
+  __syncthreads();
+  float var = 0.f;
+  for (int k = 0; k < nw; ++k) var += red[1][k];
+  const float is = 1.0f / sqrtf(var / float(d) + 1e-5f);
+  if (act) {
+    const float4 gg = *reinterpret_cast<const float4*>(g + j), bb = *reinterpret_cast<const float4*>(b + j);
+    const float o0 = gg.x * (c.x * is) + bb.x, o1 = gg.y * (c.y * is) + bb.y, o2 = gg.z * (c.z * is) + bb.z,
+                o3 = gg.w * (c.w * is) + bb.w;
+    if (y) {
+      T* yr = y + r * d + j;
+      yr[0] = from_f<T>(o0);
+      yr[1] = from_f<T>(o1);
+      yr[2] = from_f<T>(o2);
+      yr[3] = from_f<T>(o3);
+    }
+    if (head) {
+      const float4 hh = *reinterpret_cast<const float4*>(head + j);
+      s = o0 * hh.x + o1 * hh.y + o2 * hh.z + o3 * hh.w;
+    }
+  } else {
+    s = 0.f;
+  }
+  if (head) {
+    __syncthreads();
+    s = warp_sum(s);
+    if (lane == 0) red[0][w] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      float t = 0.f;
+      for (int k = 0; k < nw; ++k) t += red[0][k];
+      head_out[r] = t;
+    }
+  }
+}
+
 template <class T>
 void launch_layernorm(Ctx& c, const float* x, int64_t rows, int64_t d, const float* g, const float* b, T* y,
                       const int32_t* gather, const float* head, float* head_out) {
   if (rows <= 0) return;
   if (d > 256 * 32) throw ContractError("layernorm: d_model above 8192 unsupported");
   c.launch("layernorm", double(rows) * d * (4 + (y ? sizeof(T) : 0)), 0, [&] {
-    layernorm_kernel<T><<<rows, 256, 0, c.stream>>>(x, rows, d, g, b, y, gather, head, head_out);
+    if (d % 4 == 0 && d <= 4096 && rows <= 1024) {
+      const int th = int((d / 4 + 31) / 32 * 32);
+      launch_kernel(c, layernorm_vec_kernel<T>, dim3(rows), dim3(th), 0, 1, x, d, g, b, y, gather, head, head_out);
+    } else if (d <= 1024)
+      launch_kernel(c, layernorm_warp_kernel<T>, dim3(ceil_div(rows, 8)), dim3(256), 0, 1, x, rows, d, g, b, y, gather, head, head_out);
+    else
+      launch_kernel(c, layernorm_kernel<T>, dim3(rows), dim3(256), 0, 1, x, rows, d, g, b, y, gather, head, head_out);
   });
 }
 
@@ -182,6 +299,7 @@ template <class T>
 __global__ void kv_scatter_kernel(const T* __restrict__ qkv, int64_t rows, int64_t d,
                                   const int32_t* __restrict__ seq_of_row, const int32_t* __restrict__ pos_of_row,
                                   const int32_t* __restrict__ block_table, int layer, KvGeom g, T* __restrict__ kv) {
+  PDL_ENTRY();
   const int64_t r = blockIdx.x;
   if (r >= rows) return;
   const int64_t s = seq_of_row[r], p = pos_of_row[r];
@@ -200,7 +318,7 @@ void launch_kv_scatter(Ctx& c, const T* qkv, int64_t rows, int64_t d, const int3
                        const int32_t* pos_of_row, const int32_t* block_table, int layer, const KvGeom& g, T* kv) {
   if (rows <= 0) return;
   c.launch("kv_scatter", double(rows) * 2 * d * sizeof(T) * 2, 0, [&] {
-    kv_scatter_kernel<T><<<rows, 256, 0, c.stream>>>(qkv, rows, d, seq_of_row, pos_of_row, block_table, layer, g,
+    launch_kernel(c, kv_scatter_kernel<T>, dim3(rows), dim3(256), 0, 1, qkv, rows, d, seq_of_row, pos_of_row, block_table, layer, g,
                                                      kv);
   });
 }
@@ -213,6 +331,7 @@ __device__ __forceinline__ float load_any(const void* p, int dt, int64_t i) {
 
 __global__ void convert_kernel(const void* src, int sdt, void* dst, int ddt, int64_t rows, int64_t cols,
                                bool transpose, int64_t dst_ld, int64_t dst_row0) {
+  PDL_ENTRY();
   const int64_t n = rows * cols;
   for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n; e += int64_t(gridDim.x) * blockDim.x) {
     // e indexes the destination in [dst_rows, dst_cols] order.
@@ -240,13 +359,14 @@ void launch_convert(Ctx& c, const void* src, int src_dtype, void* dst, int dst_d
   if (rows * cols <= 0) return;
   const int64_t blocks = std::min<int64_t>(ceil_div(rows * cols, 256), 148 * 16);
   c.launch("convert", 0, 0, [&] {
-    convert_kernel<<<blocks, 256, 0, c.stream>>>(src, src_dtype, dst, dst_dtype, rows, cols, transpose, dst_ld,
+    launch_kernel(c, convert_kernel, dim3(blocks), dim3(256), 0, 1, src, src_dtype, dst, dst_dtype, rows, cols, transpose, dst_ld,
                                                  dst_row0);
   });
 }
 
 __global__ void scripted_reward_kernel(int64_t B, int64_t stride, const int32_t* tokens, const int64_t* lengths,
                                        int32_t target, double* out) {
+  PDL_ENTRY();
   const int64_t b = blockIdx.x;
   if (b >= B) return;
   int n = 0;
@@ -260,11 +380,12 @@ void launch_scripted_reward(Ctx& c, int64_t B, int64_t stride, const int32_t* to
                             int32_t target, double* out) {
   if (B <= 0) return;
   c.launch("scripted_reward", 0, 0, [&] {
-    scripted_reward_kernel<<<B, 32, 0, c.stream>>>(B, stride, tokens, lengths, target, out);
+    launch_kernel(c, scripted_reward_kernel, dim3(B), dim3(32), 0, 1, B, stride, tokens, lengths, target, out);
   });
 }
 
 __global__ void f32_to_f64_kernel(const float* src, int64_t n, double* dst) {
+  PDL_ENTRY();
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
     dst[i] = double(src[i]);
 }
@@ -272,11 +393,12 @@ __global__ void f32_to_f64_kernel(const float* src, int64_t n, double* dst) {
 void launch_f32_to_f64(Ctx& c, const float* src, int64_t n, double* dst) {
   if (n <= 0) return;
   c.launch("convert", 12.0 * n, 0, [&] {
-    f32_to_f64_kernel<<<std::min<int64_t>(ceil_div(n, 256), 1184), 256, 0, c.stream>>>(src, n, dst);
+    launch_kernel(c, f32_to_f64_kernel, dim3(std::min<int64_t>(ceil_div(n, 256), 1184)), dim3(256), 0, 1, src, n, dst);
   });
 }
 
 __global__ void fill_i32_kernel(int32_t* dst, int64_t n, int32_t v) {
+  PDL_ENTRY();
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
     dst[i] = v;
 }
@@ -284,7 +406,7 @@ __global__ void fill_i32_kernel(int32_t* dst, int64_t n, int32_t v) {
 void launch_fill_i32(Ctx& c, int32_t* dst, int64_t n, int32_t v) {
   if (n <= 0) return;
   c.launch("fill", 4.0 * n, 0, [&] {
-    fill_i32_kernel<<<std::min<int64_t>(ceil_div(n, 256), 1184), 256, 0, c.stream>>>(dst, n, v);
+    launch_kernel(c, fill_i32_kernel, dim3(std::min<int64_t>(ceil_div(n, 256), 1184)), dim3(256), 0, 1, dst, n, v);
   });
 }
 

@@ -20,6 +20,7 @@ __global__ void __launch_bounds__(NTH) logprob_gather_kernel(const T* __restrict
                                                              int64_t V, const int32_t* __restrict__ target,
                                                              const int64_t* __restrict__ out_index,
                                                              double* __restrict__ out) {
+  PDL_ENTRY();
   constexpr int N = 16 / sizeof(T);
   constexpr float kLog2e = 1.4426950408889634f;
   __shared__ float sm_m[NTH / 32], sm_s[NTH / 32];
@@ -107,6 +108,7 @@ __global__ void shape_gae_kernel(int64_t B, int64_t stride, const int64_t* __res
                                  const double* __restrict__ ref, const double* __restrict__ values, double kl_coef,
                                  double gamma, double lam, double* __restrict__ shaped, double* __restrict__ adv,
                                  double* __restrict__ ret, double* __restrict__ part) {
+  PDL_ENTRY();
   const int64_t b = blockIdx.x;
   if (b >= B) return;
   const int lane = threadIdx.x;
@@ -160,6 +162,7 @@ __global__ void shape_gae_kernel(int64_t B, int64_t stride, const int64_t* __res
 
 // Fixed-order (deterministic) reduction of the per-sequence partials.
 __global__ void reduce_partials_kernel(int64_t B, const double* __restrict__ part, double* __restrict__ out5) {
+  PDL_ENTRY();
   __shared__ double sm[5][32];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;  // 5 warps, one per field
   if (w >= 5) return;
@@ -178,6 +181,7 @@ __global__ void reduce_partials_kernel(int64_t B, const double* __restrict__ par
 __global__ void whiten_apply_kernel(int64_t B, int64_t stride, const int64_t* __restrict__ lengths,
                                     const double* __restrict__ adv, const double* __restrict__ st,
                                     double* __restrict__ out) {
+  PDL_ENTRY();
   const double cnt = st[0] > 0 ? st[0] : 1.0;
   const double mean = st[1] / cnt;
   double var = st[2] / cnt - mean * mean;
@@ -195,7 +199,7 @@ void launch_logprob_gather(Ctx& c, const T* logits, int64_t ld, int64_t rows, in
   if (rows <= 0) return;
   if ((ld * sizeof(T)) % 16) throw ContractError("logprob_gather: row stride must be 16-byte aligned");
   c.launch("logprob_gather", double(rows) * V * sizeof(T) + rows * 20.0, 0, [&] {
-    logprob_gather_kernel<T, 256><<<rows, 256, 0, c.stream>>>(logits, ld, rows, V, target, out_index, out);
+    launch_kernel(c, logprob_gather_kernel<T, 256>, dim3(rows), dim3(256), 0, 1, logits, ld, rows, V, target, out_index, out);
   });
 }
 
@@ -204,21 +208,21 @@ void launch_shape_gae(Ctx& c, int64_t B, int64_t stride, const int64_t* lengths,
                       double gamma, double lam, double* shaped, double* adv, double* ret, double* part) {
   if (B <= 0) return;
   c.launch("shape_gae", double(B) * stride * 8 * 7, 0, [&] {
-    shape_gae_kernel<<<B, 32, 0, c.stream>>>(B, stride, lengths, rm_reward, actor_lp, ref_lp, values, kl_coef, gamma,
+    launch_kernel(c, shape_gae_kernel, dim3(B), dim3(32), 0, 1, B, stride, lengths, rm_reward, actor_lp, ref_lp, values, kl_coef, gamma,
                                              lam, shaped, adv, ret, part);
   });
 }
 
 void launch_reduce_partials(Ctx& c, int64_t B, const double* part, double* out5) {
   c.launch("reduce_partials", double(B) * 40, 0,
-           [&] { reduce_partials_kernel<<<1, 160, 0, c.stream>>>(B, part, out5); });
+           [&] { launch_kernel(c, reduce_partials_kernel, dim3(1), dim3(160), 0, 1, B, part, out5); });
 }
 
 void launch_whiten_apply(Ctx& c, int64_t B, int64_t stride, const int64_t* lengths, const double* adv,
                          const double* stats3, double* out) {
   if (B <= 0) return;
   c.launch("whiten", double(B) * stride * 16, 0,
-           [&] { whiten_apply_kernel<<<B, 128, 0, c.stream>>>(B, stride, lengths, adv, stats3, out); });
+           [&] { launch_kernel(c, whiten_apply_kernel, dim3(B), dim3(128), 0, 1, B, stride, lengths, adv, stats3, out); });
 }
 
 template void launch_logprob_gather<float>(Ctx&, const float*, int64_t, int64_t, int64_t, const int32_t*,

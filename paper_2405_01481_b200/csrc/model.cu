@@ -276,6 +276,7 @@ void score_head(Model& m, const float* x, const int32_t* gather, const int64_t* 
 
 // ------------------------------------------------------------------ helpers
 __global__ void scatter_f32_f64_kernel(const float* src, const int64_t* index, int64_t n, double* dst) {
+  PDL_ENTRY();
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
     dst[index ? index[i] : i] = double(src[i]);
 }
@@ -283,7 +284,7 @@ __global__ void scatter_f32_f64_kernel(const float* src, const int64_t* index, i
 void launch_scatter_f32_f64(Ctx& c, const float* src, const int64_t* index, int64_t n, double* dst) {
   if (n <= 0) return;
   c.launch("convert", 20.0 * n, 0, [&] {
-    scatter_f32_f64_kernel<<<std::min<int64_t>(ceil_div(n, 256), 1184), 256, 0, c.stream>>>(src, index, n, dst);
+    launch_kernel(c, scatter_f32_f64_kernel, dim3(std::min<int64_t>(ceil_div(n, 256), 1184)), dim3(256), 0, 1, src, index, n, dst);
   });
 }
 
@@ -293,6 +294,7 @@ __global__ void response_meta_kernel(int64_t B, const int64_t* offsets_full, con
                                      const int64_t* resp_len, int64_t stride, const int32_t* tokens_full,
                                      int32_t* gather, int32_t* target, int64_t* out_index,
                                      const int64_t* resp_offsets) {
+  PDL_ENTRY();
   const int64_t b = blockIdx.x;
   const int64_t n = resp_len[b], P = prompt_len[b], o = offsets_full[b], ro = resp_offsets[b];
   for (int64_t t = threadIdx.x; t < n; t += blockDim.x) {
@@ -307,7 +309,7 @@ void launch_response_meta(Ctx& c, int64_t B, const int64_t* offsets_full, const 
                           int32_t* target, int64_t* out_index, const int64_t* resp_offsets) {
   if (B <= 0) return;
   c.launch("meta", 0, 0, [&] {
-    response_meta_kernel<<<B, 128, 0, c.stream>>>(B, offsets_full, prompt_len, resp_len, stride, tokens_full, gather,
+    launch_kernel(c, response_meta_kernel, dim3(B), dim3(128), 0, 1, B, offsets_full, prompt_len, resp_len, stride, tokens_full, gather,
                                                    target, out_index, resp_offsets);
   });
 }
@@ -315,6 +317,7 @@ void launch_response_meta(Ctx& c, int64_t B, const int64_t* offsets_full, const 
 __global__ void concat_pack_kernel(int64_t B, const int32_t* prompts, const int64_t* p_offsets, const int32_t* gen,
                                    int64_t gstride, const int64_t* gen_len, const int64_t* full_offsets,
                                    int32_t* full) {
+  PDL_ENTRY();
   const int64_t b = blockIdx.x;
   const int64_t P = p_offsets[b + 1] - p_offsets[b], n = gen_len[b], o = full_offsets[b];
   for (int64_t t = threadIdx.x; t < P + n; t += blockDim.x)
@@ -325,7 +328,7 @@ void launch_concat_pack(Ctx& c, int64_t B, const int32_t* prompts, const int64_t
                         int64_t gstride, const int64_t* gen_len, const int64_t* full_offsets, int32_t* full) {
   if (B <= 0) return;
   c.launch("pack", 0, 0, [&] {
-    concat_pack_kernel<<<B, 256, 0, c.stream>>>(B, prompts, p_offsets, gen, gstride, gen_len, full_offsets, full);
+    launch_kernel(c, concat_pack_kernel, dim3(B), dim3(256), 0, 1, B, prompts, p_offsets, gen, gstride, gen_len, full_offsets, full);
   });
 }
 

@@ -9,6 +9,7 @@
 #include <memory>
 #include <mutex>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "common.cuh"
@@ -114,6 +115,33 @@ struct Ctx {
   void* pinned_staging(size_t bytes);
   void sync() { PPOEXP_CUDA(cudaStreamSynchronize(stream)); }
 };
+
+// Launch with programmatic stream serialization (PDL) and an optional
+// cluster along y.  Every kernel in the library calls pdl_wait() before it
+// touches data produced by earlier work, so the attribute is always safe.
+template <class... KArgs, class... Args>
+void launch_kernel(Ctx& c, void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, int cluster_y, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = c.stream;
+  cudaLaunchAttribute at[2];
+  int n = 0;
+  at[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[n].val.programmaticStreamSerializationAllowed = 1;
+  ++n;
+  if (cluster_y > 1) {
+    at[n].id = cudaLaunchAttributeClusterDimension;
+    at[n].val.clusterDim.x = 1;
+    at[n].val.clusterDim.y = cluster_y;
+    at[n].val.clusterDim.z = 1;
+    ++n;
+  }
+  cfg.attrs = at;
+  cfg.numAttrs = n;
+  PPOEXP_CUDA(cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...));
+}
 
 // Copy helpers that honour ppoexp_where (0 = host, 1 = device).
 void copy_in(Ctx& c, void* dst_dev, const void* src, size_t bytes, int where);

@@ -5,15 +5,18 @@
 //   greedy : argmax, first index wins on ties (argmax_index, :428-434)
 //   sampled: q_j = exp((l_j - max)/max(tau,1e-12)); u = uniform()*sum(q);
 //            first j with u < cumsum_j (index order), fallback V-1 (:455-473)
-// North-star extension (oracle/ppoexp_oracle.c orc_filter_topk_topp): top-k
-// then top-p filtering of q before the inverse CDF; with k = 0 and p >= 1 the
-// kernel is exactly the reference sampler.
+// North-star extension (convention in oracle/ppoexp_oracle.c,
+// orc_filter_topk_topp): top-k then top-p over q sorted by (q desc, index
+// asc); the inverse CDF then runs in index order over the kept tokens.  With
+// k = 0 and p >= 1 this is exactly the reference sampler.
 //
-// One 1024-thread CTA per sequence.  Thresholds for top-k / top-p come from a
-// 4-pass radix select over the fp32 bit patterns of q (positive floats sort
-// like their bits), with 256-bin (count, fp64 sum) histograms in smem; the
-// inverse CDF runs over warp-contiguous index ranges with warp shuffles, so
-// every pass reads the row coalesced.
+// One 1024-thread CTA per sequence.  Sampled rows cache q in shared memory
+// (V <= 52k) so every pass after the first is on-chip.  Thresholds: a
+// 1024-bucket histogram keyed by the fp32 bit pattern of q (monotone in q and
+// log-spaced, so flat and peaked rows both spread), a block scan to find the
+// crossing bucket, and an exact (q desc, index asc) bitonic sort of that
+// bucket alone.  The kept set is {q > t} ∪ {q == t, index <= cut}.  The
+// inverse CDF runs over warp-contiguous index ranges with warp scans.
 #include <cfloat>
 
 #include "kernels.hpp"
@@ -21,109 +24,124 @@
 namespace ppoexp {
 
 namespace {
-constexpr int NT = 1024, NW = NT / 32;
+constexpr int NT = 1024, NW = NT / 32, NB = 1024, LIST = 1024;
+constexpr int64_t kCacheMaxV = 52000;
 
 struct Shared {
-  float fm[NW];
+  unsigned hcnt[NB];
+  float hsum[NB];
+  unsigned long long list[LIST];
+  float fm[NW], fmn[NW], fs[NW];
   int fi[NW];
-  float fs[NW];
   double dsum[NW];
-  int icount[NW];
-  unsigned cnt[256];
-  double hs[256];
-  double zsum;
-  unsigned prefix, mask;
-  double s_above;
-  unsigned c_above;
-  int chosen_bin;
+  unsigned uwarp[NW + 1];
+  double dwarp[NW + 1];
+  int lk[NW];
+  int list_n;
   int result;
+  // selection state
+  int bk, bp;
+  unsigned c_above;
+  double s_above, zk, zk_bucket;
+  unsigned t_final;
+  int idx_cut;
+  int overflow;
 };
 
-__device__ __forceinline__ float qval(const float* row, int64_t j, float M, float inv_tau) {
-  return expf((row[j] - M) * inv_tau);
+__device__ __forceinline__ unsigned qbits_of(float q) { return __float_as_uint(q); }
+
+// bucket 0 = largest q (bits of 1.0), NB-1 = smallest.  scale = NB / span;
+// every step (int->float, multiply by a positive constant, truncation) is
+// monotone, so equal q map to equal buckets and larger q to lower buckets.
+__device__ __forceinline__ int bucket_of(unsigned bits, unsigned top, float scale) {
+  const int b = int(float(top - bits) * scale);  // bits <= top
+  return b >= NB ? NB - 1 : b;
 }
 
-// mode 0: select by count (top-k: want k), mode 1: select by sum (top-p: want target).
-// On exit: sh.prefix = threshold bits t; sh.c_above = #(q > t); sh.s_above = sum(q > t);
-// returns #(q == t) via sh.cnt[chosen_bin] of the last pass.
-__device__ void radix_select(const float* row, int64_t V, float M, float inv_tau, int mode, double want, Shared& sh,
-                             unsigned& eq_count) {
-  const int tid = threadIdx.x;
-  if (tid == 0) {
-    sh.prefix = 0;
-    sh.mask = 0;
-    sh.s_above = 0.0;
-    sh.c_above = 0;
+template <class T>
+__device__ T block_excl_scan(T v, T* wtot, T& total) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  T inc = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const T t = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += t;
+  }
+  if (lane == 31) wtot[w] = inc;
+  __syncthreads();
+  if (w == 0) {
+    T x = wtot[lane];
+    T xi = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const T t = __shfl_up_sync(0xffffffffu, xi, o);
+      if (lane >= o) xi += t;
+    }
+    wtot[lane] = xi - x;  // exclusive warp prefix
+    if (lane == 31) wtot[NW] = xi;
   }
   __syncthreads();
-  for (int pass = 0; pass < 4; ++pass) {
-    const int shift = 24 - 8 * pass;
-    for (int i = tid; i < 256; i += NT) {
-      sh.cnt[i] = 0;
-      sh.hs[i] = 0.0;
-    }
-    __syncthreads();
-    const unsigned prefix = sh.prefix, mask = sh.mask;
-    for (int64_t j = tid; j < V; j += NT) {
-      const float q = qval(row, j, M, inv_tau);
-      const unsigned bits = __float_as_uint(q);
-      if ((bits & mask) == prefix) {
-        const int bin = (bits >> shift) & 255;
-        atomicAdd(&sh.cnt[bin], 1u);
-        if (mode == 1) atomicAdd(&sh.hs[bin], double(q));
-      }
-    }
-    __syncthreads();
-    if (tid == 0) {
-      // Walk bins from the largest q down; stop at the first bin whose
-      // inclusion reaches `want`.  c_above / s_above exclude the chosen bin.
-      unsigned ca = sh.c_above;
-      double sa = sh.s_above;
-      int chosen = -1, lowest = -1;
-      for (int bin = 255; bin >= 0; --bin) {
-        if (sh.cnt[bin] == 0) continue;
-        lowest = bin;
-        const bool hit = mode == 0 ? double(ca + sh.cnt[bin]) >= want : sa + sh.hs[bin] >= want;
-        if (hit) {
-          chosen = bin;
-          break;
+  const T res = wtot[w] + inc - v;
+  total = wtot[NW];
+  __syncthreads();
+  return res;
+}
+
+__device__ double block_sum_d(double v, Shared& sh) {
+  v = warp_sum_d(v);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) sh.dsum[w] = v;
+  __syncthreads();
+  double t = 0.0;
+  for (int k = 0; k < NW; ++k) t += sh.dsum[k];  // fixed order
+  __syncthreads();
+  return t;
+}
+
+// sort a[0..n) ascending (padded to a power of two with ~0 keys)
+__device__ void bitonic_sort(unsigned long long* a, int n) {
+  int m = 1;
+  while (m < n) m <<= 1;
+  for (int i = n + threadIdx.x; i < m; i += NT) a[i] = ~0ull;
+  __syncthreads();
+  for (int k = 2; k <= m; k <<= 1)
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < m; i += NT) {
+        const int l = i ^ j;
+        if (l > i) {
+          const bool up = (i & k) == 0;
+          const unsigned long long x = a[i], y = a[l];
+          if ((x > y) == up) {
+            a[i] = y;
+            a[l] = x;
+          }
         }
-        ca += sh.cnt[bin];
-        sa += sh.hs[bin];
       }
-      if (chosen < 0) {  // rounding: nothing reached `want`; keep down to the lowest bin
-        chosen = lowest < 0 ? 0 : lowest;
-        ca -= sh.cnt[chosen];
-        sa -= sh.hs[chosen];
-      }
-      sh.chosen_bin = chosen;
-      sh.c_above = ca;
-      sh.s_above = sa;
-      sh.prefix = prefix | (unsigned(chosen) << shift);
-      sh.mask = mask | (255u << shift);
+      __syncthreads();
     }
-    __syncthreads();
-  }
-  eq_count = sh.cnt[sh.chosen_bin];
-  __syncthreads();
 }
 
+// key = (q desc, index asc) ascending
+__device__ __forceinline__ unsigned long long sort_key(unsigned qb, int idx) {
+  return ((unsigned long long)(~qb) << 32) | unsigned(idx);
+}
+__device__ __forceinline__ float key_q(unsigned long long e) { return __uint_as_float(~unsigned(e >> 32)); }
+
+template <bool CACHED>
 __global__ void __launch_bounds__(NT) sampler_kernel(const float* __restrict__ logits, int64_t ld, int64_t V,
                                                      SamplerState s) {
+  PDL_ENTRY();
+  extern __shared__ float qcache[];  // CACHED: q[V]
   __shared__ Shared sh;
   const int64_t b = blockIdx.x;
-  const SampleParams prm = s.params[b];
-  const int greedy = prm.greedy;
-  const float temperature = prm.temperature;
-  const int64_t top_k = prm.top_k;
-  const double top_p = prm.top_p;
   if (s.done[b]) return;
+  const SampleParams prm = s.params[b];
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
   const float* row = logits + b * ld;
   const int i = s.n_gen[b];
 
-  // pass 1: max, first argmax, online sum of exp(l - max)
-  float m = -INFINITY, se = 0.f;
+  // ---- pass 1: max, min, first argmax, online sum exp(l - max)
+  float m = -INFINITY, mn = INFINITY, se = 0.f;
   int am = 0x7fffffff;
   for (int64_t j = tid; j < V; j += NT) {
     const float v = row[j];
@@ -134,144 +152,273 @@ __global__ void __launch_bounds__(NT) sampler_kernel(const float* __restrict__ l
     } else {
       se += expf(v - m);
     }
+    mn = fminf(mn, v);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     const float m2 = __shfl_xor_sync(0xffffffffu, m, o);
     const int a2 = __shfl_xor_sync(0xffffffffu, am, o);
     const float s2 = __shfl_xor_sync(0xffffffffu, se, o);
-    const float M = fmaxf(m, m2);
-    const float sc = (m == -INFINITY ? 0.f : se * expf(m - M)) + (m2 == -INFINITY ? 0.f : s2 * expf(m2 - M));
+    mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    const float Mx = fmaxf(m, m2);
+    const float sc = (m == -INFINITY ? 0.f : se * expf(m - Mx)) + (m2 == -INFINITY ? 0.f : s2 * expf(m2 - Mx));
     am = m > m2 ? am : (m2 > m ? a2 : min(am, a2));
-    m = M;
+    m = Mx;
     se = sc;
   }
   if (lane == 0) {
     sh.fm[w] = m;
     sh.fi[w] = am;
     sh.fs[w] = se;
+    sh.fmn[w] = mn;
   }
   __syncthreads();
-  float M = sh.fm[0];
+  float M = sh.fm[0], MN = sh.fmn[0];
   int AM = sh.fi[0];
   for (int k = 1; k < NW; ++k) {
     if (sh.fm[k] > M || (sh.fm[k] == M && sh.fi[k] < AM)) AM = sh.fm[k] > M ? sh.fi[k] : min(AM, sh.fi[k]);
     M = fmaxf(M, sh.fm[k]);
+    MN = fminf(MN, sh.fmn[k]);
   }
   float SE = 0.f;
   for (int k = 0; k < NW; ++k) SE += sh.fm[k] == -INFINITY ? 0.f : sh.fs[k] * expf(sh.fm[k] - M);
   const float lse = M + logf(SE);
 
   int chosen = AM;
-  if (!greedy) {
-    const float tau = fmaxf(temperature, 1e-12f);
+  if (!prm.greedy) {
+    const float tau = fmaxf(prm.temperature, 1e-12f);
     const float inv_tau = 1.0f / tau;
-    const bool filt_k = top_k > 0 && top_k < V;
-    const bool filt_p = top_p < 1.0;
-    // kept(j): q > t_final, or q == t_final and tie-rank(j) < c_final
-    unsigned t_final = 0;      // bits; 0 with c_final = ~0 keeps everything
-    unsigned c_final = 0xffffffffu;
-    bool filtering = filt_k || filt_p;
-    if (filtering) {
-      unsigned eq = 0, tk = 0, ck = 0xffffffffu;
-      double zk = 0.0;
-      if (filt_k) {
-        radix_select(row, V, M, inv_tau, 0, double(top_k), sh, eq);
-        tk = sh.prefix;
-        ck = unsigned(top_k) - sh.c_above;
-        zk = sh.s_above + double(ck) * double(__uint_as_float(tk));
-        // s_above for mode 0 was not accumulated; recompute sum(q > tk) directly
-        double part = 0.0;
-        for (int64_t j = tid; j < V; j += NT) {
-          const float q = qval(row, j, M, inv_tau);
-          if (__float_as_uint(q) > tk) part += double(q);
-        }
-        part = warp_sum_d(part);
-        if (lane == 0) sh.dsum[w] = part;
-        __syncthreads();
-        double sa = 0.0;
-        for (int k = 0; k < NW; ++k) sa += sh.dsum[k];
-        __syncthreads();
-        zk = sa + double(ck) * double(__uint_as_float(tk));
-        t_final = tk;
-        c_final = ck;
+    const bool filt_k = prm.top_k > 0 && prm.top_k < V;
+    const bool filt_p = prm.top_p < 1.0;
+    const bool filtering = filt_k || filt_p;
+    auto Q = [&](int64_t j) -> float {
+      if constexpr (CACHED) return qcache[j];
+      else return expf((row[j] - M) * inv_tau);
+    };
+    // bucket span: bits(1.0) .. bits(q_min); q is monotone in the logit
+    const unsigned top = qbits_of(1.0f);
+    const unsigned botb = qbits_of(expf((MN - M) * inv_tau));
+    const float span = float(top - botb) + 1.0f;
+    const float scale = float(NB) / span;
+    // ---- pass 2: q (cached), histogram
+    if (filtering)
+      for (int k = tid; k < NB; k += NT) {
+        sh.hcnt[k] = 0;
+        sh.hsum[k] = 0.f;
       }
-      if (filt_p) {
-        if (!filt_k) {
-          double part = 0.0;
-          for (int64_t j = tid; j < V; j += NT) part += double(qval(row, j, M, inv_tau));
-          part = warp_sum_d(part);
-          if (lane == 0) sh.dsum[w] = part;
-          __syncthreads();
-          zk = 0.0;
-          for (int k = 0; k < NW; ++k) zk += sh.dsum[k];
-          __syncthreads();
-        }
-        const double target = top_p * zk;
-        radix_select(row, V, M, inv_tau, 1, target, sh, eq);
-        unsigned tp = sh.prefix;
-        const double tq = double(__uint_as_float(tp));
-        double need = tq > 0.0 ? ceil((target - sh.s_above) / tq) : double(eq);
-        if (need < 1.0) need = 1.0;
-        if (need > double(eq)) need = double(eq);
-        unsigned cp = unsigned(need);
-        if (filt_k) {
-          if (tp < tk) {
-            tp = tk;
-            cp = ck;
-          } else if (tp == tk) {
-            cp = min(cp, ck);
+    __syncthreads();
+    double zloc = 0.0;
+    for (int64_t j = tid; j < V; j += NT) {
+      const float q = expf((row[j] - M) * inv_tau);
+      if constexpr (CACHED) qcache[j] = q;
+      if (filtering) {
+        zloc += double(q);
+        const int bk = bucket_of(qbits_of(q), top, scale);
+        atomicAdd(&sh.hcnt[bk], 1u);
+        atomicAdd(&sh.hsum[bk], q);
+      }
+    }
+    __syncthreads();
+    unsigned t_final = 0;
+    int idx_cut = int(V);  // keep everything
+    if (filtering) {
+      const double Z = block_sum_d(zloc, sh);
+      if (tid == 0) {
+        sh.overflow = 0;
+        sh.bk = NB;  // top-k bucket (NB = no top-k)
+        sh.zk = Z;
+        sh.zk_bucket = 0.0;
+      }
+      __syncthreads();
+      // collect the members of bucket `bkt` into sh.list and sort them
+      auto collect_sort = [&](int bkt) {
+        if (tid == 0) sh.list_n = 0;
+        __syncthreads();
+        for (int64_t j = tid; j < V; j += NT) {
+          const unsigned qb = qbits_of(Q(j));
+          if (bucket_of(qb, top, scale) == bkt) {
+            const int slot = atomicAdd(&sh.list_n, 1);
+            if (slot < LIST) sh.list[slot] = sort_key(qb, int(j));
           }
         }
-        t_final = tp;
-        c_final = cp;
-      }
-    }
-    // ---- inverse CDF over warp-contiguous ranges
-    const int64_t CW = ((V + NW - 1) / NW + 31) / 32 * 32;  // elements per warp, multiple of 32
-    const int64_t w0 = int64_t(w) * CW, w1 = (V < w0 + CW ? V : w0 + CW);
-    // tie counts per warp (only needed when ties are partially kept)
-    int tie_base = 0;
-    if (filtering) {
-      int ties = 0;
-      for (int64_t j = w0 + lane; j < w1; j += 32)
-        ties += __float_as_uint(qval(row, j, M, inv_tau)) == t_final;
-      ties = __reduce_add_sync(0xffffffffu, ties);
-      if (lane == 0) sh.icount[w] = ties;
-      __syncthreads();
-      for (int k = 0; k < w; ++k) tie_base += sh.icount[k];
-    }
-    auto kept_step = [&](int64_t j, int& tie_run, float& q) -> bool {
-      // all 32 lanes call this together for j = base + lane
-      q = j < w1 ? qval(row, j, M, inv_tau) : 0.f;
-      if (!filtering) return j < w1;
-      const unsigned bits = __float_as_uint(q);
-      const bool tie = j < w1 && bits == t_final;
-      const unsigned tb = __ballot_sync(0xffffffffu, tie);
-      const int rank = tie_run + __popc(tb & ((1u << lane) - 1u));
-      tie_run += __popc(tb);
-      return j < w1 && (bits > t_final || (tie && unsigned(rank) < c_final));
-    };
-    double wsum = 0.0;
-    int last_kept = -1;
-    {
-      int tie_run = tie_base;
-      for (int64_t base = w0; base < w1; base += 32) {
-        float q;
-        const bool k = kept_step(base + lane, tie_run, q);
-        if (k) {
-          wsum += double(q);
-          last_kept = int(base + lane);
+        __syncthreads();
+        const int n = sh.list_n;
+        if (n > LIST) {
+          if (tid == 0) sh.overflow = 1;
+          __syncthreads();
+          return;
         }
+        bitonic_sort(sh.list, n);
+      };
+      unsigned k_t = 0;
+      int k_cut = int(V), k_take = 0;
+      if (filt_k) {
+        const unsigned c = sh.hcnt[tid];
+        unsigned tot;
+        const unsigned ex = block_excl_scan<unsigned>(c, sh.uwarp, tot);
+        if (c > 0 && ex < unsigned(prm.top_k) && unsigned(prm.top_k) <= ex + c) {
+          sh.bk = tid;
+          sh.c_above = ex;
+        }
+        double dtot;
+        const double sex = block_excl_scan<double>(double(sh.hsum[tid]), sh.dwarp, dtot);
+        if (tid == sh.bk) sh.s_above = sex;
+        __syncthreads();
+        collect_sort(sh.bk);
+        if (!sh.overflow) {
+          k_take = int(unsigned(prm.top_k) - sh.c_above);
+          if (tid == 0) {
+            double zb = 0.0;
+            for (int r = 0; r < k_take; ++r) zb += double(key_q(sh.list[r]));
+            sh.zk_bucket = zb;
+            sh.zk = sh.s_above + zb;
+            const unsigned long long e = sh.list[k_take - 1];
+            sh.t_final = ~unsigned(e >> 32);
+            sh.idx_cut = int(e & 0xffffffffu);
+          }
+          __syncthreads();
+          k_t = sh.t_final;
+          k_cut = sh.idx_cut;
+        }
+      }
+      if (!sh.overflow && filt_p) {
+        const double target = prm.top_p * sh.zk;
+        const int bk = sh.bk;
+        // effective bucket sums: beyond the top-k bucket nothing is kept
+        const double hs = tid < bk ? double(sh.hsum[tid]) : (tid == bk ? sh.zk_bucket : 0.0);
+        double dtot;
+        const double ex = block_excl_scan<double>(hs, sh.dwarp, dtot);
+        if (tid == 0) sh.bp = -1;
+        __syncthreads();
+        if (hs > 0.0 && ex < target && target <= ex + hs) sh.bp = tid;
+        __syncthreads();
+        if (sh.bp < 0) {  // rounding: the crossing is the last kept bucket
+          if (hs > 0.0) atomicMax(&sh.bp, tid);
+          __syncthreads();
+        }
+        const int bp = sh.bp;
+        if (tid == bp) sh.s_above = ex;
+        __syncthreads();
+        if (bp != bk) collect_sort(bp);  // bp == bk reuses the top-k sorted list
+        if (!sh.overflow && tid == 0) {
+          const int limit = bp == bk ? k_take : min(sh.list_n, LIST);
+          double acc = sh.s_above;
+          int r = 0;
+          for (; r < limit; ++r) {
+            acc += double(key_q(sh.list[r]));
+            if (acc >= target) break;
+          }
+          if (r >= limit) r = limit - 1;
+          const unsigned long long e = sh.list[r];
+          sh.t_final = ~unsigned(e >> 32);
+          sh.idx_cut = int(e & 0xffffffffu);
+        }
+        __syncthreads();
+        k_t = sh.t_final;
+        k_cut = sh.idx_cut;
+      }
+      if (sh.overflow) {
+        // exact but slow path (a crossing bucket with > LIST members, i.e.
+        // massive ties): binary search on the threshold bits with block
+        // reductions, ties resolved by index.
+        unsigned tk = botb;
+        int cutk = int(V);
+        if (filt_k) {
+          unsigned lo = botb, hi = top;
+          while (lo < hi) {
+            const unsigned mid = lo + (hi - lo + 1) / 2;
+            double c = 0;
+            for (int64_t j = tid; j < V; j += NT) c += qbits_of(Q(j)) >= mid;
+            c = block_sum_d(c, sh);
+            if (c >= double(prm.top_k)) lo = mid; else hi = mid - 1;
+          }
+          tk = lo;
+          double above = 0;
+          for (int64_t j = tid; j < V; j += NT) above += qbits_of(Q(j)) > tk;
+          above = block_sum_d(above, sh);
+          const int need = int(prm.top_k - int64_t(above));
+          if (tid == 0) {
+            int cnt = 0;
+            for (int64_t j = 0; j < V; ++j)
+              if (qbits_of(Q(j)) == tk && ++cnt == need) {
+                sh.idx_cut = int(j);
+                break;
+              }
+          }
+          __syncthreads();
+          cutk = sh.idx_cut;
+        }
+        auto keptk = [&](int64_t j) {
+          const unsigned qb = qbits_of(Q(j));
+          return !filt_k || qb > tk || (qb == tk && j <= cutk);
+        };
+        double zk = 0;
+        for (int64_t j = tid; j < V; j += NT)
+          if (keptk(j)) zk += double(Q(j));
+        zk = block_sum_d(zk, sh);
+        unsigned tp = tk;
+        int cutp = cutk;
+        if (filt_p) {
+          const double target = prm.top_p * zk;
+          unsigned lo = tk, hi = top;
+          while (lo < hi) {
+            const unsigned mid = lo + (hi - lo + 1) / 2;
+            double sacc = 0;
+            for (int64_t j = tid; j < V; j += NT)
+              if (keptk(j) && qbits_of(Q(j)) >= mid) sacc += double(Q(j));
+            sacc = block_sum_d(sacc, sh);
+            if (sacc >= target) lo = mid; else hi = mid - 1;
+          }
+          tp = lo;
+          double above = 0;
+          for (int64_t j = tid; j < V; j += NT)
+            if (keptk(j) && qbits_of(Q(j)) > tp) above += double(Q(j));
+          above = block_sum_d(above, sh);
+          if (tid == 0) {
+            double acc = above;
+            int cut = -1;
+            for (int64_t j = 0; j < V; ++j)
+              if (keptk(j) && qbits_of(Q(j)) == tp) {
+                acc += double(Q(j));
+                cut = int(j);
+                if (acc >= target) break;
+              }
+            sh.idx_cut = cut;
+          }
+          __syncthreads();
+          cutp = sh.idx_cut;
+        }
+        k_t = tp;
+        k_cut = cutp;
+        __syncthreads();
+      }
+      t_final = k_t;
+      idx_cut = k_cut;
+    }
+    // ---- inverse CDF in index order over the kept tokens
+    auto kept = [&](int64_t j, float& q) -> bool {
+      q = Q(j);
+      if (!filtering) return true;
+      const unsigned qb = qbits_of(q);
+      return qb > t_final || (qb == t_final && j <= idx_cut);
+    };
+    const int64_t CW = ((V + NW - 1) / NW + 31) / 32 * 32;
+    const int64_t w0 = int64_t(w) * CW, w1 = (V < w0 + CW ? V : w0 + CW);
+    double wsum = 0.0;
+    int last = -1;
+    for (int64_t j = w0 + lane; j < w1; j += 32) {
+      float q;
+      if (kept(j, q)) {
+        wsum += double(q);
+        last = int(j);
       }
     }
     wsum = warp_sum_d(wsum);
-    int lk = last_kept;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) lk = max(lk, __shfl_xor_sync(0xffffffffu, lk, o));
+    for (int o = 16; o > 0; o >>= 1) last = max(last, __shfl_xor_sync(0xffffffffu, last, o));
     if (lane == 0) {
       sh.dsum[w] = wsum;
-      sh.fi[w] = lk;
+      sh.lk[w] = last;
     }
     if (tid == 0) sh.result = 0x7fffffff;
     __syncthreads();
@@ -280,26 +427,23 @@ __global__ void __launch_bounds__(NT) sampler_kernel(const float* __restrict__ l
     for (int k = 0; k < NW; ++k) {
       if (k < w) prefix += sh.dsum[k];
       total += sh.dsum[k];
-      fallback = max(fallback, sh.fi[k]);
+      fallback = max(fallback, sh.lk[k]);
     }
     const double u = s.uniforms[b * s.ustride + i];
     const double target = u * total;
-    // the crossing can only be in a warp whose [prefix, prefix + wsum] brackets target
     if (prefix <= target && target < prefix + sh.dsum[w] * (1.0 + 1e-12) + 1e-300) {
-      int tie_run = tie_base;
       double acc = prefix;
       for (int64_t base = w0; base < w1; base += 32) {
-        float q;
-        const bool k = kept_step(base + lane, tie_run, q);
-        // inclusive warp scan of kept q (index order)
+        const int64_t j = base + lane;
+        float q = 0.f;
+        const bool k = j < w1 && kept(j, q);
         double v = k ? double(q) : 0.0;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
           const double t = __shfl_up_sync(0xffffffffu, v, o);
           if (lane >= o) v += t;
         }
-        const double cum = acc + v;
-        const unsigned hit = __ballot_sync(0xffffffffu, k && target < cum);
+        const unsigned hit = __ballot_sync(0xffffffffu, k && target < acc + v);
         if (hit) {
           if (lane == 0) atomicMin(&sh.result, int(base + __ffs(hit) - 1));
           break;
@@ -326,7 +470,20 @@ __global__ void __launch_bounds__(NT) sampler_kernel(const float* __restrict__ l
 
 void launch_sampler(Ctx& c, const float* logits, int64_t ld, int64_t B, int64_t V, const SamplerState& s) {
   if (B <= 0) return;
-  c.launch("sampler", double(B) * V * 4, 0, [&] { sampler_kernel<<<B, NT, 0, c.stream>>>(logits, ld, V, s); });
+  if (V <= kCacheMaxV) {
+    const size_t smem = size_t(V) * sizeof(float);
+    static bool attr = false;
+    if (!attr) {
+      PPOEXP_CUDA(cudaFuncSetAttribute(sampler_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       int(kCacheMaxV * sizeof(float))));
+      attr = true;
+    }
+    c.launch("sampler", double(B) * V * 4, 0,
+             [&] { launch_kernel(c, sampler_kernel<true>, dim3(B), dim3(NT), smem, 1, logits, ld, V, s); });
+  } else {
+    c.launch("sampler", double(B) * V * 4, 0,
+             [&] { launch_kernel(c, sampler_kernel<false>, dim3(B), dim3(NT), 0, 1, logits, ld, V, s); });
+  }
 }
 
 }  // namespace ppoexp

@@ -1,0 +1,55 @@
+"""Kernel-level numerics against a plain PyTorch fp32 reference of the same op
+(GPU only): the tcgen05 GEMM (all epilogues, ragged M/N/K, decode-sized M)."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def glib():
+    from paper_2405_01481_b200 import ppoexp as px
+    L = px.lib()
+    f = L.ppoexp_testing_gemm_bf16
+    f.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_int64,
+                  C.c_int32, C.c_void_p, C.c_int64, C.c_int32]
+    f.restype = C.c_int32
+    return px, f
+
+
+SHAPES = [(64, 2304, 768), (64, 768, 3072), (300, 1000, 768), (2048, 50257, 768), (4096, 3072, 768), (128, 256, 64),
+          (17, 96, 16), (1024, 1024, 4096), (640, 768, 3072)]
+
+
+@pytest.mark.parametrize("M,N,K", SHAPES)
+@pytest.mark.parametrize("epi", [0, 1, 2, 3])
+@pytest.mark.parametrize("path", [0, 1])
+def test_gemm_vs_torch(glib, ctx, M, N, K, epi, path):
+    import torch
+    px, f = glib
+    if path == 1 and M * N * K > 2e10:
+        pytest.skip("SIMT path too slow for this size")
+    g = torch.Generator(device="cuda").manual_seed(M * 7 + N * 3 + K)
+    A = torch.randn(M, K, generator=g, device="cuda").to(torch.bfloat16)
+    B = (torch.randn(N, K, generator=g, device="cuda") * 0.05).to(torch.bfloat16)
+    ref = A.float() @ B.float().T
+    ldc = (N + 63) // 64 * 64
+    if epi in (0, 1):
+        Cm = torch.zeros(M, ldc, dtype=torch.bfloat16, device="cuda")
+    else:
+        Cm = torch.randn(M, ldc, generator=g, device="cuda") if epi == 2 else torch.zeros(M, ldc, device="cuda")
+    base = Cm.clone()
+    torch.cuda.synchronize()
+    px._check(f(ctx.h, A.data_ptr(), K, B.data_ptr(), K, M, N, K, epi, Cm.data_ptr(), ldc, path))
+    out = Cm[:, :N].float()
+    if epi == 1:
+        ref = torch.nn.functional.gelu(ref, approximate="tanh")
+    if epi == 2:
+        ref = ref + base[:, :N]
+    tol = 2e-2 if epi in (0, 1) else 2e-3
+    err = (out - ref).abs() - tol * (1 + ref.abs())
+    assert err.max().item() <= 0, f"max abs err {(out - ref).abs().max().item():.3e}"
+    if epi in (0, 1):  # untouched padding
+        assert torch.all(Cm[:, N:] == 0)

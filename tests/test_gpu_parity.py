@@ -288,3 +288,21 @@ def test_shape_gae_kernel_vs_oracle(px, ctx, oracle):
 
 def test_kernel_launches_counted(px, ctx):
     assert ctx.launch_count > 0
+
+
+@pytest.mark.parametrize("top_k,top_p", [(5, 1.0), (0, 0.3), (7, 0.5)])
+def test_sampler_massive_ties(px, ctx, oracle, top_k, top_p):
+    """All-equal logits (zero tok_embed): the crossing bucket holds the whole
+    vocabulary, exercising the exact tie path; ties resolve to lower indices."""
+    cfg = ModelCfg(2048, 32, 1, 2, 64, 32)
+    w = oracle.init_params(cfg, 3).astype(np.float32).astype(np.float64)
+    w[:cfg.V * cfg.d] = 0.0  # tied head → every logit is 0
+    eng = engine(px, ctx, cfg, w, px.F32)
+    seeds = [oracle.mix_seed(2, i) for i in range(4)]
+    prompts = [[1, 2, 3], [4], [5, 6], [7, 8, 9, 10]]
+    res = eng.generate_batch([px.GenTask(p, 6, px.SamplingSpec.temperature_spec(1.0, s, top_k, top_p))
+                              for p, s in zip(prompts, seeds)])
+    u = np.stack([oracle.uniforms(s, 6) for s in seeds])
+    t_o, _ = oracle.generate(cfg, w, prompts, 6, greedy=False, top_k=top_k, top_p=top_p, uniforms=u)
+    for r, t in zip(res, t_o):
+        assert np.array_equal(r.tokens, t)
