@@ -93,27 +93,33 @@ __global__ void __launch_bounds__(64 * (DH / 16)) attn_prefill_kernel(const T* _
 }
 
 // ---------------------------------------------------------------- decode
-// CTA per (sequence, head), 4 warps splitting the context into 32-token
-// tiles.  Q·K: lane-per-token (each lane streams whole K rows of its token
-// with 16-byte loads; LPT lanes per token when a row exceeds 128 bytes), no
-// per-token shuffles.  Online softmax per tile.  P·V: lane-per-dim with
-// coalesced V-row loads and the tile's probabilities broadcast by shuffle.
-// The four warps' (max, sum, acc) are merged through shared memory.
+// CTA per (sequence, head); each of the 4 warps streams its own 32-token
+// tiles of the paged K/V cache into shared memory with coalesced,
+// double-buffered cp.async (a tile never straddles a page: page_size % 32 == 0).
+// Q·K: lane-per-token dot products out of padded smem rows (no per-token
+// shuffles).  Online softmax per tile.  P·V: lane-per-dim with the tile's
+// probabilities broadcast by shuffle.  The warps' (max, sum, acc) are merged
+// through shared memory at the end.
+__device__ __forceinline__ void cp_async16_dec(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+               "l"(src)
+               : "memory");
+}
+
 template <class T, int DH>
 __global__ void __launch_bounds__(128) attn_decode_kernel(const T* __restrict__ qkv, const int32_t* __restrict__ pos,
                                                           const int32_t* __restrict__ done,
                                                           const int32_t* __restrict__ block_table, int layer,
                                                           KvGeom g, T* __restrict__ kv, T* __restrict__ out) {
   PDL_ENTRY();
-  constexpr int NW = 4;
-  constexpr int ROWB = DH * int(sizeof(T));          // bytes per K/V row
-  constexpr int LPT = ROWB > 128 ? ROWB / 128 : 1;   // lanes per token (Q·K)
-  constexpr int EPL = DH / LPT;                      // elements per lane (Q·K)
-  constexpr int TT = 32 / LPT;                       // tokens per tile
-  constexpr int NV = EPL * int(sizeof(T)) / 16;      // 16-byte vectors per lane
-  constexpr int VE = 16 / int(sizeof(T));            // elements per vector
-  constexpr int DPL = DH >= 32 ? DH / 32 : 1;        // dims per lane (P·V)
-  constexpr int DLANES = DH / DPL;                   // lanes holding dims
+  constexpr int NW = 4, TT = 32;
+  constexpr int ROWB = DH * int(sizeof(T));   // bytes per K/V row
+  constexpr int LDB = ROWB + 16;              // padded smem row (bytes)
+  constexpr int CPR = ROWB / 16;              // 16-byte chunks per row
+  constexpr int EPT = DH;                     // lane-per-token: whole row
+  constexpr int DPL = DH >= 32 ? DH / 32 : 1; // dims per lane (P·V)
+  constexpr int DLANES = DH / DPL;
+  extern __shared__ __align__(16) uint8_t smem_dec[];
   __shared__ float sm_m[NW], sm_l[NW];
   __shared__ float sm_acc[NW][DH];
   const int64_t b = blockIdx.y, h = blockIdx.x;
@@ -122,10 +128,9 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(const T* __restrict__ 
   const int64_t d = g.H * DH, PS = g.page_size;
   const T* row = qkv + b * 3 * d;
   const int32_t* bt = block_table + b * g.max_pages_per_seq;
-  const int64_t head_stride = PS * DH;
   auto base = [&](int64_t t, int which) -> T* {
     const int64_t page = bt[t / PS];
-    return kv + ((((int64_t)layer * g.n_pages + page) * 2 + which) * g.H + h) * head_stride + (t % PS) * DH;
+    return kv + ((((int64_t)layer * g.n_pages + page) * 2 + which) * g.H + h) * PS * DH + (t % PS) * DH;
   };
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
   // append this step's K/V row (KvSession::step, src/model.cpp:305-308)
@@ -134,42 +139,63 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(const T* __restrict__ 
     base(p, 1)[i] = row[2 * d + h * DH + i];
   }
   __syncthreads();  // the appended row is visible to the whole CTA
-  const int part = lane % LPT, tok = lane / LPT;
-  float q[EPL];
+  // per-warp double-buffered tiles: [buf][K|V][TT rows][LDB bytes]
+  uint8_t* wsm = smem_dec + size_t(w) * 2 * 2 * TT * LDB;
+  auto tile_ptr = [&](int buf, int which) { return wsm + (buf * 2 + which) * TT * LDB; };
+  auto issue = [&](int64_t t0, int buf) {
+    const int64_t n = (ctx - t0) < TT ? (ctx - t0) : TT;
+    const T* k0 = base(t0, 0);  // contiguous within the page
+    const T* v0 = base(t0, 1);
+    for (int e = lane; e < TT * CPR; e += 32) {
+      const int r = e / CPR, c = e % CPR;
+      if (r < n) {
+        cp_async16_dec(tile_ptr(buf, 0) + r * LDB + c * 16, reinterpret_cast<const uint8_t*>(k0) + r * ROWB + c * 16);
+        cp_async16_dec(tile_ptr(buf, 1) + r * LDB + c * 16, reinterpret_cast<const uint8_t*>(v0) + r * ROWB + c * 16);
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  float q[EPT];
 #pragma unroll
-  for (int i = 0; i < EPL; ++i) q[i] = to_f(row[h * DH + part * EPL + i]);
+  for (int i = 0; i < EPT; ++i) q[i] = to_f(row[h * DH + i]);
   const float inv_sqrt_dh = 1.0f / sqrtf(float(DH));
   float m = -FLT_MAX, l = 0.f, acc[DPL];
 #pragma unroll
   for (int i = 0; i < DPL; ++i) acc[i] = 0.f;
   const int dl = lane < DLANES ? lane : 0;
-  for (int64_t t0 = int64_t(w) * TT; t0 < ctx; t0 += int64_t(NW) * TT) {
-    // ---- scores for the tile
-    const int64_t t = t0 + tok;
-    float s = -FLT_MAX;
-    {
-      float dot = 0.f;
-      if (t < ctx) {
-        const uint4* kr = reinterpret_cast<const uint4*>(base(t, 0) + part * EPL);
-        Vec16<T> kv4[NV];
-#pragma unroll
-        for (int v = 0; v < NV; ++v) kv4[v].u = kr[v];
-#pragma unroll
-        for (int v = 0; v < NV; ++v)
-#pragma unroll
-          for (int e = 0; e < VE; ++e) dot = fmaf(to_f(kv4[v].v[e]), q[v * VE + e], dot);
-      }
-#pragma unroll
-      for (int o = LPT / 2; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
-      if (t < ctx) s = dot * inv_sqrt_dh;
+  int64_t t0 = int64_t(w) * TT;
+  int buf = 0;
+  if (t0 < ctx) issue(t0, 0);
+  for (; t0 < ctx; t0 += int64_t(NW) * TT, buf ^= 1) {
+    const int64_t tn = t0 + int64_t(NW) * TT;
+    if (tn < ctx) {
+      issue(tn, buf ^ 1);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
     }
-    // ---- online softmax over the tile
+    __syncwarp();
+    const int nt = int((ctx - t0) < TT ? (ctx - t0) : TT);
+    // ---- scores: lane = token
+    float s = -FLT_MAX;
+    if (lane < nt) {
+      const uint8_t* kr = tile_ptr(buf, 0) + lane * LDB;
+      float dot = 0.f;
+#pragma unroll
+      for (int c = 0; c < CPR; ++c) {
+        Vec16<T> v4;
+        v4.u = *reinterpret_cast<const uint4*>(kr + c * 16);
+#pragma unroll
+        for (int e = 0; e < Vec16<T>::N; ++e) dot = fmaf(to_f(v4.v[e]), q[c * Vec16<T>::N + e], dot);
+      }
+      s = dot * inv_sqrt_dh;
+    }
     float tm = s;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) tm = fmaxf(tm, __shfl_xor_sync(0xffffffffu, tm, o));
     const float mnew = fmaxf(m, tm);
     const float corr = m == -FLT_MAX ? 0.f : expf(m - mnew);
-    const float pr = t < ctx && part == 0 ? expf(s - mnew) : 0.f;
+    const float pr = lane < nt ? expf(s - mnew) : 0.f;
     float ps = pr;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) ps += __shfl_xor_sync(0xffffffffu, ps, o);
@@ -177,26 +203,15 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(const T* __restrict__ 
     m = mnew;
 #pragma unroll
     for (int i = 0; i < DPL; ++i) acc[i] *= corr;
-    // ---- P·V over the tile
-    const int nt = int((ctx - t0) < TT ? (ctx - t0) : TT);
-    constexpr int U = 8;
-    for (int j0 = 0; j0 < nt; j0 += U) {
-      T vv[U][DPL];
+    // ---- P·V: lane = dims
+    const uint8_t* vt = tile_ptr(buf, 1) + dl * DPL * int(sizeof(T));
+    for (int j = 0; j < nt; ++j) {
+      const float pj = __shfl_sync(0xffffffffu, pr, j);
+      const T* vr = reinterpret_cast<const T*>(vt + j * LDB);
 #pragma unroll
-      for (int u = 0; u < U; ++u)
-        if (j0 + u < nt) {
-          const T* vr = base(t0 + j0 + u, 1) + dl * DPL;
-#pragma unroll
-          for (int i = 0; i < DPL; ++i) vv[u][i] = vr[i];
-        }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const float pj = __shfl_sync(0xffffffffu, pr, ((j0 + u) & (TT - 1)) * LPT);
-        if (j0 + u < nt)
-#pragma unroll
-          for (int i = 0; i < DPL; ++i) acc[i] = fmaf(pj, to_f(vv[u][i]), acc[i]);
-      }
+      for (int i = 0; i < DPL; ++i) acc[i] = fmaf(pj, to_f(vr[i]), acc[i]);
     }
+    __syncwarp();  // this buffer is refilled two tiles from now
   }
   // ---- merge the warps
   if (lane == 0) {
@@ -239,19 +254,31 @@ void prefill_impl(Ctx& c, const T* qkv, const int64_t* seq_offsets, int64_t B, i
 template <class T, int DH>
 void decode_impl(Ctx& c, const T* qkv, int64_t B, const int32_t* pos, const int32_t* done, const int32_t* block_table,
                  int layer, const KvGeom& g, T* kv, T* out, double bytes) {
+  if (g.page_size % 32) throw ContractError("engine: page_size must be a multiple of 32");
   auto k = attn_decode_kernel<T, DH>;
+  const size_t smem = size_t(4) * 2 * 2 * 32 * (DH * sizeof(T) + 16);
+  static bool attr = false;
+  if (!attr) {
+    PPOEXP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    attr = true;
+  }
   dim3 grid(g.H, B);
-  c.launch("decode_attention", bytes, 0, [&] {
-    launch_kernel(c, k, dim3(grid), dim3(128), 0, 1, qkv, pos, done, block_table, layer, g, kv, out);
-  });
+  c.launch("decode_attention", bytes, 0, [&] { launch_kernel(c, k, grid, dim3(128), smem, 1, qkv, pos, done,
+                                                              block_table, layer, g, kv, out); });
 }
 
 }  // namespace
+
+bool attention_prefill_mma(Ctx& c, const bf16* qkv, const int64_t* seq_offsets, int64_t B, int64_t max_len,
+                           int64_t H, int64_t DH, bf16* out);
 
 template <class T>
 void launch_attention_prefill(Ctx& c, const T* qkv, const int64_t* seq_offsets, int64_t B, int64_t max_len,
                               int64_t H, int64_t DH, T* out) {
   if (B <= 0 || max_len <= 0) return;
+  if constexpr (std::is_same_v<T, bf16>) {
+    if (attention_prefill_mma(c, qkv, seq_offsets, B, max_len, H, DH, out)) return;
+  }
   switch (DH) {
     case 16: return prefill_impl<T, 16>(c, qkv, seq_offsets, B, max_len, H, out);
     case 32: return prefill_impl<T, 32>(c, qkv, seq_offsets, B, max_len, H, out);
