@@ -106,6 +106,9 @@ ppoexp_status ppoexp_ctx_synchronize(ppoexp_ctx ctx);
  * enable=1 starts accumulating; query returns total ms, launches and the
  * algorithmic bytes (or flops) those launches moved. */
 ppoexp_status ppoexp_ctx_profile(ppoexp_ctx ctx, int32_t enable);
+/* Restrict profiling to a comma-separated list of kernel classes (NULL or ""
+ * = all), so a timed region can carry events around its dominant kernel only. */
+ppoexp_status ppoexp_ctx_profile_filter(ppoexp_ctx ctx, const char* classes_csv);
 ppoexp_status ppoexp_ctx_profile_query(ppoexp_ctx ctx, const char* kernel_class, double* total_ms,
                                        int64_t* launches, double* algorithmic_bytes, double* flops);
 /* Number of library kernel launches issued on this context so far (graph

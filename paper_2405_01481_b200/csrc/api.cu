@@ -171,6 +171,24 @@ ppoexp_status ppoexp_ctx_profile(ppoexp_ctx ctx, int32_t enable) {
   });
 }
 
+ppoexp_status ppoexp_ctx_profile_filter(ppoexp_ctx ctx, const char* csv) {
+  return guard([&] {
+    need(ctx, "ctx");
+    std::lock_guard<std::recursive_mutex> lk(ctx->c->mu);
+    ctx->c->profile_filter.clear();
+    if (!csv) return;
+    std::string s(csv), item;
+    size_t i = 0;
+    while (i <= s.size()) {
+      const size_t j = s.find(',', i);
+      item = s.substr(i, j == std::string::npos ? std::string::npos : j - i);
+      if (!item.empty()) ctx->c->profile_filter.insert(item);
+      if (j == std::string::npos) break;
+      i = j + 1;
+    }
+  });
+}
+
 ppoexp_status ppoexp_ctx_profile_query(ppoexp_ctx ctx, const char* cls, double* total_ms, int64_t* launches,
                                        double* bytes, double* flops) {
   return guard([&] {

@@ -156,8 +156,13 @@ void Engine::run_unit(int64_t B, int64_t unit) {
 }
 
 Engine::GraphSet& Engine::graph_for(int64_t B) {
+  std::string sig;
+  if (c->profiling) {
+    sig = "prof:";
+    for (const auto& k : c->profile_filter) sig += k + ",";
+  }
   auto it = graphs.find(B);
-  if (it != graphs.end() && it->second.profiled == c->profiling) return it->second;
+  if (it != graphs.end() && it->second.prof_sig == sig) return it->second;
   if (it != graphs.end()) {
     for (int j = 0; j < 2; ++j) {
       cudaGraphExecDestroy(it->second.exec[j]);
@@ -170,6 +175,7 @@ Engine::GraphSet& Engine::graph_for(int64_t B) {
   }
   GraphSet& gs = graphs[B];
   gs.profiled = c->profiling;
+  gs.prof_sig = sig;
   gs.units = kUnitsPerGraph;
   for (int j = 0; j < 2; ++j) {
     cudaGraph_t graph;

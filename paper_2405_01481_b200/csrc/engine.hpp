@@ -2,6 +2,7 @@
 #pragma once
 
 #include <map>
+#include <string>
 #include <vector>
 
 #include "model.hpp"
@@ -35,6 +36,7 @@ struct Engine {
     int64_t nodes = 0;
     int units = 8;
     bool profiled = false;
+    std::string prof_sig;
   };
   std::map<int64_t, GraphSet> graphs;
 

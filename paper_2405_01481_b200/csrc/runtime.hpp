@@ -8,6 +8,7 @@
 #include <map>
 #include <memory>
 #include <mutex>
+#include <set>
 #include <string>
 #include <utility>
 #include <vector>
@@ -55,6 +56,7 @@ struct Ctx {
   cudaStream_t stream = nullptr;
   std::recursive_mutex mu;
   bool profiling = false;
+  std::set<std::string> profile_filter;  // empty = every class
   bool capturing = false;
   int64_t launches = 0;          // eager launches + graph-replayed kernel nodes
   int64_t capture_launches = 0;  // kernels recorded into the graph being captured
@@ -77,7 +79,7 @@ struct Ctx {
   // `cls`, with the algorithmic bytes / flops it moves.
   template <class F>
   void launch(const char* cls, double bytes, double flops, F&& f) {
-    if (profiling) {
+    if (profiling && (profile_filter.empty() || profile_filter.count(cls))) {
       TimedLaunch t{cls, new_event(), new_event(), bytes, flops};
       // inside stream capture a plain record is only a dependency marker;
       // cudaEventRecordExternal materialises a timing node in the graph

@@ -115,6 +115,7 @@ def lib():
             "ppoexp_ctx_stream": [P, P],
             "ppoexp_ctx_synchronize": [P],
             "ppoexp_ctx_profile": [P, I32],
+            "ppoexp_ctx_profile_filter": [P, C.c_char_p],
             "ppoexp_ctx_profile_query": [P, C.c_char_p, P, P, P, P],
             "ppoexp_ctx_launch_count": [P, P],
             "ppoexp_model_create": [P, P, P, I64, I32, P],
@@ -279,6 +280,10 @@ class Context:
 
     def profile(self, enable=True):
         _check(lib().ppoexp_ctx_profile(self.h, 1 if enable else 0))
+
+    def profile_filter(self, classes=None):
+        """Profile only these kernel classes (None = all)."""
+        _check(lib().ppoexp_ctx_profile_filter(self.h, ",".join(classes).encode() if classes else None))
 
     def profile_query(self, cls: str):
         ms, n, b, f = C.c_double(), C.c_int64(), C.c_double(), C.c_double()

@@ -1,0 +1,104 @@
+// Compiled C++ use of the facade (include/ppoexp.hpp) — the way a reference
+// maintainer would call it.  Prints "FACADE OK" and exits 0 on success.
+#include <cmath>
+#include <cstdio>
+#include <random>
+#include <vector>
+
+#include "ppoexp.hpp"
+
+using namespace ppoexp;
+
+static std::vector<std::vector<double>> g_store;
+
+static ModelParams random_params(const ModelConfig& c, unsigned seed) {
+  std::mt19937_64 rng(seed);
+  std::normal_distribution<double> nd(0.0, 0.02);
+  ModelParams p;
+  auto add = [&](const std::string& n, std::vector<std::size_t> shape, double fill, bool rnd) {
+    std::size_t k = 1;
+    for (auto s : shape) k *= s;
+    std::vector<double> v(k, fill);
+    if (rnd)
+      for (auto& x : v) x = double(float(nd(rng)));
+    g_store.push_back(std::move(v));
+    p.push_back({n, shape, g_store.back().data()});
+  };
+  const std::size_t d = c.d_model, f = c.d_ff;
+  add("tok_embed.weight", {c.vocab_size, d}, 0, true);
+  add("pos_embed.weight", {c.max_seq_len, d}, 0, true);
+  for (std::size_t l = 0; l < c.n_layers; ++l) {
+    const std::string b = "layers." + std::to_string(l) + ".";
+    add(b + "attn_norm.weight", {d}, 1, false);
+    add(b + "attn_norm.bias", {d}, 0, false);
+    for (auto pr : {"q_proj", "k_proj", "v_proj", "o_proj"}) add(b + "attn." + pr + ".weight", {d, d}, 0, true);
+    add(b + "ffn_norm.weight", {d}, 1, false);
+    add(b + "ffn_norm.bias", {d}, 0, false);
+    add(b + "ffn.up_proj.weight", {d, f}, 0, true);
+    add(b + "ffn.down_proj.weight", {f, d}, 0, true);
+  }
+  add("final_norm.weight", {d}, 1, false);
+  add("final_norm.bias", {d}, 0, false);
+  if (c.scalar_head) add("scalar_head.weight", {d, 1}, 0, true);
+  return p;
+}
+
+int main() {
+  g_store.reserve(1000);
+  Context ctx(0);
+  ModelConfig cfg;
+  cfg.vocab_size = 258;
+  cfg.d_model = 64;
+  cfg.n_layers = 2;
+  cfg.n_heads = 4;
+  cfg.d_ff = 128;
+  cfg.max_seq_len = 48;
+  auto params = random_params(cfg, 1);
+  Engine engine(ctx, params, cfg, {}, PPOEXP_F32);
+  std::vector<GenTask> tasks(3);
+  for (int i = 0; i < 3; ++i) {
+    tasks[i].prompt = {1 + i, 2, 3};
+    tasks[i].max_new = 8;
+    tasks[i].sampling = i == 0 ? SamplingSpec::greedy_spec() : SamplingSpec::temperature_spec(1.0, 7 + i);
+  }
+  auto res = engine.generate_batch(tasks);
+  for (auto& r : res)
+    if (r.tokens.empty() || r.tokens.size() != r.logprobs.size()) return 2;
+  // teacher-forced scoring reproduces the generation log-probs (test_model.cpp:183-195 analog)
+  TokenSeq full = tasks[0].prompt;
+  full.insert(full.end(), res[0].tokens.begin(), res[0].tokens.end());
+  auto lp = sequence_logprobs(engine.model(), full);
+  for (std::size_t t = 0; t < res[0].tokens.size(); ++t)
+    if (std::fabs(lp[3 + t] - res[0].logprobs[t]) > 1e-4) return 3;
+  // refit bumps the counter; a bad name set throws RefitError and leaves it
+  engine.refit(params);
+  if (engine.generation_counter() != 1) return 4;
+  auto bad = params;
+  bad.pop_back();
+  try {
+    engine.refit(bad);
+    return 5;
+  } catch (const RefitError& e) {
+    if (std::string(e.what()).find("rebuild") == std::string::npos) return 6;
+  }
+  // experience step
+  ModelConfig hc = cfg;
+  hc.scalar_head = true;
+  auto cparams = random_params(hc, 2);
+  DeviceModel ref(ctx, params, cfg, PPOEXP_F32), critic(ctx, cparams, hc, PPOEXP_F32);
+  ExperienceMaker xm(engine, ref, critic, nullptr, 'e');
+  double st[8];
+  auto batch = xm.run({{5, 6, 7}, {8, 9}}, 6, SamplingSpec::temperature_spec(1.0, 0), 11, 2, 0, nullptr, nullptr, st);
+  if (batch.size() != 2 || batch[0].advantages.size() != batch[0].response.size()) return 7;
+  // same weights for policy and reference → KL is 0 (test_ppo.cpp:227-254 analog)
+  if (std::fabs(st[0]) > 1e-9) return 8;
+  auto g = shaped_gae(ctx, 0.0, {-1.0}, {-1.0}, {0.5}, 0.1, 1.0, 1.0);  // r=[0]+R... V=[.5]
+  if (std::fabs(g.advantages[0] - (-0.5)) > 1e-12) return 9;
+  try {
+    DeviceModel x(ctx, params, ModelConfig{258, 30, 1, 4, 64, 16, false}, PPOEXP_F32);
+    return 10;
+  } catch (const ContractError&) {
+  }
+  std::printf("FACADE OK\n");
+  return 0;
+}

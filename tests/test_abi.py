@@ -65,3 +65,24 @@ def test_product_does_not_import_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".hpp", ".cpp")):
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "oracle" not in re.sub(r"#.*|//.*", "", txt).lower().replace("oracle/ppoexp_oracle.c", ""), f
+
+
+def _build_facade_test():
+    import subprocess
+    out = os.path.join(ROOT, "build", "test_facade")
+    os.makedirs(os.path.dirname(out), exist_ok=True)
+    subprocess.check_call(["g++", "-std=c++17", "-O2", f"-I{ROOT}/include", f"{ROOT}/tests/cpp/test_facade.cpp",
+                           f"-L{ROOT}/paper_2405_01481_b200", "-lppoexp",
+                           f"-Wl,-rpath,{ROOT}/paper_2405_01481_b200", "-o", out])
+    return out
+
+
+def test_cpp_facade_compiles_and_links(lib):
+    assert os.path.exists(_build_facade_test())
+
+
+@pytest.mark.gpu
+def test_cpp_facade_runs_on_gpu(lib):
+    import subprocess
+    r = subprocess.run([_build_facade_test()], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "FACADE OK" in r.stdout, (r.returncode, r.stdout, r.stderr)
