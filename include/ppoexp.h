@@ -38,6 +38,13 @@ extern "C" {
 
 #define PPOEXP_ABI_VERSION 1
 
+/* Only the C ABI is exported from libppoexp.so (built -fvisibility=hidden). */
+#if defined(__GNUC__)
+#define PPOEXP_API __attribute__((visibility("default")))
+#else
+#define PPOEXP_API
+#endif
+
 typedef enum {
   PPOEXP_OK = 0,
   PPOEXP_ERR_CONTRACT = 1, /* aligner::ContractError */
@@ -90,30 +97,30 @@ typedef struct {
 } ppoexp_sampling;
 
 /* ---------------------------------------------------------------- misc */
-const char* ppoexp_last_error(void);
-int32_t ppoexp_abi_version(void);
+PPOEXP_API const char* ppoexp_last_error(void);
+PPOEXP_API int32_t ppoexp_abi_version(void);
 
 /* ------------------------------------------------------------- context */
 /* One device + one CUDA stream + workspace.  Calls on one context are
  * serialised (Engine's shared_mutex semantics, src/engine.cpp:78, :149). */
-ppoexp_status ppoexp_ctx_create(int32_t device, ppoexp_ctx* out);
-ppoexp_status ppoexp_ctx_destroy(ppoexp_ctx ctx);
+PPOEXP_API ppoexp_status ppoexp_ctx_create(int32_t device, ppoexp_ctx* out);
+PPOEXP_API ppoexp_status ppoexp_ctx_destroy(ppoexp_ctx ctx);
 /* The cudaStream_t the context launches on (for event timing / interop). */
-ppoexp_status ppoexp_ctx_stream(ppoexp_ctx ctx, void** stream_out);
-ppoexp_status ppoexp_ctx_synchronize(ppoexp_ctx ctx);
+PPOEXP_API ppoexp_status ppoexp_ctx_stream(ppoexp_ctx ctx, void** stream_out);
+PPOEXP_API ppoexp_status ppoexp_ctx_synchronize(ppoexp_ctx ctx);
 /* Kernel-class timing (CUDA events around each launch of the named class;
  * classes: "decode_attention", "logprob_gather", "gemm", "sampler", ...).
  * enable=1 starts accumulating; query returns total ms, launches and the
  * algorithmic bytes (or flops) those launches moved. */
-ppoexp_status ppoexp_ctx_profile(ppoexp_ctx ctx, int32_t enable);
+PPOEXP_API ppoexp_status ppoexp_ctx_profile(ppoexp_ctx ctx, int32_t enable);
 /* Restrict profiling to a comma-separated list of kernel classes (NULL or ""
  * = all), so a timed region can carry events around its dominant kernel only. */
-ppoexp_status ppoexp_ctx_profile_filter(ppoexp_ctx ctx, const char* classes_csv);
-ppoexp_status ppoexp_ctx_profile_query(ppoexp_ctx ctx, const char* kernel_class, double* total_ms,
+PPOEXP_API ppoexp_status ppoexp_ctx_profile_filter(ppoexp_ctx ctx, const char* classes_csv);
+PPOEXP_API ppoexp_status ppoexp_ctx_profile_query(ppoexp_ctx ctx, const char* kernel_class, double* total_ms,
                                        int64_t* launches, double* algorithmic_bytes, double* flops);
 /* Number of library kernel launches issued on this context so far (graph
  * replays count every kernel node). */
-ppoexp_status ppoexp_ctx_launch_count(ppoexp_ctx ctx, int64_t* out);
+PPOEXP_API ppoexp_status ppoexp_ctx_launch_count(ppoexp_ctx ctx, int64_t* out);
 
 /* --------------------------------------------------------------- model */
 /* A device-resident weight snapshot.  Replaces Engine's deep copy at build
@@ -121,18 +128,18 @@ ppoexp_status ppoexp_ctx_launch_count(ppoexp_ctx ctx, int64_t* out);
  * copied (and cast to compute_dtype) into HBM; the caller keeps its arrays.
  * Name/shape set must equal ModelParams::expected_names(config) exactly
  * (ContractError otherwise, like param_shape, src/model.cpp:92-115). */
-ppoexp_status ppoexp_model_create(ppoexp_ctx ctx, const ppoexp_model_config* config,
+PPOEXP_API ppoexp_status ppoexp_model_create(ppoexp_ctx ctx, const ppoexp_model_config* config,
                                   const ppoexp_tensor_view* params, int64_t n_params,
                                   int32_t compute_dtype, ppoexp_model* out);
 /* Engine::refit, src/engine.cpp:60-90: validates the whole name/shape set
  * first (RefitError "... (rebuild required)", nothing touched), then copies
  * in place (no re-allocation, captured graphs stay valid) and bumps the
  * generation counter. */
-ppoexp_status ppoexp_model_refit(ppoexp_model model, const ppoexp_tensor_view* params, int64_t n_params);
+PPOEXP_API ppoexp_status ppoexp_model_refit(ppoexp_model model, const ppoexp_tensor_view* params, int64_t n_params);
 /* Engine::generation_counter, include/aligner/engine.hpp:65 */
-ppoexp_status ppoexp_model_generation(ppoexp_model model, uint64_t* out);
-ppoexp_status ppoexp_model_config_get(ppoexp_model model, ppoexp_model_config* out);
-ppoexp_status ppoexp_model_destroy(ppoexp_model model);
+PPOEXP_API ppoexp_status ppoexp_model_generation(ppoexp_model model, uint64_t* out);
+PPOEXP_API ppoexp_status ppoexp_model_config_get(ppoexp_model model, ppoexp_model_config* out);
+PPOEXP_API ppoexp_status ppoexp_model_destroy(ppoexp_model model);
 
 /* -------------------------------------------------------------- engine */
 /* The TensorRT-LLM analog (Engine, include/aligner/engine.hpp:49-92) over a
@@ -145,8 +152,8 @@ typedef struct {
   int32_t reserved;
 } ppoexp_engine_options;
 
-ppoexp_status ppoexp_engine_create(ppoexp_model policy, const ppoexp_engine_options* opts, ppoexp_engine* out);
-ppoexp_status ppoexp_engine_destroy(ppoexp_engine engine);
+PPOEXP_API ppoexp_status ppoexp_engine_create(ppoexp_model policy, const ppoexp_engine_options* opts, ppoexp_engine* out);
+PPOEXP_API ppoexp_status ppoexp_engine_destroy(ppoexp_engine engine);
 
 /* Engine::generate_batch (src/engine.cpp:148-182) / generate()
  * (src/model.cpp:438-482) for B tasks at once.
@@ -162,7 +169,7 @@ ppoexp_status ppoexp_engine_destroy(ppoexp_engine engine);
  *    (src/model.cpp:450, :477).  Generation stops after EOT (257), which is
  *    kept (src/model.cpp:476-478).
  *  ms_out (optional): device time of the call in milliseconds. */
-ppoexp_status ppoexp_engine_generate(ppoexp_engine engine, int64_t B, const int32_t* prompts,
+PPOEXP_API ppoexp_status ppoexp_engine_generate(ppoexp_engine engine, int64_t B, const int32_t* prompts,
                                      const int64_t* offsets, const int64_t* max_new,
                                      const ppoexp_sampling* sampling, const uint64_t* seeds,
                                      int64_t out_stride, int32_t* out_tokens, double* out_logprobs,
@@ -173,21 +180,21 @@ ppoexp_status ppoexp_engine_generate(ppoexp_engine engine, int64_t B, const int3
  * out (same ragged layout as tokens) gets out[start] = 0 and
  * out[t] = log p(tokens[t] | tokens[<t]).  One batched forward plus the
  * fused log-softmax+gather kernel. */
-ppoexp_status ppoexp_sequence_logprobs(ppoexp_model model, int64_t B, const int32_t* tokens,
+PPOEXP_API ppoexp_status ppoexp_sequence_logprobs(ppoexp_model model, int64_t B, const int32_t* tokens,
                                        const int64_t* offsets, double* out, int32_t where);
 /* value_estimates (src/losses.cpp:117-127) with the model's scalar head:
  * out is ragged over responses (out_offsets[b] = sum_{i<b} (T_i - rs_i)). */
-ppoexp_status ppoexp_value_estimates(ppoexp_model critic, int64_t B, const int32_t* tokens,
+PPOEXP_API ppoexp_status ppoexp_value_estimates(ppoexp_model critic, int64_t B, const int32_t* tokens,
                                      const int64_t* offsets, const int64_t* response_start, double* out,
                                      int32_t where);
 /* reward_head (src/losses.cpp:105-115) with the model's scalar head: out[B]. */
-ppoexp_status ppoexp_reward_head(ppoexp_model rm, int64_t B, const int32_t* tokens, const int64_t* offsets,
+PPOEXP_API ppoexp_status ppoexp_reward_head(ppoexp_model rm, int64_t B, const int32_t* tokens, const int64_t* offsets,
                                  double* out, int32_t where);
 
 /* ----------------------------------------------------------- shaping */
 /* kl_penalized_rewards (src/losses.cpp:188-199) + gae (src/losses.cpp:168-186)
  * for B padded sequences [B, stride] with lengths[B]. */
-ppoexp_status ppoexp_shape_gae(int64_t B, int64_t stride, const int64_t* lengths, const double* rm_reward,
+PPOEXP_API ppoexp_status ppoexp_shape_gae(int64_t B, int64_t stride, const int64_t* lengths, const double* rm_reward,
                                const double* actor_lp, const double* ref_lp, const double* values,
                                double kl_coef, double gamma, double lam, double* out_rewards,
                                double* out_adv, double* out_ret, ppoexp_ctx ctx, int32_t where);
@@ -195,9 +202,9 @@ ppoexp_status ppoexp_shape_gae(int64_t B, int64_t stride, const int64_t* lengths
  * receives (n_tokens, sum adv, sum adv^2); the caller reduces them across
  * ranks (one NCCL all-reduce / all-gather) and hands the global triple to
  * apply: w = (adv - mean) / sqrt(var + 1e-8), population variance. */
-ppoexp_status ppoexp_whiten_partials(int64_t B, int64_t stride, const int64_t* lengths, const double* adv,
+PPOEXP_API ppoexp_status ppoexp_whiten_partials(int64_t B, int64_t stride, const int64_t* lengths, const double* adv,
                                      double* partials3, ppoexp_ctx ctx, int32_t where);
-ppoexp_status ppoexp_whiten_apply(int64_t B, int64_t stride, const int64_t* lengths, const double* adv,
+PPOEXP_API ppoexp_status ppoexp_whiten_apply(int64_t B, int64_t stride, const int64_t* lengths, const double* adv,
                                   const double* global_partials3, double* out, ppoexp_ctx ctx, int32_t where);
 
 /* ---------------------------------------------------- experience step */
@@ -263,7 +270,7 @@ typedef struct {
   double* stats;        /* [8] */
 } ppoexp_rollout_batch;
 
-ppoexp_status ppoexp_make_experience(const ppoexp_experience_request* req, int64_t B, const int32_t* prompts,
+PPOEXP_API ppoexp_status ppoexp_make_experience(const ppoexp_experience_request* req, int64_t B, const int32_t* prompts,
                                      const int64_t* offsets, const ppoexp_rollout_batch* out, int32_t where);
 
 #ifdef __cplusplus

@@ -11,7 +11,7 @@
 #include "../../include/ppoexp_testing.h"
 #include "engine.hpp"
 
-using namespace ppoexp;
+using namespace ppx;
 
 struct ppoexp_ctx_s {
   std::unique_ptr<Ctx> c;
@@ -740,7 +740,7 @@ ppoexp_status ppoexp_make_experience(const ppoexp_experience_request* req, int64
 }  // extern "C"
 
 // ------------------------------------------------------------------ testing
-namespace ppoexp {
+namespace ppx {
 template <class T>
 void launch_gemm_simt(Ctx& c, const T* A, int64_t lda, const T* B, int64_t ldb, int64_t M, int64_t N, int64_t K,
                       Epi epi, void* C, int64_t ldc);

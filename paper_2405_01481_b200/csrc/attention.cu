@@ -14,7 +14,7 @@
 
 #include "kernels.hpp"
 
-namespace ppoexp {
+namespace ppx {
 
 namespace {
 
@@ -311,4 +311,4 @@ template void launch_attention_decode<float>(Ctx&, const float*, int64_t, const 
 template void launch_attention_decode<bf16>(Ctx&, const bf16*, int64_t, const int32_t*, const int32_t*,
                                             const int32_t*, int, const KvGeom&, bf16*, bf16*, double);
 
-}  // namespace ppoexp
+}  // namespace ppx

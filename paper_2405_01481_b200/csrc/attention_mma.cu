@@ -13,7 +13,7 @@
 
 #include "kernels.hpp"
 
-namespace ppoexp {
+namespace ppx {
 
 namespace {
 
@@ -247,4 +247,4 @@ bool attention_prefill_mma(Ctx& c, const bf16* qkv, const int64_t* seq_offsets, 
   }
 }
 
-}  // namespace ppoexp
+}  // namespace ppx

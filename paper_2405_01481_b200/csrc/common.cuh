@@ -8,7 +8,7 @@
 #include <stdexcept>
 #include <string>
 
-namespace ppoexp {
+namespace ppx {
 
 using bf16 = __nv_bfloat16;
 
@@ -30,7 +30,7 @@ inline Error PpoError(const std::string& m) { return Error(5, m); }
     cudaError_t e_ = (expr);                                                                    \
     if (e_ != cudaSuccess) {                                                                    \
       (void)cudaGetLastError();                                                                 \
-      throw ::ppoexp::Error(e_ == cudaErrorMemoryAllocation ? 7 : 6,                            \
+      throw ::ppx::Error(e_ == cudaErrorMemoryAllocation ? 7 : 6,                            \
                             std::string("cuda: ") + cudaGetErrorString(e_) + " at " #expr);     \
     }                                                                                           \
   } while (0)
@@ -100,4 +100,4 @@ constexpr int kEotToken = 257;  // include/aligner/model.hpp:18
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
-}  // namespace ppoexp
+}  // namespace ppx

@@ -15,7 +15,7 @@
 
 #include "engine.hpp"
 
-namespace ppoexp {
+namespace ppx {
 
 namespace {
 constexpr int kUnitsPerGraph = 8;
@@ -493,4 +493,4 @@ void Engine::harvest_snapshot(const ReplayTimes& r) {
   }
 }
 
-}  // namespace ppoexp
+}  // namespace ppx

@@ -7,7 +7,7 @@
 
 #include "model.hpp"
 
-namespace ppoexp {
+namespace ppx {
 
 struct Engine {
   Model* m;
@@ -73,4 +73,4 @@ struct Engine {
   void harvest_snapshot(const ReplayTimes& r);
 };
 
-}  // namespace ppoexp
+}  // namespace ppx

@@ -15,7 +15,7 @@
 
 namespace cg = cooperative_groups;
 
-namespace ppoexp {
+namespace ppx {
 
 CUtensorMap make_map(const void* ptr, int64_t rows, int64_t cols, int64_t ld, int box_rows);  // gemm_tc.cu
 
@@ -249,9 +249,17 @@ void launch_dec(Ctx& c, const bf16* X, int64_t ldx, const bf16* W, int64_t ldw, 
   }
   const int tiles = int(ceil_div(N, BMW));
   const int nk = int(ceil_div(K, BK));
-  // K-split: aim for >= ~148 CTAs, at most 8 (portable cluster), >= 1 k-block each
+  // K-split: aim for >= ~148 CTAs, at most 8 (portable cluster), >= 2 k-blocks each
+  static const int smax = [] {
+    const char* e = getenv("PPOEXP_DECODE_SPLIT_MAX");
+    return e ? atoi(e) : 4;
+  }();
+  static const int target = [] {
+    const char* e = getenv("PPOEXP_DECODE_CTA_TARGET");
+    return e ? atoi(e) : 148;
+  }();
   int S = 1;
-  while (S < 8 && tiles * S < 148 && nk >= 2 * S) S *= 2;
+  while (S < smax && tiles * S < target && nk >= 2 * S) S *= 2;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(tiles, S, 1);
   cfg.blockDim = dim3(kThreads, 1, 1);
@@ -296,4 +304,4 @@ bool gemm_decode_bf16(Ctx& c, const bf16* A, int64_t lda, const bf16* B, int64_t
   return dispatch<256>(c, A, lda, B, ldb, M, N, K, epi, C, ldc), true;
 }
 
-}  // namespace ppoexp
+}  // namespace ppx

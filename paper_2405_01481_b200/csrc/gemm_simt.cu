@@ -4,7 +4,7 @@
 // reference).  bf16 GEMMs on the hot path go to gemm_tc.cu (tcgen05).
 #include "kernels.hpp"
 
-namespace ppoexp {
+namespace ppx {
 
 namespace {
 constexpr int BM = 64, BN = 64, BK = 16;
@@ -101,4 +101,4 @@ template void launch_gemm_simt<float>(Ctx&, const float*, int64_t, const float*,
 template void launch_gemm_simt<bf16>(Ctx&, const bf16*, int64_t, const bf16*, int64_t, int64_t, int64_t, int64_t,
                                      Epi, void*, int64_t);
 
-}  // namespace ppoexp
+}  // namespace ppx

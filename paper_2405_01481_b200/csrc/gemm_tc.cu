@@ -21,7 +21,7 @@
 
 #include "kernels.hpp"
 
-namespace ppoexp {
+namespace ppx {
 
 namespace {
 
@@ -358,4 +358,4 @@ bool gemm_tc_bf16(Ctx& c, const bf16* A, int64_t lda, const bf16* B, int64_t ldb
   return dispatch_epi<128>(c, A, lda, B, ldb, M, N, K, epi, C, ldc), true;
 }
 
-}  // namespace ppoexp
+}  // namespace ppx

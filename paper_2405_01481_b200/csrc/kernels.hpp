@@ -7,7 +7,7 @@
 
 #include "runtime.hpp"
 
-namespace ppoexp {
+namespace ppx {
 
 // Paged KV cache geometry.  Pool layout (elements of T):
 //   kv[(((layer * n_pages + page) * 2 + kv) * H + h) * page_size * DH + slot * DH + i]
@@ -101,4 +101,4 @@ void launch_scripted_reward(Ctx& c, int64_t B, int64_t stride, const int32_t* to
 void launch_f32_to_f64(Ctx& c, const float* src, int64_t n, double* dst);
 void launch_fill_i32(Ctx& c, int32_t* dst, int64_t n, int32_t v);
 
-}  // namespace ppoexp
+}  // namespace ppx

@@ -4,7 +4,7 @@
 
 #include "kernels.hpp"
 
-namespace ppoexp {
+namespace ppx {
 
 // ===================================================================== runtime
 Ctx::Ctx(int dev) : device(dev) {
@@ -421,4 +421,4 @@ INST(float)
 INST(bf16)
 #undef INST
 
-}  // namespace ppoexp
+}  // namespace ppx

@@ -4,7 +4,7 @@
 
 #include "kernels.hpp"
 
-namespace ppoexp {
+namespace ppx {
 
 namespace {
 
@@ -230,4 +230,4 @@ template void launch_logprob_gather<float>(Ctx&, const float*, int64_t, int64_t,
 template void launch_logprob_gather<bf16>(Ctx&, const bf16*, int64_t, int64_t, int64_t, const int32_t*,
                                           const int64_t*, double*);
 
-}  // namespace ppoexp
+}  // namespace ppx

@@ -5,7 +5,7 @@
 
 #include "model.hpp"
 
-namespace ppoexp {
+namespace ppx {
 
 // ------------------------------------------------------------------ names
 std::vector<std::pair<std::string, std::vector<int64_t>>> Model::expected(const ppoexp_model_config& c) {
@@ -332,4 +332,4 @@ void launch_concat_pack(Ctx& c, int64_t B, const int32_t* prompts, const int64_t
   });
 }
 
-}  // namespace ppoexp
+}  // namespace ppx

@@ -8,7 +8,7 @@
 #include "../../include/ppoexp.h"
 #include "kernels.hpp"
 
-namespace ppoexp {
+namespace ppx {
 
 struct Layer {
   void *wqkv, *wo, *wup, *wdown;  // T: [3d,d], [d,d], [f,d], [d,f] (K-major, i.e. W^T of the reference)
@@ -77,4 +77,4 @@ void launch_response_meta(Ctx& c, int64_t B, const int64_t* offsets_full, const 
 void launch_concat_pack(Ctx& c, int64_t B, const int32_t* prompts, const int64_t* p_offsets, const int32_t* gen,
                         int64_t gstride, const int64_t* gen_len, const int64_t* full_offsets, int32_t* full);
 
-}  // namespace ppoexp
+}  // namespace ppx

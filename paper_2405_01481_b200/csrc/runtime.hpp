@@ -15,7 +15,7 @@
 
 #include "common.cuh"
 
-namespace ppoexp {
+namespace ppx {
 
 struct ClassStats {
   double ms = 0.0;
@@ -170,4 +170,4 @@ struct DeviceGuard {
   }
 };
 
-}  // namespace ppoexp
+}  // namespace ppx

@@ -21,15 +21,16 @@
 
 #include "kernels.hpp"
 
-namespace ppoexp {
+namespace ppx {
 
 namespace {
 constexpr int NT = 1024, NW = NT / 32, NB = 1024, LIST = 1024;
-constexpr int64_t kCacheMaxV = 52000;
+constexpr int64_t kCacheMaxV = 50600;
+constexpr double kFix = 1.0 / 4294967296.0;  // 2^-32
 
 struct Shared {
   unsigned hcnt[NB];
-  float hsum[NB];
+  unsigned long long hsum[NB];  // fixed point q * 2^32 (native 64-bit smem atomics; no CAS loop)
   unsigned long long list[LIST];
   float fm[NW], fmn[NW], fs[NW];
   int fi[NW];
@@ -143,16 +144,33 @@ __global__ void __launch_bounds__(NT) sampler_kernel(const float* __restrict__ l
   // ---- pass 1: max, min, first argmax, online sum exp(l - max)
   float m = -INFINITY, mn = INFINITY, se = 0.f;
   int am = 0x7fffffff;
-  for (int64_t j = tid; j < V; j += NT) {
-    const float v = row[j];
+  auto visit = [&](float v, int j) {
     if (v > m) {
       se = se * expf(m - v) + 1.f;
       m = v;
-      am = int(j);
+      am = j;
     } else {
       se += expf(v - m);
     }
     mn = fminf(mn, v);
+  };
+  {
+    // 16-byte loads, 2 in flight per thread; index order within a thread is
+    // ascending, so "first index wins" ties stay exact
+    const int64_t nv = V / 4;
+    const float4* r4 = reinterpret_cast<const float4*>(row);
+    int64_t k = tid;
+    for (; k + NT < nv; k += 2 * NT) {
+      const float4 a = r4[k], c = r4[k + NT];
+      visit(a.x, int(4 * k)); visit(a.y, int(4 * k + 1)); visit(a.z, int(4 * k + 2)); visit(a.w, int(4 * k + 3));
+      visit(c.x, int(4 * (k + NT))); visit(c.y, int(4 * (k + NT) + 1));
+      visit(c.z, int(4 * (k + NT) + 2)); visit(c.w, int(4 * (k + NT) + 3));
+    }
+    for (; k < nv; k += NT) {
+      const float4 a = r4[k];
+      visit(a.x, int(4 * k)); visit(a.y, int(4 * k + 1)); visit(a.z, int(4 * k + 2)); visit(a.w, int(4 * k + 3));
+    }
+    for (int64_t j = nv * 4 + tid; j < V; j += NT) visit(row[j], int(j));
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -204,7 +222,7 @@ __global__ void __launch_bounds__(NT) sampler_kernel(const float* __restrict__ l
     if (filtering)
       for (int k = tid; k < NB; k += NT) {
         sh.hcnt[k] = 0;
-        sh.hsum[k] = 0.f;
+        sh.hsum[k] = 0ull;
       }
     __syncthreads();
     double zloc = 0.0;
@@ -215,7 +233,7 @@ __global__ void __launch_bounds__(NT) sampler_kernel(const float* __restrict__ l
         zloc += double(q);
         const int bk = bucket_of(qbits_of(q), top, scale);
         atomicAdd(&sh.hcnt[bk], 1u);
-        atomicAdd(&sh.hsum[bk], q);
+        atomicAdd(&sh.hsum[bk], (unsigned long long)(double(q) * 4294967296.0));
       }
     }
     __syncthreads();
@@ -261,7 +279,7 @@ __global__ void __launch_bounds__(NT) sampler_kernel(const float* __restrict__ l
           sh.c_above = ex;
         }
         double dtot;
-        const double sex = block_excl_scan<double>(double(sh.hsum[tid]), sh.dwarp, dtot);
+        const double sex = block_excl_scan<double>(double(sh.hsum[tid]) * kFix, sh.dwarp, dtot);
         if (tid == sh.bk) sh.s_above = sex;
         __syncthreads();
         collect_sort(sh.bk);
@@ -285,7 +303,7 @@ __global__ void __launch_bounds__(NT) sampler_kernel(const float* __restrict__ l
         const double target = prm.top_p * sh.zk;
         const int bk = sh.bk;
         // effective bucket sums: beyond the top-k bucket nothing is kept
-        const double hs = tid < bk ? double(sh.hsum[tid]) : (tid == bk ? sh.zk_bucket : 0.0);
+        const double hs = tid < bk ? double(sh.hsum[tid]) * kFix : (tid == bk ? sh.zk_bucket : 0.0);
         double dtot;
         const double ex = block_excl_scan<double>(hs, sh.dwarp, dtot);
         if (tid == 0) sh.bp = -1;
@@ -486,4 +504,4 @@ void launch_sampler(Ctx& c, const float* logits, int64_t ld, int64_t B, int64_t 
   }
 }
 
-}  // namespace ppoexp
+}  // namespace ppx

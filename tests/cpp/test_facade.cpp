@@ -1,5 +1,9 @@
 // Compiled C++ use of the facade (include/ppoexp.hpp) — the way a reference
 // maintainer would call it.  Prints "FACADE OK" and exits 0 on success.
+#include <execinfo.h>
+#include <signal.h>
+#include <unistd.h>
+
 #include <cmath>
 #include <cstdio>
 #include <random>
@@ -43,9 +47,30 @@ static ModelParams random_params(const ModelConfig& c, unsigned seed) {
   return p;
 }
 
+static int run(Context& ctx);
+static void on_segv(int) {
+  void* bt[64];
+  const int n = backtrace(bt, 64);
+  backtrace_symbols_fd(bt, n, 2);
+  _exit(139);
+}
+static void step(const char* m) { std::fprintf(stderr, "step: %s\n", m); std::fflush(stderr); }
+
 int main() {
+  signal(SIGSEGV, on_segv);
   g_store.reserve(1000);
-  Context ctx(0);
+  step("start");
+  auto* ctxp = new Context(0);
+  Context& ctx = *ctxp;
+  int rc = run(ctx);
+  step("run returned");
+  delete ctxp;
+  step("ctx destroyed");
+  if (rc == 0) std::printf("FACADE OK\n");
+  return rc;
+}
+
+static int run(Context& ctx) {
   ModelConfig cfg;
   cfg.vocab_size = 258;
   cfg.d_model = 64;
@@ -54,7 +79,9 @@ int main() {
   cfg.d_ff = 128;
   cfg.max_seq_len = 48;
   auto params = random_params(cfg, 1);
+  step("params");
   Engine engine(ctx, params, cfg, {}, PPOEXP_F32);
+  step("engine");
   std::vector<GenTask> tasks(3);
   for (int i = 0; i < 3; ++i) {
     tasks[i].prompt = {1 + i, 2, 3};
@@ -62,12 +89,14 @@ int main() {
     tasks[i].sampling = i == 0 ? SamplingSpec::greedy_spec() : SamplingSpec::temperature_spec(1.0, 7 + i);
   }
   auto res = engine.generate_batch(tasks);
+  step("generated");
   for (auto& r : res)
     if (r.tokens.empty() || r.tokens.size() != r.logprobs.size()) return 2;
   // teacher-forced scoring reproduces the generation log-probs (test_model.cpp:183-195 analog)
   TokenSeq full = tasks[0].prompt;
   full.insert(full.end(), res[0].tokens.begin(), res[0].tokens.end());
   auto lp = sequence_logprobs(engine.model(), full);
+  step("scored");
   for (std::size_t t = 0; t < res[0].tokens.size(); ++t)
     if (std::fabs(lp[3 + t] - res[0].logprobs[t]) > 1e-4) return 3;
   // refit bumps the counter; a bad name set throws RefitError and leaves it
@@ -86,19 +115,23 @@ int main() {
   hc.scalar_head = true;
   auto cparams = random_params(hc, 2);
   DeviceModel ref(ctx, params, cfg, PPOEXP_F32), critic(ctx, cparams, hc, PPOEXP_F32);
+  step("models");
   ExperienceMaker xm(engine, ref, critic, nullptr, 'e');
   double st[8];
   auto batch = xm.run({{5, 6, 7}, {8, 9}}, 6, SamplingSpec::temperature_spec(1.0, 0), 11, 2, 0, nullptr, nullptr, st);
+  step("experience");
   if (batch.size() != 2 || batch[0].advantages.size() != batch[0].response.size()) return 7;
   // same weights for policy and reference → KL is 0 (test_ppo.cpp:227-254 analog)
   if (std::fabs(st[0]) > 1e-9) return 8;
+  step("kl ok");
   auto g = shaped_gae(ctx, 0.0, {-1.0}, {-1.0}, {0.5}, 0.1, 1.0, 1.0);  // r=[0]+R... V=[.5]
+  step("gae");
   if (std::fabs(g.advantages[0] - (-0.5)) > 1e-12) return 9;
   try {
     DeviceModel x(ctx, params, ModelConfig{258, 30, 1, 4, 64, 16, false}, PPOEXP_F32);
     return 10;
   } catch (const ContractError&) {
   }
-  std::printf("FACADE OK\n");
+  step("contract");
   return 0;
 }
