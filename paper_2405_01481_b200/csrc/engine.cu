@@ -59,6 +59,9 @@ Engine::Engine(Model* model, const ppoexp_engine_options* o) : m(model), c(model
   const size_t o_olp = sbytes; sbytes += al(mb * S * 4);
   const size_t o_uni = sbytes; sbytes += al(mb * S * 8);
   const size_t o_last = sbytes; sbytes += al(mb * 4);
+  const int64_t max_slices = 8 * ceil_div(std::max(d, f), 128);
+  const size_t o_sta = sbytes; sbytes += al(max_slices * mb * 16);
+  const size_t o_stb = sbytes; sbytes += al(max_slices * mb * 16);
   state.ensure(sbytes);
   PPOEXP_CUDA(cudaMemset(state.ptr, 0, sbytes));
   char* p = static_cast<char*>(state.ptr);
@@ -80,6 +83,13 @@ Engine::Engine(Model* model, const ppoexp_engine_options* o) : m(model), c(model
   out_lp = reinterpret_cast<float*>(p + o_olp);
   uniforms = reinterpret_cast<double*>(p + o_uni);
   last_rows = reinterpret_cast<int32_t*>(p + o_last);
+  stats_a = reinterpret_cast<double*>(p + o_sta);
+  stats_b = reinterpret_cast<double*>(p + o_stb);
+  {
+    // opt-in: measured slower on B200 at the C2 shape (consumers re-read fp32 rows)
+    const char* ev = getenv("PPOEXP_FUSE_LN");
+    fuse_ln = m->dtype == PPOEXP_BF16 && ev && ev[0] == '1' && mb <= 256 && d % 8 == 0;
+  }
   PPOEXP_CUDA(cudaMallocHost(&host_flags, 64));
   PPOEXP_CUDA(cudaEventCreateWithFlags(&poll_ev[0], cudaEventDisableTiming));
   PPOEXP_CUDA(cudaEventCreateWithFlags(&poll_ev[1], cudaEventDisableTiming));
@@ -132,6 +142,35 @@ void Engine::decode_unit(int64_t B, int64_t unit) {
   T* at = static_cast<T*>(att);
   T* uu = static_cast<T*>(up);
   cur_unit = unit;
+  if constexpr (std::is_same_v<T, bf16>) {
+    if (fuse_ln) {
+      // bf16 path with LayerNorm fused into the consumer GEMMs: embed / O-proj /
+      // down-proj emit fp64 row-statistic slices, QKV / up / LM head normalise
+      // their activation slice on the fly (no standalone LayerNorm launches)
+      const RowStats sa{stats_a, int(opts.max_batch)}, sb{stats_b, int(opts.max_batch)};
+      launch_embed_stats<T>(cc, next_tok, pos, B, d, static_cast<const T*>(m->tok), static_cast<const T*>(m->pos), x,
+                            sa);
+      int na = 1, nb = 0;
+      for (int64_t l = 0; l < m->cfg.n_layers; ++l) {
+        const Layer& ly = m->layers[l];
+        const LnIn l1{x, d, stats_a, na, int(opts.max_batch), ly.ln1w, ly.ln1b, int(d)};
+        gemm_decode_fused(cc, nullptr, d, static_cast<const T*>(ly.wqkv), d, B, 3 * d, d, Epi::kStore, q3, 3 * d, &l1,
+                          nullptr);
+        launch_attention_decode<T>(cc, q3, B, pos, done, block_table, int(l), geom, static_cast<T*>(kv.ptr), at, 0.0);
+        nb = gemm_decode_fused(cc, at, d, static_cast<const T*>(ly.wo), d, B, d, d, Epi::kAddResidual, x, d, nullptr,
+                               &sb);
+        const LnIn l2{x, d, stats_b, nb, int(opts.max_batch), ly.ln2w, ly.ln2b, int(d)};
+        gemm_decode_fused(cc, nullptr, d, static_cast<const T*>(ly.wup), d, B, f, d, Epi::kGelu, uu, f, &l2, nullptr);
+        na = gemm_decode_fused(cc, uu, f, static_cast<const T*>(ly.wdown), f, B, d, f, Epi::kAddResidual, x, d,
+                               nullptr, &sa);
+      }
+      const LnIn lf{x, d, stats_a, na, int(opts.max_batch), m->lnfw, m->lnfb, int(d)};
+      gemm_decode_fused(cc, nullptr, d, static_cast<const T*>(m->tok), d, B, V, d, Epi::kStoreF32, logits, m->vpad,
+                        &lf, nullptr);
+      launch_sampler(cc, logits, m->vpad, B, V, sampler_state());
+      return;
+    }
+  }
   launch_embed<T>(cc, next_tok, pos, B, d, static_cast<const T*>(m->tok), static_cast<const T*>(m->pos), x);
   for (int64_t l = 0; l < m->cfg.n_layers; ++l) {
     const Layer& ly = m->layers[l];

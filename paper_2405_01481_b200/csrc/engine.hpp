@@ -25,6 +25,8 @@ struct Engine {
   float* out_lp;
   double* uniforms;
   int32_t* host_flags = nullptr;
+  double *stats_a = nullptr, *stats_b = nullptr;  // fused-LN row-statistic slices
+  bool fuse_ln = false;
   cudaEvent_t poll_ev[2]{}, t0{}, t1{};
   double last_ms = 0;
   int64_t cur_unit = 0;

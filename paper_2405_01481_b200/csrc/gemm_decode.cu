@@ -11,6 +11,8 @@
 #include <cooperative_groups.h>
 #include <cuda.h>
 
+#include <algorithm>
+
 #include "kernels.hpp"
 
 namespace cg = cooperative_groups;
@@ -21,7 +23,7 @@ CUtensorMap make_map(const void* ptr, int64_t rows, int64_t cols, int64_t ld, in
 
 namespace {
 
-constexpr int BMW = 128, BK = 64, kThreads = 192, kStages = 4;
+constexpr int BMW = 128, BK = 64, kThreads = 192;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -74,32 +76,47 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+// Shared memory: a ring of `wst` 16 KB weight tiles (all of this CTA's K
+// slice when it fits → fetched entirely before the grid-dependency wait), an
+// XST-deep ring of activation tiles, then barriers.  The fp32 partial used by
+// the split-K reduction reuses the weight ring after the MMAs complete.
 template <int NB>
 struct DecLayout {
   static constexpr int kW = BMW * BK * 2;  // 16 KB weight tile
   static constexpr int kX = NB * BK * 2;   // activation tile
-  static constexpr int kStage = kW + kX;
+  static constexpr int XST = NB <= 64 ? 4 : 2;
   static constexpr int kPart = NB * BMW * 4;  // fp32 partial [NB][128], feature-contiguous
-  static constexpr int kPipe = kStages * kStage;
-  static constexpr int kBody = kPipe > kPart ? kPipe : kPart;
-  static constexpr int kBytes = kBody + 1024 + 256;
-  static constexpr int kTmemCols = NB < 32 ? 32 : (NB <= 32 ? 32 : (NB <= 64 ? 64 : (NB <= 128 ? 128 : 256)));
+  // 227 KB opt-in minus the static LayerNorm scratch (2 x NB floats) and slack
+  static constexpr int kSmemMax = 232448 - 2 * NB * 4 - 256;
+  static constexpr int kFixed = XST * kX + 1024 /*align*/ + 1024 /*barriers*/;
+  static constexpr int kWcap = (kSmemMax - kFixed) / kW;
+  static constexpr int kTmemCols = NB <= 32 ? 32 : (NB <= 64 ? 64 : (NB <= 128 ? 128 : 256));
+  static int bytes(int wst) {
+    const int body = wst * kW > kPart ? wst * kW : kPart;
+    return body + XST * kX + 1024 + 1024;
+  }
 };
 
-template <int NB, int EPI>
+template <int NB, int EPI, bool LNIN>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_decode_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX, int Mrows,
-                       int N, int K, void* __restrict__ Cv, int64_t ldc, int S) {
+                       int N, int K, void* __restrict__ Cv, int64_t ldc, int S, int wst, LnIn ln, RowStats so) {
   using L = DecLayout<NB>;
+  constexpr int XST = L::XST;
+  __shared__ float ln_mu[NB], ln_rs[NB];
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int body = wst * L::kW > L::kPart ? wst * L::kW : L::kPart;
   uint8_t* sW = smem;
-  uint8_t* sX = smem + kStages * L::kW;
+  uint8_t* sX = smem + body;
   float* part = reinterpret_cast<float*>(smem);  // reused after the MMA loop
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::kBody);
-  uint64_t* empty = full + kStages;
-  uint64_t* tmem_full = empty + kStages;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sX + XST * L::kX);
+  uint64_t* xfull = bars;
+  uint64_t* xempty = xfull + XST;
+  uint64_t* tmem_full = xempty + XST;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+  uint64_t* wfull = tmem_full + 2;   // [wst]
+  uint64_t* wempty = wfull + wst;    // [wst]
   cg::cluster_group cluster = cg::this_cluster();
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -107,16 +124,27 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int r = blockIdx.y;  // K-split rank == cluster rank (cluster spans y)
   const int nk = (K + BK - 1) / BK;
   const int kb0 = int((int64_t(r) * nk) / S), kb1 = int((int64_t(r + 1) * nk) / S);
+  const int nkl = kb1 - kb0;
 
   if (warp == 0 && lane == 0) {
-    for (int s = 0; s < kStages; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+    for (int i = 0; i < XST; ++i) {
+      mbar_init(&xfull[i], LNIN ? 128 : 1);  // LN mode: the 128 epilogue threads produce X
+      mbar_init(&xempty[i], 1);
+    }
+    for (int i = 0; i < wst; ++i) {
+      mbar_init(&wfull[i], 1);
+      mbar_init(&wempty[i], 1);
     }
     mbar_init(tmem_full, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmW)) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmX)) : "memory");
+    // The weights are constant across the graph: fetch this CTA's weight slice
+    // (up to the ring size) BEFORE waiting on the predecessor grid (PDL), so
+    // the HBM stream overlaps the previous kernel.
+    const int pre = min(wst, nkl);
+    for (int it = 0; it < pre; ++it) {
+      mbar_expect_tx(&wfull[it], L::kW);
+      tma_load_2d(&tmW, &wfull[it], sW + it * L::kW, (kb0 + it) * BK, n0);
+    }
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
@@ -127,143 +155,278 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();  // upstream activations are valid from here on
+  pdl_trigger();
 
   if (warp == 0) {
     if (lane == 0) {
-      // The weights are constant across the graph: stream the first stages of
-      // them BEFORE waiting on the predecessor grid (PDL), so their HBM latency
-      // overlaps the previous kernel.  Activations are loaded after the wait.
-      const int pre = min(kStages, kb1 - kb0);
-      for (int it = 0; it < pre; ++it) {
-        mbar_expect_tx(&full[it], L::kStage);
-        tma_load_2d(&tmW, &full[it], sW + it * L::kW, (kb0 + it) * BK, n0);
+      if (!LNIN)
+        for (int it = 0; it < nkl; ++it) {
+          const int kb = kb0 + it;
+          // activation tile (L2-resident, produced upstream)
+          const int xs = it % XST, xu = it / XST;
+          if (xu > 0) mbar_wait(&xempty[xs], (xu - 1) & 1);
+          mbar_expect_tx(&xfull[xs], L::kX);
+          tma_load_2d(&tmX, &xfull[xs], sX + xs * L::kX, kb * BK, 0);
+        }
+    } else if (lane == 1) {
+      // refill the weight ring for slices larger than the ring
+      for (int it = wst; it < nkl; ++it) {
+        const int ws = it % wst, wu = it / wst;
+        mbar_wait(&wempty[ws], (wu - 1) & 1);
+        mbar_expect_tx(&wfull[ws], L::kW);
+        tma_load_2d(&tmW, &wfull[ws], sW + ws * L::kW, (kb0 + it) * BK, n0);
       }
-      pdl_wait();
-      pdl_trigger();
-      for (int it = 0; it < pre; ++it) tma_load_2d(&tmX, &full[it], sX + it * L::kX, (kb0 + it) * BK, 0);
-      for (int kb = kb0 + pre; kb < kb1; ++kb) {
-        const int it = kb - kb0, s = it % kStages, u = it / kStages;
-        if (u > 0) mbar_wait(&empty[s], (u - 1) & 1);
-        mbar_expect_tx(&full[s], L::kStage);
-        tma_load_2d(&tmW, &full[s], sW + s * L::kW, kb * BK, n0);
-        tma_load_2d(&tmX, &full[s], sX + s * L::kX, kb * BK, 0);
-      }
-    } else {
-      pdl_wait();
     }
   } else if (warp == 1) {
-    pdl_wait();
     if (lane == 0) {
       constexpr uint32_t idesc = idesc_bf16(BMW, NB);
-      for (int kb = kb0; kb < kb1; ++kb) {
-        const int it = kb - kb0, s = it % kStages, u = it / kStages;
-        mbar_wait(&full[s], u & 1);
+      for (int it = 0; it < nkl; ++it) {
+        const int ws = it % wst, wu = it / wst;
+        const int xs = it % XST, xu = it / XST;
+        mbar_wait(&wfull[ws], wu & 1);
+        mbar_wait(&xfull[xs], xu & 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint64_t dw = smem_desc_sw128(sW + s * L::kW);
-        const uint64_t dx = smem_desc_sw128(sX + s * L::kX);
+        const uint64_t dw = smem_desc_sw128(sW + ws * L::kW);
+        const uint64_t dx = smem_desc_sw128(sX + xs * L::kX);
 #pragma unroll
         for (int k = 0; k < BK / 16; ++k) mma_bf16(tmem, dw + 2 * k, dx + 2 * k, idesc, (it | k) != 0);
-        mma_commit(&empty[s]);
+        mma_commit(&xempty[xs]);
+        mma_commit(&wempty[ws]);
       }
       mma_commit(tmem_full);
     }
     __syncwarp();
   } else {
-    pdl_wait();  // the epilogue reads/writes C, produced upstream
-    // TMEM (feature rows x batch cols) → smem partial
+    const int et = threadIdx.x - 64;  // 0..127
+    if constexpr (LNIN) {
+      // ---- fused LayerNorm producer: row mean / rstd from the fp64 slices,
+      // then LN(x) -> bf16 written in the 128B-swizzled K-major layout UMMA reads
+      for (int rr = et; rr < NB; rr += 128) {
+        float mu = 0.f, rs = 0.f;
+        if (rr < Mrows) {
+          double s1 = 0.0, s2 = 0.0;
+          for (int sl = 0; sl < ln.n_slices; ++sl) {
+            s1 += ln.stats[(int64_t(sl) * ln.ld + rr) * 2];
+            s2 += ln.stats[(int64_t(sl) * ln.ld + rr) * 2 + 1];
+          }
+          const double mean = s1 / ln.d;
+          double var = s2 / ln.d - mean * mean;
+          if (var < 0) var = 0;
+          mu = float(mean);
+          rs = float(1.0 / sqrt(var + 1e-5));
+        }
+        ln_mu[rr] = mu;
+        ln_rs[rr] = rs;
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      for (int it = 0; it < nkl; ++it) {
+        const int kb = kb0 + it;
+        const int xs = it % XST, xu = it / XST;
+        if (xu > 0) mbar_wait(&xempty[xs], (xu - 1) & 1);
+        uint8_t* tile = sX + xs * L::kX;
+        for (int ch = et; ch < NB * 8; ch += 128) {
+          const int rr = ch >> 3, c8 = ch & 7;
+          const int col = kb * BK + c8 * 8;
+          Vec16<bf16> o;
+          if (rr < Mrows && col < K) {
+            const float* xr = ln.x + int64_t(rr) * ln.ldx + col;
+            const float4 a0 = *reinterpret_cast<const float4*>(xr), a1 = *reinterpret_cast<const float4*>(xr + 4);
+            const float4 g0 = *reinterpret_cast<const float4*>(ln.g + col), g1 = *reinterpret_cast<const float4*>(ln.g + col + 4);
+            const float4 b0 = *reinterpret_cast<const float4*>(ln.b + col), b1 = *reinterpret_cast<const float4*>(ln.b + col + 4);
+            const float mu = ln_mu[rr], rs = ln_rs[rr];
+            const float xv[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+            const float gv[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+            const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+            for (int e = 0; e < 8; ++e) o.v[e] = __float2bfloat16_rn(gv[e] * ((xv[e] - mu) * rs) + bv[e]);
+          } else {
+            o.u = make_uint4(0u, 0u, 0u, 0u);
+          }
+          *reinterpret_cast<uint4*>(tile + rr * 128 + ((c8 ^ (rr & 7)) << 4)) = o.u;
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor-core reads
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&xfull[xs])) : "memory");
+      }
+    }
+    // TMEM (feature rows x batch cols) → registers → (S == 1) epilogue straight
+    // to global, or (S > 1) fp32 partial in smem for the cluster reduction
     const int q = warp & 3;
     mbar_wait(tmem_full, 0);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const int f = q * 32 + lane;
+    const int n = n0 + f;
+    const int ncols = min(Mrows, NB);
 #pragma unroll 1
     for (int c = 0; c < NB; c += 16) {
       uint32_t v[16];
       tmem_ld16(tmem + (uint32_t(q * 32) << 16) + uint32_t(c), v);
+      if (S > 1) {
 #pragma unroll
-      for (int e = 0; e < 16; ++e) part[(c + e) * BMW + f] = __uint_as_float(v[e]);
+        for (int e = 0; e < 16; ++e) part[(c + e) * BMW + f] = __uint_as_float(v[e]);
+      } else if (n < N) {
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          const int bcol = c + e;
+          if (bcol >= ncols) break;
+          const float a = __uint_as_float(v[e]);
+          const int64_t o = int64_t(bcol) * ldc + n;
+          if constexpr (EPI == int(Epi::kStore)) {
+            static_cast<bf16*>(Cv)[o] = __float2bfloat16_rn(a);
+          } else if constexpr (EPI == int(Epi::kGelu)) {
+            static_cast<bf16*>(Cv)[o] = __float2bfloat16_rn(gelu_tanh(a));
+          } else if constexpr (EPI == int(Epi::kAddResidual)) {
+            static_cast<float*>(Cv)[o] += a;
+          } else {
+            static_cast<float*>(Cv)[o] = a;
+          }
+        }
+      }
+      if (EPI == int(Epi::kAddResidual) && S == 1 && so.p) {
+        // per-row partial statistics of the updated residual over this tile's
+        // 128 features: warp reduce, 4 warp partials parked in smem (sX is free)
+        float* wred = reinterpret_cast<float*>(sX);  // [4][NB][2]
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          const int bcol = c + e;
+          float xv = 0.f;
+          if (n < N && bcol < ncols) xv = static_cast<const float*>(Cv)[int64_t(bcol) * ldc + n];
+          const float s1 = warp_sum(xv), s2 = warp_sum(xv * xv);
+          if (lane == 0) {
+            wred[(q * NB + bcol) * 2] = s1;
+            wred[(q * NB + bcol) * 2 + 1] = s2;
+          }
+        }
+      }
+    }
+    if (EPI == int(Epi::kAddResidual) && S == 1 && so.p) {
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      const float* wred = reinterpret_cast<const float*>(sX);
+      for (int bcol = threadIdx.x - 64; bcol < ncols; bcol += 128) {
+        double s1 = 0.0, s2 = 0.0;
+        for (int w4 = 0; w4 < 4; ++w4) {
+          s1 += wred[(w4 * NB + bcol) * 2];
+          s2 += wred[(w4 * NB + bcol) * 2 + 1];
+        }
+        so.p[(int64_t(blockIdx.x) * so.ld + bcol) * 2] = s1;
+        so.p[(int64_t(blockIdx.x) * so.ld + bcol) * 2 + 1] = s2;
+      }
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  cluster.sync();  // all partials of the cluster are parked in smem
-  // reduce feature rows [f0, f1) of this CTA over the S partials, in rank
-  // order: float4 DSMEM loads, all S issued before the adds
-  const int rows_per = ((BMW / S) + 3) & ~3;  // multiple of 4 features
-  const int f0 = r * rows_per, f1 = min(BMW, f0 + rows_per);
-  const int nf4 = (f1 - f0) / 4;
-  const int ncols = min(Mrows, NB);
-  const float4* parts[8];
-  for (int k = 0; k < 8; ++k) parts[k] = reinterpret_cast<const float4*>(cluster.map_shared_rank(part, k < S ? k : 0));
-  for (int e = threadIdx.x; e < nf4 * ncols; e += kThreads) {
-    const int fl = f0 + 4 * (e % nf4), bcol = e / nf4;
-    const int idx = (bcol * BMW + fl) >> 2;
-    float4 v[8];
-#pragma unroll
+  if (S > 1) {
+    cluster.sync();  // all partials of the cluster are parked in smem
+    // reduce feature rows [f0, f1) of this CTA over the S partials, in rank
+    // order: float4 DSMEM loads, all S issued before the adds
+    const int rows_per = ((BMW / S) + 3) & ~3;  // multiple of 4 features
+    const int f0 = r * rows_per, f1 = min(BMW, f0 + rows_per);
+    const int nf4 = (f1 - f0) / 4;
+    const int ncols = min(Mrows, NB);
+    const float4* parts[8];
     for (int k = 0; k < 8; ++k)
-      if (k < S) v[k] = parts[k][idx];
-    float4 acc = v[0];
+      parts[k] = reinterpret_cast<const float4*>(cluster.map_shared_rank(part, k < S ? k : 0));
+    for (int e = threadIdx.x; e < nf4 * ncols; e += kThreads) {
+      const int fl = f0 + 4 * (e % nf4), bcol = e / nf4;
+      const int idx = (bcol * BMW + fl) >> 2;
+      float4 v[8];
 #pragma unroll
-    for (int k = 1; k < 8; ++k)
-      if (k < S) {
-        acc.x += v[k].x;
-        acc.y += v[k].y;
-        acc.z += v[k].z;
-        acc.w += v[k].w;
+      for (int k = 0; k < 8; ++k)
+        if (k < S) v[k] = parts[k][idx];
+      float4 acc = v[0];
+#pragma unroll
+      for (int k = 1; k < 8; ++k)
+        if (k < S) {
+          acc.x += v[k].x;
+          acc.y += v[k].y;
+          acc.z += v[k].z;
+          acc.w += v[k].w;
+        }
+      const float a4[4] = {acc.x, acc.y, acc.z, acc.w};
+      double ps = 0.0, pq = 0.0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int nn = n0 + fl + j;
+        if (nn >= N) break;
+        const float a = a4[j];
+        const int64_t o = int64_t(bcol) * ldc + nn;
+        if constexpr (EPI == int(Epi::kStore)) {
+          static_cast<bf16*>(Cv)[o] = __float2bfloat16_rn(a);
+        } else if constexpr (EPI == int(Epi::kGelu)) {
+          static_cast<bf16*>(Cv)[o] = __float2bfloat16_rn(gelu_tanh(a));
+        } else if constexpr (EPI == int(Epi::kAddResidual)) {
+          float* xp = static_cast<float*>(Cv) + o;
+          const float nv = *xp + a;
+          *xp = nv;
+          ps += double(nv);
+          pq += double(nv) * double(nv);
+        } else {
+          static_cast<float*>(Cv)[o] = a;
+        }
       }
-    const float a4[4] = {acc.x, acc.y, acc.z, acc.w};
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int n = n0 + fl + j;
-      if (n >= N) break;
-      const float a = a4[j];
-      const int64_t o = int64_t(bcol) * ldc + n;
-      if constexpr (EPI == int(Epi::kStore)) {
-        static_cast<bf16*>(Cv)[o] = __float2bfloat16_rn(a);
-      } else if constexpr (EPI == int(Epi::kGelu)) {
-        static_cast<bf16*>(Cv)[o] = __float2bfloat16_rn(gelu_tanh(a));
-      } else if constexpr (EPI == int(Epi::kAddResidual)) {
-        static_cast<float*>(Cv)[o] += a;
-      } else {
-        static_cast<float*>(Cv)[o] = a;
+      if (EPI == int(Epi::kAddResidual) && so.p) {
+        double2* red = reinterpret_cast<double2*>(sX);  // [ncols][nf4], the X ring is idle now
+        red[bcol * nf4 + (e % nf4)] = make_double2(ps, pq);
       }
     }
+    if (EPI == int(Epi::kAddResidual) && so.p) {
+      __syncthreads();
+      const double2* red = reinterpret_cast<const double2*>(sX);
+      const int slice = blockIdx.x * S + r;
+      for (int bcol = threadIdx.x; bcol < ncols; bcol += kThreads) {
+        double s1 = 0.0, s2 = 0.0;
+        for (int g4 = 0; g4 < nf4; ++g4) {
+          s1 += red[bcol * nf4 + g4].x;
+          s2 += red[bcol * nf4 + g4].y;
+        }
+        so.p[(int64_t(slice) * so.ld + bcol) * 2] = s1;
+        so.p[(int64_t(slice) * so.ld + bcol) * 2 + 1] = s2;
+      }
+    }
+    cluster.sync();  // keep our smem alive until every peer has read it
+  } else {
+    __syncthreads();
   }
-  cluster.sync();  // keep our smem alive until every peer has read it
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(L::kTmemCols));
   }
 }
 
-template <int NB, int EPI>
-void launch_dec(Ctx& c, const bf16* X, int64_t ldx, const bf16* W, int64_t ldw, int64_t M, int64_t N, int64_t K,
-                void* C, int64_t ldc) {
+template <int NB, int EPI, bool LNIN>
+int launch_dec(Ctx& c, const bf16* X, int64_t ldx, const bf16* W, int64_t ldw, int64_t M, int64_t N, int64_t K,
+               void* C, int64_t ldc, const LnIn* ln, const RowStats* so) {
   using L = DecLayout<NB>;
   const CUtensorMap tw = make_map(W, N, K, ldw, BMW);
-  const CUtensorMap tx = make_map(X, M, K, ldx, NB);
-  auto k = gemm_decode_kernel<NB, EPI>;
+  // LN mode never reads X through TMA; any valid map will do
+  const CUtensorMap tx = LNIN ? tw : make_map(X, M, K, ldx, NB);
+  auto k = gemm_decode_kernel<NB, EPI, LNIN>;
   static bool attr = false;
   if (!attr) {
-    PPOEXP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kBytes));
+    PPOEXP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kSmemMax));
     PPOEXP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     attr = true;
   }
   const int tiles = int(ceil_div(N, BMW));
   const int nk = int(ceil_div(K, BK));
-  // K-split: aim for >= ~148 CTAs, at most 8 (portable cluster), >= 2 k-blocks each
+  // K-split over a cluster: enough CTAs to stream the weights in parallel
+  // (~148 target, <= 4 ranks: measured best on B200), >= 2 k-blocks each, and
+  // always enough that a CTA's slice fits the smem weight ring.
   static const int smax = [] {
     const char* e = getenv("PPOEXP_DECODE_SPLIT_MAX");
     return e ? atoi(e) : 4;
   }();
-  static const int target = [] {
-    const char* e = getenv("PPOEXP_DECODE_CTA_TARGET");
-    return e ? atoi(e) : 148;
-  }();
   int S = 1;
-  while (S < smax && tiles * S < target && nk >= 2 * S) S *= 2;
+  while (S < smax && tiles * S < 148 && nk >= 2 * S) S *= 2;
+  while (S < 8 && ceil_div(nk, S) > L::kWcap) S *= 2;
+  static const int wring = [] {
+    const char* e = getenv("PPOEXP_DECODE_WRING");
+    return e ? atoi(e) : 4;
+  }();
+  const int wst = int(std::min<int64_t>(std::min<int64_t>(L::kWcap, wring), ceil_div(nk, S)));
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(tiles, S, 1);
   cfg.blockDim = dim3(kThreads, 1, 1);
-  cfg.dynamicSmemBytes = L::kBytes;
+  cfg.dynamicSmemBytes = L::bytes(wst) + wst * 16;
   cfg.stream = c.stream;
   cudaLaunchAttribute attrs[2];
   attrs[0].id = cudaLaunchAttributeClusterDimension;
@@ -274,22 +437,35 @@ void launch_dec(Ctx& c, const bf16* X, int64_t ldx, const bf16* W, int64_t ldw, 
   attrs[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attrs;
   cfg.numAttrs = 2;
+  const LnIn lnv = ln ? *ln : LnIn{};
+  const RowStats sov = (so && EPI == int(Epi::kAddResidual)) ? *so : RowStats{nullptr, 0};
   const double flops = 2.0 * M * N * K;
-  const double bytes = 2.0 * (N * K + M * K) + double(M) * N * ((EPI == 0 || EPI == 1) ? 2 : 4);
+  const double bytes = 2.0 * N * K + double(M) * K * (LNIN ? 4 : 2) + double(M) * N * ((EPI == 0 || EPI == 1) ? 2 : 4);
   c.launch("gemm_decode", bytes, flops, [&] {
-    PPOEXP_CUDA(cudaLaunchKernelEx(&cfg, k, tw, tx, int(M), int(N), int(K), C, ldc, S));
+    PPOEXP_CUDA(cudaLaunchKernelEx(&cfg, k, tw, tx, int(M), int(N), int(K), C, ldc, S, wst, lnv, sov));
   });
+  return sov.p ? (S > 1 ? tiles * S : tiles) : 0;
 }
 
-template <int NB>
-void dispatch(Ctx& c, const bf16* X, int64_t ldx, const bf16* W, int64_t ldw, int64_t M, int64_t N, int64_t K,
-              Epi epi, void* C, int64_t ldc) {
+template <int NB, bool LNIN>
+int dispatch(Ctx& c, const bf16* X, int64_t ldx, const bf16* W, int64_t ldw, int64_t M, int64_t N, int64_t K, Epi epi,
+             void* C, int64_t ldc, const LnIn* ln, const RowStats* so) {
   switch (epi) {
-    case Epi::kStore: return launch_dec<NB, 0>(c, X, ldx, W, ldw, M, N, K, C, ldc);
-    case Epi::kGelu: return launch_dec<NB, 1>(c, X, ldx, W, ldw, M, N, K, C, ldc);
-    case Epi::kAddResidual: return launch_dec<NB, 2>(c, X, ldx, W, ldw, M, N, K, C, ldc);
-    case Epi::kStoreF32: return launch_dec<NB, 3>(c, X, ldx, W, ldw, M, N, K, C, ldc);
+    case Epi::kStore: return launch_dec<NB, 0, LNIN>(c, X, ldx, W, ldw, M, N, K, C, ldc, ln, so);
+    case Epi::kGelu: return launch_dec<NB, 1, LNIN>(c, X, ldx, W, ldw, M, N, K, C, ldc, ln, so);
+    case Epi::kAddResidual: return launch_dec<NB, 2, LNIN>(c, X, ldx, W, ldw, M, N, K, C, ldc, ln, so);
+    case Epi::kStoreF32: return launch_dec<NB, 3, LNIN>(c, X, ldx, W, ldw, M, N, K, C, ldc, ln, so);
   }
+  return 0;
+}
+
+template <bool LNIN>
+int dispatch_nb(Ctx& c, const bf16* X, int64_t ldx, const bf16* W, int64_t ldw, int64_t M, int64_t N, int64_t K,
+                Epi epi, void* C, int64_t ldc, const LnIn* ln, const RowStats* so) {
+  if (M <= 32) return dispatch<32, LNIN>(c, X, ldx, W, ldw, M, N, K, epi, C, ldc, ln, so);
+  if (M <= 64) return dispatch<64, LNIN>(c, X, ldx, W, ldw, M, N, K, epi, C, ldc, ln, so);
+  if (M <= 128) return dispatch<128, LNIN>(c, X, ldx, W, ldw, M, N, K, epi, C, ldc, ln, so);
+  return dispatch<256, LNIN>(c, X, ldx, W, ldw, M, N, K, epi, C, ldc, ln, so);
 }
 
 }  // namespace
@@ -298,10 +474,18 @@ void dispatch(Ctx& c, const bf16* X, int64_t ldx, const bf16* W, int64_t ldw, in
 bool gemm_decode_bf16(Ctx& c, const bf16* A, int64_t lda, const bf16* B, int64_t ldb, int64_t M, int64_t N, int64_t K,
                       Epi epi, void* C, int64_t ldc) {
   if (M > 256 || M <= 0) return false;
-  if (M <= 32) return dispatch<32>(c, A, lda, B, ldb, M, N, K, epi, C, ldc), true;
-  if (M <= 64) return dispatch<64>(c, A, lda, B, ldb, M, N, K, epi, C, ldc), true;
-  if (M <= 128) return dispatch<128>(c, A, lda, B, ldb, M, N, K, epi, C, ldc), true;
-  return dispatch<256>(c, A, lda, B, ldb, M, N, K, epi, C, ldc), true;
+  dispatch_nb<false>(c, A, lda, B, ldb, M, N, K, epi, C, ldc, nullptr, nullptr);
+  return true;
+}
+
+int gemm_decode_fused(Ctx& c, const bf16* X, int64_t ldx, const bf16* W, int64_t ldw, int64_t M, int64_t N, int64_t K,
+                      Epi epi, void* C, int64_t ldc, const LnIn* ln, const RowStats* so) {
+  if (M > 256 || M <= 0) throw ContractError("decode GEMM: batch above 256");
+  if (ln) {
+    if (K % 8 || ln->d != K) throw ContractError("decode GEMM: fused LayerNorm needs K == d_model, K % 8 == 0");
+    return dispatch_nb<true>(c, X, ldx, W, ldw, M, N, K, epi, C, ldc, ln, so);
+  }
+  return dispatch_nb<false>(c, X, ldx, W, ldw, M, N, K, epi, C, ldc, ln, so);
 }
 
 }  // namespace ppx

@@ -34,6 +34,35 @@ template <class T>
 void launch_gemm(Ctx& c, const T* A, int64_t lda, const T* B, int64_t ldb, int64_t M, int64_t N, int64_t K,
                  Epi epi, void* C, int64_t ldc);
 
+// ---- decode-path LayerNorm fusion (bf16 engine) ----
+// Row statistics travel as fp64 partial sums in slices:
+//   p[(slice * ld + row) * 2 + {0, 1}] = {sum x, sum x^2} over that slice's features.
+// Residual-producing decode GEMMs (and the embedding) write them; consumer
+// GEMMs normalise their activation K-slice on the fly (LN = src/model.cpp:387-400).
+struct RowStats {
+  double* p;
+  int ld;
+};
+struct LnIn {
+  const float* x;      // fp32 residual stream [rows, d]
+  int64_t ldx;
+  const double* stats; // RowStats of x
+  int n_slices;
+  int ld;
+  const float* g;
+  const float* b;
+  int d;
+};
+// Decode GEMM with optional fused LN on the activation operand (ln != null:
+// X is ignored) and optional row statistics of the updated residual (so != null,
+// Epi::kAddResidual only).  Returns the number of stat slices written.
+int gemm_decode_fused(Ctx& c, const bf16* X, int64_t ldx, const bf16* W, int64_t ldw, int64_t M, int64_t N, int64_t K,
+                      Epi epi, void* C, int64_t ldc, const LnIn* ln, const RowStats* so);
+// Embedding that also writes the row statistics of x (one slice).
+template <class T>
+void launch_embed_stats(Ctx& c, const int32_t* tokens, const int32_t* positions, int64_t rows, int64_t d,
+                        const T* tok, const T* pos, float* x, RowStats so);
+
 // K4: scatter the K/V columns of packed qkv rows into the paged pool
 // (prefill).  seq_of_row / pos_of_row per packed row; block_table [B, max_pages].
 template <class T>

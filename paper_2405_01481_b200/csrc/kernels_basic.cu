@@ -107,6 +107,52 @@ void launch_embed(Ctx& c, const int32_t* tokens, const int32_t* positions, int64
   });
 }
 
+template <class T>
+__global__ void __launch_bounds__(256) embed_stats_kernel(const int32_t* __restrict__ tokens,
+                                                          const int32_t* __restrict__ positions, int64_t rows,
+                                                          int64_t d, const T* __restrict__ tok,
+                                                          const T* __restrict__ pos, float* __restrict__ x,
+                                                          RowStats so) {
+  PDL_ENTRY();
+  __shared__ double red[2][8];
+  const int64_t r = blockIdx.x;
+  if (r >= rows) return;
+  const int64_t t = tokens[r], p = positions[r];
+  double s = 0.0, q = 0.0;
+  for (int64_t j = threadIdx.x; j < d; j += blockDim.x) {
+    const float v = to_f(tok[t * d + j]) + to_f(pos[p * d + j]);
+    x[r * d + j] = v;
+    s += double(v);
+    q += double(v) * double(v);
+  }
+  s = warp_sum_d(s);
+  q = warp_sum_d(q);
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) {
+    red[0][w] = s;
+    red[1][w] = q;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0, c = 0.0;
+    for (int k = 0; k < 8; ++k) {
+      a += red[0][k];
+      c += red[1][k];
+    }
+    so.p[(int64_t(0) * so.ld + r) * 2] = a;
+    so.p[(int64_t(0) * so.ld + r) * 2 + 1] = c;
+  }
+}
+
+template <class T>
+void launch_embed_stats(Ctx& c, const int32_t* tokens, const int32_t* positions, int64_t rows, int64_t d,
+                        const T* tok, const T* pos, float* x, RowStats so) {
+  if (rows <= 0) return;
+  c.launch("embed", double(rows) * d * (2 * sizeof(T) + 4), 0, [&] {
+    launch_kernel(c, embed_stats_kernel<T>, dim3(rows), dim3(256), 0, 1, tokens, positions, rows, d, tok, pos, x, so);
+  });
+}
+
 template <int NT>
 __device__ __forceinline__ float block_sum(float v, float* red) {
   v = warp_sum(v);
@@ -411,6 +457,8 @@ void launch_fill_i32(Ctx& c, int32_t* dst, int64_t n, int32_t v) {
 }
 
 #define INST(T)                                                                                                   \
+  template void launch_embed_stats<T>(Ctx&, const int32_t*, const int32_t*, int64_t, int64_t, const T*, const T*, \
+                                      float*, RowStats);                                                         \
   template void launch_embed<T>(Ctx&, const int32_t*, const int32_t*, int64_t, int64_t, const T*, const T*,      \
                                 float*);                                                                        \
   template void launch_layernorm<T>(Ctx&, const float*, int64_t, int64_t, const float*, const float*, T*,       \

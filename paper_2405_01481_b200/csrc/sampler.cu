@@ -26,11 +26,11 @@ namespace ppx {
 namespace {
 constexpr int NT = 1024, NW = NT / 32, NB = 1024, LIST = 1024;
 constexpr int64_t kCacheMaxV = 50600;
-constexpr double kFix = 1.0 / 4294967296.0;  // 2^-32
+constexpr double kFix = 1.0 / 65536.0;  // 2^-16 (V * 2^16 < 2^32: no overflow)
 
 struct Shared {
   unsigned hcnt[NB];
-  unsigned long long hsum[NB];  // fixed point q * 2^32 (native 64-bit smem atomics; no CAS loop)
+  unsigned hsum[NB];  // approximate bucket sums, fixed point q * 2^16 (native 32-bit smem atomics)
   unsigned long long list[LIST];
   float fm[NW], fmn[NW], fs[NW];
   int fi[NW];
@@ -141,22 +141,18 @@ __global__ void __launch_bounds__(NT) sampler_kernel(const float* __restrict__ l
   const float* row = logits + b * ld;
   const int i = s.n_gen[b];
 
-  // ---- pass 1: max, min, first argmax, online sum exp(l - max)
-  float m = -INFINITY, mn = INFINITY, se = 0.f;
+  // ---- pass 1: max, min, first argmax (16-byte loads; ascending index per
+  // thread keeps "first index wins" exact)
+  float m = -INFINITY, mn = INFINITY;
   int am = 0x7fffffff;
   auto visit = [&](float v, int j) {
     if (v > m) {
-      se = se * expf(m - v) + 1.f;
       m = v;
       am = j;
-    } else {
-      se += expf(v - m);
     }
     mn = fminf(mn, v);
   };
   {
-    // 16-byte loads, 2 in flight per thread; index order within a thread is
-    // ascending, so "first index wins" ties stay exact
     const int64_t nv = V / 4;
     const float4* r4 = reinterpret_cast<const float4*>(row);
     int64_t k = tid;
@@ -176,18 +172,13 @@ __global__ void __launch_bounds__(NT) sampler_kernel(const float* __restrict__ l
   for (int o = 16; o > 0; o >>= 1) {
     const float m2 = __shfl_xor_sync(0xffffffffu, m, o);
     const int a2 = __shfl_xor_sync(0xffffffffu, am, o);
-    const float s2 = __shfl_xor_sync(0xffffffffu, se, o);
     mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-    const float Mx = fmaxf(m, m2);
-    const float sc = (m == -INFINITY ? 0.f : se * expf(m - Mx)) + (m2 == -INFINITY ? 0.f : s2 * expf(m2 - Mx));
     am = m > m2 ? am : (m2 > m ? a2 : min(am, a2));
-    m = Mx;
-    se = sc;
+    m = fmaxf(m, m2);
   }
   if (lane == 0) {
     sh.fm[w] = m;
     sh.fi[w] = am;
-    sh.fs[w] = se;
     sh.fmn[w] = mn;
   }
   __syncthreads();
@@ -198,9 +189,21 @@ __global__ void __launch_bounds__(NT) sampler_kernel(const float* __restrict__ l
     M = fmaxf(M, sh.fm[k]);
     MN = fminf(MN, sh.fmn[k]);
   }
-  float SE = 0.f;
-  for (int k = 0; k < NW; ++k) SE += sh.fm[k] == -INFINITY ? 0.f : sh.fs[k] * expf(sh.fm[k] - M);
-  const float lse = M + logf(SE);
+  // sum exp(l - M) for the untempered log-prob (src/model.cpp:450); when the
+  // row is sampled at tau == 1 it is folded into pass 2 (q == exp(l - M))
+  const bool fold = !prm.greedy && prm.temperature == 1.0f;
+  float lse = 0.f;
+  if (!fold) {
+    float se = 0.f;
+    for (int64_t j = tid; j < V; j += NT) se += expf(row[j] - M);
+    se = warp_sum(se);
+    __syncthreads();
+    if (lane == 0) sh.fs[w] = se;
+    __syncthreads();
+    float SE = 0.f;
+    for (int k = 0; k < NW; ++k) SE += sh.fs[k];
+    lse = M + logf(SE);
+  }
 
   int chosen = AM;
   if (!prm.greedy) {
@@ -222,19 +225,29 @@ __global__ void __launch_bounds__(NT) sampler_kernel(const float* __restrict__ l
     if (filtering)
       for (int k = tid; k < NB; k += NT) {
         sh.hcnt[k] = 0;
-        sh.hsum[k] = 0ull;
+        sh.hsum[k] = 0u;
       }
     __syncthreads();
     double zloc = 0.0;
+    float fsum = 0.f;
     for (int64_t j = tid; j < V; j += NT) {
       const float q = expf((row[j] - M) * inv_tau);
       if constexpr (CACHED) qcache[j] = q;
+      fsum += q;
       if (filtering) {
         zloc += double(q);
         const int bk = bucket_of(qbits_of(q), top, scale);
         atomicAdd(&sh.hcnt[bk], 1u);
-        atomicAdd(&sh.hsum[bk], (unsigned long long)(double(q) * 4294967296.0));
+        atomicAdd(&sh.hsum[bk], __float2uint_rn(q * 65536.0f));
       }
+    }
+    if (fold) {  // lse from the same exp pass (tau == 1)
+      fsum = warp_sum(fsum);
+      if (lane == 0) sh.fs[w] = fsum;
+      __syncthreads();
+      float SE = 0.f;
+      for (int k = 0; k < NW; ++k) SE += sh.fs[k];
+      lse = M + logf(SE);
     }
     __syncthreads();
     unsigned t_final = 0;
@@ -314,22 +327,50 @@ __global__ void __launch_bounds__(NT) sampler_kernel(const float* __restrict__ l
           if (hs > 0.0) atomicMax(&sh.bp, tid);
           __syncthreads();
         }
-        const int bp = sh.bp;
-        if (tid == bp) sh.s_above = ex;
+        // the fixed-point histogram only locates the crossing approximately:
+        // confirm it with exact fp64 sums (no atomics) and step to a neighbour
+        // bucket if rounding put it one off
+        int bp = sh.bp;
+        for (int guard = 0; guard < NB; ++guard) {
+          double lt = 0.0, eq = 0.0;
+          for (int64_t j = tid; j < V; j += NT) {
+            const float q = Q(j);
+            const unsigned qb = qbits_of(q);
+            const int bj = bucket_of(qb, top, scale);
+            const bool inK = bj < bk || (bj == bk && (qb > k_t || (qb == k_t && j <= k_cut)));
+            if (!inK) continue;
+            if (bj < bp) lt += double(q);
+            else if (bj == bp) eq += double(q);
+          }
+          lt = block_sum_d(lt, sh);
+          eq = block_sum_d(eq, sh);
+          if (target <= lt && bp > 0) {
+            --bp;
+          } else if (target > lt + eq && bp < min(bk, NB - 1) && eq >= 0.0 && lt + eq < target) {
+            ++bp;
+          } else {
+            if (tid == 0) sh.s_above = lt;
+            break;
+          }
+        }
         __syncthreads();
         if (bp != bk) collect_sort(bp);  // bp == bk reuses the top-k sorted list
-        if (!sh.overflow && tid == 0) {
+        if (!sh.overflow) {
+          // first sorted member r with s_above + sum_{<=r} q >= target, as a block scan
           const int limit = bp == bk ? k_take : min(sh.list_n, LIST);
-          double acc = sh.s_above;
-          int r = 0;
-          for (; r < limit; ++r) {
-            acc += double(key_q(sh.list[r]));
-            if (acc >= target) break;
+          const double qv = tid < limit ? double(key_q(sh.list[tid])) : 0.0;
+          double tot;
+          const double ex = block_excl_scan<double>(qv, sh.dwarp, tot);
+          if (tid == 0) sh.result = 0x7fffffff;
+          __syncthreads();
+          if (tid < limit && sh.s_above + ex + qv >= target) atomicMin(&sh.result, tid);
+          __syncthreads();
+          if (tid == 0) {
+            const int r = sh.result != 0x7fffffff ? sh.result : limit - 1;
+            const unsigned long long e = sh.list[r];
+            sh.t_final = ~unsigned(e >> 32);
+            sh.idx_cut = int(e & 0xffffffffu);
           }
-          if (r >= limit) r = limit - 1;
-          const unsigned long long e = sh.list[r];
-          sh.t_final = ~unsigned(e >> 32);
-          sh.idx_cut = int(e & 0xffffffffu);
         }
         __syncthreads();
         k_t = sh.t_final;
@@ -413,60 +454,49 @@ __global__ void __launch_bounds__(NT) sampler_kernel(const float* __restrict__ l
       t_final = k_t;
       idx_cut = k_cut;
     }
-    // ---- inverse CDF in index order over the kept tokens
+    // ---- inverse CDF in index order over the kept tokens: every thread owns a
+    // contiguous chunk (sequential fp64 sums), one block scan, and the thread
+    // whose chunk brackets u*Z walks it (src/model.cpp:464-473 semantics)
     auto kept = [&](int64_t j, float& q) -> bool {
       q = Q(j);
       if (!filtering) return true;
       const unsigned qb = qbits_of(q);
       return qb > t_final || (qb == t_final && j <= idx_cut);
     };
-    const int64_t CW = ((V + NW - 1) / NW + 31) / 32 * 32;
-    const int64_t w0 = int64_t(w) * CW, w1 = (V < w0 + CW ? V : w0 + CW);
-    double wsum = 0.0;
+    const int64_t CH = (V + NT - 1) / NT;
+    const int64_t c0 = int64_t(tid) * CH, c1 = (V < c0 + CH ? V : c0 + CH);
+    double csum = 0.0;
     int last = -1;
-    for (int64_t j = w0 + lane; j < w1; j += 32) {
+    for (int64_t j = c0; j < c1; ++j) {
       float q;
       if (kept(j, q)) {
-        wsum += double(q);
+        csum += double(q);
         last = int(j);
       }
     }
-    wsum = warp_sum_d(wsum);
+    double total;
+    const double prefix = block_excl_scan<double>(csum, sh.dwarp, total);
+    int lk = last;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) last = max(last, __shfl_xor_sync(0xffffffffu, last, o));
-    if (lane == 0) {
-      sh.dsum[w] = wsum;
-      sh.lk[w] = last;
-    }
+    for (int o = 16; o > 0; o >>= 1) lk = max(lk, __shfl_xor_sync(0xffffffffu, lk, o));
+    if (lane == 0) sh.lk[w] = lk;
     if (tid == 0) sh.result = 0x7fffffff;
     __syncthreads();
-    double prefix = 0.0, total = 0.0;
     int fallback = -1;
-    for (int k = 0; k < NW; ++k) {
-      if (k < w) prefix += sh.dsum[k];
-      total += sh.dsum[k];
-      fallback = max(fallback, sh.lk[k]);
-    }
+    for (int k = 0; k < NW; ++k) fallback = max(fallback, sh.lk[k]);
     const double u = s.uniforms[b * s.ustride + i];
     const double target = u * total;
-    if (prefix <= target && target < prefix + sh.dsum[w] * (1.0 + 1e-12) + 1e-300) {
+    if (csum > 0.0 && prefix <= target && target < prefix + csum * (1.0 + 1e-12)) {
       double acc = prefix;
-      for (int64_t base = w0; base < w1; base += 32) {
-        const int64_t j = base + lane;
-        float q = 0.f;
-        const bool k = j < w1 && kept(j, q);
-        double v = k ? double(q) : 0.0;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const double t = __shfl_up_sync(0xffffffffu, v, o);
-          if (lane >= o) v += t;
+      for (int64_t j = c0; j < c1; ++j) {
+        float q;
+        if (kept(j, q)) {
+          acc += double(q);
+          if (target < acc) {
+            atomicMin(&sh.result, int(j));
+            break;
+          }
         }
-        const unsigned hit = __ballot_sync(0xffffffffu, k && target < acc + v);
-        if (hit) {
-          if (lane == 0) atomicMin(&sh.result, int(base + __ffs(hit) - 1));
-          break;
-        }
-        acc += __shfl_sync(0xffffffffu, v, 31);
       }
     }
     __syncthreads();

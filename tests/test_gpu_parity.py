@@ -306,3 +306,28 @@ def test_sampler_massive_ties(px, ctx, oracle, top_k, top_p):
     t_o, _ = oracle.generate(cfg, w, prompts, 6, greedy=False, top_k=top_k, top_p=top_p, uniforms=u)
     for r, t in zip(res, t_o):
         assert np.array_equal(r.tokens, t)
+
+
+def test_bf16_fused_layernorm_matches_unfused(px, ctx, oracle, monkeypatch):
+    """The decode path's fused LayerNorm (row-statistic slices + on-the-fly
+    normalisation in the consumer GEMMs) against the standalone LN kernels."""
+    cfg = ModelCfg(V=4096, d=256, L=3, H=4, f=1024, S=128)
+    wb = bf16_round(oracle.init_params(cfg, 21))
+    prompts = synthetic_prompts(8, 16, 12, ragged_lengths=True)
+    outs = {}
+    for flag in ("0", "1"):
+        monkeypatch.setenv("PPOEXP_FUSE_LN", flag)
+        eng = engine(px, ctx, cfg, wb, px.BF16)
+        outs[flag] = eng.generate_batch([px.GenTask(p, 40) for p in prompts])
+    same = 0
+    for a, b, p in zip(outs["0"], outs["1"], prompts):
+        n = 0
+        while n < min(len(a.tokens), len(b.tokens)) and a.tokens[n] == b.tokens[n]:
+            n += 1
+        same += n == len(a.tokens)
+        close(b.logprobs[:n], a.logprobs[:n], atol=2e-2, rtol=2e-3)
+        # and the fused run is itself consistent with the oracle, teacher-forced
+        full = np.concatenate([p, b.tokens])
+        lp = oracle.sequence_logprobs(cfg, wb, [full])[0][len(p):]
+        close(b.logprobs, lp, atol=3e-2, rtol=3e-3)
+    assert same >= len(prompts) // 2
