@@ -415,8 +415,13 @@ int launch_dec(Ctx& c, const bf16* X, int64_t ldx, const bf16* W, int64_t ldw, i
     const char* e = getenv("PPOEXP_DECODE_SPLIT_MAX");
     return e ? atoi(e) : 4;
   }();
+  static const int smax_small = [] {  // narrow outputs (N <= 1024: O / down projections)
+    const char* e = getenv("PPOEXP_DECODE_SPLIT_SMALLN");
+    return e ? atoi(e) : 8;
+  }();
+  const int cap = tiles <= 8 ? smax_small : smax;
   int S = 1;
-  while (S < smax && tiles * S < 148 && nk >= 2 * S) S *= 2;
+  while (S < cap && tiles * S < 148 && nk >= 2 * S) S *= 2;
   while (S < 8 && ceil_div(nk, S) > L::kWcap) S *= 2;
   static const int wring = [] {
     const char* e = getenv("PPOEXP_DECODE_WRING");

@@ -18,8 +18,11 @@ def launches(path, out, skip=0.0):
             hdr, start = r, i + 1
             break
     ki, vi, gi, bi = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Grid Size"), hdr.index("Block Size")
-    data = [(re.sub(r"\(.*", "", r[ki]).replace("void ", ""), r[gi], r[bi], float(r[vi].replace(",", "")) / 1000)
-            for r in rows[start:] if len(r) > vi]
+    mi, ui = hdr.index("Metric Name"), hdr.index("Metric Unit")
+    scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}
+    data = [(re.sub(r"\(.*", "", r[ki]).replace("void ", ""), r[gi], r[bi],
+             float(r[vi].replace(",", "")) * scale.get(r[ui], 1e-3))
+            for r in rows[start:] if len(r) > vi and r[mi] == "gpu__time_duration.sum"]
     data = data[int(len(data) * skip):]
     agg = collections.defaultdict(lambda: [0, 0.0])
     for n, g, b, v in data:
@@ -41,7 +44,7 @@ def full(rep, out):
     mi, vi, ui, si, ki = (h.index(x) for x in ("Metric Name", "Metric Value", "Metric Unit", "Section Name", "Kernel Name"))
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rr = list(csv.reader(io.StringIO(raw)))
-    rawv = dict(zip(rr[0], rr[2])) if len(rr) > 2 else {}
+    rawv = {k: f"{v} {u}" for k, u, v in zip(rr[0], rr[1], rr[2])} if len(rr) > 2 else {}
     src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"], capture_output=True,
                          text=True).stdout
     s = list(csv.reader(io.StringIO(src)))
