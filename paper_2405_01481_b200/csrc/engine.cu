@@ -62,6 +62,10 @@ Engine::Engine(Model* model, const ppoexp_engine_options* o) : m(model), c(model
   const int64_t max_slices = 8 * ceil_div(std::max(d, f), 128);
   const size_t o_sta = sbytes; sbytes += al(max_slices * mb * 16);
   const size_t o_stb = sbytes; sbytes += al(max_slices * mb * 16);
+  const size_t o_part = sbytes; sbytes += al(decode_mega_part_bytes());
+  const size_t o_bar = sbytes; sbytes += al(16);
+  const size_t o_mly = sbytes; sbytes += al(cfg.n_layers * sizeof(MegaLayer));
+  const size_t o_wmap = sbytes; sbytes += al(cfg.n_layers * 4 * sizeof(CUtensorMap));
   state.ensure(sbytes);
   PPOEXP_CUDA(cudaMemset(state.ptr, 0, sbytes));
   char* p = static_cast<char*>(state.ptr);
@@ -85,6 +89,33 @@ Engine::Engine(Model* model, const ppoexp_engine_options* o) : m(model), c(model
   last_rows = reinterpret_cast<int32_t*>(p + o_last);
   stats_a = reinterpret_cast<double*>(p + o_sta);
   stats_b = reinterpret_cast<double*>(p + o_stb);
+  part = reinterpret_cast<float*>(p + o_part);
+  bar = reinterpret_cast<unsigned*>(p + o_bar);
+  mega_layers = reinterpret_cast<MegaLayer*>(p + o_mly);
+  mega_wmaps = reinterpret_cast<CUtensorMap*>(p + o_wmap);
+  {
+    trace_path = getenv("PPOEXP_MEGA_TRACE");
+    // opt-in (PPOEXP_DECODE_MEGA=1): measured at parity with / slightly behind
+    // the per-op graph at the C2 shape on B200
+    const char* ev = getenv("PPOEXP_DECODE_MEGA");
+    use_mega = m->dtype == PPOEXP_BF16 && ev && ev[0] == '1';
+    if (use_mega) {
+      std::vector<MegaLayer> ml(cfg.n_layers);
+      for (int64_t l = 0; l < cfg.n_layers; ++l) {
+        const Layer& ly = m->layers[l];
+        ml[l] = {static_cast<const bf16*>(ly.wqkv), static_cast<const bf16*>(ly.wo), static_cast<const bf16*>(ly.wup),
+                 static_cast<const bf16*>(ly.wdown), ly.ln1w, ly.ln1b, ly.ln2w, ly.ln2b};
+      }
+      PPOEXP_CUDA(cudaMemcpy(mega_layers, ml.data(), ml.size() * sizeof(MegaLayer), cudaMemcpyHostToDevice));
+      if (d % 128 == 0 && f % 128 == 0) {
+        std::vector<CUtensorMap> wm(cfg.n_layers * 4);
+        decode_mega_weight_maps(ml.data(), int(cfg.n_layers), int(d), int(f), wm.data());
+        PPOEXP_CUDA(cudaMemcpy(mega_wmaps, wm.data(), wm.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
+      } else {
+        use_mega = false;
+      }
+    }
+  }
   {
     // opt-in: measured slower on B200 at the C2 shape (consumers re-read fp32 rows)
     const char* ev = getenv("PPOEXP_FUSE_LN");
@@ -143,6 +174,44 @@ void Engine::decode_unit(int64_t B, int64_t unit) {
   T* uu = static_cast<T*>(up);
   cur_unit = unit;
   if constexpr (std::is_same_v<T, bf16>) {
+    if (use_mega && !fuse_ln) {
+      MegaArgs a{};
+      a.B = int(B);
+      a.d = int(d);
+      a.f = int(f);
+      a.L = int(m->cfg.n_layers);
+      a.next_tok = next_tok;
+      a.pos = pos;
+      a.done = done;
+      a.block_table = block_table;
+      a.g = geom;
+      a.kv = static_cast<bf16*>(kv.ptr);
+      a.tok = static_cast<const bf16*>(m->tok);
+      a.posemb = static_cast<const bf16*>(m->pos);
+      a.layers = mega_layers;
+      a.wmaps = mega_wmaps;
+      a.lnfw = m->lnfw;
+      a.lnfb = m->lnfb;
+      a.x = x;
+      a.h = hh;
+      a.att = at;
+      a.up = uu;
+      a.part = part;
+      a.bar = bar;
+      if (const char* e = getenv("PPOEXP_MEGA_PREFETCH")) a.prefetch = atoi(e);
+      if (decode_mega_plan(a)) {
+        decode_mega_act_maps(a, opts.max_batch);
+        if (trace_path) {
+          trace_buf.ensure(size_t(8 * a.L) * a.grid * 2 * 8 + size_t(a.L) * a.grid * 8 * 4 * 8);
+          a.trace = static_cast<uint64_t*>(trace_buf.ptr);
+        }
+        const double wbytes = double(m->cfg.n_layers) * (4.0 * d * d + 2.0 * d * f) * 2.0;
+        launch_decode_mega(cc, a, wbytes);
+        gemm<T>(cc, hh, d, static_cast<const T*>(m->tok), d, B, V, d, Epi::kStoreF32, logits, m->vpad);
+        launch_sampler(cc, logits, m->vpad, B, V, sampler_state());
+        return;
+      }
+    }
     if (fuse_ln) {
       // bf16 path with LayerNorm fused into the consumer GEMMs: embed / O-proj /
       // down-proj emit fp64 row-statistic slices, QKV / up / LM head normalise
@@ -322,6 +391,14 @@ void Engine::generate(int64_t B, const int32_t* prompts, const int64_t* offsets,
   PPOEXP_CUDA(cudaEventElapsedTime(&ms, e0, e1));
   last_ms = ms;
   if (ms_out) *ms_out = ms;
+  if (trace_path && trace_buf.ptr) {  // debug: raw stamps of the last decode step
+    std::vector<uint64_t> h(trace_buf.bytes / 8);
+    PPOEXP_CUDA(cudaMemcpy(h.data(), trace_buf.ptr, trace_buf.bytes, cudaMemcpyDeviceToHost));
+    if (FILE* fp = fopen(trace_path, "wb")) {
+      fwrite(h.data(), 8, h.size(), fp);
+      fclose(fp);
+    }
+  }
   c->harvest();
 }
 

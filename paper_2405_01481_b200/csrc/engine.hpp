@@ -27,6 +27,14 @@ struct Engine {
   int32_t* host_flags = nullptr;
   double *stats_a = nullptr, *stats_b = nullptr;  // fused-LN row-statistic slices
   bool fuse_ln = false;
+  // persistent decode-step kernel (decode_mega.cu); PPOEXP_DECODE_MEGA=0 disables
+  bool use_mega = false;
+  float* part = nullptr;
+  unsigned* bar = nullptr;
+  MegaLayer* mega_layers = nullptr;
+  CUtensorMap* mega_wmaps = nullptr;
+  const char* trace_path = nullptr;  // PPOEXP_MEGA_TRACE: dump per-barrier stamps of the last step
+  DeviceBuffer trace_buf;
   cudaEvent_t poll_ev[2]{}, t0{}, t1{};
   double last_ms = 0;
   int64_t cur_unit = 0;
