@@ -32,6 +32,7 @@
 
 #include <cfloat>
 
+#include "attn_core.cuh"
 #include "kernels.hpp"
 
 namespace ppx {
@@ -44,6 +45,7 @@ constexpr int kThreads = 256, kWarps = 8, kNB = 64, kBM = 128, kBK = 64, kMaxCh 
 constexpr int kWTile = kBM * kBK * 2;  // 16 KB weight chunk
 constexpr int kXTile = kNB * kBK * 2;  // 8 KB activation chunk
 constexpr int kTmemCols = 64;
+constexpr int kMaxSplit = 32;  // K splits per GEMM
 
 // ------------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ uint32_t su32(const void* p) {
@@ -132,38 +134,36 @@ __device__ __forceinline__ void prefetch_layer(const MegaLayer& ly, int d, int f
 }
 
 // ------------------------------------------------------------------ grid barrier
-// Split-phase barrier over co-resident CTAs: bar[0] = arrivals, bar[1] =
-// generation.  arrive(): every thread makes its global writes visible to the
-// async proxy (later TMA reads), CTA sync, then thread 0 releases with one
-// acq_rel atomic; the last arriver resets the count and publishes gen+1.
+// Counting barrier over co-resident CTAs on a monotonically increasing 64-bit
+// arrival counter bar[0]: barrier k of this launch completes when the counter
+// reaches base + (k+1)·G, base = bar[1] = the counter value the previous
+// launch ended at (stored by CTA 0 at exit; launches are stream-ordered).
+// arrive(): CTA sync, then thread 0 adds 1 with a fire-and-forget RELEASE
+// reduction (no return trip, no reset, no separate generation word).
 // wait(): thread 0 spins with RELAXED loads and acquires once.  Independent
 // work (the next phase's weight TMA) goes between the two.
 // Optional trace (PPOEXP_MEGA_TRACE): per barrier k and CTA, {arrive, depart}.
-__device__ __forceinline__ void grid_arrive(unsigned* bar, unsigned gen, uint64_t* trace, int k) {
-  asm volatile("fence.proxy.async.global;" ::: "memory");
+__device__ __forceinline__ void grid_arrive(unsigned long long* bar, uint64_t* trace, int k) {
   __syncthreads();
   if (threadIdx.x == 0) {
     if (trace) trace[(size_t(k) * gridDim.x + blockIdx.x) * 2] = gtimer();
-    unsigned old;
-    asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(bar) : "memory");
-    if (old == gridDim.x - 1) {
-      asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(bar), "r"(0u) : "memory");
-      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(bar + 1), "r"(gen + 1) : "memory");
-    }
+    asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(bar) : "memory");
   }
 }
-__device__ __forceinline__ void grid_wait(unsigned* bar, unsigned& gen, uint64_t* trace, int k) {
+__device__ __forceinline__ void grid_wait(unsigned long long* bar, unsigned long long target, uint64_t* trace, int k) {
   if (threadIdx.x == 0) {
-    unsigned g;
+    unsigned long long v;
     do {
-      asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(g) : "l"(bar + 1) : "memory");
-    } while (g == gen);
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(g) : "l"(bar + 1) : "memory");
+      asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(bar) : "memory");
+    } while (v < target);
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(bar) : "memory");
     if (trace) trace[(size_t(k) * gridDim.x + blockIdx.x) * 2 + 1] = gtimer();
   }
-  ++gen;
   __syncthreads();
 }
+// Writes that a later phase reads through TMA (h, att, up) are made visible
+// to the async proxy by their writers before the barrier.
+__device__ __forceinline__ void fence_for_tma() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
 
 // ------------------------------------------------------------------ CTA state
 struct Ctl {
@@ -263,6 +263,7 @@ __device__ __noinline__ void row_phase(const MegaArgs& a, int mode, int nsplit, 
     }
     __syncthreads();
   }
+  fence_for_tma();
 }
 
 // ------------------------------------------------------------------ GELU reduce
@@ -296,6 +297,7 @@ __device__ __noinline__ void gelu_phase(const MegaArgs& a, int nsplit) {
     u.y = *reinterpret_cast<uint32_t*>(&hi);
     reinterpret_cast<uint2*>(a.up)[e] = u;
   }
+  fence_for_tma();
 }
 
 // ------------------------------------------------------------------ GEMM phase
@@ -382,85 +384,83 @@ __device__ __noinline__ void gemm_phase(uint8_t* sm, Ctl& c, const GemmJob& j, i
 // ------------------------------------------------------------------ attention
 // Warp per (sequence, head).  q/k/v = Σ_s QKV partials (split order); K/V
 // are appended at pos in bf16 (src/model.cpp:305-308), then the paged cache
-// is streamed in 32-token tiles through a 3-stage cp.async ring (two tiles in
-// flight while one is consumed): lane-per-token scores, lane-per-dim P·V,
-// online softmax (src/model.cpp:313-333).  Tiles that do not hold the new
-// position are requested before the partial reduction, so the prologue's L2
-// round trip overlaps the first KV loads.
+// is streamed in 32-token tiles through a 3-stage cp.async ring into the
+// lane-per-token WarpAttn core (attn_core.cuh).  The partial loads are issued
+// first, together with the sequence's state and block-table row.
 constexpr int kStages = 3;
 template <int DH>
 __device__ __noinline__ void attn_phase(const MegaArgs& a, int layer, int nsplit, uint8_t* smr) {
-  uint64_t* st = (a.trace && (threadIdx.x & 31) == 0)
-                     ? a.trace + size_t(8 * a.L) * gridDim.x * 2 + ((size_t(layer) * gridDim.x + blockIdx.x) * kWarps + (threadIdx.x >> 5)) * 4
-                     : nullptr;
-  if (st) st[0] = st[1] = st[2] = st[3] = 0;
   constexpr int ROWB = DH * 2, LDB = ROWB + 16, CPR = ROWB / 16, DPL = DH / 32;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint64_t* st = (a.trace && lane == 0) ? a.trace + size_t(8 * a.L) * gridDim.x * 2 +
+                                              ((size_t(layer) * gridDim.x + blockIdx.x) * kWarps + w) * 4
+                                        : nullptr;
+  if (st) st[0] = st[1] = st[2] = st[3] = 0;
   uint8_t* wsm = smr + size_t(w) * kStages * 2 * kTT * LDB;
   float* qs = reinterpret_cast<float*>(smr + size_t(kWarps) * kStages * 2 * kTT * LDB) + w * DH;
-  auto tile_ptr = [&](int st, int which) { return wsm + (st * 2 + which) * kTT * LDB; };
+  auto tile_ptr = [&](int stg, int which) { return wsm + (stg * 2 + which) * kTT * LDB; };
   const int d = int(a.g.H) * DH, PS = int(a.g.page_size), d3 = 3 * d;
-  const float inv_sqrt_dh = 1.0f / sqrtf(float(DH));
+  const float scale = 1.0f / sqrtf(float(DH));
   const int64_t pstride = int64_t(a.B) * d3;
   for (int item = blockIdx.x * kWarps + w; item < a.B * a.g.H; item += gridDim.x * kWarps) {
     const int b = item / int(a.g.H), h = item % int(a.g.H);
-    if (a.done[b]) continue;
-    const int p = a.pos[b], ctx = p + 1;
     if (st) st[0] = clock64();
-    const int npg = (ctx + PS - 1) / PS;
-    const int32_t my_page = lane < npg ? a.block_table[int64_t(b) * a.g.max_pages_per_seq + lane] : 0;
+    // everything independent first: QKV partials, state, block-table row
+    float tq[8][DPL], tk[8][DPL], tv[8][DPL];
+    const float* pp = a.part + int64_t(b) * d3 + h * DH + lane * DPL;
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      if (k < nsplit) {
+        const float* ps = pp + k * pstride;
+#pragma unroll
+        for (int i = 0; i < DPL; ++i) {
+          tq[k][i] = __ldcg(ps + i);
+          tk[k][i] = __ldcg(ps + d + i);
+          tv[k][i] = __ldcg(ps + 2 * d + i);
+        }
+      }
+    const int isdone = a.done[b];
+    const int p = a.pos[b], ctx = p + 1;
+    const int32_t my_page = lane < a.g.max_pages_per_seq ? a.block_table[int64_t(b) * a.g.max_pages_per_seq + lane] : 0;
+    if (isdone) continue;
     const int64_t lbase = ((int64_t)layer * a.g.n_pages) * 2;
-    auto base = [&](int tk, int which) -> bf16* {
-      const int64_t page = __shfl_sync(0xffffffffu, my_page, tk / PS);
-      return a.kv + (((lbase + page * 2) + which) * a.g.H + h) * PS * DH + (tk % PS) * DH;
+    auto base = [&](int tk_, int which) -> bf16* {
+      const int64_t page = __shfl_sync(0xffffffffu, my_page, tk_ / PS);
+      return a.kv + (((lbase + page * 2) + which) * a.g.H + h) * PS * DH + (tk_ % PS) * DH;
     };
     auto issue = [&](int t) {  // tile t (tokens [32t, 32t+32)) into stage t % kStages
-      const int t0 = t * kTT, n = (ctx - t0) < kTT ? (ctx - t0) : kTT, st = t % kStages;
+      const int t0 = t * kTT, n = (ctx - t0) < kTT ? (ctx - t0) : kTT, stg = t % kStages;
       const uint8_t* k0 = reinterpret_cast<const uint8_t*>(base(t0, 0));
       const uint8_t* v0 = reinterpret_cast<const uint8_t*>(base(t0, 1));
       for (int e = lane; e < kTT * CPR; e += 32) {
         const int r = e / CPR, cc = e % CPR;
         if (r < n) {
-          cp16(tile_ptr(st, 0) + r * LDB + cc * 16, k0 + r * ROWB + cc * 16);
-          cp16(tile_ptr(st, 1) + r * LDB + cc * 16, v0 + r * ROWB + cc * 16);
+          cp16(tile_ptr(stg, 0) + r * LDB + cc * 16, k0 + r * ROWB + cc * 16);
+          cp16(tile_ptr(stg, 1) + r * LDB + cc * 16, v0 + r * ROWB + cc * 16);
         }
       }
     };
-    const int ntiles = (ctx + kTT - 1) / kTT, tlast = ntiles - 1;
-    // groups 0 and 1 (tiles 0, 1) are committed before the first wait; the
-    // tile holding the new position is issued only after the append
-    if (0 < tlast) issue(0);
-    cp_commit();
-    if (1 < tlast) issue(1);
-    cp_commit();
-    // q, k, v for this (b, h): lane owns dims [lane*DPL, lane*DPL + DPL)
+    const int ntiles = (ctx + kTT - 1) / kTT;
+    // remaining partials (nsplit > 8), then the sums in split order
     float qv[DPL], kv[DPL], vv[DPL];
 #pragma unroll
     for (int i = 0; i < DPL; ++i) qv[i] = kv[i] = vv[i] = 0.f;
-    {
-      const float* pp = a.part + int64_t(b) * d3 + h * DH + lane * DPL;
-      for (int s0 = 0; s0 < nsplit; s0 += 8) {
-        float tq[8][DPL], tk[8][DPL], tv[8][DPL];
 #pragma unroll
-        for (int k = 0; k < 8; ++k)
-          if (s0 + k < nsplit) {
-            const float* ps = pp + (s0 + k) * pstride;
+    for (int k = 0; k < 8; ++k)
+      if (k < nsplit)
 #pragma unroll
-            for (int i = 0; i < DPL; ++i) {
-              tq[k][i] = __ldcg(ps + i);
-              tk[k][i] = __ldcg(ps + d + i);
-              tv[k][i] = __ldcg(ps + 2 * d + i);
-            }
-          }
+        for (int i = 0; i < DPL; ++i) {
+          qv[i] += tq[k][i];
+          kv[i] += tk[k][i];
+          vv[i] += tv[k][i];
+        }
+    for (int k = 8; k < nsplit; ++k) {
+      const float* ps = pp + k * pstride;
 #pragma unroll
-        for (int k = 0; k < 8; ++k)
-          if (s0 + k < nsplit)
-#pragma unroll
-            for (int i = 0; i < DPL; ++i) {
-              qv[i] += tq[k][i];
-              kv[i] += tk[k][i];
-              vv[i] += tv[k][i];
-            }
+      for (int i = 0; i < DPL; ++i) {
+        qv[i] += __ldcg(ps + i);
+        kv[i] += __ldcg(ps + d + i);
+        vv[i] += __ldcg(ps + 2 * d + i);
       }
     }
     bf16* const kdst = base(p, 0);
@@ -476,68 +476,33 @@ __device__ __noinline__ void attn_phase(const MegaArgs& a, int layer, int nsplit
 #pragma unroll
     for (int i = 0; i < DH; ++i) q[i] = qs[i];
     if (st) st[1] = clock64();
-    float m = -FLT_MAX, l = 0.f, acc[DPL];
-#pragma unroll
-    for (int i = 0; i < DPL; ++i) acc[i] = 0.f;
-    // ntiles >= 3: group g carries tile g; at iteration t groups 0 .. t+2 are
-    // committed and wait_group 2 completes group t.  ntiles <= 2: the tile
-    // holding the new position is issued here and every load is waited for.
-    if (tlast <= 1) {
-      issue(tlast);
-      cp_commit();
-    }
+    // group g carries tile g: two tiles in flight ahead of the one consumed
+    issue(0);
+    cp_commit();
+    if (1 < ntiles) issue(1);
+    cp_commit();
+    WarpAttn<DH> wa;
+    wa.init();
     for (int t = 0; t < ntiles; ++t) {
       if (t + 2 < ntiles) issue(t + 2);
       cp_commit();
-      if (ntiles <= 2)
-        cp_wait_all();
-      else
-        asm volatile("cp.async.wait_group 2;" ::: "memory");
+      asm volatile("cp.async.wait_group 2;" ::: "memory");
       __syncwarp();
-      const int t0 = t * kTT, st = t % kStages;
-      const int nt = (ctx - t0) < kTT ? (ctx - t0) : kTT;
-      float sc = -FLT_MAX;
-      if (lane < nt) {
-        const uint8_t* kr = tile_ptr(st, 0) + lane * LDB;
-        float dot = 0.f;
-#pragma unroll
-        for (int cc = 0; cc < CPR; ++cc) {
-          Vec16<bf16> v;
-          v.u = *reinterpret_cast<const uint4*>(kr + cc * 16);
-#pragma unroll
-          for (int e = 0; e < 8; ++e) dot = fmaf(to_f(v.v[e]), q[cc * 8 + e], dot);
-        }
-        sc = dot * inv_sqrt_dh;
-      }
-      float tm = sc;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) tm = fmaxf(tm, __shfl_xor_sync(0xffffffffu, tm, o));
-      const float mnew = fmaxf(m, tm);
-      const float corr = m == -FLT_MAX ? 0.f : expf(m - mnew);
-      const float pr = lane < nt ? expf(sc - mnew) : 0.f;
-      l = l * corr + warp_sum(pr);
-      m = mnew;
-#pragma unroll
-      for (int i = 0; i < DPL; ++i) acc[i] *= corr;
-      const uint8_t* vt = tile_ptr(st, 1) + lane * DPL * 2;
-      for (int jj = 0; jj < nt; ++jj) {
-        const float pj = __shfl_sync(0xffffffffu, pr, jj);
-        const bf16* vr = reinterpret_cast<const bf16*>(vt + jj * LDB);
-#pragma unroll
-        for (int i = 0; i < DPL; ++i) acc[i] = fmaf(pj, to_f(vr[i]), acc[i]);
-      }
-      __syncwarp();  // stage st is refilled three tiles from now
+      const int t0 = t * kTT, stg = t % kStages;
+      wa.tile(q, tile_ptr(stg, 0), tile_ptr(stg, 1), LDB, (ctx - t0) < kTT ? (ctx - t0) : kTT, scale);
+      __syncwarp();  // stage stg is refilled three tiles from now
     }
     cp_wait_all();
+    const float inv = 1.0f / wa.finish();
     if (st) {
       st[2] = clock64();
       st[3] = ntiles;
     }
-    const float inv = 1.0f / l;
 #pragma unroll
-    for (int i = 0; i < DPL; ++i) a.att[int64_t(b) * d + h * DH + lane * DPL + i] = from_f<bf16>(acc[i] * inv);
+    for (int i = 0; i < DPL; ++i) a.att[int64_t(b) * d + h * DH + lane * DPL + i] = from_f<bf16>(wa.acc[i] * inv);
     __syncwarp();  // qs is rewritten by the next item
   }
+  fence_for_tma();
 }
 
 template <int DH>
@@ -570,16 +535,17 @@ __global__ void __launch_bounds__(kThreads, 1) decode_mega_kernel(const __grid_c
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  unsigned gen = 0;
-  if (threadIdx.x == 0) asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(gen) : "l"(a.bar + 1) : "memory");
+  unsigned long long* bar = reinterpret_cast<unsigned long long*>(a.bar);
+  const unsigned long long base = bar[1];  // counter value at the end of the previous launch
+  const unsigned long long G = gridDim.x;
   uint32_t cnt = 0;
   int kb = 0;
   const int d = a.d, f = a.f;
   if (a.prefetch) prefetch_layer(a.layers[0], d, f);
-#define BARRIER_THEN(pre)                   \
-  grid_arrive(a.bar, gen, a.trace, kb);     \
-  pre;                                      \
-  grid_wait(a.bar, gen, a.trace, kb);       \
+#define BARRIER_THEN(pre)                                 \
+  grid_arrive(bar, a.trace, kb);                          \
+  pre;                                                    \
+  grid_wait(bar, base + (kb + 1) * G, a.trace, kb);       \
   ++kb;
   for (int l = 0; l < a.L; ++l) {
     const MegaLayer ly = a.layers[l];
@@ -609,6 +575,8 @@ __global__ void __launch_bounds__(kThreads, 1) decode_mega_kernel(const __grid_c
   }
 #undef BARRIER_THEN
   row_phase(a, 1, a.split[3], a.lnfw, a.lnfb, c.red);
+  // every CTA has passed the last barrier, so all kb·G arrivals are in
+  if (blockIdx.x == 0 && threadIdx.x == 0) bar[1] = base + (unsigned long long)kb * G;
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (threadIdx.x < 32)
@@ -620,7 +588,7 @@ int pick_split(int N, int K, int grid) {
   const int T = N / kBM, nk = K / kBK;
   int best = 0;
   for (int S = 1; S <= nk; ++S) {
-    if (nk % S || nk / S > kMaxCh || T * S > grid) continue;
+    if (nk % S || nk / S > kMaxCh || T * S > grid || S > kMaxSplit) continue;
     if (best == 0 || S > best) best = S;
   }
   return best;

@@ -63,7 +63,7 @@ Engine::Engine(Model* model, const ppoexp_engine_options* o) : m(model), c(model
   const size_t o_sta = sbytes; sbytes += al(max_slices * mb * 16);
   const size_t o_stb = sbytes; sbytes += al(max_slices * mb * 16);
   const size_t o_part = sbytes; sbytes += al(decode_mega_part_bytes());
-  const size_t o_bar = sbytes; sbytes += al(16);
+  const size_t o_bar = sbytes; sbytes += al(16);  // 2 x u64 grid-barrier counter / base
   const size_t o_mly = sbytes; sbytes += al(cfg.n_layers * sizeof(MegaLayer));
   const size_t o_wmap = sbytes; sbytes += al(cfg.n_layers * 4 * sizeof(CUtensorMap));
   state.ensure(sbytes);
