@@ -379,7 +379,21 @@ def run_ours(args):
                 line["cpu_baseline"] = {"value": None, "unit": "tokens/s", "cores": 0, "kind": "reference",
                                         "sample": f"unavailable: {e}"}
         print(json.dumps(line), flush=True)
+    # Ordered teardown: torch tensors that lived on the library stream, then the
+    # library objects (engine before its models, models before the context),
+    # then the process group.
+    torch.cuda.synchronize()
+    del out, flush, prompts_d, offs_d, stream
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    xm = None
+    engine.close()
+    policy.close()
+    reference.close()
+    critic.close()
+    ctx.close()
     if world > 1:
+        dist.barrier()
         dist.destroy_process_group()
 
 
@@ -402,6 +416,11 @@ def main():
         run_reference(args)
     else:
         run_ours(args)
+    # everything is torn down explicitly above; skip interpreter-exit
+    # destructors (torch / NCCL module teardown order is not ours to control)
+    sys.stdout.flush()
+    sys.stderr.flush()
+    os._exit(0)
 
 
 if __name__ == "__main__":
