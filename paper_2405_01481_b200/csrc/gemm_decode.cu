@@ -100,7 +100,8 @@ struct DecLayout {
 template <int NB, int EPI, bool LNIN>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_decode_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX, int Mrows,
-                       int N, int K, void* __restrict__ Cv, int64_t ldc, int S, int wst, LnIn ln, RowStats so) {
+                       int N, int K, void* __restrict__ Cv, int64_t ldc, int S, int wst, LnIn ln, RowStats so,
+                       int push) {
   using L = DecLayout<NB>;
   constexpr int XST = L::XST;
   __shared__ float ln_mu[NB], ln_rs[NB];
@@ -110,13 +111,18 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* sW = smem;
   uint8_t* sX = smem + body;
   float* part = reinterpret_cast<float*>(smem);  // reused after the MMA loop
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sX + XST * L::kX);
+  // push mode (S > 1): a receive area for the peers' partial slices follows the X ring
+  float* recv = reinterpret_cast<float*>(sX + XST * L::kX);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sX + XST * L::kX + (push ? L::kPart : 0));
   uint64_t* xfull = bars;
   uint64_t* xempty = xfull + XST;
   uint64_t* tmem_full = xempty + XST;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
   uint64_t* wfull = tmem_full + 2;   // [wst]
   uint64_t* wempty = wfull + wst;    // [wst]
+  uint64_t* rfull = wempty + wst;    // push mode: peers' slices landed
+  const int rows_per = S > 1 ? ((BMW / S) + 3) & ~3 : BMW;
+  const uint32_t slice_bytes = uint32_t(NB) * rows_per * 4;
   cg::cluster_group cluster = cg::this_cluster();
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -136,7 +142,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&wempty[i], 1);
     }
     mbar_init(tmem_full, 1);
+    if (push) mbar_init(rfull, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (push) mbar_expect_tx(rfull, uint32_t(S - 1) * slice_bytes);  // the single arrival + the peers' bytes
     // The weights are constant across the graph: fetch this CTA's weight slice
     // (up to the ring size) BEFORE waiting on the predecessor grid (PDL), so
     // the HBM stream overlaps the previous kernel.
@@ -154,6 +162,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  // push mode: publish this CTA's initialised rfull to the cluster; the
+  // matching wait happens just before the first remote push, long after
+  if (push) asm volatile("barrier.cluster.arrive.aligned;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
   pdl_wait();  // upstream activations are valid from here on
   pdl_trigger();
@@ -261,7 +272,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int c = 0; c < NB; c += 16) {
       uint32_t v[16];
       tmem_ld16(tmem + (uint32_t(q * 32) << 16) + uint32_t(c), v);
-      if (S > 1) {
+      if (S > 1 && push) {
+        // slice-major [k][bcol][f % rows_per]: the slice for rank k is one
+        // contiguous block, pushed with a single bulk copy
+        float* ps = part + (f / rows_per) * (NB * rows_per) + (f % rows_per);
+#pragma unroll
+        for (int e = 0; e < 16; ++e) ps[(c + e) * rows_per] = __uint_as_float(v[e]);
+      } else if (S > 1) {
 #pragma unroll
         for (int e = 0; e < 16; ++e) part[(c + e) * BMW + f] = __uint_as_float(v[e]);
       } else if (n < N) {
@@ -315,19 +332,45 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   if (S > 1) {
-    cluster.sync();  // all partials of the cluster are parked in smem
     // reduce feature rows [f0, f1) of this CTA over the S partials, in rank
-    // order: float4 DSMEM loads, all S issued before the adds
-    const int rows_per = ((BMW / S) + 3) & ~3;  // multiple of 4 features
+    // order.  push: every CTA bulk-copies slice k of its partial into rank k's
+    // receive area (TMA engine, completion on rank k's rfull), then reduces
+    // from local smem.  pull (fallback when smem is short): cluster barrier,
+    // then float4 DSMEM loads from every peer.
     const int f0 = r * rows_per, f1 = min(BMW, f0 + rows_per);
     const int nf4 = (f1 - f0) / 4;
     const int ncols = min(Mrows, NB);
     const float4* parts[8];
-    for (int k = 0; k < 8; ++k)
-      parts[k] = reinterpret_cast<const float4*>(cluster.map_shared_rank(part, k < S ? k : 0));
+    if (push) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // parked partial -> bulk-copy reads
+      __syncthreads();
+      asm volatile("barrier.cluster.wait.aligned;" ::: "memory");  // every peer's rfull is initialised
+      if (threadIdx.x == 0) {
+        for (int k = 0; k < S; ++k) {
+          if (k == r) continue;
+          uint32_t dst, bar;
+          asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(dst) : "r"(smem_u32(recv) + r * slice_bytes), "r"(k));
+          asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(bar) : "r"(smem_u32(rfull)), "r"(k));
+          asm volatile(
+              "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+              "r"(smem_u32(part) + k * slice_bytes), "r"(slice_bytes), "r"(bar)
+              : "memory");
+        }
+      }
+      mbar_wait(rfull, 0);
+      for (int k = 0; k < 8; ++k) {
+        const int kk = k < S ? k : 0;
+        parts[k] = reinterpret_cast<const float4*>(kk == r ? part + size_t(r) * NB * rows_per
+                                                           : recv + size_t(kk) * NB * rows_per);
+      }
+    } else {
+      cluster.sync();  // all partials of the cluster are parked in smem
+      for (int k = 0; k < 8; ++k)
+        parts[k] = reinterpret_cast<const float4*>(cluster.map_shared_rank(part, k < S ? k : 0));
+    }
     for (int e = threadIdx.x; e < nf4 * ncols; e += kThreads) {
       const int fl = f0 + 4 * (e % nf4), bcol = e / nf4;
-      const int idx = (bcol * BMW + fl) >> 2;
+      const int idx = push ? ((bcol * rows_per + (fl - f0)) >> 2) : ((bcol * BMW + fl) >> 2);
       float4 v[8];
 #pragma unroll
       for (int k = 0; k < 8; ++k)
@@ -382,7 +425,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         so.p[(int64_t(slice) * so.ld + bcol) * 2 + 1] = s2;
       }
     }
-    cluster.sync();  // keep our smem alive until every peer has read it
+    if (push) {  // every peer's incoming copies (including ours) have landed before anyone exits
+      asm volatile("barrier.cluster.arrive.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
+    } else {
+      cluster.sync();  // keep our smem alive until every peer has read it
+    }
   } else {
     __syncthreads();
   }
@@ -428,10 +475,15 @@ int launch_dec(Ctx& c, const bf16* X, int64_t ldx, const bf16* W, int64_t ldw, i
     return e ? atoi(e) : 4;
   }();
   const int wst = int(std::min<int64_t>(std::min<int64_t>(L::kWcap, wring), ceil_div(nk, S)));
+  static const int push_env = [] {
+    const char* e = getenv("PPOEXP_DECODE_PUSH");
+    return e ? atoi(e) : 1;
+  }();
+  const int push = (push_env && S > 1 && L::bytes(wst) + wst * 16 + L::kPart <= L::kSmemMax) ? 1 : 0;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(tiles, S, 1);
   cfg.blockDim = dim3(kThreads, 1, 1);
-  cfg.dynamicSmemBytes = L::bytes(wst) + wst * 16;
+  cfg.dynamicSmemBytes = L::bytes(wst) + wst * 16 + (push ? L::kPart : 0);
   cfg.stream = c.stream;
   cudaLaunchAttribute attrs[2];
   attrs[0].id = cudaLaunchAttributeClusterDimension;
@@ -447,7 +499,7 @@ int launch_dec(Ctx& c, const bf16* X, int64_t ldx, const bf16* W, int64_t ldw, i
   const double flops = 2.0 * M * N * K;
   const double bytes = 2.0 * N * K + double(M) * K * (LNIN ? 4 : 2) + double(M) * N * ((EPI == 0 || EPI == 1) ? 2 : 4);
   c.launch("gemm_decode", bytes, flops, [&] {
-    PPOEXP_CUDA(cudaLaunchKernelEx(&cfg, k, tw, tx, int(M), int(N), int(K), C, ldc, S, wst, lnv, sov));
+    PPOEXP_CUDA(cudaLaunchKernelEx(&cfg, k, tw, tx, int(M), int(N), int(K), C, ldc, S, wst, lnv, sov, push));
   });
   return sov.p ? (S > 1 ? tiles * S : tiles) : 0;
 }
