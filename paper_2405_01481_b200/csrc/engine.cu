@@ -17,6 +17,8 @@
 
 namespace ppx {
 
+void dump_gemm_trace(Ctx& c, const char* path);  // gemm_decode.cu
+
 namespace {
 constexpr int kUnitsPerGraph = 8;
 }
@@ -391,6 +393,7 @@ void Engine::generate(int64_t B, const int32_t* prompts, const int64_t* offsets,
   PPOEXP_CUDA(cudaEventElapsedTime(&ms, e0, e1));
   last_ms = ms;
   if (ms_out) *ms_out = ms;
+  if (const char* gp = getenv("PPOEXP_GEMM_TRACE")) dump_gemm_trace(*c, gp);
   if (trace_path && trace_buf.ptr) {  // debug: raw stamps of the last decode step
     std::vector<uint64_t> h(trace_buf.bytes / 8);
     PPOEXP_CUDA(cudaMemcpy(h.data(), trace_buf.ptr, trace_buf.bytes, cudaMemcpyDeviceToHost));

@@ -12,6 +12,7 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <vector>
 
 #include "kernels.hpp"
 
@@ -101,7 +102,17 @@ template <int NB, int EPI, bool LNIN>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_decode_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX, int Mrows,
                        int N, int K, void* __restrict__ Cv, int64_t ldc, int S, int wst, LnIn ln, RowStats so,
-                       int push) {
+                       int push, uint64_t* dbg) {
+  // debug timeline (PPOEXP_GEMM_TRACE): CTA (0, 0) stamps %globaltimer at each stage
+  const bool trace = dbg != nullptr && blockIdx.x == 0 && blockIdx.y == 0;
+  auto stamp = [&](int k) {
+    if (trace) {
+      uint64_t t;
+      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+      dbg[k] = t;
+    }
+  };
+  if (threadIdx.x == 0) stamp(0);
   using L = DecLayout<NB>;
   constexpr int XST = L::XST;
   __shared__ float ln_mu[NB], ln_rs[NB];
@@ -166,7 +177,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   // matching wait happens just before the first remote push, long after
   if (push) asm volatile("barrier.cluster.arrive.aligned;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 0) stamp(1);
   pdl_wait();  // upstream activations are valid from here on
+  if (threadIdx.x == 0) stamp(2);
   pdl_trigger();
 
   if (warp == 0) {
@@ -197,6 +210,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int xs = it % XST, xu = it / XST;
         mbar_wait(&wfull[ws], wu & 1);
         mbar_wait(&xfull[xs], xu & 1);
+        if (it == 0) stamp(3);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint64_t dw = smem_desc_sw128(sW + ws * L::kW);
         const uint64_t dx = smem_desc_sw128(sX + xs * L::kX);
@@ -264,6 +278,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // to global, or (S > 1) fp32 partial in smem for the cluster reduction
     const int q = warp & 3;
     mbar_wait(tmem_full, 0);
+    if (threadIdx.x == 64) stamp(4);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const int f = q * 32 + lane;
     const int n = n0 + f;
@@ -341,6 +356,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int nf4 = (f1 - f0) / 4;
     const int ncols = min(Mrows, NB);
     const float4* parts[8];
+    float4 xpre[4];
     if (push) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // parked partial -> bulk-copy reads
       __syncthreads();
@@ -357,18 +373,48 @@ __global__ void __launch_bounds__(kThreads, 1)
               : "memory");
         }
       }
+      // residual epilogue: the x values this thread updates are loaded while
+      // the peers' slices are in flight (after the proxy fence, which would
+      // otherwise wait for these loads)
+      if constexpr (EPI == int(Epi::kAddResidual)) {
+#pragma unroll
+        for (int it = 0; it < 4; ++it) {
+          const int e = threadIdx.x + it * kThreads;
+          xpre[it] = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (e < nf4 * ncols) {
+            const int fl = f0 + 4 * (e % nf4), bcol = e / nf4;
+            const int64_t o = int64_t(bcol) * ldc + n0 + fl;
+            if (n0 + fl + 3 < N && (o & 3) == 0) xpre[it] = __ldcg(reinterpret_cast<const float4*>(static_cast<float*>(Cv) + o));
+          }
+        }
+      }
+      if (threadIdx.x == 0) stamp(5);
       mbar_wait(rfull, 0);
+      if (threadIdx.x == 0) stamp(6);
       for (int k = 0; k < 8; ++k) {
         const int kk = k < S ? k : 0;
         parts[k] = reinterpret_cast<const float4*>(kk == r ? part + size_t(r) * NB * rows_per
                                                            : recv + size_t(kk) * NB * rows_per);
       }
     } else {
+      if constexpr (EPI == int(Epi::kAddResidual)) {
+#pragma unroll
+        for (int it = 0; it < 4; ++it) {
+          const int e = threadIdx.x + it * kThreads;
+          xpre[it] = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (e < nf4 * ncols) {
+            const int fl = f0 + 4 * (e % nf4), bcol = e / nf4;
+            const int64_t o = int64_t(bcol) * ldc + n0 + fl;
+            if (n0 + fl + 3 < N && (o & 3) == 0) xpre[it] = __ldcg(reinterpret_cast<const float4*>(static_cast<float*>(Cv) + o));
+          }
+        }
+      }
       cluster.sync();  // all partials of the cluster are parked in smem
       for (int k = 0; k < 8; ++k)
         parts[k] = reinterpret_cast<const float4*>(cluster.map_shared_rank(part, k < S ? k : 0));
     }
-    for (int e = threadIdx.x; e < nf4 * ncols; e += kThreads) {
+    int it = 0;
+    for (int e = threadIdx.x; e < nf4 * ncols; e += kThreads, ++it) {
       const int fl = f0 + 4 * (e % nf4), bcol = e / nf4;
       const int idx = push ? ((bcol * rows_per + (fl - f0)) >> 2) : ((bcol * BMW + fl) >> 2);
       float4 v[8];
@@ -398,7 +444,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           static_cast<bf16*>(Cv)[o] = __float2bfloat16_rn(gelu_tanh(a));
         } else if constexpr (EPI == int(Epi::kAddResidual)) {
           float* xp = static_cast<float*>(Cv) + o;
-          const float nv = *xp + a;
+          const int64_t o4 = int64_t(bcol) * ldc + n0 + fl;
+          const bool pre = it < 4 && n0 + fl + 3 < N && (o4 & 3) == 0;
+          const float xo = pre ? (j == 0 ? xpre[it & 3].x : j == 1 ? xpre[it & 3].y : j == 2 ? xpre[it & 3].z : xpre[it & 3].w)
+                               : *xp;
+          const float nv = xo + a;
           *xp = nv;
           ps += double(nv);
           pq += double(nv) * double(nv);
@@ -426,7 +476,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
     if (push) {  // every peer's incoming copies (including ours) have landed before anyone exits
+      if (threadIdx.x == 0) stamp(7);
       asm volatile("barrier.cluster.arrive.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
+      if (threadIdx.x == 0) stamp(8);
     } else {
       cluster.sync();  // keep our smem alive until every peer has read it
     }
@@ -472,7 +524,7 @@ int launch_dec(Ctx& c, const bf16* X, int64_t ldx, const bf16* W, int64_t ldw, i
   while (S < 8 && ceil_div(nk, S) > L::kWcap) S *= 2;
   static const int wring = [] {
     const char* e = getenv("PPOEXP_DECODE_WRING");
-    return e ? atoi(e) : 4;
+    return e ? atoi(e) : 8;
   }();
   const int wst = int(std::min<int64_t>(std::min<int64_t>(L::kWcap, wring), ceil_div(nk, S)));
   static const int push_env = [] {
@@ -499,7 +551,15 @@ int launch_dec(Ctx& c, const bf16* X, int64_t ldx, const bf16* W, int64_t ldw, i
   const double flops = 2.0 * M * N * K;
   const double bytes = 2.0 * N * K + double(M) * K * (LNIN ? 4 : 2) + double(M) * N * ((EPI == 0 || EPI == 1) ? 2 : 4);
   c.launch("gemm_decode", bytes, flops, [&] {
-    PPOEXP_CUDA(cudaLaunchKernelEx(&cfg, k, tw, tx, int(M), int(N), int(K), C, ldc, S, wst, lnv, sov, push));
+    uint64_t* dbg = nullptr;
+    static const bool gtrace = getenv("PPOEXP_GEMM_TRACE") != nullptr;
+    if (gtrace) {  // debug: slot per launch (graph nodes keep their slot)
+      auto* buf = static_cast<uint64_t*>(c.workspace("gemm_decode.trace", size_t(4096) * 16 * 8));
+      const int64_t slot = int64_t(c.gemm_trace_meta.size()) % 4096;
+      c.gemm_trace_meta.push_back({int(N), int(K), EPI, S});
+      dbg = buf + slot * 16;
+    }
+    PPOEXP_CUDA(cudaLaunchKernelEx(&cfg, k, tw, tx, int(M), int(N), int(K), C, ldc, S, wst, lnv, sov, push, dbg));
   });
   return sov.p ? (S > 1 ? tiles * S : tiles) : 0;
 }
@@ -526,6 +586,24 @@ int dispatch_nb(Ctx& c, const bf16* X, int64_t ldx, const bf16* W, int64_t ldw, 
 }
 
 }  // namespace
+
+// Debug (PPOEXP_GEMM_TRACE): write the per-launch stage stamps + {N, K, epi, S}
+// of every traced decode-GEMM launch to `path` (binary: n, meta[n][4] int32,
+// stamps[n][16] u64).
+void dump_gemm_trace(Ctx& c, const char* path) {
+  const int64_t n = std::min<int64_t>(int64_t(c.gemm_trace_meta.size()), 4096);
+  if (n == 0) return;
+  std::vector<uint64_t> h(size_t(n) * 16);
+  PPOEXP_CUDA(cudaMemcpy(h.data(), c.workspace("gemm_decode.trace", size_t(4096) * 16 * 8), h.size() * 8,
+                         cudaMemcpyDeviceToHost));
+  if (FILE* fp = fopen(path, "wb")) {
+    const int32_t nn = int32_t(n);
+    fwrite(&nn, 4, 1, fp);
+    for (int64_t i = 0; i < n; ++i) fwrite(c.gemm_trace_meta[i].data(), 4, 4, fp);
+    fwrite(h.data(), 8, h.size(), fp);
+    fclose(fp);
+  }
+}
 
 // Decode-sized GEMM (M <= 256).  Returns false if not eligible.
 bool gemm_decode_bf16(Ctx& c, const bf16* A, int64_t lda, const bf16* B, int64_t ldb, int64_t M, int64_t N, int64_t K,

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <functional>
+#include <array>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -65,6 +66,7 @@ struct Ctx {
   std::vector<TimedLaunch>* capture_events = nullptr;  // events recorded while capturing
   std::vector<cudaEvent_t> event_pool;
   std::map<std::string, std::unique_ptr<DeviceBuffer>> ws;
+  std::vector<std::array<int, 4>> gemm_trace_meta;  // debug: PPOEXP_GEMM_TRACE launch metadata
   // pinned host staging for HOST-where API calls
   void* pinned = nullptr;
   size_t pinned_bytes = 0;

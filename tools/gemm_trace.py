@@ -1,0 +1,31 @@
+"""Stage breakdown of the decode GEMM (gemm_decode.cu) from a PPOEXP_GEMM_TRACE dump.
+
+    PPOEXP_GEMM_TRACE=/tmp/g.bin python tools/profile_decode.py --new 24
+    python tools/gemm_trace.py /tmp/g.bin
+
+Stamps (CTA (0,0), %globaltimer): 0 entry, 1 setup done, 2 PDL wait released,
+3 first activation tile landed, 4 accumulator complete, 5 partial parked +
+pushed, 6 peers' slices landed, 7 reduce + epilogue stored, 8 cluster exit.
+"""
+import collections
+import sys
+
+import numpy as np
+
+raw = open(sys.argv[1], "rb").read()
+n = int(np.frombuffer(raw[:4], np.int32)[0])
+meta = np.frombuffer(raw[4:4 + n * 16], np.int32).reshape(n, 4)
+st = np.frombuffer(raw[4 + n * 16:], np.uint64).astype(np.int64).reshape(n, 16)
+names = ["setup", "pdl wait", "X landed", "MMA done", "park+push", "peers in", "reduce+store", "cluster exit"]
+groups = collections.defaultdict(list)
+for i in range(n):
+    if st[i, 0] == 0 or st[i, 8] == 0:
+        continue
+    groups[tuple(meta[i])].append(st[i])
+print(f"{'N,K,epi,S':22s} {'n':>4s} " + " ".join(f"{x:>12s}" for x in names) + f" {'total':>8s}")
+for key, rows in sorted(groups.items()):
+    r = np.array(rows)
+    d = np.diff(r[:, :9], axis=1) / 1e3
+    med = np.median(d, axis=0)
+    print(f"{str(key):22s} {len(rows):4d} " + " ".join(f"{x:12.2f}" for x in med) +
+          f" {np.median((r[:, 8] - r[:, 0]) / 1e3):8.2f}")
