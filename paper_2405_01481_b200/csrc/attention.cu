@@ -107,14 +107,19 @@ __device__ __forceinline__ void cp_async16_dec(void* dst, const void* src) {
 }
 
 template <class T, int DH>
-__global__ void __launch_bounds__(128) attn_decode_kernel(const T* __restrict__ qkv, const int32_t* __restrict__ pos,
+__global__ void __launch_bounds__(128, 6) attn_decode_kernel(const T* __restrict__ qkv, const int32_t* __restrict__ pos,
                                                           const int32_t* __restrict__ done,
                                                           const int32_t* __restrict__ block_table, int layer,
                                                           KvGeom g, T* __restrict__ kv, T* __restrict__ out) {
   PDL_ENTRY();
   constexpr int NW = 4, TT = 32;
   constexpr int ROWB = DH * int(sizeof(T));   // bytes per K/V row
-  constexpr int LDB = ROWB + 16;              // padded smem row (bytes)
+  // 128-byte rows (bf16, dh 64) are stored unpadded with the 16-byte chunks
+  // XOR-swizzled by (row & 7): conflict-free for lane-per-token K reads and
+  // per-row V reads, and 32 KB of tiles per CTA (6 CTAs/SM: one wave of 768).
+  // Other row sizes keep a 16-byte pad.
+  constexpr bool SWZ = ROWB == 128;
+  constexpr int LDB = SWZ ? ROWB : ROWB + 16;  // smem row stride (bytes)
   constexpr int CPR = ROWB / 16;              // 16-byte chunks per row
   constexpr int EPT = DH;                     // lane-per-token: whole row
   constexpr int DPL = DH >= 32 ? DH / 32 : 1; // dims per lane (P·V)
@@ -122,6 +127,7 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(const T* __restrict__ 
   extern __shared__ __align__(16) uint8_t smem_dec[];
   __shared__ float sm_m[NW], sm_l[NW];
   __shared__ float sm_acc[NW][DH];
+  __shared__ __align__(16) float sm_q[DH];  // the query (lane-uniform reads: broadcast)
   const int64_t b = blockIdx.y, h = blockIdx.x;
   if (done[b]) return;
   const int64_t p = pos[b], ctx = p + 1;
@@ -138,10 +144,12 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(const T* __restrict__ 
     base(p, 0)[i] = row[d + h * DH + i];
     base(p, 1)[i] = row[2 * d + h * DH + i];
   }
-  __syncthreads();  // the appended row is visible to the whole CTA
+  for (int i = tid; i < DH; i += 128) sm_q[i] = to_f(row[h * DH + i]);
+  __syncthreads();  // the appended row and the query are visible to the whole CTA
   // per-warp double-buffered tiles: [buf][K|V][TT rows][LDB bytes]
   uint8_t* wsm = smem_dec + size_t(w) * 2 * 2 * TT * LDB;
   auto tile_ptr = [&](int buf, int which) { return wsm + (buf * 2 + which) * TT * LDB; };
+  auto chunk = [](int r, int c) { return r * LDB + ((SWZ ? (c ^ (r & 7)) : c) << 4); };
   auto issue = [&](int64_t t0, int buf) {
     const int64_t n = (ctx - t0) < TT ? (ctx - t0) : TT;
     const T* k0 = base(t0, 0);  // contiguous within the page
@@ -149,15 +157,13 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(const T* __restrict__ 
     for (int e = lane; e < TT * CPR; e += 32) {
       const int r = e / CPR, c = e % CPR;
       if (r < n) {
-        cp_async16_dec(tile_ptr(buf, 0) + r * LDB + c * 16, reinterpret_cast<const uint8_t*>(k0) + r * ROWB + c * 16);
-        cp_async16_dec(tile_ptr(buf, 1) + r * LDB + c * 16, reinterpret_cast<const uint8_t*>(v0) + r * ROWB + c * 16);
+        cp_async16_dec(tile_ptr(buf, 0) + chunk(r, c), reinterpret_cast<const uint8_t*>(k0) + r * ROWB + c * 16);
+        cp_async16_dec(tile_ptr(buf, 1) + chunk(r, c), reinterpret_cast<const uint8_t*>(v0) + r * ROWB + c * 16);
       }
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
-  float q[EPT];
-#pragma unroll
-  for (int i = 0; i < EPT; ++i) q[i] = to_f(row[h * DH + i]);
+  const float* q = sm_q;
   const float inv_sqrt_dh = 1.0f / sqrtf(float(DH));
   float m = -FLT_MAX, l = 0.f, acc[DPL];
 #pragma unroll
@@ -179,12 +185,12 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(const T* __restrict__ 
     // ---- scores: lane = token
     float s = -FLT_MAX;
     if (lane < nt) {
-      const uint8_t* kr = tile_ptr(buf, 0) + lane * LDB;
+      const uint8_t* kt = tile_ptr(buf, 0);
       float dot = 0.f;
 #pragma unroll
       for (int c = 0; c < CPR; ++c) {
         Vec16<T> v4;
-        v4.u = *reinterpret_cast<const uint4*>(kr + c * 16);
+        v4.u = *reinterpret_cast<const uint4*>(kt + chunk(lane, c));
 #pragma unroll
         for (int e = 0; e < Vec16<T>::N; ++e) dot = fmaf(to_f(v4.v[e]), q[c * Vec16<T>::N + e], dot);
       }
@@ -204,10 +210,11 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(const T* __restrict__ 
 #pragma unroll
     for (int i = 0; i < DPL; ++i) acc[i] *= corr;
     // ---- P·V: lane = dims
-    const uint8_t* vt = tile_ptr(buf, 1) + dl * DPL * int(sizeof(T));
+    const uint8_t* vt = tile_ptr(buf, 1);
+    const int vb = dl * DPL * int(sizeof(T));  // byte offset of this lane's dims in an unswizzled row
     for (int j = 0; j < nt; ++j) {
       const float pj = __shfl_sync(0xffffffffu, pr, j);
-      const T* vr = reinterpret_cast<const T*>(vt + j * LDB);
+      const T* vr = reinterpret_cast<const T*>(vt + chunk(j, vb >> 4) + (vb & 15));
 #pragma unroll
       for (int i = 0; i < DPL; ++i) acc[i] = fmaf(pj, to_f(vr[i]), acc[i]);
     }
@@ -256,7 +263,8 @@ void decode_impl(Ctx& c, const T* qkv, int64_t B, const int32_t* pos, const int3
                  int layer, const KvGeom& g, T* kv, T* out, double bytes) {
   if (g.page_size % 32) throw ContractError("engine: page_size must be a multiple of 32");
   auto k = attn_decode_kernel<T, DH>;
-  const size_t smem = size_t(4) * 2 * 2 * 32 * (DH * sizeof(T) + 16);
+  const size_t row = DH * sizeof(T) == 128 ? 128 : DH * sizeof(T) + 16;  // kernel's LDB
+  const size_t smem = size_t(4) * 2 * 2 * 32 * row;
   static bool attr = false;
   if (!attr) {
     PPOEXP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));

@@ -526,7 +526,11 @@ int launch_dec(Ctx& c, const bf16* X, int64_t ldx, const bf16* W, int64_t ldw, i
     const char* e = getenv("PPOEXP_DECODE_WRING");
     return e ? atoi(e) : 8;
   }();
-  const int wst = int(std::min<int64_t>(std::min<int64_t>(L::kWcap, wring), ceil_div(nk, S)));
+  // K-split launches hold their whole slice (one wave, the ring is filled
+  // before the PDL wait); multi-wave launches (tiles > #SMs, e.g. the LM
+  // head) keep a 4-deep ring so two CTAs share an SM
+  const int ring = tiles * S > 148 ? std::min(wring, 4) : wring;
+  const int wst = int(std::min<int64_t>(std::min<int64_t>(L::kWcap, ring), ceil_div(nk, S)));
   static const int push_env = [] {
     const char* e = getenv("PPOEXP_DECODE_PUSH");
     return e ? atoi(e) : 1;
