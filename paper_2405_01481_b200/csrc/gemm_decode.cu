@@ -103,13 +103,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     gemm_decode_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX, int Mrows,
                        int N, int K, void* __restrict__ Cv, int64_t ldc, int S, int wst, LnIn ln, RowStats so,
                        int push, uint64_t* dbg) {
-  // debug timeline (PPOEXP_GEMM_TRACE): CTA (0, 0) stamps %globaltimer at each stage
+  // debug timeline (PPOEXP_GEMM_TRACE): CTA (0, 0) stamps clock64 at each stage
   const bool trace = dbg != nullptr && blockIdx.x == 0 && blockIdx.y == 0;
   auto stamp = [&](int k) {
     if (trace) {
-      uint64_t t;
-      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-      dbg[k] = t;
+      dbg[k] = clock64();  // one CTA, one SM: cycle counts are comparable
     }
   };
   if (threadIdx.x == 0) stamp(0);
@@ -202,6 +200,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tma_load_2d(&tmW, &wfull[ws], sW + ws * L::kW, (kb0 + it) * BK, n0);
       }
     }
+    __syncwarp();  // reconverge before any block-wide barrier
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr uint32_t idesc = idesc_bf16(BMW, NB);
@@ -359,8 +358,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     float4 xpre[4];
     if (push) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // parked partial -> bulk-copy reads
+      if (threadIdx.x == 64) stamp(9);
       __syncthreads();
+      if (threadIdx.x == 0) stamp(10);
       asm volatile("barrier.cluster.wait.aligned;" ::: "memory");  // every peer's rfull is initialised
+      if (threadIdx.x == 0) stamp(11);
       if (threadIdx.x == 0) {
         for (int k = 0; k < S; ++k) {
           if (k == r) continue;

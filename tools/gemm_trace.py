@@ -3,7 +3,7 @@
     PPOEXP_GEMM_TRACE=/tmp/g.bin python tools/profile_decode.py --new 24
     python tools/gemm_trace.py /tmp/g.bin
 
-Stamps (CTA (0,0), %globaltimer): 0 entry, 1 setup done, 2 PDL wait released,
+Stamps (CTA (0,0), clock64 converted at 1.965 GHz): 0 entry, 1 setup done, 2 PDL wait released,
 3 first activation tile landed, 4 accumulator complete, 5 partial parked +
 pushed, 6 peers' slices landed, 7 reduce + epilogue stored, 8 cluster exit.
 """
@@ -22,10 +22,18 @@ for i in range(n):
     if st[i, 0] == 0 or st[i, 8] == 0:
         continue
     groups[tuple(meta[i])].append(st[i])
+sub = ["drain(4-9)", "sync(9-10)", "clwait(10-11)", "push+x(11-5)"]
+print(f"{'N,K,epi,S':22s} " + " ".join(f"{x:>14s}" for x in sub))
+for key, rows in sorted(groups.items()):
+    r = np.array(rows)
+    if (r[:, 9] == 0).all():
+        continue
+    d = [(r[:, 9] - r[:, 4]), (r[:, 10] - r[:, 9]), (r[:, 11] - r[:, 10]), (r[:, 5] - r[:, 11])]
+    print(f"{str(tuple(int(x) for x in key)):22s} " + " ".join(f"{np.median(x) / 1.965e3:14.2f}" for x in d))
 print(f"{'N,K,epi,S':22s} {'n':>4s} " + " ".join(f"{x:>12s}" for x in names) + f" {'total':>8s}")
 for key, rows in sorted(groups.items()):
     r = np.array(rows)
-    d = np.diff(r[:, :9], axis=1) / 1e3
+    d = np.diff(r[:, :9], axis=1) / 1.965e3
     med = np.median(d, axis=0)
     print(f"{str(key):22s} {len(rows):4d} " + " ".join(f"{x:12.2f}" for x in med) +
-          f" {np.median((r[:, 8] - r[:, 0]) / 1e3):8.2f}")
+          f" {np.median((r[:, 8] - r[:, 0]) / 1.965e3):8.2f}")
