@@ -349,8 +349,22 @@ def run_ours(args):
             return {"bound": "tensor" if tensor else "hbm", "achieved": ach, "peak": peak, "unit": unit,
                     "frac": ach / peak, "per_launch_ms": v["ms"] / v["launches"], "launches": v["launches"],
                     "algorithmic_per_launch": (v["flops"] if tensor else v["bytes"]) / v["launches"]}
+        # measured DRAM traffic per launch of the roofline class, from the newest
+        # committed ncu launch list (profiles/<round>/traffic.json)
+        traffic, traffic_src = None, None
+        try:
+            import glob
+            tj = sorted(glob.glob(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "*",
+                                               "traffic.json")))
+            if tj:
+                tdoc = json.load(open(tj[-1]))
+                traffic = tdoc["bytes_per_launch"].get(roof_cls)
+                traffic_src = os.path.relpath(tj[-1], os.path.dirname(os.path.abspath(__file__)))
+        except Exception:
+            pass
         if prof.get(roof_cls, {}).get("launches"):
-            line["roofline"] = {"kernel": roof_cls, **rf(prof[roof_cls], roof_cls in ("gemm_tc",)), "traffic": None,
+            line["roofline"] = {"kernel": roof_cls, **rf(prof[roof_cls], roof_cls in ("gemm_tc",)), "traffic": traffic,
+                                "traffic_source": traffic_src,
                                 "peak_source": "MEASURED_PEAKS.json" + (" (fallback)" if pk.get("fallback") else ""),
                                 "timing": "CUDA events on the library stream around every launch of this class, "
                                           "one extra step of the same workload after the timed region (events inside "

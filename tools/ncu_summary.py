@@ -18,23 +18,41 @@ def launches(path, out, skip=0.0):
             hdr, start = r, i + 1
             break
     ki, vi, gi, bi = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Grid Size"), hdr.index("Block Size")
-    mi, ui = hdr.index("Metric Name"), hdr.index("Metric Unit")
-    scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}
-    data = [(re.sub(r"\(.*", "", r[ki]).replace("void ", ""), r[gi], r[bi],
-             float(r[vi].replace(",", "")) * scale.get(r[ui], 1e-3))
-            for r in rows[start:] if len(r) > vi and r[mi] == "gpu__time_duration.sum"]
+    mi, ui, ii = hdr.index("Metric Name"), hdr.index("Metric Unit"), hdr.index("ID")
+    tscale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}
+    bscale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9}
+    per = collections.OrderedDict()  # launch id -> {name, grid, block, t, dram}
+    for r in rows[start:]:
+        if len(r) <= vi:
+            continue
+        e = per.setdefault(r[ii], {"n": re.sub(r"\(.*", "", r[ki].replace("(anonymous namespace)::", "")).replace("void ", ""),
+                                   "g": r[gi], "b": r[bi], "t": 0.0, "dram": 0.0, "has_dram": False})
+        v = float(r[vi].replace(",", ""))
+        if r[mi] == "gpu__time_duration.sum":
+            e["t"] = v * tscale.get(r[ui], 1e-3)
+        elif r[mi].startswith("dram__bytes_"):
+            e["dram"] += v * bscale.get(r[ui], 1.0)
+            e["has_dram"] = True
+    data = list(per.values())
     data = data[int(len(data) * skip):]
-    agg = collections.defaultdict(lambda: [0, 0.0])
-    for n, g, b, v in data:
-        agg[(n, g, b)][0] += 1
-        agg[(n, g, b)][1] += v
+    agg = collections.defaultdict(lambda: [0, 0.0, 0.0])
+    has_dram = any(x["has_dram"] for x in data)
+    for x in data:
+        a = agg[(x["n"], x["g"], x["b"])]
+        a[0] += 1
+        a[1] += x["t"]
+        a[2] += x["dram"]
     tot = sum(a[1] for a in agg.values())
     with open(out, "w") as f:
-        f.write(f"# ncu launch list summary ({len(data)} launches, gpu__time_duration.sum, "
-                f"--clock-control none; serialized, so compare SHARES)\n\n")
-        f.write(f"source: `{path}`\n\n| kernel | grid | block | launches | us/launch | total us | share |\n|---|---|---|---|---|---|---|\n")
-        for (n, g, b), (c, t) in sorted(agg.items(), key=lambda x: -x[1][1]):
-            f.write(f"| `{n[:70]}` | {g} | {b} | {c} | {t / c:.2f} | {t:.1f} | {100 * t / tot:.1f}% |\n")
+        f.write(f"# ncu launch list summary ({len(data)} launches, gpu__time_duration.sum"
+                f"{' + dram__bytes_{read,write}.sum' if has_dram else ''}, --clock-control none; "
+                f"serialized, so compare SHARES)\n\n")
+        f.write(f"source: `{path}`\n\n| kernel | grid | block | launches | us/launch | total us | share |"
+                f"{' DRAM MB/launch |' if has_dram else ''}\n|---|---|---|---|---|---|---|{'---|' if has_dram else ''}\n")
+        for (n, g, b), (c, t, d) in sorted(agg.items(), key=lambda x: -x[1][1]):
+            f.write(f"| `{n[:70]}` | {g} | {b} | {c} | {t / c:.2f} | {t:.1f} | {100 * t / tot:.1f}% |"
+                    f"{f' {d / c / 1e6:.2f} |' if has_dram else ''}\n")
+    return agg
 
 
 def full(rep, out):
@@ -68,6 +86,24 @@ def full(rep, out):
             f.write("\n## top stall sites (SASS)\n\n| share | executed | instruction |\n|---|---|---|\n")
             for a, t, smp, n in sorted(rows, key=lambda x: -x[2])[:20]:
                 f.write(f"| {100 * smp / tot:.1f}% | {n:.0f} | `{t[:90]}` |\n")
+        cs = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+                            capture_output=True, text=True).stdout
+        cur, hdr, lines = None, None, []
+        for x in csv.reader(io.StringIO(cs)):
+            if len(x) >= 2 and x[0] == "File Path":
+                cur = x[1].split("/")[-1]
+            elif len(x) > 2 and x[0] == "Line No":
+                hdr = x
+            elif hdr and len(x) > 5 and x[0]:
+                try:
+                    lines.append((float(x[4] or 0), cur, x[0], x[1].strip()))
+                except ValueError:
+                    pass
+        tot = sum(x[0] for x in lines) or 1
+        if lines:
+            f.write("\n## top stall sites (CUDA source lines)\n\n| share | line | source |\n|---|---|---|\n")
+            for smp, fn, ln, src_ in sorted(lines, reverse=True)[:20]:
+                f.write(f"| {100 * smp / tot:.1f}% | {fn}:{ln} | `{src_[:90]}` |\n")
 
 
 if __name__ == "__main__":
