@@ -106,13 +106,16 @@ struct SmemLayout {
   static constexpr int kA = BM * BK * 2;   // 16 KB
   static constexpr int kB = BN * BK * 2;
   static constexpr int kStage = kA + kB;
-  static constexpr int kStages = (200 * 1024) / kStage > 8 ? 8 : (200 * 1024) / kStage;
+  // ~110 KB of stages: two CTAs share an SM (TMEM: 2 x BN <= 512 columns), so
+  // one CTA's epilogue (TMEM -> registers -> global, fp32 residual RMW)
+  // overlaps the other's TMA/MMA main loop
+  static constexpr int kStages = (110 * 1024) / kStage > 8 ? 8 : (110 * 1024) / kStage;
   static constexpr int kBytes = kStages * kStage + 1024 /*align*/ + 256 /*barriers*/;
   static constexpr int kTmemCols = BN < 32 ? 32 : BN;
 };
 
 template <int BN, int EPI>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreads, 2)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
                    int K, void* __restrict__ Cv, int64_t ldc, int group_m) {
   using L = SmemLayout<BN>;
