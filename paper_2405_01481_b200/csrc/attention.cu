@@ -11,6 +11,8 @@
 //    (src/model.cpp:313-333): scale by 1/sqrt(dh) before the max, exp(s-max),
 //    normalise, weighted V sum.
 #include <cfloat>
+#include <cstdio>
+#include <cstdlib>
 
 #include "kernels.hpp"
 
@@ -106,7 +108,7 @@ __device__ __forceinline__ void cp_async16_dec(void* dst, const void* src) {
                : "memory");
 }
 
-template <class T, int DH>
+template <class T, int DH, int NS>  // NS: K/V tile stages per warp (1 = 6 CTAs/SM for dh 64 bf16)
 __global__ void __launch_bounds__(128, 6) attn_decode_kernel(const T* __restrict__ qkv, const int32_t* __restrict__ pos,
                                                           const int32_t* __restrict__ done,
                                                           const int32_t* __restrict__ block_table, int layer,
@@ -147,7 +149,7 @@ __global__ void __launch_bounds__(128, 6) attn_decode_kernel(const T* __restrict
   for (int i = tid; i < DH; i += 128) sm_q[i] = to_f(row[h * DH + i]);
   __syncthreads();  // the appended row and the query are visible to the whole CTA
   // per-warp double-buffered tiles: [buf][K|V][TT rows][LDB bytes]
-  uint8_t* wsm = smem_dec + size_t(w) * 2 * 2 * TT * LDB;
+  uint8_t* wsm = smem_dec + size_t(w) * NS * 2 * TT * LDB;
   auto tile_ptr = [&](int buf, int which) { return wsm + (buf * 2 + which) * TT * LDB; };
   auto chunk = [](int r, int c) { return r * LDB + ((SWZ ? (c ^ (r & 7)) : c) << 4); };
   auto issue = [&](int64_t t0, int buf) {
@@ -172,9 +174,9 @@ __global__ void __launch_bounds__(128, 6) attn_decode_kernel(const T* __restrict
   int64_t t0 = int64_t(w) * TT;
   int buf = 0;
   if (t0 < ctx) issue(t0, 0);
-  for (; t0 < ctx; t0 += int64_t(NW) * TT, buf ^= 1) {
+  for (; t0 < ctx; t0 += int64_t(NW) * TT) {
     const int64_t tn = t0 + int64_t(NW) * TT;
-    if (tn < ctx) {
+    if (NS == 2 && tn < ctx) {
       issue(tn, buf ^ 1);
       asm volatile("cp.async.wait_group 1;" ::: "memory");
     } else {
@@ -218,7 +220,12 @@ __global__ void __launch_bounds__(128, 6) attn_decode_kernel(const T* __restrict
 #pragma unroll
       for (int i = 0; i < DPL; ++i) acc[i] = fmaf(pj, to_f(vr[i]), acc[i]);
     }
-    __syncwarp();  // this buffer is refilled two tiles from now
+    __syncwarp();  // this buffer is refilled next (NS == 1) or two tiles from now
+    if (NS == 1) {
+      if (tn < ctx) issue(tn, 0);
+    } else {
+      buf ^= 1;
+    }
   }
   // ---- merge the warps
   if (lane == 0) {
@@ -258,21 +265,41 @@ void prefill_impl(Ctx& c, const T* qkv, const int64_t* seq_offsets, int64_t B, i
   c.launch("attention_prefill", 0, flops, [&] { launch_kernel(c, k, dim3(grid), dim3(64 * TPQ), smem, 1, qkv, seq_offsets, H, out); });
 }
 
-template <class T, int DH>
-void decode_impl(Ctx& c, const T* qkv, int64_t B, const int32_t* pos, const int32_t* done, const int32_t* block_table,
-                 int layer, const KvGeom& g, T* kv, T* out, double bytes) {
-  if (g.page_size % 32) throw ContractError("engine: page_size must be a multiple of 32");
-  auto k = attn_decode_kernel<T, DH>;
+template <class T, int DH, int NS>
+void decode_launch(Ctx& c, const T* qkv, int64_t B, const int32_t* pos, const int32_t* done,
+                   const int32_t* block_table, int layer, const KvGeom& g, T* kv, T* out, double bytes) {
+  auto k = attn_decode_kernel<T, DH, NS>;
   const size_t row = DH * sizeof(T) == 128 ? 128 : DH * sizeof(T) + 16;  // kernel's LDB
-  const size_t smem = size_t(4) * 2 * 2 * 32 * row;
+  const size_t smem = size_t(4) * NS * 2 * 32 * row;                     // 4 warps x NS x (K, V) x 32 rows
   static bool attr = false;
   if (!attr) {
     PPOEXP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     attr = true;
+    if (getenv("PPOEXP_DEBUG_ATTN")) {
+      int per_sm = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 128, smem);
+      fprintf(stderr, "attn_decode<%d,%d,%d>: dynamic smem %zu, %d CTAs/SM\n", int(sizeof(T)), DH, NS, smem, per_sm);
+    }
   }
   dim3 grid(g.H, B);
   c.launch("decode_attention", bytes, 0, [&] { launch_kernel(c, k, grid, dim3(128), smem, 1, qkv, pos, done,
                                                               block_table, layer, g, kv, out); });
+}
+
+template <class T, int DH>
+void decode_impl(Ctx& c, const T* qkv, int64_t B, const int32_t* pos, const int32_t* done, const int32_t* block_table,
+                 int layer, const KvGeom& g, T* kv, T* out, double bytes) {
+  if (g.page_size % 32) throw ContractError("engine: page_size must be a multiple of 32");
+  // single-stage tiles halve the CTA's shared memory (6 resident CTAs/SM for dh 64 bf16: one wave of
+  // 768 (sequence, head) CTAs at C2); other warps on the SM hide each warp's tile latency
+  static const int stages = [] {
+    const char* e = getenv("PPOEXP_ATTN_STAGES");
+    return e ? atoi(e) : 1;
+  }();
+  if (stages == 2)
+    decode_launch<T, DH, 2>(c, qkv, B, pos, done, block_table, layer, g, kv, out, bytes);
+  else
+    decode_launch<T, DH, 1>(c, qkv, B, pos, done, block_table, layer, g, kv, out, bytes);
 }
 
 }  // namespace
