@@ -162,6 +162,10 @@ SamplerState Engine::sampler_state() const {
   s.out_lps = out_lp;
   s.ostride = m->cfg.max_seq_len;
   s.n_active = n_active;
+  if (getenv("PPOEXP_SAMPLER_TRACE")) {
+    auto* buf = static_cast<unsigned long long*>(c->workspace("sampler.trace", 16 * 8));
+    s.dbg = buf;
+  }
   return s;
 }
 
@@ -394,6 +398,17 @@ void Engine::generate(int64_t B, const int32_t* prompts, const int64_t* offsets,
   last_ms = ms;
   if (ms_out) *ms_out = ms;
   if (const char* gp = getenv("PPOEXP_GEMM_TRACE")) dump_gemm_trace(*c, gp);
+  if (const char* sp = getenv("PPOEXP_SAMPLER_TRACE")) {  // debug: last sampler launch, row 0
+    unsigned long long h[16];
+    PPOEXP_CUDA(cudaMemcpy(h, c->workspace("sampler.trace", 16 * 8), sizeof(h), cudaMemcpyDeviceToHost));
+    if (FILE* fp = fopen(sp, "w")) {
+      const char* nm[8] = {"entry", "pass1 max", "pass2 q+hist", "Z", "confirm", "collect+sort", "threshold", "cdf+pick"};
+      for (int k = 1; k < 8; ++k)
+        fprintf(fp, "%-14s %8.2f us\n", nm[k], h[k] > h[k - 1] ? (h[k] - h[k - 1]) / 1965.0 : 0.0);
+      fprintf(fp, "total %.2f us, crossing-bucket members %llu\n", (h[7] - h[0]) / 1965.0, h[8]);
+      fclose(fp);
+    }
+  }
   if (trace_path && trace_buf.ptr) {  // debug: raw stamps of the last decode step
     std::vector<uint64_t> h(trace_buf.bytes / 8);
     PPOEXP_CUDA(cudaMemcpy(h.data(), trace_buf.ptr, trace_buf.bytes, cudaMemcpyDeviceToHost));

@@ -105,6 +105,7 @@ struct SamplerState {
   float* out_lps;       // [B, ostride]
   int64_t ostride;
   int32_t* n_active;    // [1] sequences still running after this step
+  unsigned long long* dbg = nullptr;  // debug (PPOEXP_SAMPLER_TRACE): row-0 stage clocks
 };
 void launch_sampler(Ctx& c, const float* logits, int64_t ld, int64_t B, int64_t V, const SamplerState& s);
 

@@ -32,6 +32,7 @@ struct Shared {
   unsigned hcnt[NB];
   unsigned hsum[NB];  // approximate bucket sums, fixed point q * 2^16 (native 32-bit smem atomics)
   unsigned long long list[LIST];
+  unsigned long long list2[256];  // rank-sort output for small crossing buckets
   float fm[NW], fmn[NW], fs[NW];
   int fi[NW];
   double dsum[NW];
@@ -51,11 +52,12 @@ struct Shared {
 
 __device__ __forceinline__ unsigned qbits_of(float q) { return __float_as_uint(q); }
 
-// bucket 0 = largest q (bits of 1.0), NB-1 = smallest.  scale = NB / span;
-// every step (int->float, multiply by a positive constant, truncation) is
-// monotone, so equal q map to equal buckets and larger q to lower buckets.
-__device__ __forceinline__ int bucket_of(unsigned bits, unsigned top, float scale) {
-  const int b = int(float(top - bits) * scale);  // bits <= top
+// bucket 0 = largest q (bits of 1.0), NB-1 = smallest:
+//   b = floor((top - bits) * scale / 2^32),  scale = floor(2^32 * NB / span).
+// Integer multiply-high only (no conversions: they are quarter-rate); monotone
+// in the bits, so equal q map to equal buckets and larger q to lower ones.
+__device__ __forceinline__ int bucket_of(unsigned bits, unsigned top, unsigned scale) {
+  const int b = int(__umulhi(top - bits, scale));  // bits <= top
   return b >= NB ? NB - 1 : b;
 }
 
@@ -122,6 +124,26 @@ __device__ void bitonic_sort(unsigned long long* a, int n) {
     }
 }
 
+// sort sh.list[0..n) ascending: small lists (the usual crossing bucket) by
+// rank counting (keys are unique: the index is part of the key), one pass and
+// one barrier; larger ones by the bitonic network
+template <class S>
+__device__ void sort_list(S& sh, int n) {
+  if (n <= 256) {
+    if (threadIdx.x < n) {
+      const unsigned long long key = sh.list[threadIdx.x];
+      int rank = 0;
+      for (int k = 0; k < n; ++k) rank += sh.list[k] < key;
+      sh.list2[rank] = key;
+    }
+    __syncthreads();
+    if (threadIdx.x < n) sh.list[threadIdx.x] = sh.list2[threadIdx.x];
+    __syncthreads();
+  } else {
+    bitonic_sort(sh.list, n);
+  }
+}
+
 // key = (q desc, index asc) ascending
 __device__ __forceinline__ unsigned long long sort_key(unsigned qb, int idx) {
   return ((unsigned long long)(~qb) << 32) | unsigned(idx);
@@ -137,6 +159,10 @@ __global__ void __launch_bounds__(NT) sampler_kernel(const float* __restrict__ l
   const int64_t b = blockIdx.x;
   if (s.done[b]) return;
   const SampleParams prm = s.params[b];
+  auto stamp = [&](int k) {
+    if (s.dbg && b == 0 && threadIdx.x == 0) s.dbg[k] = clock64();
+  };
+  stamp(0);
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
   const float* row = logits + b * ld;
   const int i = s.n_gen[b];
@@ -156,17 +182,27 @@ __global__ void __launch_bounds__(NT) sampler_kernel(const float* __restrict__ l
     const int64_t nv = V / 4;
     const float4* r4 = reinterpret_cast<const float4*>(row);
     int64_t k = tid;
+    float4* c4 = reinterpret_cast<float4*>(qcache);  // CACHED: the raw logits, transformed in place by pass 2
     for (; k + NT < nv; k += 2 * NT) {
       const float4 a = r4[k], c = r4[k + NT];
+      if constexpr (CACHED) {
+        c4[k] = a;
+        c4[k + NT] = c;
+      }
       visit(a.x, int(4 * k)); visit(a.y, int(4 * k + 1)); visit(a.z, int(4 * k + 2)); visit(a.w, int(4 * k + 3));
       visit(c.x, int(4 * (k + NT))); visit(c.y, int(4 * (k + NT) + 1));
       visit(c.z, int(4 * (k + NT) + 2)); visit(c.w, int(4 * (k + NT) + 3));
     }
     for (; k < nv; k += NT) {
       const float4 a = r4[k];
+      if constexpr (CACHED) c4[k] = a;
       visit(a.x, int(4 * k)); visit(a.y, int(4 * k + 1)); visit(a.z, int(4 * k + 2)); visit(a.w, int(4 * k + 3));
     }
-    for (int64_t j = nv * 4 + tid; j < V; j += NT) visit(row[j], int(j));
+    for (int64_t j = nv * 4 + tid; j < V; j += NT) {
+      const float v = row[j];
+      if constexpr (CACHED) qcache[j] = v;
+      visit(v, int(j));
+    }
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -189,6 +225,7 @@ __global__ void __launch_bounds__(NT) sampler_kernel(const float* __restrict__ l
     M = fmaxf(M, sh.fm[k]);
     MN = fminf(MN, sh.fmn[k]);
   }
+  stamp(1);
   // sum exp(l - M) for the untempered log-prob (src/model.cpp:450); when the
   // row is sampled at tau == 1 it is folded into pass 2 (q == exp(l - M))
   const bool fold = !prm.greedy && prm.temperature == 1.0f;
@@ -219,8 +256,8 @@ __global__ void __launch_bounds__(NT) sampler_kernel(const float* __restrict__ l
     // bucket span: bits(1.0) .. bits(q_min); q is monotone in the logit
     const unsigned top = qbits_of(1.0f);
     const unsigned botb = qbits_of(expf((MN - M) * inv_tau));
-    const float span = float(top - botb) + 1.0f;
-    const float scale = float(NB) / span;
+    const unsigned long long span = (unsigned long long)(top - botb) + 1ull;
+    const unsigned scale = unsigned(((unsigned long long)NB << 32) / span);  // (span - 1) * scale < NB * 2^32
     // ---- pass 2: q (cached), histogram
     if (filtering)
       for (int k = tid; k < NB; k += NT) {
@@ -230,9 +267,7 @@ __global__ void __launch_bounds__(NT) sampler_kernel(const float* __restrict__ l
     __syncthreads();
     double zloc = 0.0;
     float fsum = 0.f;
-    for (int64_t j = tid; j < V; j += NT) {
-      const float q = expf((row[j] - M) * inv_tau);
-      if constexpr (CACHED) qcache[j] = q;
+    auto pass2 = [&](float q) {
       fsum += q;
       if (filtering) {
         zloc += double(q);
@@ -240,6 +275,30 @@ __global__ void __launch_bounds__(NT) sampler_kernel(const float* __restrict__ l
         atomicAdd(&sh.hcnt[bk], 1u);
         atomicAdd(&sh.hsum[bk], __float2uint_rn(q * 65536.0f));
       }
+    };
+    if constexpr (CACHED) {
+      // the logits are in shared memory (pass 1): float4 in-place transform
+      float4* c4 = reinterpret_cast<float4*>(qcache);
+      const int nv = int(V / 4);
+      for (int k4 = tid; k4 < nv; k4 += NT) {
+        float4 l = c4[k4];
+        l.x = expf((l.x - M) * inv_tau);
+        l.y = expf((l.y - M) * inv_tau);
+        l.z = expf((l.z - M) * inv_tau);
+        l.w = expf((l.w - M) * inv_tau);
+        c4[k4] = l;
+        pass2(l.x);
+        pass2(l.y);
+        pass2(l.z);
+        pass2(l.w);
+      }
+      for (int j = nv * 4 + tid; j < int(V); j += NT) {
+        const float q = expf((qcache[j] - M) * inv_tau);
+        qcache[j] = q;
+        pass2(q);
+      }
+    } else {
+      for (int64_t j = tid; j < V; j += NT) pass2(expf((row[j] - M) * inv_tau));
     }
     if (fold) {  // lse from the same exp pass (tau == 1)
       fsum = warp_sum(fsum);
@@ -250,10 +309,12 @@ __global__ void __launch_bounds__(NT) sampler_kernel(const float* __restrict__ l
       lse = M + logf(SE);
     }
     __syncthreads();
+    stamp(2);
     unsigned t_final = 0;
     int idx_cut = int(V);  // keep everything
     if (filtering) {
       const double Z = block_sum_d(zloc, sh);
+      stamp(3);
       if (tid == 0) {
         sh.overflow = 0;
         sh.bk = NB;  // top-k bucket (NB = no top-k)
@@ -279,7 +340,7 @@ __global__ void __launch_bounds__(NT) sampler_kernel(const float* __restrict__ l
           __syncthreads();
           return;
         }
-        bitonic_sort(sh.list, n);
+        sort_list(sh, n);
       };
       unsigned k_t = 0;
       int k_cut = int(V), k_take = 0;
@@ -331,16 +392,42 @@ __global__ void __launch_bounds__(NT) sampler_kernel(const float* __restrict__ l
         // confirm it with exact fp64 sums (no atomics) and step to a neighbour
         // bucket if rounding put it one off
         int bp = sh.bp;
+        bool listed = false;  // sh.list holds the members of bucket bp (collected by the confirm pass)
         for (int guard = 0; guard < NB; ++guard) {
+          const bool col = bp != bk;  // bp == bk reuses the top-k sorted list
+          if (col) {
+            if (tid == 0) sh.list_n = 0;
+            __syncthreads();
+          }
           double lt = 0.0, eq = 0.0;
-          for (int64_t j = tid; j < V; j += NT) {
-            const float q = Q(j);
+          auto one = [&](float q, int j) {
             const unsigned qb = qbits_of(q);
             const int bj = bucket_of(qb, top, scale);
             const bool inK = bj < bk || (bj == bk && (qb > k_t || (qb == k_t && j <= k_cut)));
-            if (!inK) continue;
-            if (bj < bp) lt += double(q);
-            else if (bj == bp) eq += double(q);
+            if (!inK) return;
+            if (bj < bp) {
+              lt += double(q);
+            } else if (bj == bp) {
+              eq += double(q);
+              if (col) {
+                const int slot = atomicAdd(&sh.list_n, 1);
+                if (slot < LIST) sh.list[slot] = sort_key(qb, j);
+              }
+            }
+          };
+          if constexpr (CACHED) {
+            const float4* c4 = reinterpret_cast<const float4*>(qcache);
+            const int nv = int(V / 4);
+            for (int k4 = tid; k4 < nv; k4 += NT) {
+              const float4 q4 = c4[k4];
+              one(q4.x, 4 * k4);
+              one(q4.y, 4 * k4 + 1);
+              one(q4.z, 4 * k4 + 2);
+              one(q4.w, 4 * k4 + 3);
+            }
+            for (int j = nv * 4 + tid; j < int(V); j += NT) one(qcache[j], j);
+          } else {
+            for (int64_t j = tid; j < V; j += NT) one(Q(j), int(j));
           }
           lt = block_sum_d(lt, sh);
           eq = block_sum_d(eq, sh);
@@ -350,11 +437,27 @@ __global__ void __launch_bounds__(NT) sampler_kernel(const float* __restrict__ l
             ++bp;
           } else {
             if (tid == 0) sh.s_above = lt;
+            listed = col;
             break;
           }
         }
         __syncthreads();
-        if (bp != bk) collect_sort(bp);  // bp == bk reuses the top-k sorted list
+        stamp(4);
+        if (bp != bk) {
+          if (listed) {  // members already collected: sort them
+            const int n = sh.list_n;
+            if (n > LIST) {
+              if (tid == 0) sh.overflow = 1;
+              __syncthreads();
+            } else {
+              sort_list(sh, n);
+            }
+          } else {
+            collect_sort(bp);
+          }
+        }
+        stamp(5);
+        if (s.dbg && b == 0 && threadIdx.x == 0) s.dbg[8] = sh.list_n;
         if (!sh.overflow) {
           // first sorted member r with s_above + sum_{<=r} q >= target, as a block scan
           const int limit = bp == bk ? k_take : min(sh.list_n, LIST);
@@ -454,6 +557,7 @@ __global__ void __launch_bounds__(NT) sampler_kernel(const float* __restrict__ l
       t_final = k_t;
       idx_cut = k_cut;
     }
+    stamp(6);
     // ---- inverse CDF in index order over the kept tokens: every thread owns a
     // contiguous chunk (sequential fp64 sums), one block scan, and the thread
     // whose chunk brackets u*Z walks it (src/model.cpp:464-473 semantics)
@@ -501,6 +605,7 @@ __global__ void __launch_bounds__(NT) sampler_kernel(const float* __restrict__ l
     }
     __syncthreads();
     chosen = sh.result != 0x7fffffff ? sh.result : (fallback >= 0 ? fallback : int(V - 1));
+    stamp(7);
   }
   if (tid == 0) {
     if (i > 0) s.pos[b] += 1;
