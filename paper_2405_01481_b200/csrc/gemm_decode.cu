@@ -25,6 +25,7 @@ CUtensorMap make_map(const void* ptr, int64_t rows, int64_t cols, int64_t ld, in
 namespace {
 
 constexpr int BMW = 128, BK = 64, kThreads = 192;
+constexpr int kMaxS = 16;  // K-split ranks per cluster (16 = non-portable cluster size)
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -354,7 +355,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int f0 = r * rows_per, f1 = min(BMW, f0 + rows_per);
     const int nf4 = (f1 - f0) / 4;
     const int ncols = min(Mrows, NB);
-    const float4* parts[8];
     float4 xpre[4];
     if (push) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // parked partial -> bulk-copy reads
@@ -393,11 +393,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (threadIdx.x == 0) stamp(5);
       mbar_wait(rfull, 0);
       if (threadIdx.x == 0) stamp(6);
-      for (int k = 0; k < 8; ++k) {
-        const int kk = k < S ? k : 0;
-        parts[k] = reinterpret_cast<const float4*>(kk == r ? part + size_t(r) * NB * rows_per
-                                                           : recv + size_t(kk) * NB * rows_per);
-      }
+
     } else {
       if constexpr (EPI == int(Epi::kAddResidual)) {
 #pragma unroll
@@ -412,26 +408,39 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       cluster.sync();  // all partials of the cluster are parked in smem
-      for (int k = 0; k < 8; ++k)
-        parts[k] = reinterpret_cast<const float4*>(cluster.map_shared_rank(part, k < S ? k : 0));
+
     }
     int it = 0;
+    // rank k's partial: push -> own slice (k == r) or the receive area; pull -> DSMEM of rank k
+    auto part_of = [&](int k) -> const float4* {
+      if (push)
+        return reinterpret_cast<const float4*>(k == r ? part + size_t(r) * NB * rows_per
+                                                      : recv + size_t(k) * NB * rows_per);
+      return reinterpret_cast<const float4*>(cluster.map_shared_rank(part, k));
+    };
     for (int e = threadIdx.x; e < nf4 * ncols; e += kThreads, ++it) {
       const int fl = f0 + 4 * (e % nf4), bcol = e / nf4;
       const int idx = push ? ((bcol * rows_per + (fl - f0)) >> 2) : ((bcol * BMW + fl) >> 2);
-      float4 v[8];
+      // rank order, 8 partials in flight at a time
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int k0 = 0; k0 < S; k0 += 8) {
+        float4 v[8];
 #pragma unroll
-      for (int k = 0; k < 8; ++k)
-        if (k < S) v[k] = parts[k][idx];
-      float4 acc = v[0];
+        for (int k = 0; k < 8; ++k)
+          if (k0 + k < S) v[k] = part_of(k0 + k)[idx];
 #pragma unroll
-      for (int k = 1; k < 8; ++k)
-        if (k < S) {
-          acc.x += v[k].x;
-          acc.y += v[k].y;
-          acc.z += v[k].z;
-          acc.w += v[k].w;
-        }
+        for (int k = 0; k < 8; ++k)
+          if (k0 + k < S) {
+            if (k0 + k == 0) {
+              acc = v[0];
+            } else {
+              acc.x += v[k].x;
+              acc.y += v[k].y;
+              acc.z += v[k].z;
+              acc.w += v[k].w;
+            }
+          }
+      }
       const float a4[4] = {acc.x, acc.y, acc.z, acc.w};
       double ps = 0.0, pq = 0.0;
 #pragma unroll
@@ -518,12 +527,12 @@ int launch_dec(Ctx& c, const bf16* X, int64_t ldx, const bf16* W, int64_t ldw, i
   }();
   static const int smax_small = [] {  // narrow outputs (N <= 1024: O / down projections)
     const char* e = getenv("PPOEXP_DECODE_SPLIT_SMALLN");
-    return e ? atoi(e) : 8;
+    return std::min(e ? atoi(e) : 16, kMaxS);
   }();
   const int cap = tiles <= 8 ? smax_small : smax;
   int S = 1;
   while (S < cap && tiles * S < 148 && nk >= 2 * S) S *= 2;
-  while (S < 8 && ceil_div(nk, S) > L::kWcap) S *= 2;
+  while (S < kMaxS && ceil_div(nk, S) > L::kWcap) S *= 2;
   static const int wring = [] {
     const char* e = getenv("PPOEXP_DECODE_WRING");
     return e ? atoi(e) : 8;
