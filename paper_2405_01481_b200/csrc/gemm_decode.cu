@@ -152,9 +152,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&wempty[i], 1);
     }
     mbar_init(tmem_full, 1);
-    if (push) mbar_init(rfull, 1);
+    if (push) mbar_init(rfull, push == 2 ? 128 : 1);  // direct: one arrival per feature row of the slice
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    if (push) mbar_expect_tx(rfull, uint32_t(S - 1) * slice_bytes);  // the single arrival + the peers' bytes
+    if (push == 1) mbar_expect_tx(rfull, uint32_t(S - 1) * slice_bytes);  // the single arrival + the peers' bytes
     // The weights are constant across the graph: fetch this CTA's weight slice
     // (up to the ring size) BEFORE waiting on the predecessor grid (PDL), so
     // the HBM stream overlaps the previous kernel.
@@ -283,11 +283,24 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int f = q * 32 + lane;
     const int n = n0 + f;
     const int ncols = min(Mrows, NB);
+    // direct push (push == 2): this thread's feature row goes straight from
+    // registers into the owner rank's receive area, [sender][bcol][f % rows_per]
+    uint32_t rdst = 0;
+    if (S > 1 && push == 2) {
+      asm volatile("barrier.cluster.wait.aligned;" ::: "memory");  // every rank's rfull is initialised
+      const uint32_t loc = smem_u32(recv) + uint32_t((r * NB * rows_per + (f % rows_per)) * 4);
+      asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rdst) : "r"(loc), "r"(f / rows_per));
+    }
 #pragma unroll 1
     for (int c = 0; c < NB; c += 16) {
       uint32_t v[16];
       tmem_ld16(tmem + (uint32_t(q * 32) << 16) + uint32_t(c), v);
-      if (S > 1 && push) {
+      if (S > 1 && push == 2) {
+#pragma unroll
+        for (int e = 0; e < 16; ++e)
+          asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(rdst + uint32_t((c + e) * rows_per * 4)), "r"(v[e])
+                       : "memory");
+      } else if (S > 1 && push) {
         // slice-major [k][bcol][f % rows_per]: the slice for rank k is one
         // contiguous block, pushed with a single bulk copy
         float* ps = part + (f / rows_per) * (NB * rows_per) + (f % rows_per);
@@ -331,6 +344,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
+    if (S > 1 && push == 2) {  // release this row's stores to the owner rank
+      uint32_t rbar;
+      asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rbar) : "r"(smem_u32(rfull)), "r"(f / rows_per));
+      asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(rbar) : "memory");
+    }
     if (EPI == int(Epi::kAddResidual) && S == 1 && so.p) {
       asm volatile("bar.sync 1, 128;" ::: "memory");
       const float* wred = reinterpret_cast<const float*>(sX);
@@ -356,7 +374,26 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int nf4 = (f1 - f0) / 4;
     const int ncols = min(Mrows, NB);
     float4 xpre[4];
-    if (push) {
+    if (push == 2) {
+      if constexpr (EPI == int(Epi::kAddResidual)) {
+#pragma unroll
+        for (int it = 0; it < 4; ++it) {
+          const int e = threadIdx.x + it * kThreads;
+          xpre[it] = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (e < nf4 * ncols) {
+            const int fl = f0 + 4 * (e % nf4), bcol = e / nf4;
+            const int64_t o = int64_t(bcol) * ldc + n0 + fl;
+            if (n0 + fl + 3 < N && (o & 3) == 0) xpre[it] = __ldcg(reinterpret_cast<const float4*>(static_cast<float*>(Cv) + o));
+          }
+        }
+      }
+      if (threadIdx.x == 0) stamp(5);
+      asm volatile(  // acquire the peers' releases (cluster scope)
+          "{\n .reg .pred p;\n WAITC_%=:\n mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], 0;\n @!p bra WAITC_%=;\n}" ::"r"(
+              smem_u32(rfull))
+          : "memory");
+      if (threadIdx.x == 0) stamp(6);
+    } else if (push) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // parked partial -> bulk-copy reads
       if (threadIdx.x == 64) stamp(9);
       __syncthreads();
@@ -413,6 +450,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     int it = 0;
     // rank k's partial: push -> own slice (k == r) or the receive area; pull -> DSMEM of rank k
     auto part_of = [&](int k) -> const float4* {
+      if (push == 2) return reinterpret_cast<const float4*>(recv + size_t(k) * NB * rows_per);
       if (push)
         return reinterpret_cast<const float4*>(k == r ? part + size_t(r) * NB * rows_per
                                                       : recv + size_t(k) * NB * rows_per);
@@ -486,7 +524,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         so.p[(int64_t(slice) * so.ld + bcol) * 2 + 1] = s2;
       }
     }
-    if (push) {  // every peer's incoming copies (including ours) have landed before anyone exits
+    if (push == 2) {
+      // nothing reads this CTA's shared memory remotely, and every rank waits for all
+      // stores into its own receive area before it exits: no exit barrier
+    } else if (push) {  // every peer's incoming copies (including ours) have landed before anyone exits
       if (threadIdx.x == 0) stamp(7);
       asm volatile("barrier.cluster.arrive.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
       if (threadIdx.x == 0) stamp(8);
@@ -543,10 +584,11 @@ int launch_dec(Ctx& c, const bf16* X, int64_t ldx, const bf16* W, int64_t ldw, i
   const int ring = tiles * S > 148 ? std::min(wring, 4) : wring;
   const int wst = int(std::min<int64_t>(std::min<int64_t>(L::kWcap, ring), ceil_div(nk, S)));
   static const int push_env = [] {
+    // 2 = direct register -> remote-smem stores (default), 1 = park + bulk copy, 0 = pull
     const char* e = getenv("PPOEXP_DECODE_PUSH");
-    return e ? atoi(e) : 1;
+    return e ? atoi(e) : 2;
   }();
-  const int push = (push_env && S > 1 && L::bytes(wst) + wst * 16 + L::kPart <= L::kSmemMax) ? 1 : 0;
+  const int push = (push_env && S > 1 && L::bytes(wst) + wst * 16 + L::kPart <= L::kSmemMax) ? push_env : 0;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(tiles, S, 1);
   cfg.blockDim = dim3(kThreads, 1, 1);

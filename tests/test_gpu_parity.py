@@ -357,3 +357,21 @@ def test_bf16_persistent_decode_matches_per_op(px, ctx, oracle, monkeypatch, hea
         lp = oracle.sequence_logprobs(cfg, wb, [full])[0][len(p):]
         close(b.logprobs, lp, atol=3e-2, rtol=3e-3)
     assert same >= len(prompts) // 2
+
+
+def test_bf16_decode_is_deterministic(px, ctx, oracle):
+    """bf16 decode (split-K decode GEMMs with the direct DSMEM push reduction and
+    no exit barrier) is bitwise reproducible: a lost, late or reordered partial
+    would show up as run-to-run differences in tokens or log-probs."""
+    cfg = ModelCfg(V=4096, d=768, L=2, H=12, f=3072, S=128)
+    wb = bf16_round(oracle.init_params(cfg, 29))
+    prompts = synthetic_prompts(31, 64, 16, ragged_lengths=True)
+    tasks = [px.GenTask(p, 40, px.SamplingSpec.temperature_spec(1.0, 1000 + i, 0, 0.9)) for i, p in enumerate(prompts)]
+    runs = []
+    for _ in range(3):
+        eng = engine(px, ctx, cfg, wb, px.BF16)
+        runs.append(eng.generate_batch(tasks))
+    for r in runs[1:]:
+        for a, b in zip(runs[0], r):
+            assert np.array_equal(a.tokens, b.tokens)
+            assert np.array_equal(a.logprobs, b.logprobs)
