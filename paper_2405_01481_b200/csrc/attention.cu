@@ -113,7 +113,12 @@ __global__ void __launch_bounds__(128, 6) attn_decode_kernel(const T* __restrict
                                                           const int32_t* __restrict__ done,
                                                           const int32_t* __restrict__ block_table, int layer,
                                                           KvGeom g, T* __restrict__ kv, T* __restrict__ out) {
-  PDL_ENTRY();
+  // Programmatic dependent launch: only this step's q/k/v (the immediately
+  // preceding QKV GEMM) is produced by the predecessor grid.  Every earlier
+  // kernel has completed when this grid starts (each kernel triggers its
+  // dependents only after its own griddepcontrol.wait), so the sequence
+  // state, the block table and the cached K/V rows < pos are read BEFORE the
+  // wait: the first tile's HBM latency overlaps the QKV GEMM's tail.
   constexpr int NW = 4, TT = 32;
   constexpr int ROWB = DH * int(sizeof(T));   // bytes per K/V row
   // 128-byte rows (bf16, dh 64) are stored unpadded with the 16-byte chunks
@@ -131,7 +136,7 @@ __global__ void __launch_bounds__(128, 6) attn_decode_kernel(const T* __restrict
   __shared__ float sm_acc[NW][DH];
   __shared__ __align__(16) float sm_q[DH];  // the query (lane-uniform reads: broadcast)
   const int64_t b = blockIdx.y, h = blockIdx.x;
-  if (done[b]) return;
+  if (done[b]) return;  // (implicit trigger at exit)
   const int64_t p = pos[b], ctx = p + 1;
   const int64_t d = g.H * DH, PS = g.page_size;
   const T* row = qkv + b * 3 * d;
@@ -141,14 +146,7 @@ __global__ void __launch_bounds__(128, 6) attn_decode_kernel(const T* __restrict
     return kv + ((((int64_t)layer * g.n_pages + page) * 2 + which) * g.H + h) * PS * DH + (t % PS) * DH;
   };
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
-  // append this step's K/V row (KvSession::step, src/model.cpp:305-308)
-  for (int i = tid; i < DH; i += 128) {
-    base(p, 0)[i] = row[d + h * DH + i];
-    base(p, 1)[i] = row[2 * d + h * DH + i];
-  }
-  for (int i = tid; i < DH; i += 128) sm_q[i] = to_f(row[h * DH + i]);
-  __syncthreads();  // the appended row and the query are visible to the whole CTA
-  // per-warp double-buffered tiles: [buf][K|V][TT rows][LDB bytes]
+  // per-warp tiles: [stage][K|V][TT rows][LDB bytes]
   uint8_t* wsm = smem_dec + size_t(w) * NS * 2 * TT * LDB;
   auto tile_ptr = [&](int buf, int which) { return wsm + (buf * 2 + which) * TT * LDB; };
   auto chunk = [](int r, int c) { return r * LDB + ((SWZ ? (c ^ (r & 7)) : c) << 4); };
@@ -173,7 +171,19 @@ __global__ void __launch_bounds__(128, 6) attn_decode_kernel(const T* __restrict
   const int dl = lane < DLANES ? lane : 0;
   int64_t t0 = int64_t(w) * TT;
   int buf = 0;
-  if (t0 < ctx) issue(t0, 0);
+  // this warp's first tile, unless it holds the new position (appended below)
+  const bool early = t0 < ctx && !(p >= t0 && p < t0 + TT);
+  if (early) issue(t0, 0);
+  pdl_wait();  // this step's q/k/v are valid from here on
+  pdl_trigger();
+  // append this step's K/V row (KvSession::step, src/model.cpp:305-308)
+  for (int i = tid; i < DH; i += 128) {
+    base(p, 0)[i] = row[d + h * DH + i];
+    base(p, 1)[i] = row[2 * d + h * DH + i];
+  }
+  for (int i = tid; i < DH; i += 128) sm_q[i] = to_f(row[h * DH + i]);
+  __syncthreads();  // the appended row and the query are visible to the whole CTA
+  if (t0 < ctx && !early) issue(t0, 0);
   for (; t0 < ctx; t0 += int64_t(NW) * TT) {
     const int64_t tn = t0 + int64_t(NW) * TT;
     if (NS == 2 && tn < ctx) {
