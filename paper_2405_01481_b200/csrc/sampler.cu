@@ -17,9 +17,13 @@
 // crossing bucket, and an exact (q desc, index asc) bitonic sort of that
 // bucket alone.  The kept set is {q > t} ∪ {q == t, index <= cut}.  The
 // inverse CDF runs over warp-contiguous index ranges with warp scans.
+#include <cooperative_groups.h>
+
 #include <cfloat>
 
 #include "kernels.hpp"
+
+namespace cg = cooperative_groups;
 
 namespace ppx {
 
@@ -48,6 +52,11 @@ struct Shared {
   unsigned t_final;
   int idx_cut;
   int overflow;
+  // CTA-pair exchange slots (two, alternating)
+  float xf[2][4];
+  int xi[2][4];
+  unsigned xu[2][4];
+  double xd[2][4];
 };
 
 __device__ __forceinline__ unsigned qbits_of(float q) { return __float_as_uint(q); }
@@ -150,25 +159,48 @@ __device__ __forceinline__ unsigned long long sort_key(unsigned qb, int idx) {
 }
 __device__ __forceinline__ float key_q(unsigned long long e) { return __uint_as_float(~unsigned(e >> 32)); }
 
-template <bool CACHED>
+// Cluster helpers (CL = 2: a row split over a CTA pair).  A row-global value
+// is combined by writing this CTA's part to a shared slot, one cluster
+// barrier, and reading the partner's slot through DSMEM; parts are combined in
+// rank order, so both CTAs hold identical, deterministic results.
+__device__ __forceinline__ void cl_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ unsigned cl_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+template <class T>
+__device__ __forceinline__ const T* peer_ptr(const T* p, unsigned rank) {
+  return static_cast<const T*>(cg::this_cluster().map_shared_rank(const_cast<T*>(p), rank));
+}
+
+template <bool CACHED, int CL>
 __global__ void __launch_bounds__(NT) sampler_kernel(const float* __restrict__ logits, int64_t ld, int64_t V,
                                                      SamplerState s) {
   PDL_ENTRY();
-  extern __shared__ float qcache[];  // CACHED: q[V]
+  extern __shared__ __align__(16) float qcache[];  // CACHED: this CTA's part of the row (logits, then q)
   __shared__ Shared sh;
-  const int64_t b = blockIdx.x;
-  if (s.done[b]) return;
+  const unsigned r = CL > 1 ? cl_rank() : 0u, pr = r ^ 1u;
+  const int64_t b = blockIdx.x / CL;
+  if (s.done[b]) return;  // both CTAs of a row return together
+  // this CTA's index range [jlo, jhi): halves rounded to 16 bytes
+  const int64_t half = CL > 1 ? (V + 7) / 8 * 4 : V;
+  const int64_t jlo = int64_t(r) * half, jhi = V < jlo + half ? V : jlo + half;
   const SampleParams prm = s.params[b];
   auto stamp = [&](int k) {
-    if (s.dbg && b == 0 && threadIdx.x == 0) s.dbg[k] = clock64();
+    if (s.dbg && b == 0 && r == 0 && threadIdx.x == 0) s.dbg[k] = clock64();
   };
   stamp(0);
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
   const float* row = logits + b * ld;
   const int i = s.n_gen[b];
+  int xs = 0;  // exchange slot (alternates: a slot is rewritten only two barriers later)
 
-  // ---- pass 1: max, min, first argmax (16-byte loads; ascending index per
-  // thread keeps "first index wins" exact)
+  // ---- pass 1: max, min, first argmax over [jlo, jhi) (16-byte loads;
+  // ascending index per thread keeps "first index wins" exact); the logits
+  // are cached in shared memory on the way
   float m = -INFINITY, mn = INFINITY;
   int am = 0x7fffffff;
   auto visit = [&](float v, int j) {
@@ -179,28 +211,29 @@ __global__ void __launch_bounds__(NT) sampler_kernel(const float* __restrict__ l
     mn = fminf(mn, v);
   };
   {
-    const int64_t nv = V / 4;
-    const float4* r4 = reinterpret_cast<const float4*>(row);
+    const int64_t nv = (jhi - jlo) / 4;
+    const float4* r4 = reinterpret_cast<const float4*>(row + jlo);
+    float4* c4 = reinterpret_cast<float4*>(qcache);
     int64_t k = tid;
-    float4* c4 = reinterpret_cast<float4*>(qcache);  // CACHED: the raw logits, transformed in place by pass 2
     for (; k + NT < nv; k += 2 * NT) {
       const float4 a = r4[k], c = r4[k + NT];
       if constexpr (CACHED) {
         c4[k] = a;
         c4[k + NT] = c;
       }
-      visit(a.x, int(4 * k)); visit(a.y, int(4 * k + 1)); visit(a.z, int(4 * k + 2)); visit(a.w, int(4 * k + 3));
-      visit(c.x, int(4 * (k + NT))); visit(c.y, int(4 * (k + NT) + 1));
-      visit(c.z, int(4 * (k + NT) + 2)); visit(c.w, int(4 * (k + NT) + 3));
+      const int j0 = int(jlo + 4 * k), j1 = int(jlo + 4 * (k + NT));
+      visit(a.x, j0); visit(a.y, j0 + 1); visit(a.z, j0 + 2); visit(a.w, j0 + 3);
+      visit(c.x, j1); visit(c.y, j1 + 1); visit(c.z, j1 + 2); visit(c.w, j1 + 3);
     }
     for (; k < nv; k += NT) {
       const float4 a = r4[k];
       if constexpr (CACHED) c4[k] = a;
-      visit(a.x, int(4 * k)); visit(a.y, int(4 * k + 1)); visit(a.z, int(4 * k + 2)); visit(a.w, int(4 * k + 3));
+      const int j0 = int(jlo + 4 * k);
+      visit(a.x, j0); visit(a.y, j0 + 1); visit(a.z, j0 + 2); visit(a.w, j0 + 3);
     }
-    for (int64_t j = nv * 4 + tid; j < V; j += NT) {
+    for (int64_t j = jlo + nv * 4 + tid; j < jhi; j += NT) {
       const float v = row[j];
-      if constexpr (CACHED) qcache[j] = v;
+      if constexpr (CACHED) qcache[j - jlo] = v;
       visit(v, int(j));
     }
   }
@@ -225,21 +258,61 @@ __global__ void __launch_bounds__(NT) sampler_kernel(const float* __restrict__ l
     M = fmaxf(M, sh.fm[k]);
     MN = fminf(MN, sh.fmn[k]);
   }
+  if constexpr (CL > 1) {
+    if (tid == 0) {
+      sh.xf[xs][0] = M;
+      sh.xf[xs][1] = MN;
+      sh.xi[xs][0] = AM;
+    }
+    cl_sync();
+    const float M2 = peer_ptr(&sh.xf[xs][0], pr)[0], MN2 = peer_ptr(&sh.xf[xs][0], pr)[1];
+    const int AM2 = peer_ptr(&sh.xi[xs][0], pr)[0];
+    AM = M > M2 ? AM : (M2 > M ? AM2 : min(AM, AM2));
+    M = fmaxf(M, M2);
+    MN = fminf(MN, MN2);
+    xs ^= 1;
+  }
   stamp(1);
+  // row-global float sum of per-CTA block totals, in rank order
+  auto row_sum_f = [&](float v) -> float {
+    if constexpr (CL > 1) {
+      if (tid == 0) sh.xf[xs][2] = v;
+      cl_sync();
+      const float o = peer_ptr(&sh.xf[xs][0], pr)[2];
+      xs ^= 1;
+      return r == 0 ? v + o : o + v;
+    } else {
+      return v;
+    }
+  };
+  auto row_sum_d2 = [&](double& a, double& c) {  // two fp64 block totals, rank order
+    if constexpr (CL > 1) {
+      if (tid == 0) {
+        sh.xd[xs][0] = a;
+        sh.xd[xs][1] = c;
+      }
+      cl_sync();
+      const double* o = peer_ptr(&sh.xd[xs][0], pr);
+      const double oa = o[0], oc = o[1];
+      a = r == 0 ? a + oa : oa + a;
+      c = r == 0 ? c + oc : oc + c;
+      xs ^= 1;
+    }
+  };
   // sum exp(l - M) for the untempered log-prob (src/model.cpp:450); when the
   // row is sampled at tau == 1 it is folded into pass 2 (q == exp(l - M))
   const bool fold = !prm.greedy && prm.temperature == 1.0f;
   float lse = 0.f;
   if (!fold) {
     float se = 0.f;
-    for (int64_t j = tid; j < V; j += NT) se += expf(row[j] - M);
+    for (int64_t j = jlo + tid; j < jhi; j += NT) se += expf(row[j] - M);
     se = warp_sum(se);
     __syncthreads();
     if (lane == 0) sh.fs[w] = se;
     __syncthreads();
     float SE = 0.f;
     for (int k = 0; k < NW; ++k) SE += sh.fs[k];
-    lse = M + logf(SE);
+    lse = M + logf(row_sum_f(SE));
   }
 
   int chosen = AM;
@@ -249,9 +322,19 @@ __global__ void __launch_bounds__(NT) sampler_kernel(const float* __restrict__ l
     const bool filt_k = prm.top_k > 0 && prm.top_k < V;
     const bool filt_p = prm.top_p < 1.0;
     const bool filtering = filt_k || filt_p;
-    auto Q = [&](int64_t j) -> float {
-      if constexpr (CACHED) return qcache[j];
+    auto Q = [&](int64_t j) -> float {  // j in [jlo, jhi)
+      if constexpr (CACHED) return qcache[j - jlo];
       else return expf((row[j] - M) * inv_tau);
+    };
+    // any j (the overflow path, run by rank 0 alone): the partner's part through DSMEM
+    const float* pq = CL > 1 ? peer_ptr(qcache, pr) : qcache;
+    auto Qall = [&](int64_t j) -> float {
+      if constexpr (CACHED) {
+        if (j >= jlo && j < jhi) return qcache[j - jlo];
+        return pq[j - int64_t(pr) * half];
+      } else {
+        return expf((row[j] - M) * inv_tau);
+      }
     };
     // bucket span: bits(1.0) .. bits(q_min); q is monotone in the logit
     const unsigned top = qbits_of(1.0f);
@@ -279,7 +362,7 @@ __global__ void __launch_bounds__(NT) sampler_kernel(const float* __restrict__ l
     if constexpr (CACHED) {
       // the logits are in shared memory (pass 1): float4 in-place transform
       float4* c4 = reinterpret_cast<float4*>(qcache);
-      const int nv = int(V / 4);
+      const int nloc = int(jhi - jlo), nv = nloc / 4;
       for (int k4 = tid; k4 < nv; k4 += NT) {
         float4 l = c4[k4];
         l.x = expf((l.x - M) * inv_tau);
@@ -292,13 +375,13 @@ __global__ void __launch_bounds__(NT) sampler_kernel(const float* __restrict__ l
         pass2(l.z);
         pass2(l.w);
       }
-      for (int j = nv * 4 + tid; j < int(V); j += NT) {
+      for (int j = nv * 4 + tid; j < nloc; j += NT) {
         const float q = expf((qcache[j] - M) * inv_tau);
         qcache[j] = q;
         pass2(q);
       }
     } else {
-      for (int64_t j = tid; j < V; j += NT) pass2(expf((row[j] - M) * inv_tau));
+      for (int64_t j = jlo + tid; j < jhi; j += NT) pass2(expf((row[j] - M) * inv_tau));
     }
     if (fold) {  // lse from the same exp pass (tau == 1)
       fsum = warp_sum(fsum);
@@ -306,14 +389,31 @@ __global__ void __launch_bounds__(NT) sampler_kernel(const float* __restrict__ l
       __syncthreads();
       float SE = 0.f;
       for (int k = 0; k < NW; ++k) SE += sh.fs[k];
-      lse = M + logf(SE);
+      lse = M + logf(row_sum_f(SE));
     }
     __syncthreads();
     stamp(2);
     unsigned t_final = 0;
     int idx_cut = int(V);  // keep everything
     if (filtering) {
-      const double Z = block_sum_d(zloc, sh);
+      double Z = block_sum_d(zloc, sh), unused = 0.0;
+      if constexpr (CL > 1) {
+        // the pair's histograms are merged into hcnt/hsum of both CTAs: partner
+        // values are read into registers first, then (after a barrier that keeps
+        // the partner from reading half-updated bins) added in rank order
+        row_sum_d2(Z, unused);  // (the barrier here also publishes the histograms)
+        unsigned pc = 0, psum = 0;
+        if (tid < NB) {
+          pc = peer_ptr(sh.hcnt, pr)[tid];
+          psum = peer_ptr(sh.hsum, pr)[tid];
+        }
+        cl_sync();
+        if (tid < NB) {
+          sh.hcnt[tid] += pc;  // integer sums: order-independent
+          sh.hsum[tid] += psum;
+        }
+        __syncthreads();
+      }
       stamp(3);
       if (tid == 0) {
         sh.overflow = 0;
@@ -322,11 +422,30 @@ __global__ void __launch_bounds__(NT) sampler_kernel(const float* __restrict__ l
         sh.zk_bucket = 0.0;
       }
       __syncthreads();
+      // union of the pair's collected lists: own entries first, then the
+      // partner's (both CTAs end with the same multiset; sorting makes it canonical)
+      auto merge_lists = [&]() {
+        if constexpr (CL > 1) {
+          const int n_own = sh.list_n;
+          if (tid == 0) sh.xi[xs][1] = n_own;
+          cl_sync();
+          const int n_p = peer_ptr(&sh.xi[xs][0], pr)[1];
+          const unsigned long long* plist = peer_ptr(sh.list, pr);
+          const bool fits = n_own <= LIST && n_p <= LIST && n_own + n_p <= LIST;
+          if (fits)
+            for (int k = tid; k < n_p; k += NT) sh.list[n_own + k] = plist[k];
+          cl_sync();  // the partner has copied our entries before either list is permuted
+          if (tid == 0) sh.list_n = fits ? n_own + n_p : LIST + 1;
+          xs ^= 1;
+          __syncthreads();
+        }
+      };
       // collect the members of bucket `bkt` into sh.list and sort them
       auto collect_sort = [&](int bkt) {
+        if constexpr (CL > 1) cl_sync();  // the previous union has been consumed by both CTAs
         if (tid == 0) sh.list_n = 0;
         __syncthreads();
-        for (int64_t j = tid; j < V; j += NT) {
+        for (int64_t j = jlo + tid; j < jhi; j += NT) {
           const unsigned qb = qbits_of(Q(j));
           if (bucket_of(qb, top, scale) == bkt) {
             const int slot = atomicAdd(&sh.list_n, 1);
@@ -334,6 +453,7 @@ __global__ void __launch_bounds__(NT) sampler_kernel(const float* __restrict__ l
           }
         }
         __syncthreads();
+        merge_lists();
         const int n = sh.list_n;
         if (n > LIST) {
           if (tid == 0) sh.overflow = 1;
@@ -361,7 +481,7 @@ __global__ void __launch_bounds__(NT) sampler_kernel(const float* __restrict__ l
           k_take = int(unsigned(prm.top_k) - sh.c_above);
           if (tid == 0) {
             double zb = 0.0;
-            for (int r = 0; r < k_take; ++r) zb += double(key_q(sh.list[r]));
+            for (int rr = 0; rr < k_take; ++rr) zb += double(key_q(sh.list[rr]));
             sh.zk_bucket = zb;
             sh.zk = sh.s_above + zb;
             const unsigned long long e = sh.list[k_take - 1];
@@ -390,12 +510,14 @@ __global__ void __launch_bounds__(NT) sampler_kernel(const float* __restrict__ l
         }
         // the fixed-point histogram only locates the crossing approximately:
         // confirm it with exact fp64 sums (no atomics) and step to a neighbour
-        // bucket if rounding put it one off
+        // bucket if rounding put it one off; the same pass collects the
+        // members of the crossing bucket
         int bp = sh.bp;
-        bool listed = false;  // sh.list holds the members of bucket bp (collected by the confirm pass)
+        bool listed = false;  // sh.list holds the members of bucket bp
         for (int guard = 0; guard < NB; ++guard) {
           const bool col = bp != bk;  // bp == bk reuses the top-k sorted list
           if (col) {
+            if constexpr (CL > 1) cl_sync();  // the previous union has been consumed by both CTAs
             if (tid == 0) sh.list_n = 0;
             __syncthreads();
           }
@@ -417,20 +539,23 @@ __global__ void __launch_bounds__(NT) sampler_kernel(const float* __restrict__ l
           };
           if constexpr (CACHED) {
             const float4* c4 = reinterpret_cast<const float4*>(qcache);
-            const int nv = int(V / 4);
+            const int nloc = int(jhi - jlo), nv = nloc / 4;
             for (int k4 = tid; k4 < nv; k4 += NT) {
               const float4 q4 = c4[k4];
-              one(q4.x, 4 * k4);
-              one(q4.y, 4 * k4 + 1);
-              one(q4.z, 4 * k4 + 2);
-              one(q4.w, 4 * k4 + 3);
+              const int j0 = int(jlo) + 4 * k4;
+              one(q4.x, j0);
+              one(q4.y, j0 + 1);
+              one(q4.z, j0 + 2);
+              one(q4.w, j0 + 3);
             }
-            for (int j = nv * 4 + tid; j < int(V); j += NT) one(qcache[j], j);
+            for (int j = nv * 4 + tid; j < nloc; j += NT) one(qcache[j], int(jlo) + j);
           } else {
-            for (int64_t j = tid; j < V; j += NT) one(Q(j), int(j));
+            for (int64_t j = jlo + tid; j < jhi; j += NT) one(Q(j), int(j));
           }
           lt = block_sum_d(lt, sh);
           eq = block_sum_d(eq, sh);
+          row_sum_d2(lt, eq);
+          if (col) merge_lists();
           if (target <= lt && bp > 0) {
             --bp;
           } else if (target > lt + eq && bp < min(bk, NB - 1) && eq >= 0.0 && lt + eq < target) {
@@ -444,7 +569,7 @@ __global__ void __launch_bounds__(NT) sampler_kernel(const float* __restrict__ l
         __syncthreads();
         stamp(4);
         if (bp != bk) {
-          if (listed) {  // members already collected: sort them
+          if (listed) {  // members already collected (and merged): sort them
             const int n = sh.list_n;
             if (n > LIST) {
               if (tid == 0) sh.overflow = 1;
@@ -457,7 +582,7 @@ __global__ void __launch_bounds__(NT) sampler_kernel(const float* __restrict__ l
           }
         }
         stamp(5);
-        if (s.dbg && b == 0 && threadIdx.x == 0) s.dbg[8] = sh.list_n;
+        if (s.dbg && b == 0 && r == 0 && threadIdx.x == 0) s.dbg[8] = sh.list_n;
         if (!sh.overflow) {
           // first sorted member r with s_above + sum_{<=r} q >= target, as a block scan
           const int limit = bp == bk ? k_take : min(sh.list_n, LIST);
@@ -469,8 +594,8 @@ __global__ void __launch_bounds__(NT) sampler_kernel(const float* __restrict__ l
           if (tid < limit && sh.s_above + ex + qv >= target) atomicMin(&sh.result, tid);
           __syncthreads();
           if (tid == 0) {
-            const int r = sh.result != 0x7fffffff ? sh.result : limit - 1;
-            const unsigned long long e = sh.list[r];
+            const int rr = sh.result != 0x7fffffff ? sh.result : limit - 1;
+            const unsigned long long e = sh.list[rr];
             sh.t_final = ~unsigned(e >> 32);
             sh.idx_cut = int(e & 0xffffffffu);
           }
@@ -482,73 +607,89 @@ __global__ void __launch_bounds__(NT) sampler_kernel(const float* __restrict__ l
       if (sh.overflow) {
         // exact but slow path (a crossing bucket with > LIST members, i.e.
         // massive ties): binary search on the threshold bits with block
-        // reductions, ties resolved by index.
-        unsigned tk = botb;
-        int cutk = int(V);
-        if (filt_k) {
-          unsigned lo = botb, hi = top;
-          while (lo < hi) {
-            const unsigned mid = lo + (hi - lo + 1) / 2;
-            double c = 0;
-            for (int64_t j = tid; j < V; j += NT) c += qbits_of(Q(j)) >= mid;
-            c = block_sum_d(c, sh);
-            if (c >= double(prm.top_k)) lo = mid; else hi = mid - 1;
+        // reductions, ties resolved by index.  With a CTA pair, rank 0 runs it
+        // over the whole row (the partner's part through DSMEM) and shares the
+        // threshold.
+        unsigned tk = botb, tp = botb;
+        int cutk = int(V), cutp = int(V);
+        if (r == 0) {
+          if (filt_k) {
+            unsigned lo = botb, hi = top;
+            while (lo < hi) {
+              const unsigned mid = lo + (hi - lo + 1) / 2;
+              double c = 0;
+              for (int64_t j = tid; j < V; j += NT) c += qbits_of(Qall(j)) >= mid;
+              c = block_sum_d(c, sh);
+              if (c >= double(prm.top_k)) lo = mid; else hi = mid - 1;
+            }
+            tk = lo;
+            double above = 0;
+            for (int64_t j = tid; j < V; j += NT) above += qbits_of(Qall(j)) > tk;
+            above = block_sum_d(above, sh);
+            const int need = int(prm.top_k - int64_t(above));
+            if (tid == 0) {
+              int cnt = 0;
+              for (int64_t j = 0; j < V; ++j)
+                if (qbits_of(Qall(j)) == tk && ++cnt == need) {
+                  sh.idx_cut = int(j);
+                  break;
+                }
+            }
+            __syncthreads();
+            cutk = sh.idx_cut;
           }
-          tk = lo;
-          double above = 0;
-          for (int64_t j = tid; j < V; j += NT) above += qbits_of(Q(j)) > tk;
-          above = block_sum_d(above, sh);
-          const int need = int(prm.top_k - int64_t(above));
-          if (tid == 0) {
-            int cnt = 0;
-            for (int64_t j = 0; j < V; ++j)
-              if (qbits_of(Q(j)) == tk && ++cnt == need) {
-                sh.idx_cut = int(j);
-                break;
-              }
-          }
-          __syncthreads();
-          cutk = sh.idx_cut;
-        }
-        auto keptk = [&](int64_t j) {
-          const unsigned qb = qbits_of(Q(j));
-          return !filt_k || qb > tk || (qb == tk && j <= cutk);
-        };
-        double zk = 0;
-        for (int64_t j = tid; j < V; j += NT)
-          if (keptk(j)) zk += double(Q(j));
-        zk = block_sum_d(zk, sh);
-        unsigned tp = tk;
-        int cutp = cutk;
-        if (filt_p) {
-          const double target = prm.top_p * zk;
-          unsigned lo = tk, hi = top;
-          while (lo < hi) {
-            const unsigned mid = lo + (hi - lo + 1) / 2;
-            double sacc = 0;
-            for (int64_t j = tid; j < V; j += NT)
-              if (keptk(j) && qbits_of(Q(j)) >= mid) sacc += double(Q(j));
-            sacc = block_sum_d(sacc, sh);
-            if (sacc >= target) lo = mid; else hi = mid - 1;
-          }
-          tp = lo;
-          double above = 0;
+          auto keptk = [&](int64_t j) {
+            const unsigned qb = qbits_of(Qall(j));
+            return !filt_k || qb > tk || (qb == tk && j <= cutk);
+          };
+          double zk = 0;
           for (int64_t j = tid; j < V; j += NT)
-            if (keptk(j) && qbits_of(Q(j)) > tp) above += double(Q(j));
-          above = block_sum_d(above, sh);
-          if (tid == 0) {
-            double acc = above;
-            int cut = -1;
-            for (int64_t j = 0; j < V; ++j)
-              if (keptk(j) && qbits_of(Q(j)) == tp) {
-                acc += double(Q(j));
-                cut = int(j);
-                if (acc >= target) break;
-              }
-            sh.idx_cut = cut;
+            if (keptk(j)) zk += double(Qall(j));
+          zk = block_sum_d(zk, sh);
+          tp = tk;
+          cutp = cutk;
+          if (filt_p) {
+            const double target = prm.top_p * zk;
+            unsigned lo = tk, hi = top;
+            while (lo < hi) {
+              const unsigned mid = lo + (hi - lo + 1) / 2;
+              double sacc = 0;
+              for (int64_t j = tid; j < V; j += NT)
+                if (keptk(j) && qbits_of(Qall(j)) >= mid) sacc += double(Qall(j));
+              sacc = block_sum_d(sacc, sh);
+              if (sacc >= target) lo = mid; else hi = mid - 1;
+            }
+            tp = lo;
+            double above = 0;
+            for (int64_t j = tid; j < V; j += NT)
+              if (keptk(j) && qbits_of(Qall(j)) > tp) above += double(Qall(j));
+            above = block_sum_d(above, sh);
+            if (tid == 0) {
+              double acc = above;
+              int cut = -1;
+              for (int64_t j = 0; j < V; ++j)
+                if (keptk(j) && qbits_of(Qall(j)) == tp) {
+                  acc += double(Qall(j));
+                  cut = int(j);
+                  if (acc >= target) break;
+                }
+              sh.idx_cut = cut;
+            }
+            __syncthreads();
+            cutp = sh.idx_cut;
           }
-          __syncthreads();
-          cutp = sh.idx_cut;
+        }
+        if constexpr (CL > 1) {  // share rank 0's threshold
+          if (tid == 0) {
+            sh.xu[xs][0] = tp;
+            sh.xi[xs][2] = cutp;
+          }
+          cl_sync();
+          if (r == 1) {
+            tp = peer_ptr(&sh.xu[xs][0], 0u)[0];
+            cutp = peer_ptr(&sh.xi[xs][0], 0u)[2];
+          }
+          xs ^= 1;
         }
         k_t = tp;
         k_cut = cutp;
@@ -559,16 +700,18 @@ __global__ void __launch_bounds__(NT) sampler_kernel(const float* __restrict__ l
     }
     stamp(6);
     // ---- inverse CDF in index order over the kept tokens: every thread owns a
-    // contiguous chunk (sequential fp64 sums), one block scan, and the thread
-    // whose chunk brackets u*Z walks it (src/model.cpp:464-473 semantics)
+    // contiguous chunk of this CTA's range (sequential fp64 sums), one block
+    // scan, rank 0's total ahead of rank 1's, and the thread whose chunk
+    // brackets u*Z walks it (src/model.cpp:464-473 semantics)
     auto kept = [&](int64_t j, float& q) -> bool {
       q = Q(j);
       if (!filtering) return true;
       const unsigned qb = qbits_of(q);
       return qb > t_final || (qb == t_final && j <= idx_cut);
     };
-    const int64_t CH = (V + NT - 1) / NT;
-    const int64_t c0 = int64_t(tid) * CH, c1 = (V < c0 + CH ? V : c0 + CH);
+    const int64_t nloc = jhi - jlo;
+    const int64_t CH = (nloc + NT - 1) / NT;
+    const int64_t c0 = jlo + int64_t(tid) * CH, c1 = (jhi < c0 + CH ? jhi : c0 + CH);
     double csum = 0.0;
     int last = -1;
     for (int64_t j = c0; j < c1; ++j) {
@@ -579,7 +722,7 @@ __global__ void __launch_bounds__(NT) sampler_kernel(const float* __restrict__ l
       }
     }
     double total;
-    const double prefix = block_excl_scan<double>(csum, sh.dwarp, total);
+    double prefix = block_excl_scan<double>(csum, sh.dwarp, total);
     int lk = last;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) lk = max(lk, __shfl_xor_sync(0xffffffffu, lk, o));
@@ -588,6 +731,18 @@ __global__ void __launch_bounds__(NT) sampler_kernel(const float* __restrict__ l
     __syncthreads();
     int fallback = -1;
     for (int k = 0; k < NW; ++k) fallback = max(fallback, sh.lk[k]);
+    if constexpr (CL > 1) {
+      if (tid == 0) {
+        sh.xd[xs][2] = total;
+        sh.xi[xs][3] = fallback;
+      }
+      cl_sync();
+      const double ot = peer_ptr(&sh.xd[xs][0], pr)[2];
+      fallback = max(fallback, peer_ptr(&sh.xi[xs][0], pr)[3]);
+      if (r == 1) prefix += ot;
+      total = r == 0 ? total + ot : ot + total;
+      xs ^= 1;
+    }
     const double u = s.uniforms[b * s.ustride + i];
     const double target = u * total;
     if (csum > 0.0 && prefix <= target && target < prefix + csum * (1.0 + 1e-12)) {
@@ -604,10 +759,17 @@ __global__ void __launch_bounds__(NT) sampler_kernel(const float* __restrict__ l
       }
     }
     __syncthreads();
-    chosen = sh.result != 0x7fffffff ? sh.result : (fallback >= 0 ? fallback : int(V - 1));
+    int res = sh.result;
+    if constexpr (CL > 1) {
+      if (tid == 0) sh.xi[xs][0] = res;
+      cl_sync();
+      res = min(res, peer_ptr(&sh.xi[xs][0], pr)[0]);
+      xs ^= 1;
+    }
+    chosen = res != 0x7fffffff ? res : (fallback >= 0 ? fallback : int(V - 1));
     stamp(7);
   }
-  if (tid == 0) {
+  if (r == 0 && tid == 0) {
     if (i > 0) s.pos[b] += 1;
     s.out_tokens[b * s.ostride + i] = chosen;
     s.out_lps[b * s.ostride + i] = row[chosen] - lse;
@@ -618,24 +780,64 @@ __global__ void __launch_bounds__(NT) sampler_kernel(const float* __restrict__ l
       atomicSub(s.n_active, 1);
     }
   }
+  if constexpr (CL > 1) cl_sync();  // the partner may still read this CTA's shared memory
 }
 }  // namespace
 
 void launch_sampler(Ctx& c, const float* logits, int64_t ld, int64_t B, int64_t V, const SamplerState& s) {
   if (B <= 0) return;
-  if (V <= kCacheMaxV) {
+  // a CTA pair per row while the pairs fit one wave (rows <= #SMs / 2); each
+  // CTA caches half the row
+  static const int cl_env = [] {
+    const char* e = getenv("PPOEXP_SAMPLER_CL");
+    return e ? atoi(e) : 2;
+  }();
+  int sms = 0;
+  {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const bool pair = cl_env == 2 && 2 * B <= sms && (V + 7) / 8 * 4 <= kCacheMaxV && V >= 64 && (ld % 4) == 0;
+  if (pair) {
+    const int64_t half = (V + 7) / 8 * 4;
+    const size_t smem = size_t(half) * sizeof(float);
+    static bool attr = false;
+    if (!attr) {
+      PPOEXP_CUDA(cudaFuncSetAttribute(sampler_kernel<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       int(kCacheMaxV * sizeof(float))));
+      attr = true;
+    }
+    c.launch("sampler", double(B) * V * 4, 0, [&] {
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(unsigned(2 * B));
+      cfg.blockDim = dim3(NT);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = c.stream;
+      cudaLaunchAttribute at[2];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = 2;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[1].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 2;
+      PPOEXP_CUDA(cudaLaunchKernelEx(&cfg, sampler_kernel<true, 2>, logits, ld, V, s));
+    });
+  } else if (V <= kCacheMaxV) {
     const size_t smem = size_t(V) * sizeof(float);
     static bool attr = false;
     if (!attr) {
-      PPOEXP_CUDA(cudaFuncSetAttribute(sampler_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      PPOEXP_CUDA(cudaFuncSetAttribute(sampler_kernel<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        int(kCacheMaxV * sizeof(float))));
       attr = true;
     }
     c.launch("sampler", double(B) * V * 4, 0,
-             [&] { launch_kernel(c, sampler_kernel<true>, dim3(B), dim3(NT), smem, 1, logits, ld, V, s); });
+             [&] { launch_kernel(c, sampler_kernel<true, 1>, dim3(B), dim3(NT), smem, 1, logits, ld, V, s); });
   } else {
     c.launch("sampler", double(B) * V * 4, 0,
-             [&] { launch_kernel(c, sampler_kernel<false>, dim3(B), dim3(NT), 0, 1, logits, ld, V, s); });
+             [&] { launch_kernel(c, sampler_kernel<false, 1>, dim3(B), dim3(NT), 0, 1, logits, ld, V, s); });
   }
 }
 
