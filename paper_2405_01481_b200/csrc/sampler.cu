@@ -214,22 +214,21 @@ __global__ void __launch_bounds__(NT) sampler_kernel(const float* __restrict__ l
     const int64_t nv = (jhi - jlo) / 4;
     const float4* r4 = reinterpret_cast<const float4*>(row + jlo);
     float4* c4 = reinterpret_cast<float4*>(qcache);
-    int64_t k = tid;
-    for (; k + NT < nv; k += 2 * NT) {
-      const float4 a = r4[k], c = r4[k + NT];
-      if constexpr (CACHED) {
-        c4[k] = a;
-        c4[k + NT] = c;
+    // up to 8 float4 per thread in flight before the first compare
+    for (int64_t k0 = tid; k0 < nv; k0 += 8 * NT) {
+      float4 a[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (k0 + u * NT < nv) a[u] = r4[k0 + u * NT];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int64_t k = k0 + u * NT;
+        if (k < nv) {
+          if constexpr (CACHED) c4[k] = a[u];
+          const int j0 = int(jlo + 4 * k);
+          visit(a[u].x, j0); visit(a[u].y, j0 + 1); visit(a[u].z, j0 + 2); visit(a[u].w, j0 + 3);
+        }
       }
-      const int j0 = int(jlo + 4 * k), j1 = int(jlo + 4 * (k + NT));
-      visit(a.x, j0); visit(a.y, j0 + 1); visit(a.z, j0 + 2); visit(a.w, j0 + 3);
-      visit(c.x, j1); visit(c.y, j1 + 1); visit(c.z, j1 + 2); visit(c.w, j1 + 3);
-    }
-    for (; k < nv; k += NT) {
-      const float4 a = r4[k];
-      if constexpr (CACHED) c4[k] = a;
-      const int j0 = int(jlo + 4 * k);
-      visit(a.x, j0); visit(a.y, j0 + 1); visit(a.z, j0 + 2); visit(a.w, j0 + 3);
     }
     for (int64_t j = jlo + nv * 4 + tid; j < jhi; j += NT) {
       const float v = row[j];
