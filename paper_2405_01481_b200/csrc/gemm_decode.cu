@@ -580,8 +580,12 @@ int launch_dec(Ctx& c, const bf16* X, int64_t ldx, const bf16* W, int64_t ldw, i
   }();
   // K-split launches hold their whole slice (one wave, the ring is filled
   // before the PDL wait); multi-wave launches (tiles > #SMs, e.g. the LM
-  // head) keep a 4-deep ring so two CTAs share an SM
-  const int ring = tiles * S > 148 ? std::min(wring, 4) : wring;
+  // head) keep a 2-deep ring so three CTAs share an SM
+  static const int wring_wide = [] {
+    const char* e = getenv("PPOEXP_DECODE_WRING_WIDE");  // 2: three CTAs per SM (the LM head fits one wave)
+    return e ? atoi(e) : 2;
+  }();
+  const int ring = tiles * S > 148 ? std::min(wring, wring_wide) : wring;
   const int wst = int(std::min<int64_t>(std::min<int64_t>(L::kWcap, ring), ceil_div(nk, S)));
   static const int push_env = [] {
     // 2 = direct register -> remote-smem stores (default), 1 = park + bulk copy, 0 = pull
