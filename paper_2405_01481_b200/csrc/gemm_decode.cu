@@ -568,7 +568,7 @@ int launch_dec(Ctx& c, const bf16* X, int64_t ldx, const bf16* W, int64_t ldw, i
   }();
   static const int smax_small = [] {  // narrow outputs (N <= 1024: O / down projections)
     const char* e = getenv("PPOEXP_DECODE_SPLIT_SMALLN");
-    return std::min(e ? atoi(e) : 16, kMaxS);
+    return std::min(e ? atoi(e) : 8, kMaxS);  // 8: measured best with the direct push exchange
   }();
   const int cap = tiles <= 8 ? smax_small : smax;
   int S = 1;
