@@ -108,18 +108,26 @@ __device__ __forceinline__ void cp_async16_dec(void* dst, const void* src) {
                : "memory");
 }
 
-template <class T, int DH, int NS>  // NS: K/V tile stages per warp (1 = 6 CTAs/SM for dh 64 bf16)
+// NS: K/V tile stages per warp, TT: tokens per tile.  (NS, TT) = (2, 16) keeps the
+// (1, 32) footprint (32 KB per CTA for dh 64 bf16: 6 CTAs/SM) but double-buffers.
+template <class T, int DH, int NS, int TT>
 __global__ void __launch_bounds__(128, 6) attn_decode_kernel(const T* __restrict__ qkv, const int32_t* __restrict__ pos,
                                                           const int32_t* __restrict__ done,
                                                           const int32_t* __restrict__ block_table, int layer,
-                                                          KvGeom g, T* __restrict__ kv, T* __restrict__ out) {
+                                                          KvGeom g, T* __restrict__ kv, T* __restrict__ out,
+                                                          unsigned long long* dbg) {
+  // debug (PPOEXP_ATTN_TRACE): CTA (0, 0) thread 0 stage clocks
+  auto stamp = [&](int k) {
+    if (dbg && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) dbg[k] = clock64();
+  };
+  stamp(0);
   // Programmatic dependent launch: only this step's q/k/v (the immediately
   // preceding QKV GEMM) is produced by the predecessor grid.  Every earlier
   // kernel has completed when this grid starts (each kernel triggers its
   // dependents only after its own griddepcontrol.wait), so the sequence
   // state, the block table and the cached K/V rows < pos are read BEFORE the
   // wait: the first tile's HBM latency overlaps the QKV GEMM's tail.
-  constexpr int NW = 4, TT = 32;
+  constexpr int NW = 4;
   constexpr int ROWB = DH * int(sizeof(T));   // bytes per K/V row
   // 128-byte rows (bf16, dh 64) are stored unpadded with the 16-byte chunks
   // XOR-swizzled by (row & 7): conflict-free for lane-per-token K reads and
@@ -170,12 +178,18 @@ __global__ void __launch_bounds__(128, 6) attn_decode_kernel(const T* __restrict
   for (int i = 0; i < DPL; ++i) acc[i] = 0.f;
   const int dl = lane < DLANES ? lane : 0;
   int64_t t0 = int64_t(w) * TT;
-  int buf = 0;
-  // this warp's first tile, unless it holds the new position (appended below)
-  const bool early = t0 < ctx && !(p >= t0 && p < t0 + TT);
-  if (early) issue(t0, 0);
+  auto holds_p = [&](int64_t t) { return p >= t && p < t + TT; };
+  // this warp's first tile (and second, when double-buffered), unless it
+  // holds the new position (appended below)
+  const bool early0 = t0 < ctx && !holds_p(t0);
+  const int64_t t1 = t0 + int64_t(NW) * TT;
+  const bool early1 = NS == 2 && t1 < ctx && !holds_p(t1);
+  if (early0) issue(t0, 0);
+  if (early1) issue(t1, 1);
+  stamp(1);
   pdl_wait();  // this step's q/k/v are valid from here on
   pdl_trigger();
+  stamp(2);
   // append this step's K/V row (KvSession::step, src/model.cpp:305-308)
   for (int i = tid; i < DH; i += 128) {
     base(p, 0)[i] = row[d + h * DH + i];
@@ -183,12 +197,26 @@ __global__ void __launch_bounds__(128, 6) attn_decode_kernel(const T* __restrict
   }
   for (int i = tid; i < DH; i += 128) sm_q[i] = to_f(row[h * DH + i]);
   __syncthreads();  // the appended row and the query are visible to the whole CTA
-  if (t0 < ctx && !early) issue(t0, 0);
-  for (; t0 < ctx; t0 += int64_t(NW) * TT) {
+  stamp(3);
+  bool nxt_issued = early1;          // tile it+1 already committed
+  bool zero_last = false;            // tile 0 committed after tile 1: wait for everything
+  if (t0 < ctx && !early0) {
+    issue(t0, 0);
+    zero_last = early1;
+  }
+  int it = 0;
+  for (; t0 < ctx; t0 += int64_t(NW) * TT, ++it) {
     const int64_t tn = t0 + int64_t(NW) * TT;
-    if (NS == 2 && tn < ctx) {
-      issue(tn, buf ^ 1);
-      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    const int buf = NS == 2 ? (it & 1) : 0;
+    if (NS == 2) {
+      if (!nxt_issued && tn < ctx) {
+        issue(tn, buf ^ 1);
+        nxt_issued = true;
+      }
+      if (nxt_issued && !zero_last && tn < ctx)
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+      else
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
     } else {
       asm volatile("cp.async.wait_group 0;" ::: "memory");
     }
@@ -231,12 +259,11 @@ __global__ void __launch_bounds__(128, 6) attn_decode_kernel(const T* __restrict
       for (int i = 0; i < DPL; ++i) acc[i] = fmaf(pj, to_f(vr[i]), acc[i]);
     }
     __syncwarp();  // this buffer is refilled next (NS == 1) or two tiles from now
-    if (NS == 1) {
-      if (tn < ctx) issue(tn, 0);
-    } else {
-      buf ^= 1;
-    }
+    if (NS == 1 && tn < ctx) issue(tn, 0);
+    nxt_issued = false;
+    zero_last = false;
   }
+  stamp(4);
   // ---- merge the warps
   if (lane == 0) {
     sm_m[w] = m;
@@ -262,6 +289,8 @@ __global__ void __launch_bounds__(128, 6) attn_decode_kernel(const T* __restrict
     for (int k = 0; k < NW; ++k) o += sm_acc[k][i] * sc[k];
     out[b * d + h * DH + i] = from_f<T>(o * inv);
   }
+  stamp(5);
+  if (dbg && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) dbg[6] = ctx;
 }
 
 template <class T, int DH>
@@ -275,12 +304,12 @@ void prefill_impl(Ctx& c, const T* qkv, const int64_t* seq_offsets, int64_t B, i
   c.launch("attention_prefill", 0, flops, [&] { launch_kernel(c, k, dim3(grid), dim3(64 * TPQ), smem, 1, qkv, seq_offsets, H, out); });
 }
 
-template <class T, int DH, int NS>
+template <class T, int DH, int NS, int TT>
 void decode_launch(Ctx& c, const T* qkv, int64_t B, const int32_t* pos, const int32_t* done,
                    const int32_t* block_table, int layer, const KvGeom& g, T* kv, T* out, double bytes) {
-  auto k = attn_decode_kernel<T, DH, NS>;
+  auto k = attn_decode_kernel<T, DH, NS, TT>;
   const size_t row = DH * sizeof(T) == 128 ? 128 : DH * sizeof(T) + 16;  // kernel's LDB
-  const size_t smem = size_t(4) * NS * 2 * 32 * row;                     // 4 warps x NS x (K, V) x 32 rows
+  const size_t smem = size_t(4) * NS * 2 * TT * row;                     // 4 warps x NS x (K, V) x TT rows
   static bool attr = false;
   if (!attr) {
     PPOEXP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
@@ -288,12 +317,16 @@ void decode_launch(Ctx& c, const T* qkv, int64_t B, const int32_t* pos, const in
     if (getenv("PPOEXP_DEBUG_ATTN")) {
       int per_sm = 0;
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 128, smem);
-      fprintf(stderr, "attn_decode<%d,%d,%d>: dynamic smem %zu, %d CTAs/SM\n", int(sizeof(T)), DH, NS, smem, per_sm);
+      fprintf(stderr, "attn_decode<%d,%d,%d,%d>: dynamic smem %zu, %d CTAs/SM\n", int(sizeof(T)), DH, NS, TT, smem,
+              per_sm);
     }
   }
   dim3 grid(g.H, B);
+  unsigned long long* dbg = nullptr;
+  if (getenv("PPOEXP_ATTN_TRACE"))  // debug: stamps of the last launch
+    dbg = static_cast<unsigned long long*>(c.workspace("attn.trace", 16 * 8));
   c.launch("decode_attention", bytes, 0, [&] { launch_kernel(c, k, grid, dim3(128), smem, 1, qkv, pos, done,
-                                                              block_table, layer, g, kv, out); });
+                                                              block_table, layer, g, kv, out, dbg); });
 }
 
 template <class T, int DH>
@@ -302,14 +335,18 @@ void decode_impl(Ctx& c, const T* qkv, int64_t B, const int32_t* pos, const int3
   if (g.page_size % 32) throw ContractError("engine: page_size must be a multiple of 32");
   // single-stage tiles halve the CTA's shared memory (6 resident CTAs/SM for dh 64 bf16: one wave of
   // 768 (sequence, head) CTAs at C2); other warps on the SM hide each warp's tile latency
-  static const int stages = [] {
-    const char* e = getenv("PPOEXP_ATTN_STAGES");
-    return e ? atoi(e) : 1;
+  // 32-token tiles, single stage (default), or 16-token tiles double buffered:
+  // both 32 KB per CTA for dh 64 bf16 (6 CTAs/SM: one wave of 768 (sequence,
+  // head) CTAs at C2).  Measured: the tile loop streams KV at the HBM roofline
+  // (9.1 us for 61.5 MB at context 313), and 16-token tiles are ~3% slower.
+  static const int tile = [] {
+    const char* e = getenv("PPOEXP_ATTN_TILE");
+    return e ? atoi(e) : 32;
   }();
-  if (stages == 2)
-    decode_launch<T, DH, 2>(c, qkv, B, pos, done, block_table, layer, g, kv, out, bytes);
+  if (tile == 16 && DH * sizeof(T) == 128)
+    decode_launch<T, DH, 2, 16>(c, qkv, B, pos, done, block_table, layer, g, kv, out, bytes);
   else
-    decode_launch<T, DH, 1>(c, qkv, B, pos, done, block_table, layer, g, kv, out, bytes);
+    decode_launch<T, DH, 1, 32>(c, qkv, B, pos, done, block_table, layer, g, kv, out, bytes);
 }
 
 }  // namespace

@@ -398,6 +398,17 @@ void Engine::generate(int64_t B, const int32_t* prompts, const int64_t* offsets,
   last_ms = ms;
   if (ms_out) *ms_out = ms;
   if (const char* gp = getenv("PPOEXP_GEMM_TRACE")) dump_gemm_trace(*c, gp);
+  if (const char* ap = getenv("PPOEXP_ATTN_TRACE")) {  // debug: last decode-attention launch, CTA (0, 0)
+    unsigned long long hh[16];
+    PPOEXP_CUDA(cudaMemcpy(hh, c->workspace("attn.trace", 16 * 8), sizeof(hh), cudaMemcpyDeviceToHost));
+    if (FILE* fp = fopen(ap, "w")) {
+      const char* nm[6] = {"entry", "state+early tile", "pdl wait", "append+q", "tile loop", "merge+store"};
+      for (int k = 1; k < 6; ++k)
+        fprintf(fp, "%-18s %8.2f us\n", nm[k], hh[k] > hh[k - 1] ? (hh[k] - hh[k - 1]) / 1965.0 : 0.0);
+      fprintf(fp, "context %llu\n", hh[6]);
+      fclose(fp);
+    }
+  }
   if (const char* sp = getenv("PPOEXP_SAMPLER_TRACE")) {  // debug: last sampler launch, row 0
     unsigned long long h[16];
     PPOEXP_CUDA(cudaMemcpy(h, c->workspace("sampler.trace", 16 * 8), sizeof(h), cudaMemcpyDeviceToHost));
