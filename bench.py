@@ -143,6 +143,17 @@ def reference_sample(cfg_t, threads, n_new, steps=1, seed=SEED):
     return float(np.median(rates)), secs
 
 
+def workload_config(args, world, B=None):
+    """The `config` object of the JSON line (identical for both arms)."""
+    V, d, L, H, f, S, Bc, P, N, samp, desc = CONFIGS[args.config]
+    B = B if B is not None else (args.batch or Bc)
+    return {"workload": args.config, "description": desc, "vocab": V, "d_model": d, "n_layers": L,
+            "n_heads": H, "d_ff": f, "max_seq_len": S, "prompts_per_rank": B, "global_batch": B * world,
+            "prompt_len": P, "max_new": N, "sampling": samp if samp == "greedy" else f"top_p={TOP_P}",
+            "models": "policy+reference+critic, scripted reward", "parallelism": f"dp{world}",
+            "l2": "flushed between timed steps (256 MiB write); weights+KV > L2"}
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -158,11 +169,12 @@ def run_reference(args):
     sample = (f"{threads} sequences (one per host thread) x {P}-token prompt x {n_new} sampled tokens through the "
               f"reference's Engine::generate_batch (n_workers={threads}, fp64) per step; prompts fed token-by-token "
               f"as the reference does")
-    line = {"impl": "reference", "metric": "rollout_tokens_per_s", "value": val, "unit": "tokens/s", "n_gpus": 0,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * float(np.mean(secs)),
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    line = {"impl": "reference", "metric": "rollout_tokens_per_s", "value": val, "unit": "tokens/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * float(np.mean(secs)),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": args.config, "description": desc, "vocab": V, "d_model": d, "n_layers": L,
-                       "n_heads": H, "d_ff": f, "prompt_len": P, "max_new": N, "prompts_per_rank": B},
+            "config": workload_config(args, world),
+            "note": "the reference's own CPU path on this box's host cores (no GPU used)",
             "cpu_baseline": {"value": val, "unit": "tokens/s", "cores": threads, "kind": "reference",
                              "sample": sample},
             "e2e": {"value": val, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -328,11 +340,7 @@ def run_ours(args):
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_step_s * 1000 / args.steps,
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
                 "data": "synthetic prompts, random-init weights",
-                "config": {"workload": args.config, "description": desc, "vocab": V, "d_model": d, "n_layers": L,
-                           "n_heads": H, "d_ff": f, "max_seq_len": S, "prompts_per_rank": B, "global_batch": B * world,
-                           "prompt_len": P, "max_new": N, "sampling": samp if samp == "greedy" else f"top_p={TOP_P}",
-                           "models": "policy+reference+critic, scripted reward", "parallelism": f"dp{world}",
-                           "l2": "flushed between timed steps (256 MiB write); weights+KV > L2"},
+                "config": workload_config(args, world, B),
                 "experience_samples_per_s": samples_per_s,
                 "gen_ms_per_step": total_gen_s * 1000 / args.steps,
                 "gpu_launches": max_launches,
