@@ -2,6 +2,8 @@
 // scatter, weight conversion and small helpers; plus the Ctx runtime.
 #include <cstring>
 
+#include <type_traits>
+
 #include "kernels.hpp"
 
 namespace ppx {
@@ -219,6 +221,80 @@ __global__ void __launch_bounds__(256) layernorm_kernel(const float* __restrict_
 // Warp-per-row variant for d <= 1024 (8 rows per 256-thread CTA): the
 // decode step's LayerNorms are 64-row launches where a CTA per row wastes
 // three block barriers per row.
+// Warp per row, float4 (d % 4 == 0, d <= 1024: up to 8 float4 per lane, all
+// loads issued before the reductions); 8-byte stores of 4 T values.
+template <class T>
+__global__ void __launch_bounds__(256) layernorm_warp4_kernel(const float* __restrict__ x, int64_t rows, int64_t d,
+                                                              const float* __restrict__ g, const float* __restrict__ b,
+                                                              T* __restrict__ y, const int32_t* __restrict__ gather,
+                                                              const float* __restrict__ head,
+                                                              float* __restrict__ head_out) {
+  // gamma / beta / head are shared by the CTA's 8 rows: staged in shared memory
+  // while the row loads are in flight (they would otherwise be a dependent
+  // L2 round trip after the reductions)
+  __shared__ float4 sg[256], sb[256], sh4[256];
+  const int d4 = int(d >> 2);
+  for (int k = threadIdx.x; k < d4; k += 256) {  // parameters: not produced upstream
+    sg[k] = reinterpret_cast<const float4*>(g)[k];
+    sb[k] = reinterpret_cast<const float4*>(b)[k];
+    if (head) sh4[k] = reinterpret_cast<const float4*>(head)[k];
+  }
+  PDL_ENTRY();
+  const int lane = threadIdx.x & 31;
+  const int64_t r = int64_t(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  const bool live = r < rows;
+  const int64_t src = live ? (gather ? gather[r] : r) : 0;
+  const float4* xr = reinterpret_cast<const float4*>(x + src * d);
+  float4 v[8];
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int j4 = lane + i * 32;
+    v[i] = (live && j4 < d4) ? xr[j4] : make_float4(0.f, 0.f, 0.f, 0.f);
+    s += (v[i].x + v[i].y) + (v[i].z + v[i].w);
+  }
+  __syncthreads();  // staged parameters visible
+  if (!live) return;
+  const float mu = warp_sum(s) / float(d);
+  float q = 0.f;
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+    if (lane + i * 32 < d4) {
+      const float c0 = v[i].x - mu, c1 = v[i].y - mu, c2 = v[i].z - mu, c3 = v[i].w - mu;
+      q += (c0 * c0 + c1 * c1) + (c2 * c2 + c3 * c3);
+    }
+  const float is = 1.0f / sqrtf(warp_sum(q) / float(d) + 1e-5f);
+  float hd = 0.f;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int j4 = lane + i * 32;
+    if (j4 < d4) {
+      const float4 gg = sg[j4], bb = sb[j4];
+      const float o0 = gg.x * ((v[i].x - mu) * is) + bb.x, o1 = gg.y * ((v[i].y - mu) * is) + bb.y;
+      const float o2 = gg.z * ((v[i].z - mu) * is) + bb.z, o3 = gg.w * ((v[i].w - mu) * is) + bb.w;
+      if (y) {
+        if constexpr (std::is_same_v<T, bf16>) {
+          __nv_bfloat162 lo = __floats2bfloat162_rn(o0, o1), hi = __floats2bfloat162_rn(o2, o3);
+          uint2 u;
+          u.x = *reinterpret_cast<uint32_t*>(&lo);
+          u.y = *reinterpret_cast<uint32_t*>(&hi);
+          *reinterpret_cast<uint2*>(y + r * d + 4 * j4) = u;
+        } else {
+          *reinterpret_cast<float4*>(y + r * d + 4 * j4) = make_float4(o0, o1, o2, o3);
+        }
+      }
+      if (head) {
+        const float4 hh = sh4[j4];
+        hd += (o0 * hh.x + o1 * hh.y) + (o2 * hh.z + o3 * hh.w);
+      }
+    }
+  }
+  if (head) {
+    hd = warp_sum(hd);
+    if (lane == 0) head_out[r] = hd;
+  }
+}
+
 template <class T>
 __global__ void __launch_bounds__(256) layernorm_warp_kernel(const float* __restrict__ x, int64_t rows, int64_t d,
                                                              const float* __restrict__ g, const float* __restrict__ b,
@@ -334,10 +410,17 @@ void launch_layernorm(Ctx& c, const float* x, int64_t rows, int64_t d, const flo
     if (d % 4 == 0 && d <= 4096 && rows <= 1024) {
       const int th = int((d / 4 + 31) / 32 * 32);
       launch_kernel(c, layernorm_vec_kernel<T>, dim3(rows), dim3(th), 0, 1, x, d, g, b, y, gather, head, head_out);
-    } else if (d <= 1024)
-      launch_kernel(c, layernorm_warp_kernel<T>, dim3(ceil_div(rows, 8)), dim3(256), 0, 1, x, rows, d, g, b, y, gather, head, head_out);
-    else
+    } else if (d <= 1024) {
+      if (d % 4 == 0) {
+        launch_kernel(c, layernorm_warp4_kernel<T>, dim3(ceil_div(rows, 8)), dim3(256), 0, 1, x, rows, d, g, b, y,
+                      gather, head, head_out);
+      } else {
+        launch_kernel(c, layernorm_warp_kernel<T>, dim3(ceil_div(rows, 8)), dim3(256), 0, 1, x, rows, d, g, b, y,
+                      gather, head, head_out);
+      }
+    } else {
       launch_kernel(c, layernorm_kernel<T>, dim3(rows), dim3(256), 0, 1, x, rows, d, g, b, y, gather, head, head_out);
+    }
   });
 }
 
