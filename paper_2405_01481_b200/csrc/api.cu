@@ -633,13 +633,52 @@ ppoexp_status ppoexp_make_experience(const ppoexp_experience_request* req, int64
     PPOEXP_CUDA(cudaMemsetAsync(alp, 0, nBN * 8, c.stream));
     PPOEXP_CUDA(cudaMemsetAsync(rlp, 0, nBN * 8, c.stream));
     PPOEXP_CUDA(cudaMemsetAsync(val, 0, nBN * 8, c.stream));
+    // The policy, reference and critic forwards read the same packed tokens and
+    // write disjoint outputs: the reference and critic run on two auxiliary
+    // streams (own workspaces) concurrently with the policy on the main stream,
+    // so one forward's latency-bound kernels overlap another's GEMMs.
+    static const bool concurrent = [] {
+      const char* e = getenv("PPOEXP_SCORE_STREAMS");
+      return !(e && e[0] == '0');
+    }();
+    const bool conc = concurrent && !rm;
+    cudaStream_t main_stream = c.stream;
+    auto on_aux = [&](int i, const char* prefix, auto&& body) {
+      if (!conc) {
+        body();
+        return;
+      }
+      if (!c.aux[i]) PPOEXP_CUDA(cudaStreamCreateWithFlags(&c.aux[i], cudaStreamNonBlocking));
+      if (!c.join_ev[i]) PPOEXP_CUDA(cudaEventCreateWithFlags(&c.join_ev[i], cudaEventDisableTiming));
+      PPOEXP_CUDA(cudaStreamWaitEvent(c.aux[i], c.fork_ev, 0));
+      c.stream = c.aux[i];
+      c.ws_prefix = prefix;
+      try {
+        body();
+      } catch (...) {
+        c.stream = main_stream;
+        c.ws_prefix.clear();
+        throw;
+      }
+      PPOEXP_CUDA(cudaEventRecord(c.join_ev[i], c.aux[i]));
+      c.stream = main_stream;
+      c.ws_prefix.clear();
+    };
+    if (conc) {
+      if (!c.fork_ev) PPOEXP_CUDA(cudaEventCreateWithFlags(&c.fork_ev, cudaEventDisableTiming));
+      PPOEXP_CUDA(cudaEventRecord(c.fork_ev, main_stream));
+    }
+    on_aux(0, "ref/", [&] {
+      float* x = forward_layers(ref, pk, nullptr);
+      score_logprobs(ref, pk, x, gather, target, oidx, R, rlp);
+    });
+    on_aux(1, "crit/", [&] {
+      float* x = forward_layers(cr, pk, nullptr);
+      score_head(cr, x, gather, oidx, R, val);
+    });
     {
       float* x = forward_layers(pol, pk, nullptr);
       score_logprobs(pol, pk, x, gather, target, oidx, R, alp);
-    }
-    {
-      float* x = forward_layers(ref, pk, nullptr);
-      score_logprobs(ref, pk, x, gather, target, oidx, R, rlp);
     }
     // (4) rewards then values (CriticJob::handle_infer, src/ppo.cpp:164-193)
     double* rew = static_cast<double*>(c.workspace("xp.rew", B * 8));
@@ -654,9 +693,9 @@ ppoexp_status ppoexp_make_experience(const ppoexp_experience_request* req, int64
     } else {
       launch_scripted_reward(c, B, N, gtok, glen, req->scripted_target, rew);
     }
-    {
-      float* x = forward_layers(cr, pk, nullptr);
-      score_head(cr, x, gather, oidx, R, val);
+    if (conc) {  // join the reference and critic streams (the critic ran above in either mode)
+      PPOEXP_CUDA(cudaStreamWaitEvent(c.stream, c.join_ev[0], 0));
+      PPOEXP_CUDA(cudaStreamWaitEvent(c.stream, c.join_ev[1], 0));
     }
     // (5) KL shaping + GAE + per-sequence partials (src/ppo.cpp:382-393)
     double* shp = static_cast<double*>(c.workspace("xp.shp", nBN * 8));

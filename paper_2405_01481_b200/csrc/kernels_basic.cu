@@ -25,6 +25,14 @@ Ctx::~Ctx() {
     cudaEventDestroy(t.b);
   }
   for (auto e : event_pool) cudaEventDestroy(e);
+  for (int i = 0; i < 2; ++i) {
+    if (aux[i]) {
+      cudaStreamSynchronize(aux[i]);
+      cudaStreamDestroy(aux[i]);
+    }
+    if (join_ev[i]) cudaEventDestroy(join_ev[i]);
+  }
+  if (fork_ev) cudaEventDestroy(fork_ev);
   ws.clear();
   if (pinned) cudaFreeHost(pinned);
   cudaStreamDestroy(stream);

@@ -108,8 +108,14 @@ struct Ctx {
   void harvest();
   void harvest_list(const std::vector<TimedLaunch>& evs, bool release);
 
+  // name prefix of the workspaces used by the forward currently being issued
+  // (concurrent scoring forwards on separate streams keep separate buffers)
+  std::string ws_prefix;
+  cudaStream_t aux[2] = {nullptr, nullptr};  // concurrent scoring forwards (lazily created)
+  cudaEvent_t fork_ev = nullptr, join_ev[2] = {nullptr, nullptr};
+
   void* workspace(const std::string& name, size_t bytes) {
-    auto& b = ws[name];
+    auto& b = ws[ws_prefix + name];
     if (!b) b = std::make_unique<DeviceBuffer>();
     b->ensure(bytes);
     return b->ptr;
