@@ -573,7 +573,13 @@ int launch_dec(Ctx& c, const bf16* X, int64_t ldx, const bf16* W, int64_t ldw, i
   const int cap = tiles <= 8 ? smax_small : smax;
   int S = 1;
   while (S < cap && tiles * S < 148 && nk >= 2 * S) S *= 2;
-  while (S < kMaxS && ceil_div(nk, S) > L::kWcap) S *= 2;
+  // a slice larger than the weight ring cycles it (warp 0 lane 1 refills); only
+  // split further for that while the launch stays one wave (1 CTA/SM at batch > 64)
+  static const int onewave = [] {
+    const char* e = getenv("PPOEXP_DECODE_ONEWAVE");
+    return e ? atoi(e) : 1;
+  }();
+  while (S < kMaxS && ceil_div(nk, S) > L::kWcap && (!onewave || tiles * S * 2 <= 148)) S *= 2;
   static const int wring = [] {
     const char* e = getenv("PPOEXP_DECODE_WRING");
     return e ? atoi(e) : 8;

@@ -19,7 +19,7 @@ def glib():
     return px, f
 
 
-SHAPES = [(64, 2304, 768), (64, 768, 3072), (300, 1000, 768), (2048, 50257, 768), (4096, 3072, 768), (128, 256, 64),
+SHAPES = [(64, 2304, 768), (64, 768, 3072), (256, 2048, 8192), (256, 2048, 2048), (300, 1000, 768), (2048, 50257, 768), (4096, 3072, 768), (128, 256, 64),
           (17, 96, 16), (1024, 1024, 4096), (640, 768, 3072)]
 
 
