@@ -572,7 +572,11 @@ int launch_dec(Ctx& c, const bf16* X, int64_t ldx, const bf16* W, int64_t ldw, i
   }();
   const int cap = tiles <= 8 ? smax_small : smax;
   int S = 1;
-  while (S < cap && tiles * S < 148 && nk >= 2 * S) S *= 2;
+  static const int fit = [] {  // double only while the doubled grid still fits one wave
+    const char* e = getenv("PPOEXP_DECODE_SPLIT_FIT");
+    return e ? atoi(e) : 1;
+  }();
+  while (S < cap && (fit ? tiles * S * 2 <= 148 : tiles * S < 148) && nk >= 2 * S) S *= 2;
   // a slice larger than the weight ring cycles it (warp 0 lane 1 refills); only
   // split further for that while the launch stays one wave (1 CTA/SM at batch > 64)
   static const int onewave = [] {

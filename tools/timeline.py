@@ -24,10 +24,13 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--new", type=int, default=88)
 ap.add_argument("--mega", action="store_true")
 ap.add_argument("--steps", type=int, default=8, help="decode steps to aggregate (from the middle)")
+ap.add_argument("--config", default="c2")
+ap.add_argument("--batch", type=int, default=0)
 a = ap.parse_args()
 if a.mega:
     os.environ["PPOEXP_DECODE_MEGA"] = "1"
-V, d, L, H, f, S, B, P, N, samp, _ = bench.CONFIGS["c2"]
+V, d, L, H, f, S, B, P, N, samp, _ = bench.CONFIGS[a.config]
+B = a.batch or B
 cfg = px.ModelConfig(V, d, L, H, f, S)
 ctx = px.Context(0)
 dev = torch.device("cuda", 0)
