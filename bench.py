@@ -380,6 +380,9 @@ def run_ours(args):
                                           "events only on eagerly launched classes: see roofline_live)"}
         if live:
             line["roofline_live"] = {k: rf(v, k in ("gemm_tc",)) for k, v in live.items() if v["launches"]}
+            line["roofline_live_note"] = ("per-launch CUDA events in the timed region; the reference and critic "
+                                          "scoring forwards run on two extra streams concurrently with the policy "
+                                          "forward, so these durations include overlap with the other streams")
         if prof:
             line["kernel_classes"] = {k: {"ms": v["ms"], "launches": v["launches"],
                                           "GB_s": v["bytes"] / v["ms"] / 1e6 if v["ms"] else None,

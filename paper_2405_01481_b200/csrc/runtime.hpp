@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <functional>
+#include <algorithm>
 #include <array>
 #include <map>
 #include <memory>
@@ -40,13 +41,17 @@ struct DeviceBuffer {
   ~DeviceBuffer() {
     if (ptr) cudaFree(ptr);
   }
+  // First allocation is exact; a buffer that has to grow grows by >= 1.5x, so
+  // workspaces sized by data-dependent shapes (response lengths) settle after a
+  // few calls instead of reallocating (cudaFree synchronizes the device)
   void ensure(size_t n) {
     if (n <= bytes) return;
+    const size_t want = ptr ? std::max(n, bytes + bytes / 2) : n;
     if (ptr) PPOEXP_CUDA(cudaFree(ptr));
     ptr = nullptr;
     bytes = 0;
-    PPOEXP_CUDA(cudaMalloc(&ptr, n));
-    bytes = n;
+    PPOEXP_CUDA(cudaMalloc(&ptr, want));
+    bytes = want;
   }
   template <class T>
   T* as() const { return static_cast<T*>(ptr); }
