@@ -246,10 +246,15 @@ void Engine::decode_unit(int64_t B, int64_t unit) {
       return;
     }
   }
-  launch_embed<T>(cc, next_tok, pos, B, d, static_cast<const T*>(m->tok), static_cast<const T*>(m->pos), x);
+  const bool fused_head = m->cfg.n_layers > 0 &&
+                          launch_embed_layernorm<T>(cc, next_tok, pos, B, d, static_cast<const T*>(m->tok),
+                                                    static_cast<const T*>(m->pos), x, m->layers[0].ln1w,
+                                                    m->layers[0].ln1b, hh);
+  if (!fused_head)
+    launch_embed<T>(cc, next_tok, pos, B, d, static_cast<const T*>(m->tok), static_cast<const T*>(m->pos), x);
   for (int64_t l = 0; l < m->cfg.n_layers; ++l) {
     const Layer& ly = m->layers[l];
-    launch_layernorm<T>(cc, x, B, d, ly.ln1w, ly.ln1b, hh, nullptr, nullptr, nullptr);
+    if (l > 0 || !fused_head) launch_layernorm<T>(cc, x, B, d, ly.ln1w, ly.ln1b, hh, nullptr, nullptr, nullptr);
     gemm<T>(cc, hh, d, static_cast<const T*>(ly.wqkv), d, B, 3 * d, d, Epi::kStore, q3, 3 * d);
     launch_attention_decode<T>(cc, q3, B, pos, done, block_table, int(l), geom, static_cast<T*>(kv.ptr), at, 0.0);
     gemm<T>(cc, at, d, static_cast<const T*>(ly.wo), d, B, d, d, Epi::kAddResidual, x, d);

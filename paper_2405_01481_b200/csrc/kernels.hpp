@@ -22,6 +22,12 @@ template <class T>
 void launch_embed(Ctx& c, const int32_t* tokens, const int32_t* positions, int64_t rows, int64_t d,
                   const T* tok, const T* pos, float* x);
 
+// K1 + K2 for the decode step: embedding and the first LayerNorm in one pass
+// (false when d % 4 != 0 or d > 4096: use launch_embed + launch_layernorm).
+template <class T>
+bool launch_embed_layernorm(Ctx& c, const int32_t* tokens, const int32_t* positions, int64_t rows, int64_t d,
+                            const T* tok, const T* pos, float* x, const float* g, const float* b, T* y);
+
 // K2: LayerNorm (src/model.cpp:387-400), fp32 in, T out.  gather (nullable)
 // selects input rows; head (nullable) additionally writes head_out[r] =
 // dot(LN(x_row), head) in fp32 (K10: value / reward head) and, when y is

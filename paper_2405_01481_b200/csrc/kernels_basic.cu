@@ -409,6 +409,64 @@ __global__ void layernorm_vec_kernel(const float* __restrict__ x, int64_t d, con
   }
 }
 
+// Decode-step head: x[r] = tok[tokens[r]] + pos[positions[r]] (src/model.cpp:290-295)
+// and y[r] = LN1(x[r]) (src/model.cpp:387-400) in one CTA-per-row float4 pass.
+template <class T>
+__global__ void embed_layernorm_kernel(const int32_t* __restrict__ tokens, const int32_t* __restrict__ positions,
+                                       int64_t d, const T* __restrict__ tok, const T* __restrict__ pos,
+                                       float* __restrict__ x, const float* __restrict__ g, const float* __restrict__ b,
+                                       T* __restrict__ y) {
+  PDL_ENTRY();
+  __shared__ float red[2][32];
+  const int64_t r = blockIdx.x;
+  const int64_t t = tokens[r], p = positions[r];
+  const int j = threadIdx.x * 4;
+  const bool act = j < d;
+  float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (act) {
+    v = make_float4(to_f(tok[t * d + j]) + to_f(pos[p * d + j]), to_f(tok[t * d + j + 1]) + to_f(pos[p * d + j + 1]),
+                    to_f(tok[t * d + j + 2]) + to_f(pos[p * d + j + 2]),
+                    to_f(tok[t * d + j + 3]) + to_f(pos[p * d + j + 3]));
+    *reinterpret_cast<float4*>(x + r * d + j) = v;
+  }
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = (blockDim.x + 31) >> 5;
+  float s = warp_sum(v.x + v.y + v.z + v.w);
+  if (lane == 0) red[0][w] = s;
+  __syncthreads();
+  float mu = 0.f;
+  for (int k = 0; k < nw; ++k) mu += red[0][k];
+  mu /= float(d);
+  const float4 c = make_float4(v.x - mu, v.y - mu, v.z - mu, v.w - mu);
+  float q = act ? c.x * c.x + c.y * c.y + c.z * c.z + c.w * c.w : 0.f;
+  q = warp_sum(q);
+  if (lane == 0) red[1][w] = q;
+  __syncthreads();
+  float var = 0.f;
+  for (int k = 0; k < nw; ++k) var += red[1][k];
+  const float is = 1.0f / sqrtf(var / float(d) + 1e-5f);
+  if (act) {
+    const float4 gg = *reinterpret_cast<const float4*>(g + j), bb = *reinterpret_cast<const float4*>(b + j);
+    T* yr = y + r * d + j;
+    yr[0] = from_f<T>(gg.x * (c.x * is) + bb.x);
+    yr[1] = from_f<T>(gg.y * (c.y * is) + bb.y);
+    yr[2] = from_f<T>(gg.z * (c.z * is) + bb.z);
+    yr[3] = from_f<T>(gg.w * (c.w * is) + bb.w);
+  }
+}
+
+template <class T>
+bool launch_embed_layernorm(Ctx& c, const int32_t* tokens, const int32_t* positions, int64_t rows, int64_t d,
+                            const T* tok, const T* pos, float* x, const float* g, const float* b, T* y) {
+  if (rows <= 0) return true;
+  if (d % 4 || d > 4096) return false;
+  const int th = int((d / 4 + 31) / 32 * 32);
+  c.launch("layernorm", double(rows) * d * (2 * sizeof(T) + 4 + sizeof(T)), 0, [&] {
+    launch_kernel(c, embed_layernorm_kernel<T>, dim3(rows), dim3(th), 0, 1, tokens, positions, d, tok, pos, x, g, b,
+                  y);
+  });
+  return true;
+}
+
 template <class T>
 void launch_layernorm(Ctx& c, const float* x, int64_t rows, int64_t d, const float* g, const float* b, T* y,
                       const int32_t* gather, const float* head, float* head_out) {
@@ -552,6 +610,8 @@ void launch_fill_i32(Ctx& c, int32_t* dst, int64_t n, int32_t v) {
                                       float*, RowStats);                                                         \
   template void launch_embed<T>(Ctx&, const int32_t*, const int32_t*, int64_t, int64_t, const T*, const T*,      \
                                 float*);                                                                        \
+  template bool launch_embed_layernorm<T>(Ctx&, const int32_t*, const int32_t*, int64_t, int64_t, const T*,      \
+                                         const T*, float*, const float*, const float*, T*);                      \
   template void launch_layernorm<T>(Ctx&, const float*, int64_t, int64_t, const float*, const float*, T*,       \
                                     const int32_t*, const float*, float*);                                      \
   template void launch_kv_scatter<T>(Ctx&, const T*, int64_t, int64_t, const int32_t*, const int32_t*,          \
