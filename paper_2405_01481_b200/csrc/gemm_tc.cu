@@ -357,7 +357,12 @@ bool gemm_tc_bf16(Ctx& c, const bf16* A, int64_t lda, const bf16* B, int64_t ldb
   // decode-sized M: swap-AB + cluster split-K kernel (gemm_decode.cu)
   if (gemm_decode_bf16(c, A, lda, B, ldb, M, N, K, epi, C, ldc)) return true;
   const int64_t num_m = ceil_div(M, BM);
-  if (num_m * ceil_div(N, 256) >= 148) return dispatch_epi<256>(c, A, lda, B, ldb, M, N, K, epi, C, ldc), true;
+  static const int bn_env = [] {
+    const char* e = getenv("PPOEXP_TC_BN");
+    return e ? atoi(e) : 256;
+  }();
+  if (bn_env == 256 && num_m * ceil_div(N, 256) >= 148)
+    return dispatch_epi<256>(c, A, lda, B, ldb, M, N, K, epi, C, ldc), true;
   return dispatch_epi<128>(c, A, lda, B, ldb, M, N, K, epi, C, ldc), true;
 }
 
