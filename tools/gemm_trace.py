@@ -15,12 +15,15 @@ import numpy as np
 raw = open(sys.argv[1], "rb").read()
 n = int(np.frombuffer(raw[:4], np.int32)[0])
 meta = np.frombuffer(raw[4:4 + n * 16], np.int32).reshape(n, 4)
-st = np.frombuffer(raw[4 + n * 16:], np.uint64).astype(np.int64).reshape(n, 16)
+st = np.frombuffer(raw[4 + n * 16:], np.uint64).astype(np.int64).reshape(n, 16).copy()
 names = ["setup", "pdl wait", "X landed", "MMA done", "park+push", "peers in", "reduce+store", "cluster exit"]
 groups = collections.defaultdict(list)
 for i in range(n):
-    if st[i, 0] == 0 or st[i, 8] == 0:
+    if st[i, 0] == 0 or st[i, 6] == 0:
         continue
+    for k in (7, 8):  # direct push: no reduce/exit stamps -> zero-length stages
+        if st[i, k] == 0:
+            st[i, k] = st[i, k - 1]
     groups[tuple(meta[i])].append(st[i])
 sub = ["drain(4-9)", "sync(9-10)", "clwait(10-11)", "push+x(11-5)"]
 print(f"{'N,K,epi,S':22s} " + " ".join(f"{x:>14s}" for x in sub))
