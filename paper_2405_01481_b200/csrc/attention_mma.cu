@@ -68,8 +68,10 @@ __global__ void __launch_bounds__(128) attn_prefill_mma_kernel(const bf16* __res
   constexpr int CH = DH / 8;        // 16-byte chunks per row
   extern __shared__ __align__(128) uint8_t smem_raw[];
   bf16* sQ = reinterpret_cast<bf16*>(smem_raw);
-  bf16* sK[2] = {sQ + QT * LD, sQ + QT * LD + KT * LD};
-  bf16* sV[2] = {sQ + QT * LD + 2 * KT * LD, sQ + QT * LD + 3 * KT * LD};
+  // double-buffered K / V tiles (pointer arithmetic: a runtime-indexed pointer
+  // array would live on the stack)
+  auto sK = [&](int bf) { return sQ + QT * LD + bf * KT * LD; };
+  auto sV = [&](int bf) { return sQ + QT * LD + (2 + bf) * KT * LD; };
   const int64_t b = blockIdx.z, h = blockIdx.y, q0 = int64_t(blockIdx.x) * QT;
   const int64_t start = seq_offsets[b], len = seq_offsets[b + 1] - start;
   if (q0 >= len) return;
@@ -90,8 +92,8 @@ __global__ void __launch_bounds__(128) attn_prefill_mma_kernel(const bf16* __res
   load_rows(sQ, q0, h * DH);
   const int64_t kend = min(len, q0 + QT);  // causal: keys < last query + 1
   const int ntiles = int((kend + KT - 1) / KT);
-  load_rows(sK[0], 0, d + h * DH);
-  load_rows(sV[0], 0, 2 * d + h * DH);
+  load_rows(sK(0), 0, d + h * DH);
+  load_rows(sV(0), 0, 2 * d + h * DH);
   cp_async_commit();
 
   uint32_t qf[KC][4];
@@ -105,8 +107,8 @@ __global__ void __launch_bounds__(128) attn_prefill_mma_kernel(const bf16* __res
   for (int it = 0; it < ntiles; ++it) {
     const int buf = it & 1;
     if (it + 1 < ntiles) {
-      load_rows(sK[buf ^ 1], int64_t(it + 1) * KT, d + h * DH);
-      load_rows(sV[buf ^ 1], int64_t(it + 1) * KT, 2 * d + h * DH);
+      load_rows(sK(buf ^ 1), int64_t(it + 1) * KT, d + h * DH);
+      load_rows(sV(buf ^ 1), int64_t(it + 1) * KT, 2 * d + h * DH);
       cp_async_commit();
       cp_async_wait<1>();
     } else {
@@ -126,7 +128,7 @@ __global__ void __launch_bounds__(128) attn_prefill_mma_kernel(const bf16* __res
     float s[KT / 8][4];
 #pragma unroll
     for (int j = 0; j < KT / 8; ++j) s[j][0] = s[j][1] = s[j][2] = s[j][3] = 0.f;
-    const bf16* K = sK[buf];
+    const bf16* K = sK(buf);
 #pragma unroll
     for (int kc = 0; kc < KC; ++kc) {
 #pragma unroll
@@ -185,7 +187,7 @@ __global__ void __launch_bounds__(128) attn_prefill_mma_kernel(const bf16* __res
       o[i][3] *= corr[1];
     }
     // ---- O += P V: P (16 x 64) as A fragments straight from the S accumulators
-    const bf16* Vt = sV[buf];
+    const bf16* Vt = sV(buf);
 #pragma unroll
     for (int kk = 0; kk < KT / 16; ++kk) {
       uint32_t pa[4];

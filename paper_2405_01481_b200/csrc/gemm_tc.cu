@@ -217,11 +217,14 @@ __global__ void __launch_bounds__(kThreads, 2)
             }
             *reinterpret_cast<uint4*>(dst + j) = o.u;
           }
-        } else {
-          for (int e = 0; e < 32 && col + e < N; ++e) {
-            float f = __uint_as_float(v[e]);
-            if constexpr (EPI == int(Epi::kGelu)) f = gelu_tanh(f);
-            dst[e] = __float2bfloat16_rn(f);
+        } else {  // ragged last column block (unrolled + predicated: v stays in registers)
+#pragma unroll
+          for (int e = 0; e < 32; ++e) {
+            if (col + e < N) {
+              float f = __uint_as_float(v[e]);
+              if constexpr (EPI == int(Epi::kGelu)) f = gelu_tanh(f);
+              dst[e] = __float2bfloat16_rn(f);
+            }
           }
         }
       } else {
@@ -243,11 +246,14 @@ __global__ void __launch_bounds__(kThreads, 2)
             *reinterpret_cast<float4*>(dst + j) = o;
           }
         } else {
-          for (int e = 0; e < 32 && col + e < N; ++e) {
-            if constexpr (EPI == int(Epi::kAddResidual))
-              dst[e] += __uint_as_float(v[e]);
-            else
-              dst[e] = __uint_as_float(v[e]);
+#pragma unroll
+          for (int e = 0; e < 32; ++e) {
+            if (col + e < N) {
+              if constexpr (EPI == int(Epi::kAddResidual))
+                dst[e] += __uint_as_float(v[e]);
+              else
+                dst[e] = __uint_as_float(v[e]);
+            }
           }
         }
       }

@@ -22,7 +22,7 @@ from typing import Sequence
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libppoexp.so")
+LIB_PATH = os.environ.get("PPOEXP_LIB") or os.path.join(_PKG, "libppoexp.so")  # override: A/B runs only
 
 HOST, DEVICE = 0, 1
 F32, BF16, F64 = 0, 1, 2
