@@ -25,7 +25,7 @@ struct Engine {
   float* out_lp;
   double* uniforms;
   int32_t* host_flags = nullptr;
-  double *stats_a = nullptr, *stats_b = nullptr;  // fused-LN row-statistic slices
+  unsigned long long* stats = nullptr;  // fused-LN fixed-point row statistics [2L+1][max_batch][2]
   bool fuse_ln = false;
   // persistent decode-step kernel (decode_mega.cu); PPOEXP_DECODE_MEGA=0 disables
   bool use_mega = false;

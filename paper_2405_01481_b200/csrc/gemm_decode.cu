@@ -115,6 +115,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   using L = DecLayout<NB>;
   constexpr int XST = L::XST;
   __shared__ float ln_mu[NB], ln_rs[NB];
+  constexpr int kGB = LNIN ? 512 : 1;  // LN mode: gamma / beta of the first 8 k-blocks, staged before the PDL wait
+  __shared__ float ln_g[kGB], ln_b[kGB];
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int body = wst * L::kW > L::kPart ? wst * L::kW : L::kPart;
@@ -177,6 +179,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (push) asm volatile("barrier.cluster.arrive.aligned;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
   if (threadIdx.x == 0) stamp(1);
+  if constexpr (LNIN) {
+    if (threadIdx.x >= 64)  // LayerNorm parameters are not produced upstream
+      for (int i = threadIdx.x - 64; i < min(nkl, kGB / BK) * BK; i += 128) {
+        const int col = kb0 * BK + i;
+        ln_g[i] = col < K ? ln.g[col] : 0.f;
+        ln_b[i] = col < K ? ln.b[col] : 0.f;
+      }
+  }
   pdl_wait();  // upstream activations are valid from here on
   if (threadIdx.x == 0) stamp(2);
   pdl_trigger();
@@ -225,44 +235,85 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else {
     const int et = threadIdx.x - 64;  // 0..127
     if constexpr (LNIN) {
-      // ---- fused LayerNorm producer: row mean / rstd from the fp64 slices,
-      // then LN(x) -> bf16 written in the 128B-swizzled K-major layout UMMA reads
-      for (int rr = et; rr < NB; rr += 128) {
-        float mu = 0.f, rs = 0.f;
-        if (rr < Mrows) {
-          double s1 = 0.0, s2 = 0.0;
-          for (int sl = 0; sl < ln.n_slices; ++sl) {
-            s1 += ln.stats[(int64_t(sl) * ln.ld + rr) * 2];
-            s2 += ln.stats[(int64_t(sl) * ln.ld + rr) * 2 + 1];
-          }
-          const double mean = s1 / ln.d;
-          double var = s2 / ln.d - mean * mean;
-          if (var < 0) var = 0;
-          mu = float(mean);
-          rs = float(1.0 / sqrt(var + 1e-5));
+      // ---- fused LayerNorm producer: every independent load first (the row
+      // statistics and the x chunks of the first PF k-blocks), then row mean /
+      // rstd, then LN(x) -> bf16 in the 128B-swizzled K-major layout UMMA reads.
+      // Thread et owns chunks et + 128 c (c < CPT) of every k-block: always the
+      // same 8-column group c8.
+      constexpr int CPT = NB * 8 / 128;
+      constexpr int PF = CPT >= 8 ? 1 : (CPT >= 4 ? 3 : 4);
+      const int c8 = et & 7;
+      unsigned long long sa[2][2] = {{0ull, 0ull}, {0ull, 0ull}};
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int rr = et + u * 128;
+        if (rr < NB && rr < Mrows) {
+          sa[u][0] = __ldcg(ln.acc + rr * 2);
+          sa[u][1] = __ldcg(ln.acc + rr * 2 + 1);
         }
-        ln_mu[rr] = mu;
-        ln_rs[rr] = rs;
       }
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-      for (int it = 0; it < nkl; ++it) {
-        const int kb = kb0 + it;
+      auto load_kb = [&](int it, float4 (&xa)[CPT][2]) {
+        const int col = (kb0 + it) * BK + c8 * 8;
+#pragma unroll
+        for (int c = 0; c < CPT; ++c) {
+          const int rr = (et + c * 128) >> 3;
+          if (col < K && rr < Mrows) {
+            const float4* xr = reinterpret_cast<const float4*>(ln.x + int64_t(rr) * ln.ldx + col);
+            xa[c][0] = __ldcg(xr);
+            xa[c][1] = __ldcg(xr + 1);
+          } else {
+            xa[c][0] = xa[c][1] = make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+        }
+      };
+      float4 xpf[PF][CPT][2];
+#pragma unroll
+      for (int p = 0; p < PF; ++p)
+        if (p < nkl) load_kb(p, xpf[p]);
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int rr = et + u * 128;
+        if (rr < NB) {
+          float mu = 0.f, rs = 0.f;
+          if (rr < Mrows) {
+            const double mean = stat_of(sa[u][0]) / ln.d;
+            double var = stat_of(sa[u][1]) / ln.d - mean * mean;
+            if (var < 0) var = 0;
+            mu = float(mean);
+            rs = float(1.0 / sqrt(var + 1e-5));
+          }
+          ln_mu[rr] = mu;
+          ln_rs[rr] = rs;
+        }
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");  // mu / rstd and the staged gamma / beta
+      auto emit_kb = [&](int it, const float4 (&xa)[CPT][2]) {
         const int xs = it % XST, xu = it / XST;
+        const int col = (kb0 + it) * BK + c8 * 8;
+        float gv[8], bv[8];
+        if (it < kGB / BK) {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            gv[e] = ln_g[it * BK + c8 * 8 + e];
+            bv[e] = ln_b[it * BK + c8 * 8 + e];
+          }
+        } else {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            gv[e] = col + e < K ? __ldg(ln.g + col + e) : 0.f;
+            bv[e] = col + e < K ? __ldg(ln.b + col + e) : 0.f;
+          }
+        }
         if (xu > 0) mbar_wait(&xempty[xs], (xu - 1) & 1);
         uint8_t* tile = sX + xs * L::kX;
-        for (int ch = et; ch < NB * 8; ch += 128) {
-          const int rr = ch >> 3, c8 = ch & 7;
-          const int col = kb * BK + c8 * 8;
+#pragma unroll
+        for (int c = 0; c < CPT; ++c) {
+          const int rr = (et + c * 128) >> 3;
           Vec16<bf16> o;
-          if (rr < Mrows && col < K) {
-            const float* xr = ln.x + int64_t(rr) * ln.ldx + col;
-            const float4 a0 = *reinterpret_cast<const float4*>(xr), a1 = *reinterpret_cast<const float4*>(xr + 4);
-            const float4 g0 = *reinterpret_cast<const float4*>(ln.g + col), g1 = *reinterpret_cast<const float4*>(ln.g + col + 4);
-            const float4 b0 = *reinterpret_cast<const float4*>(ln.b + col), b1 = *reinterpret_cast<const float4*>(ln.b + col + 4);
+          if (col < K && rr < Mrows) {
             const float mu = ln_mu[rr], rs = ln_rs[rr];
-            const float xv[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-            const float gv[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
-            const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+            const float xv[8] = {xa[c][0].x, xa[c][0].y, xa[c][0].z, xa[c][0].w,
+                                 xa[c][1].x, xa[c][1].y, xa[c][1].z, xa[c][1].w};
 #pragma unroll
             for (int e = 0; e < 8; ++e) o.v[e] = __float2bfloat16_rn(gv[e] * ((xv[e] - mu) * rs) + bv[e]);
           } else {
@@ -272,6 +323,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor-core reads
         asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&xfull[xs])) : "memory");
+      };
+#pragma unroll
+      for (int p = 0; p < PF; ++p)
+        if (p < nkl) emit_kb(p, xpf[p]);
+      for (int it = PF; it < nkl; ++it) {
+        float4 xa[CPT][2];
+        load_kb(it, xa);
+        emit_kb(it, xa);
       }
     }
     // TMEM (feature rows x batch cols) → registers → (S == 1) epilogue straight
@@ -327,7 +386,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
-      if (EPI == int(Epi::kAddResidual) && S == 1 && so.p) {
+      if (EPI == int(Epi::kAddResidual) && S == 1 && so.acc) {
         // per-row partial statistics of the updated residual over this tile's
         // 128 features: warp reduce, 4 warp partials parked in smem (sX is free)
         float* wred = reinterpret_cast<float*>(sX);  // [4][NB][2]
@@ -349,7 +408,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rbar) : "r"(smem_u32(rfull)), "r"(f / rows_per));
       asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(rbar) : "memory");
     }
-    if (EPI == int(Epi::kAddResidual) && S == 1 && so.p) {
+    if (EPI == int(Epi::kAddResidual) && S == 1 && so.acc) {
       asm volatile("bar.sync 1, 128;" ::: "memory");
       const float* wred = reinterpret_cast<const float*>(sX);
       for (int bcol = threadIdx.x - 64; bcol < ncols; bcol += 128) {
@@ -358,8 +417,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           s1 += wred[(w4 * NB + bcol) * 2];
           s2 += wred[(w4 * NB + bcol) * 2 + 1];
         }
-        so.p[(int64_t(blockIdx.x) * so.ld + bcol) * 2] = s1;
-        so.p[(int64_t(blockIdx.x) * so.ld + bcol) * 2 + 1] = s2;
+        atomicAdd(&so.acc[bcol * 2], stat_fix(s1));
+        atomicAdd(&so.acc[bcol * 2 + 1], stat_fix(s2));
       }
     }
   }
@@ -505,23 +564,22 @@ __global__ void __launch_bounds__(kThreads, 1)
           static_cast<float*>(Cv)[o] = a;
         }
       }
-      if (EPI == int(Epi::kAddResidual) && so.p) {
+      if (EPI == int(Epi::kAddResidual) && so.acc) {
         double2* red = reinterpret_cast<double2*>(sX);  // [ncols][nf4], the X ring is idle now
         red[bcol * nf4 + (e % nf4)] = make_double2(ps, pq);
       }
     }
-    if (EPI == int(Epi::kAddResidual) && so.p) {
+    if (EPI == int(Epi::kAddResidual) && so.acc) {
       __syncthreads();
       const double2* red = reinterpret_cast<const double2*>(sX);
-      const int slice = blockIdx.x * S + r;
       for (int bcol = threadIdx.x; bcol < ncols; bcol += kThreads) {
         double s1 = 0.0, s2 = 0.0;
         for (int g4 = 0; g4 < nf4; ++g4) {
           s1 += red[bcol * nf4 + g4].x;
           s2 += red[bcol * nf4 + g4].y;
         }
-        so.p[(int64_t(slice) * so.ld + bcol) * 2] = s1;
-        so.p[(int64_t(slice) * so.ld + bcol) * 2 + 1] = s2;
+        atomicAdd(&so.acc[bcol * 2], stat_fix(s1));
+        atomicAdd(&so.acc[bcol * 2 + 1], stat_fix(s2));
       }
     }
     if (push == 2) {
@@ -544,16 +602,17 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 template <int NB, int EPI, bool LNIN>
-int launch_dec(Ctx& c, const bf16* X, int64_t ldx, const bf16* W, int64_t ldw, int64_t M, int64_t N, int64_t K,
+void launch_dec(Ctx& c, const bf16* X, int64_t ldx, const bf16* W, int64_t ldw, int64_t M, int64_t N, int64_t K,
                void* C, int64_t ldc, const LnIn* ln, const RowStats* so) {
   using L = DecLayout<NB>;
   const CUtensorMap tw = make_map(W, N, K, ldw, BMW);
   // LN mode never reads X through TMA; any valid map will do
   const CUtensorMap tx = LNIN ? tw : make_map(X, M, K, ldx, NB);
   auto k = gemm_decode_kernel<NB, EPI, LNIN>;
+  const int smem_max = L::kSmemMax - (LNIN ? 2 * 512 * 4 : 0);  // LN mode: static gamma / beta staging
   static bool attr = false;
   if (!attr) {
-    PPOEXP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kSmemMax));
+    PPOEXP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max));
     PPOEXP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     attr = true;
   }
@@ -602,7 +661,7 @@ int launch_dec(Ctx& c, const bf16* X, int64_t ldx, const bf16* W, int64_t ldw, i
     const char* e = getenv("PPOEXP_DECODE_PUSH");
     return e ? atoi(e) : 2;
   }();
-  const int push = (push_env && S > 1 && L::bytes(wst) + wst * 16 + L::kPart <= L::kSmemMax) ? push_env : 0;
+  const int push = (push_env && S > 1 && L::bytes(wst) + wst * 16 + L::kPart <= smem_max) ? push_env : 0;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(tiles, S, 1);
   cfg.blockDim = dim3(kThreads, 1, 1);
@@ -618,7 +677,7 @@ int launch_dec(Ctx& c, const bf16* X, int64_t ldx, const bf16* W, int64_t ldw, i
   cfg.attrs = attrs;
   cfg.numAttrs = 2;
   const LnIn lnv = ln ? *ln : LnIn{};
-  const RowStats sov = (so && EPI == int(Epi::kAddResidual)) ? *so : RowStats{nullptr, 0};
+  const RowStats sov = (so && EPI == int(Epi::kAddResidual)) ? *so : RowStats{};
   const double flops = 2.0 * M * N * K;
   const double bytes = 2.0 * N * K + double(M) * K * (LNIN ? 4 : 2) + double(M) * N * ((EPI == 0 || EPI == 1) ? 2 : 4);
   c.launch("gemm_decode", bytes, flops, [&] {
@@ -632,11 +691,10 @@ int launch_dec(Ctx& c, const bf16* X, int64_t ldx, const bf16* W, int64_t ldw, i
     }
     PPOEXP_CUDA(cudaLaunchKernelEx(&cfg, k, tw, tx, int(M), int(N), int(K), C, ldc, S, wst, lnv, sov, push, dbg));
   });
-  return sov.p ? (S > 1 ? tiles * S : tiles) : 0;
 }
 
 template <int NB, bool LNIN>
-int dispatch(Ctx& c, const bf16* X, int64_t ldx, const bf16* W, int64_t ldw, int64_t M, int64_t N, int64_t K, Epi epi,
+void dispatch(Ctx& c, const bf16* X, int64_t ldx, const bf16* W, int64_t ldw, int64_t M, int64_t N, int64_t K, Epi epi,
              void* C, int64_t ldc, const LnIn* ln, const RowStats* so) {
   switch (epi) {
     case Epi::kStore: return launch_dec<NB, 0, LNIN>(c, X, ldx, W, ldw, M, N, K, C, ldc, ln, so);
@@ -644,11 +702,10 @@ int dispatch(Ctx& c, const bf16* X, int64_t ldx, const bf16* W, int64_t ldw, int
     case Epi::kAddResidual: return launch_dec<NB, 2, LNIN>(c, X, ldx, W, ldw, M, N, K, C, ldc, ln, so);
     case Epi::kStoreF32: return launch_dec<NB, 3, LNIN>(c, X, ldx, W, ldw, M, N, K, C, ldc, ln, so);
   }
-  return 0;
 }
 
 template <bool LNIN>
-int dispatch_nb(Ctx& c, const bf16* X, int64_t ldx, const bf16* W, int64_t ldw, int64_t M, int64_t N, int64_t K,
+void dispatch_nb(Ctx& c, const bf16* X, int64_t ldx, const bf16* W, int64_t ldw, int64_t M, int64_t N, int64_t K,
                 Epi epi, void* C, int64_t ldc, const LnIn* ln, const RowStats* so) {
   if (M <= 32) return dispatch<32, LNIN>(c, X, ldx, W, ldw, M, N, K, epi, C, ldc, ln, so);
   if (M <= 64) return dispatch<64, LNIN>(c, X, ldx, W, ldw, M, N, K, epi, C, ldc, ln, so);
@@ -684,7 +741,7 @@ bool gemm_decode_bf16(Ctx& c, const bf16* A, int64_t lda, const bf16* B, int64_t
   return true;
 }
 
-int gemm_decode_fused(Ctx& c, const bf16* X, int64_t ldx, const bf16* W, int64_t ldw, int64_t M, int64_t N, int64_t K,
+void gemm_decode_fused(Ctx& c, const bf16* X, int64_t ldx, const bf16* W, int64_t ldw, int64_t M, int64_t N, int64_t K,
                       Epi epi, void* C, int64_t ldc, const LnIn* ln, const RowStats* so) {
   if (M > 256 || M <= 0) throw ContractError("decode GEMM: batch above 256");
   if (ln) {

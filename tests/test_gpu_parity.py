@@ -309,8 +309,9 @@ def test_sampler_massive_ties(px, ctx, oracle, top_k, top_p):
 
 
 def test_bf16_fused_layernorm_matches_unfused(px, ctx, oracle, monkeypatch):
-    """The decode path's fused LayerNorm (row-statistic slices + on-the-fly
-    normalisation in the consumer GEMMs) against the standalone LN kernels."""
+    """The decode path's fused LayerNorm (fixed-point row statistics accumulated
+    by the residual producers + on-the-fly normalisation in the consumer GEMMs)
+    against the standalone LN kernels."""
     cfg = ModelCfg(V=4096, d=256, L=3, H=4, f=1024, S=128)
     wb = bf16_round(oracle.init_params(cfg, 21))
     prompts = synthetic_prompts(8, 16, 12, ragged_lengths=True)
@@ -359,10 +360,13 @@ def test_bf16_persistent_decode_matches_per_op(px, ctx, oracle, monkeypatch, hea
     assert same >= len(prompts) // 2
 
 
-def test_bf16_decode_is_deterministic(px, ctx, oracle):
+@pytest.mark.parametrize("fuse_ln", ["0", "1"])
+def test_bf16_decode_is_deterministic(px, ctx, oracle, monkeypatch, fuse_ln):
     """bf16 decode (split-K decode GEMMs with the direct DSMEM push reduction and
-    no exit barrier) is bitwise reproducible: a lost, late or reordered partial
-    would show up as run-to-run differences in tokens or log-probs."""
+    no exit barrier; optionally the fused LayerNorm with atomically accumulated
+    fixed-point row statistics) is bitwise reproducible: a lost, late or
+    reordered partial would show up as run-to-run differences in tokens or log-probs."""
+    monkeypatch.setenv("PPOEXP_FUSE_LN", fuse_ln)
     cfg = ModelCfg(V=4096, d=768, L=2, H=12, f=3072, S=128)
     wb = bf16_round(oracle.init_params(cfg, 29))
     prompts = synthetic_prompts(31, 64, 16, ragged_lengths=True)
