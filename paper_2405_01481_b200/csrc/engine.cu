@@ -62,7 +62,7 @@ Engine::Engine(Model* model, const ppoexp_engine_options* o) : m(model), c(model
   const size_t o_uni = sbytes; sbytes += al(mb * S * 8);
   const size_t o_last = sbytes; sbytes += al(mb * 4);
   // fused-LN row statistics: one accumulator pair per row for each LayerNorm of a step
-  const size_t o_sta = sbytes; sbytes += al((2 * cfg.n_layers + 1) * mb * 16);
+  const size_t o_sta = sbytes; sbytes += al((2 * cfg.n_layers + 1) * mb * kStatStride * 8);
   const size_t o_part = sbytes; sbytes += al(decode_mega_part_bytes());
   const size_t o_bar = sbytes; sbytes += al(16);  // 2 x u64 grid-barrier counter / base
   const size_t o_mly = sbytes; sbytes += al(cfg.n_layers * sizeof(MegaLayer));
@@ -224,10 +224,10 @@ void Engine::decode_unit(int64_t B, int64_t unit) {
       // LayerNorm of the step), QKV / up / LM head normalise their activation
       // slice on the fly (no standalone LayerNorm launches)
       const int64_t L = m->cfg.n_layers, mb = opts.max_batch;
-      auto st = [&](int64_t i) { return stats + i * mb * 2; };  // i = 2l (LN1), 2l+1 (LN2)
+      auto st = [&](int64_t i) { return stats + i * mb * kStatStride; };  // i = 2l (LN1), 2l+1 (LN2)
       RowStats s0{st(0)};
       s0.zero = st(1);
-      s0.zero_n = (2 * L - 1) * mb * 2;
+      s0.zero_n = (2 * L - 1) * mb;
       launch_embed_stats<T>(cc, next_tok, pos, B, d, static_cast<const T*>(m->tok), static_cast<const T*>(m->pos), x,
                             s0);
       for (int64_t l = 0; l < L; ++l) {

@@ -248,8 +248,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int u = 0; u < 2; ++u) {
         const int rr = et + u * 128;
         if (rr < NB && rr < Mrows) {
-          sa[u][0] = __ldcg(ln.acc + rr * 2);
-          sa[u][1] = __ldcg(ln.acc + rr * 2 + 1);
+          sa[u][0] = __ldcg(ln.acc + rr * kStatStride);
+          sa[u][1] = __ldcg(ln.acc + rr * kStatStride + 1);
         }
       }
       auto load_kb = [&](int it, float4 (&xa)[CPT][2]) {
@@ -276,11 +276,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (rr < NB) {
           float mu = 0.f, rs = 0.f;
           if (rr < Mrows) {
-            const double mean = stat_of(sa[u][0]) / ln.d;
-            double var = stat_of(sa[u][1]) / ln.d - mean * mean;
-            if (var < 0) var = 0;
+            const double inv_d = 1.0 / ln.d;
+            const double mean = stat_of(sa[u][0]) * inv_d;
+            const double var = fmax(stat_of(sa[u][1]) * inv_d - mean * mean, 0.0);
             mu = float(mean);
-            rs = float(1.0 / sqrt(var + 1e-5));
+            rs = rsqrtf(float(var) + 1e-5f);
           }
           ln_mu[rr] = mu;
           ln_rs[rr] = rs;
@@ -417,8 +417,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           s1 += wred[(w4 * NB + bcol) * 2];
           s2 += wred[(w4 * NB + bcol) * 2 + 1];
         }
-        atomicAdd(&so.acc[bcol * 2], stat_fix(s1));
-        atomicAdd(&so.acc[bcol * 2 + 1], stat_fix(s2));
+        atomicAdd(&so.acc[bcol * kStatStride], stat_fix(s1));
+        atomicAdd(&so.acc[bcol * kStatStride + 1], stat_fix(s2));
       }
     }
   }
@@ -578,8 +578,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           s1 += red[bcol * nf4 + g4].x;
           s2 += red[bcol * nf4 + g4].y;
         }
-        atomicAdd(&so.acc[bcol * 2], stat_fix(s1));
-        atomicAdd(&so.acc[bcol * 2 + 1], stat_fix(s2));
+        atomicAdd(&so.acc[bcol * kStatStride], stat_fix(s1));
+        atomicAdd(&so.acc[bcol * kStatStride + 1], stat_fix(s2));
       }
     }
     if (push == 2) {

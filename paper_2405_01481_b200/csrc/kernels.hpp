@@ -44,12 +44,13 @@ void launch_gemm(Ctx& c, const T* A, int64_t lda, const T* B, int64_t ldb, int64
 
 // ---- decode-path LayerNorm fusion (bf16 engine) ----
 // Row statistics of the fp32 residual x travel as one pair of fixed-point
-// accumulators per row: acc[row * 2 + {0, 1}] = {sum x, sum x^2} in units of
+// accumulators per row: acc[row * kStatStride + {0, 1}] = {sum x, sum x^2} in units of
 // 2^-kStatShift (two's complement in u64).  Residual-producing decode GEMMs add
 // their per-CTA partials with integer atomics (order-independent, so the
 // statistics are bit-reproducible); consumer GEMMs normalise their activation
 // K-slice on the fly (LN = src/model.cpp:387-400, one-pass mean / variance).
 constexpr int kStatShift = 28;
+constexpr int kStatStride = 16;  // u64 per row: one 128-byte line each, so the producers' atomics spread over L2 slices
 __device__ __forceinline__ unsigned long long stat_fix(double v) {
   return static_cast<unsigned long long>(__double2ll_rn(v * double(1ll << kStatShift)));
 }
@@ -57,9 +58,9 @@ __device__ __forceinline__ double stat_of(unsigned long long a) {
   return double(static_cast<long long>(a)) * (1.0 / double(1ll << kStatShift));
 }
 struct RowStats {
-  unsigned long long* acc;            // [rows][2], zero before the first add
-  unsigned long long* zero = nullptr;  // (embedding only) accumulators to clear for this step
-  int64_t zero_n = 0;
+  unsigned long long* acc;            // [rows][kStatStride] (first two used), zero before the first add
+  unsigned long long* zero = nullptr;  // (embedding only) accumulator rows to clear for this step
+  int64_t zero_n = 0;                  // ... their number
 };
 struct LnIn {
   const float* x;                  // fp32 residual stream [rows, d]
@@ -74,7 +75,7 @@ struct LnIn {
 // Epi::kAddResidual only).
 void gemm_decode_fused(Ctx& c, const bf16* X, int64_t ldx, const bf16* W, int64_t ldw, int64_t M, int64_t N, int64_t K,
                       Epi epi, void* C, int64_t ldc, const LnIn* ln, const RowStats* so);
-// Embedding that also writes the row statistics of x and clears so.zero[0, zero_n).
+// Embedding that also writes the row statistics of x and clears so.zero's first zero_n rows.
 template <class T>
 void launch_embed_stats(Ctx& c, const int32_t* tokens, const int32_t* positions, int64_t rows, int64_t d,
                         const T* tok, const T* pos, float* x, RowStats so);

@@ -149,12 +149,15 @@ __global__ void __launch_bounds__(256) embed_stats_kernel(const int32_t* __restr
       a += red[0][k];
       c += red[1][k];
     }
-    so.acc[r * 2] = stat_fix(a);  // the sole producer of these accumulators
-    so.acc[r * 2 + 1] = stat_fix(c);
+    so.acc[r * kStatStride] = stat_fix(a);  // the sole producer of these accumulators
+    so.acc[r * kStatStride + 1] = stat_fix(c);
   }
   // clear this step's downstream accumulators (the previous step's readers
   // have completed: PDL_ENTRY waited for the predecessor grid)
-  for (int64_t k = r * blockDim.x + threadIdx.x; k < so.zero_n; k += rows * blockDim.x) so.zero[k] = 0ull;
+  for (int64_t k = r * blockDim.x + threadIdx.x; k < so.zero_n; k += rows * blockDim.x) {
+    so.zero[k * kStatStride] = 0ull;
+    so.zero[k * kStatStride + 1] = 0ull;
+  }
 }
 
 template <class T>
