@@ -182,6 +182,13 @@ PPOEXP_API ppoexp_status ppoexp_engine_generate(ppoexp_engine engine, int64_t B,
  * fused log-softmax+gather kernel. */
 PPOEXP_API ppoexp_status ppoexp_sequence_logprobs(ppoexp_model model, int64_t B, const int32_t* tokens,
                                        const int64_t* offsets, double* out, int32_t where);
+/* frozen_response_logprob_sum (src/trainers.cpp:24-29; DPO / SPIN scoring,
+ * sequences laid out by build_sft_sequence, src/data.cpp:142-167): for B
+ * ragged sequences, out[b] = sum_{t >= response_start[b]} log p(tokens[t] |
+ * tokens[<t]), accumulated in position order.  1 <= response_start[b] < T_b. */
+PPOEXP_API ppoexp_status ppoexp_response_logprob_sums(ppoexp_model model, int64_t B, const int32_t* tokens,
+                                           const int64_t* offsets, const int64_t* response_start, double* out,
+                                           int32_t where);
 /* value_estimates (src/losses.cpp:117-127) with the model's scalar head:
  * out is ragged over responses (out_offsets[b] = sum_{i<b} (T_i - rs_i)). */
 PPOEXP_API ppoexp_status ppoexp_value_estimates(ppoexp_model critic, int64_t B, const int32_t* tokens,

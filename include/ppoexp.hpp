@@ -257,6 +257,17 @@ inline std::vector<double> sequence_logprobs(DeviceModel& m, const TokenSeq& tok
   return sequence_logprobs(m, std::vector<TokenSeq>{tokens})[0];
 }
 
+// frozen_response_logprob_sum (src/trainers.cpp:24-29), batched: one sum per sequence
+inline std::vector<double> response_logprob_sums(DeviceModel& m, const std::vector<TokenSeq>& seqs,
+                                                 const std::vector<int64_t>& response_start) {
+  if (seqs.empty()) return {};
+  auto [flat, off] = detail::ragged(seqs);
+  std::vector<double> out(seqs.size());
+  check(ppoexp_response_logprob_sums(m.handle(), int64_t(seqs.size()), flat.data(), off.data(), response_start.data(),
+                                     out.data(), PPOEXP_HOST));
+  return out;
+}
+
 // value_estimates, include/aligner/losses.hpp:90-92
 inline std::vector<double> value_estimates(DeviceModel& critic, const TokenSeq& tokens, std::size_t response_start) {
   const int64_t off[2] = {0, int64_t(tokens.size())};

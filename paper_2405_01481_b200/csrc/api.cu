@@ -108,6 +108,31 @@ __global__ void seq_meta_kernel(int64_t B, const int64_t* offs, const int32_t* t
   }
 }
 
+// response rows of sequence b: positions t in [rs_b, T_b), compact row r = roff[b] + t - rs_b
+// predicts tokens[o + t] from the hidden state of row o + t - 1
+__global__ void resp_meta_kernel(int64_t B, const int64_t* offs, const int64_t* rs, const int64_t* roff,
+                                 const int32_t* tokens, int32_t* gather, int32_t* target, int64_t* out_index) {
+  PDL_ENTRY();
+  const int64_t b = blockIdx.x;
+  const int64_t o = offs[b], n = offs[b + 1] - o, s0 = rs[b], r0 = roff[b];
+  for (int64_t t = s0 + threadIdx.x; t < n; t += blockDim.x) {
+    gather[r0 + t - s0] = int32_t(o + t - 1);
+    target[r0 + t - s0] = tokens[o + t];
+    out_index[r0 + t - s0] = r0 + t - s0;
+  }
+}
+
+// out[b] = sum of lp over sequence b's response rows, in position order
+// (frozen_response_logprob_sum's accumulation order, src/trainers.cpp:24-29)
+__global__ void seg_sum_kernel(int64_t B, const int64_t* roff, const double* lp, double* out) {
+  PDL_ENTRY();
+  const int64_t b = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (b >= B) return;
+  double acc = 0.0;
+  for (int64_t r = roff[b]; r < roff[b + 1]; ++r) acc += lp[r];
+  out[b] = acc;
+}
+
 __global__ void last_content_kernel(int64_t B, const int64_t* offs, const int32_t* tokens, int32_t* gather,
                                     int64_t* out_index) {
   PDL_ENTRY();
@@ -359,6 +384,51 @@ ppoexp_status ppoexp_sequence_logprobs(ppoexp_model model, int64_t B, const int3
       score_logprobs(m, q, x, gather, target, oidx, R, out_d);
     }
     copy_out(c, out, out_d, M * 8, where);
+    if (where == PPOEXP_HOST) c.sync();
+  });
+}
+
+ppoexp_status ppoexp_response_logprob_sums(ppoexp_model model, int64_t B, const int32_t* tokens,
+                                           const int64_t* offsets, const int64_t* response_start, double* out,
+                                           int32_t where) {
+  return guard([&] {
+    need(model, "model");
+    if (B <= 0) return;
+    Model& m = model->m;
+    Ctx& c = *m.ctx;
+    std::lock_guard<std::recursive_mutex> lk(c.mu);
+    DeviceGuard g(c.device);
+    const auto off = to_host(c, offsets, B + 1, where);
+    const auto rs = to_host(c, response_start, B, where);
+    check_offsets(off, B);
+    std::vector<int64_t> roff(B + 1, 0);
+    for (int64_t b = 0; b < B; ++b) {
+      const int64_t T = off[b + 1] - off[b];
+      if (rs[b] < 1 || rs[b] >= T)  // build_sft_sequence: nonempty prompt and response (src/data.cpp:144-146)
+        throw ContractError("response_logprob_sums: response_start must leave a nonempty prompt and response");
+      roff[b + 1] = roff[b] + T - rs[b];
+    }
+    const int64_t R = roff[B];
+    if (where == PPOEXP_HOST) check_tokens_host(tokens, off[B], m.cfg.vocab_size);
+    Packed p = pack_tokens(c, tokens, off, where, "rsum");
+    int64_t* rs_d = upload(c, "rsum.rs", rs);
+    int64_t* roff_d = upload(c, "rsum.roff", roff);
+    int32_t* gather = static_cast<int32_t*>(c.workspace("rsum.gather", R * 4));
+    int32_t* target = static_cast<int32_t*>(c.workspace("rsum.target", R * 4));
+    int64_t* oidx = static_cast<int64_t*>(c.workspace("rsum.oidx", R * 8));
+    double* lp = static_cast<double*>(c.workspace("rsum.lp", R * 8));
+    double* out_d = static_cast<double*>(c.workspace("rsum.out", B * 8));
+    c.launch("meta", 0, 0, [&] {
+      launch_kernel(c, resp_meta_kernel, dim3(B), dim3(128), 0, 1, B, p.offsets_d, rs_d, roff_d, p.tokens_d, gather,
+                    target, oidx);
+    });
+    float* x = forward_layers(m, p, nullptr);
+    score_logprobs(m, p, x, gather, target, oidx, R, lp);
+    c.launch("meta", 0, 0, [&] {
+      launch_kernel(c, seg_sum_kernel, dim3(ceil_div(B, 128)), dim3(128), 0, 1, B, roff_d, static_cast<const double*>(lp),
+                    out_d);
+    });
+    copy_out(c, out, out_d, B * 8, where);
     if (where == PPOEXP_HOST) c.sync();
   });
 }

@@ -128,6 +128,7 @@ def lib():
             "ppoexp_engine_generate": [P, I64, P, P, P, P, P, I64, P, P, P, I32, P],
             "ppoexp_sequence_logprobs": [P, I64, P, P, P, I32],
             "ppoexp_value_estimates": [P, I64, P, P, P, P, I32],
+            "ppoexp_response_logprob_sums": [P, I64, P, P, P, P, I32],
             "ppoexp_reward_head": [P, I64, P, P, P, I32],
             "ppoexp_shape_gae": [I64, I64, P, P, P, P, P, D, D, D, P, P, P, P, I32],
             "ppoexp_whiten_partials": [I64, I64, P, P, P, P, I32],
@@ -459,6 +460,38 @@ def sequence_logprobs(model: DeviceModel, seqs):
     _check(lib().ppoexp_sequence_logprobs(model.h, len(seqs), flat.ctypes.data, offs.ctypes.data, out.ctypes.data,
                                           HOST))
     return [out[offs[b]:offs[b + 1]].copy() for b in range(len(seqs))]
+
+
+def build_sft_sequence(config: ModelConfig, prompt, response):
+    """build_sft_sequence (src/data.cpp:142-167): prompt + response + EOT,
+    truncated to max_seq_len.  Returns (full, response_start) — the layout
+    response_logprob_sums scores (targets = full[1:], loss on positions >=
+    response_start)."""
+    prompt, response = list(prompt), list(response)
+    if not prompt or not response:
+        raise ContractError("build_sft_sequence: prompt and response must be nonempty")
+    full = prompt + response + [EOT_TOKEN]
+    if len(full) > config.max_seq_len:
+        if len(prompt) + 2 > config.max_seq_len:
+            raise ContractError(f"build_sft_sequence: prompt of {len(prompt)} tokens leaves no room for a response "
+                                f"within max_seq_len {config.max_seq_len}")
+        full = full[:config.max_seq_len]
+    return np.asarray(full, np.int32), len(prompt)
+
+
+def response_logprob_sums(model: DeviceModel, seqs, response_starts):
+    """frozen_response_logprob_sum (src/trainers.cpp:24-29) for a batch: the
+    DPO / SPIN scoring quantity sum_{t >= rs} log p(seq[t] | seq[<t]) per
+    sequence, one batched forward + fused log-softmax/gather + a position-order
+    segmented sum on the GPU."""
+    if not len(seqs):
+        return np.zeros(0, np.float64)
+    flat, offs = ragged(seqs)
+    rs = np.ascontiguousarray(response_starts, np.int64)
+    out = np.zeros(len(seqs), np.float64)
+    _check(lib().ppoexp_response_logprob_sums(model.h, len(seqs), flat.ctypes.data, offs.ctypes.data, rs.ctypes.data,
+                                              out.ctypes.data, HOST))
+    return out
 
 
 def value_estimates(critic: DeviceModel, seqs, response_starts):

@@ -86,3 +86,18 @@ def test_cpp_facade_runs_on_gpu(lib):
     import subprocess
     r = subprocess.run([_build_facade_test()], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0 and "FACADE OK" in r.stdout, (r.returncode, r.stdout, r.stderr)
+
+
+def test_build_sft_sequence_layout():
+    """build_sft_sequence (src/data.cpp:142-167): prompt + response + EOT,
+    truncated to max_seq_len; contract errors with the reference's messages."""
+    from paper_2405_01481_b200 import ppoexp as px
+    cfg = px.ModelConfig(300, 16, 1, 2, 32, 10)
+    full, rs = px.build_sft_sequence(cfg, [1, 2, 3], [4, 5])
+    assert full.tolist() == [1, 2, 3, 4, 5, px.EOT_TOKEN] and rs == 3
+    full, rs = px.build_sft_sequence(cfg, [1, 2, 3], list(range(20)))
+    assert len(full) == 10 and rs == 3 and full[-1] == 6  # truncated: EOT dropped
+    with pytest.raises(px.ContractError, match="must be nonempty"):
+        px.build_sft_sequence(cfg, [], [1])
+    with pytest.raises(px.ContractError, match="leaves no room for a response"):
+        px.build_sft_sequence(cfg, list(range(9)), [1, 2, 3])

@@ -113,6 +113,52 @@ def test_golden_scoring(px, ctx, oracle, name):
     close(px.reward_head(rm, full), z["reward_rm"])
 
 
+@pytest.mark.parametrize("name", ["c1", "toy"])
+def test_golden_response_logprob_sums(px, ctx, oracle, name):
+    """frozen_response_logprob_sum (src/trainers.cpp:24-29): the per-sequence sum
+    of the reference-pinned sequence log-probs over the response positions."""
+    z, cfg, W, prompts = load(name, oracle)
+    lens = z["full_lens"]
+    offs = np.concatenate([[0], np.cumsum(lens)])
+    full = [z["full_tokens"][offs[i]:offs[i + 1]] for i in range(len(lens))]
+    rs = [len(p) for p in prompts]
+    ref = px.DeviceModel(ctx, to_px_cfg(cfg), W["ref"], px.F32)
+    got = px.response_logprob_sums(ref, full, rs)
+    want = []
+    for i in range(len(lens)):
+        acc = 0.0
+        for v in z["slp_ref"][offs[i] + rs[i]:offs[i + 1]]:  # position order, as the reference accumulates
+            acc += float(v)
+        want.append(acc)
+    close(got, want)
+
+
+def test_response_logprob_sums_dpo_layout(px, ctx, oracle):
+    """DPO scoring over build_sft_sequence layouts (chosen / rejected share a
+    prompt; one is truncated at max_seq_len) equals the oracle's teacher-forced
+    sums, and response_start outside [1, T) is a ContractError."""
+    cfg = ModelCfg(V=300, d=64, L=2, H=4, f=128, S=40)
+    w = oracle.init_params(cfg, 61).astype(np.float32).astype(np.float64)
+    pc = to_px_cfg(cfg)
+    m = px.DeviceModel(ctx, pc, w, px.F32)
+    rng = np.random.default_rng(5)
+    seqs, rs = [], []
+    for i in range(6):
+        prompt = rng.integers(0, 256, 5 + i).tolist()
+        for resp_len in (3 + i, 30):  # the second overflows max_seq_len = 40 for the longer prompts
+            full, r = px.build_sft_sequence(pc, prompt, rng.integers(0, 256, resp_len).tolist())
+            seqs.append(full)
+            rs.append(r)
+    got = px.response_logprob_sums(m, seqs, rs)
+    lps = oracle.sequence_logprobs(cfg, w, seqs)
+    want = [float(sum(lp[r:])) for lp, r in zip(lps, rs)]
+    close(got, want)
+    with pytest.raises(px.ContractError, match="nonempty prompt and response"):
+        px.response_logprob_sums(m, [seqs[0]], [len(seqs[0])])
+    with pytest.raises(px.ContractError, match="nonempty prompt and response"):
+        px.response_logprob_sums(m, [seqs[0]], [0])
+
+
 # ----------------------------------------------------------------- engine semantics
 def test_batch_composition_invariance(px, ctx, oracle):
     # results are index-aligned and independent of batching (tests/test_engine.cpp:213-243)

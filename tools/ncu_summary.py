@@ -2,6 +2,7 @@
 full .ncu-rep -> key metrics + top stall sites.  Usage:
     python tools/ncu_summary.py launches <launches.csv> <out.md> [skip_fraction]
     python tools/ncu_summary.py full <rep.ncu-rep> <out.md>
+    python tools/ncu_summary.py traffic <decode.csv> <scoring.csv> <out.json>   (bench.py roofline.traffic)
 """
 import collections
 import csv
@@ -106,8 +107,34 @@ def full(rep, out):
                 f.write(f"| {100 * smp / tot:.1f}% | {fn}:{ln} | `{src_[:90]}` |\n")
 
 
+CLASSES = (("gemm_decode_kernel", "gemm_decode"), ("attn_decode", "decode_attention"), ("sampler", "sampler"),
+           ("layernorm", "layernorm"), ("gemm_tc", "gemm_tc"), ("logprob_gather", "logprob_gather"))
+
+
+def traffic(dec_csv, score_csv, out):
+    """Mean DRAM bytes (read + write) per launch for each bench kernel class."""
+    import json
+    import os
+    tot = collections.defaultdict(lambda: [0, 0.0])
+    for path in (dec_csv, score_csv):
+        agg = launches(path, os.devnull)
+        for (n, _, _), (c, _, d) in agg.items():
+            for key, cls in CLASSES:
+                if key in n:
+                    tot[cls][0] += c
+                    tot[cls][1] += d
+    doc = {"source": f"{dec_csv} + {score_csv} (ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,"
+                     "dram__bytes_write.sum; decode list with --cache-control none, steady state of "
+                     "tools/profile_decode.py --new 88)",
+           "bytes_per_launch": {k: v[1] / v[0] for k, v in tot.items() if v[0]}}
+    with open(out, "w") as f:
+        json.dump(doc, f, indent=1)
+
+
 if __name__ == "__main__":
-    if sys.argv[1] == "launches":
+    if sys.argv[1] == "traffic":
+        traffic(sys.argv[2], sys.argv[3], sys.argv[4])
+    elif sys.argv[1] == "launches":
         launches(sys.argv[2], sys.argv[3], float(sys.argv[4]) if len(sys.argv) > 4 else 0.0)
     else:
         full(sys.argv[2], sys.argv[3])

@@ -21,7 +21,10 @@ ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum 
     -k regex:"gemm_tc|logprob|attn_prefill|layernorm_warp|kv_scatter" -s 420 -c 240 --csv \
     --log-file gpurun_out/prof/launches_scoring.csv $CMD > gpurun_out/prof/ncu2.log 2>&1
 # full captures of the top kernels
-ncu --set full --import-source on --clock-control none -k regex:"gemm_decode_kernel<64, 2" -s 200 -c 1 -o gpurun_out/prof/full_gemm_decode $DEC > gpurun_out/prof/ncu3.log 2>&1
+# gemm_decode launches per decode step: 12 x [QKV, O, up, down] + LM head = 49 (template args do not
+# match -k): -s 202 = an O projection (residual + row statistics), -s 201 = a QKV projection (LN fused)
+ncu --set full --import-source on --clock-control none -k regex:gemm_decode_kernel -s 202 -c 1 -o gpurun_out/prof/full_gemm_decode $DEC > gpurun_out/prof/ncu3.log 2>&1
+ncu --set full --import-source on --clock-control none -k regex:gemm_decode_kernel -s 201 -c 1 -o gpurun_out/prof/full_gemm_decode_lnin $DEC > gpurun_out/prof/ncu3b.log 2>&1
 ncu --set full --import-source on --clock-control none -k regex:attn_decode -s 100 -c 1 -o gpurun_out/prof/full_attn_decode $DEC > gpurun_out/prof/ncu4.log 2>&1
 ncu --set full --import-source on --clock-control none -k regex:logprob_gather -s 2 -c 1 -o gpurun_out/prof/full_logprob $CMD > gpurun_out/prof/ncu5.log 2>&1
 ncu --set full --import-source on --clock-control none -k regex:gemm_tc_kernel -s 100 -c 1 -o gpurun_out/prof/full_gemm_tc $CMD > gpurun_out/prof/ncu6.log 2>&1
