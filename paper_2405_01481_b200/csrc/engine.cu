@@ -117,11 +117,13 @@ Engine::Engine(Model* model, const ppoexp_engine_options* o) : m(model), c(model
     }
   }
   {
-    // default for bf16 (PPOEXP_FUSE_LN=0 restores the standalone LayerNorm
-    // launches): removes 24 of the 25 LN launches of a decode step, -6% step
-    // time at C2 on B200
+    // default for bf16 decode batches <= 64 (PPOEXP_FUSE_LN=0 disables, =1
+    // forces it up to 256): removes 24 of the 25 LN launches of a decode step,
+    // -6% step time at C2 on B200; at batch 256 every weight tile would
+    // re-normalise 4x more rows and it measured 18% slower
     const char* ev = getenv("PPOEXP_FUSE_LN");
     fuse_ln = m->dtype == PPOEXP_BF16 && !(ev && ev[0] == '0') && !use_mega && mb <= 256 && d % 8 == 0;
+    fuse_ln_max_b = ev && ev[0] == '1' ? 256 : 64;
   }
   PPOEXP_CUDA(cudaMallocHost(&host_flags, 64));
   PPOEXP_CUDA(cudaEventCreateWithFlags(&poll_ev[0], cudaEventDisableTiming));
@@ -218,7 +220,7 @@ void Engine::decode_unit(int64_t B, int64_t unit) {
         return;
       }
     }
-    if (fuse_ln) {
+    if (fuse_ln && B <= fuse_ln_max_b) {
       // bf16 path with LayerNorm fused into the consumer GEMMs: embed / O-proj /
       // down-proj accumulate fixed-point row statistics of x (one buffer per
       // LayerNorm of the step), QKV / up / LM head normalise their activation

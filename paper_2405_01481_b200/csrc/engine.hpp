@@ -27,6 +27,7 @@ struct Engine {
   int32_t* host_flags = nullptr;
   unsigned long long* stats = nullptr;  // fused-LN fixed-point row statistics [2L+1][max_batch][2]
   bool fuse_ln = false;
+  int64_t fuse_ln_max_b = 64;  // fused LayerNorm only for decode batches up to this size
   // persistent decode-step kernel (decode_mega.cu); PPOEXP_DECODE_MEGA=0 disables
   bool use_mega = false;
   float* part = nullptr;
