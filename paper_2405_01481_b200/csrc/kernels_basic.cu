@@ -506,6 +506,19 @@ __global__ void kv_scatter_kernel(const T* __restrict__ qkv, int64_t rows, int64
   const int64_t s = seq_of_row[r], p = pos_of_row[r];
   const int64_t page = block_table[s * g.max_pages_per_seq + p / g.page_size];
   const int64_t slot = p % g.page_size;
+  constexpr int E = 16 / int(sizeof(T));  // elements per 16-byte chunk
+  if (g.DH % E == 0 && d % E == 0) {
+    // 16-byte chunks: a head's K (or V) row is DH contiguous elements in both layouts
+    const int dc = int(d / E), hc = int(g.DH / E);
+    const uint4* src = reinterpret_cast<const uint4*>(qkv + r * 3 * d + d);
+    for (int j = threadIdx.x; j < 2 * dc; j += blockDim.x) {
+      const int which = j / dc, cc = j - which * dc, h = cc / hc, i = cc - h * hc;
+      const int64_t dst = ((((int64_t)layer * g.n_pages + page) * 2 + which) * g.H + h) * g.page_size * g.DH +
+                          slot * g.DH + int64_t(i) * E;
+      *reinterpret_cast<uint4*>(kv + dst) = src[j];
+    }
+    return;
+  }
   for (int64_t j = threadIdx.x; j < 2 * d; j += blockDim.x) {
     const int64_t which = j / d, col = j % d, h = col / g.DH, i = col % g.DH;
     const int64_t dst = ((((int64_t)layer * g.n_pages + page) * 2 + which) * g.H + h) * g.page_size * g.DH +
