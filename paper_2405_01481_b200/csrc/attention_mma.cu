@@ -101,7 +101,8 @@ __global__ void __launch_bounds__(128) attn_prefill_mma_kernel(const bf16* __res
 #pragma unroll
   for (int i = 0; i < NO; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
   float m_r[2] = {-FLT_MAX, -FLT_MAX}, l_r[2] = {0.f, 0.f};
-  const float scale = 1.0f / sqrtf(float(DH));
+  // softmax in the log2 domain: exp(x - m) == exp2(x * log2e - m * log2e), one MUFU.EX2 per score
+  const float scale = 1.4426950408889634f / sqrtf(float(DH));
   const int64_t qrow0 = q0 + warp * 16 + g, qrow1 = qrow0 + 8;
 
   for (int it = 0; it < ntiles; ++it) {
@@ -160,7 +161,7 @@ __global__ void __launch_bounds__(128) attn_prefill_mma_kernel(const bf16* __res
       mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 1));
       mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 2));
       const float mn = fmaxf(m_r[r], mx[r]);
-      corr[r] = m_r[r] == -FLT_MAX ? 0.f : expf(m_r[r] - mn);
+      corr[r] = m_r[r] == -FLT_MAX ? 0.f : exp2f(m_r[r] - mn);
       m_r[r] = mn;
     }
     float rs[2] = {0.f, 0.f};
@@ -169,7 +170,7 @@ __global__ void __launch_bounds__(128) attn_prefill_mma_kernel(const bf16* __res
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const int r = e >> 1;
-        const float p = s[j][e] == -FLT_MAX ? 0.f : expf(s[j][e] - m_r[r]);
+        const float p = s[j][e] == -FLT_MAX ? 0.f : exp2f(s[j][e] - m_r[r]);
         s[j][e] = p;
         rs[r] += p;
       }
