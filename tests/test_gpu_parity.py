@@ -406,6 +406,25 @@ def test_bf16_persistent_decode_matches_per_op(px, ctx, oracle, monkeypatch, hea
     assert same >= len(prompts) // 2
 
 
+def test_bf16_decode_batch_above_fused_ln_limit(px, ctx, oracle):
+    """Decode batches above 64 take the standalone-LayerNorm path (the fused
+    LayerNorm is the default only up to 64 rows): teacher-forced against the
+    oracle, and the first 64 rows agree with a 64-row batch of the same tasks."""
+    cfg = ModelCfg(V=2048, d=256, L=2, H=4, f=1024, S=96)
+    wb = bf16_round(oracle.init_params(cfg, 71))
+    prompts = synthetic_prompts(43, 100, 10, ragged_lengths=True)
+    tasks = [px.GenTask(p, 24) for p in prompts]
+    eng = engine(px, ctx, cfg, wb, px.BF16)
+    big = eng.generate_batch(tasks)
+    for r, p in zip(big[::7], prompts[::7]):
+        full = np.concatenate([p, r.tokens])
+        lp = oracle.sequence_logprobs(cfg, wb, [full])[0][len(p):]
+        close(r.logprobs, lp, atol=3e-2, rtol=3e-3)
+    small = eng.generate_batch(tasks[:64])
+    same = sum(int(np.array_equal(a.tokens, b.tokens)) for a, b in zip(big[:64], small))
+    assert same >= 32
+
+
 @pytest.mark.parametrize("fuse_ln", ["0", "1"])
 def test_bf16_decode_is_deterministic(px, ctx, oracle, monkeypatch, fuse_ln):
     """bf16 decode (split-K decode GEMMs with the direct DSMEM push reduction and
