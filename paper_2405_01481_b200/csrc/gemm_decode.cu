@@ -631,10 +631,15 @@ void launch_dec(Ctx& c, const bf16* X, int64_t ldx, const bf16* W, int64_t ldw, 
   }();
   const int cap = tiles <= 8 ? smax_small : smax;
   int S = 1;
-  static const int fit = [] {  // double only while the doubled grid still fits one wave
+  static const int fit_env = [] {  // 1: double only while the doubled grid still fits one wave
     const char* e = getenv("PPOEXP_DECODE_SPLIT_FIT");
-    return e ? atoi(e) : 1;
+    return e ? atoi(e) : -1;
   }();
+  // auto: the one-wave rule for wide batches (each CTA re-reads a 256-row
+  // activation: measured best at config 3, batch 256); small batches keep
+  // doubling while the grid is under one CTA per SM — more weight streams in
+  // flight (config 4, batch 64: 6.4k -> 7.5k tok/s; config 2 picks the same S either way)
+  const bool fit = fit_env >= 0 ? fit_env != 0 : NB > 64;
   while (S < cap && (fit ? tiles * S * 2 <= 148 : tiles * S < 148) && nk >= 2 * S) S *= 2;
   // a slice larger than the weight ring cycles it (warp 0 lane 1 refills); only
   // split further for that while the launch stays one wave (1 CTA/SM at batch > 64)
