@@ -797,8 +797,29 @@ void launch_sampler(Ctx& c, const float* logits, int64_t ld, int64_t B, int64_t 
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  const bool pair = cl_env == 2 && 2 * B <= sms && (V + 7) / 8 * 4 <= kCacheMaxV && V >= 64 && (ld % 4) == 0;
-  if (pair) {
+  const bool pair_ok = cl_env == 2 && 2 * B <= sms && V >= 64 && (ld % 4) == 0;
+  const bool pair = pair_ok && (V + 7) / 8 * 4 <= kCacheMaxV;
+  if (pair_ok && !pair) {
+    // vocabularies too large for the per-CTA logit cache (e.g. 128k): still a
+    // CTA pair per row, each streaming its half of the row from L2 every pass
+    c.launch("sampler", double(B) * V * 4, 0, [&] {
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(unsigned(2 * B));
+      cfg.blockDim = dim3(NT);
+      cfg.dynamicSmemBytes = 0;
+      cfg.stream = c.stream;
+      cudaLaunchAttribute at[2];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = 2;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[1].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 2;
+      PPOEXP_CUDA(cudaLaunchKernelEx(&cfg, sampler_kernel<false, 2>, logits, ld, V, s));
+    });
+  } else if (pair) {
     const int64_t half = (V + 7) / 8 * 4;
     const size_t smem = size_t(half) * sizeof(float);
     static bool attr = false;

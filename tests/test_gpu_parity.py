@@ -259,6 +259,26 @@ def test_topk_topp_matches_oracle(px, ctx, oracle, top_k, top_p):
         close(r.logprobs, l)
 
 
+@pytest.mark.parametrize("top_k,top_p", [(0, 0.9), (50, 0.95), (0, 1.0)])
+def test_large_vocab_sampler_matches_oracle(px, ctx, oracle, top_k, top_p):
+    """A vocabulary above the per-CTA logit cache (the 128k-vocab configs take
+    this path): the uncached CTA-pair sampler, token-exact against the oracle."""
+    cfg = ModelCfg(V=70000, d=32, L=1, H=2, f=64, S=48)
+    w = oracle.init_params(cfg, 17).astype(np.float32).astype(np.float64)
+    w[:cfg.V * cfg.d] *= 40.0  # spread the logits so top-k / top-p cut inside the row
+    prompts = synthetic_prompts(19, 6, 8, ragged_lengths=True)
+    N = 6
+    eng = engine(px, ctx, cfg, w, px.F32)
+    seeds = [oracle.mix_seed(23, i) for i in range(len(prompts))]
+    res = eng.generate_batch([px.GenTask(p, N, px.SamplingSpec.temperature_spec(1.0, s, top_k, top_p))
+                              for p, s in zip(prompts, seeds)])
+    u = np.stack([oracle.uniforms(s, N) for s in seeds])
+    t_o, l_o = oracle.generate(cfg, w, prompts, N, greedy=False, top_k=top_k, top_p=top_p, uniforms=u)
+    for r, t, l in zip(res, t_o, l_o):
+        assert np.array_equal(r.tokens, t)
+        close(r.logprobs, l)
+
+
 # ----------------------------------------------------------------- perf mode (bf16)
 def test_bf16_teacher_forced_parity(px, ctx, oracle):
     """bf16 weights/activations: generation log-probs must match the oracle's
