@@ -34,14 +34,23 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 CONFIGS = {
-    # name: (V, d, L, H, f, S, B per rank, P, N, sampling, description)
+    # name: (V, d, L, H, f, S, B per rank (c3: global, split over ranks), P, N, sampling, description)
     "c1": (1024, 128, 2, 4, 512, 128, 8, 9, 64, "greedy", "tiny GPT policy 2x128, vocab 1k, 8 prompts x 64 greedy"),
     "c2": (50257, 768, 12, 12, 3072, 512, 64, 64, 256, "top_p", "GPT-style 125M policy+reference+critic, 64 prompts x 256 tokens, top-p"),
-    "c3": (32000, 2048, 24, 16, 8192, 1024, 32, 128, 512, "top_p", "1.3B policy/critic, 256x512 global (32 per rank at 8 GPUs), vocab 32k"),
+    "c3": (32000, 2048, 24, 16, 8192, 1024, 256, 128, 512, "top_p", "1.3B policy/critic, 256 prompts x 512 tokens global (strong scaling: 256/N per rank), vocab 32k"),
     "c4": (128256, 4096, 32, 32, 14336, 2048, 64, 128, 1024, "top_p", "8B-shape reference block, paged KV, 64 prompts x 1024 per GPU"),
 }
 TOP_P = 0.9
 SEED = 20240809
+STRONG = {"c3"}  # configs whose global batch is fixed and split over the ranks
+
+
+def per_rank_batch(config, B, world):
+    if config in STRONG:
+        if B % world:
+            raise SystemExit(f"{config}: global batch {B} not divisible by {world} ranks")
+        return B // world
+    return B
 
 
 def peaks():
@@ -121,26 +130,54 @@ def prompts_for(rank, B, P, V, seed):
     return [rng.integers(0, 256, size=P).astype(np.int32) for _ in range(B)]
 
 
-def reference_sample(cfg_t, threads, n_new, steps=1, seed=SEED):
+def reference_sample(cfg_t, threads, steps=1, seed=SEED, p_s=8, n_s=4, B=None, P=None, N=None):
     """Times the REFERENCE itself (oracle/_ref = /root/reference sources compiled
-    in place) on the host: Engine::generate_batch with n_workers = threads,
-    one sequence per worker, P-token prompts, n_new sampled tokens.  Returns
-    (tokens/s, seconds per step)."""
+    in place) on the host cores and extrapolates to the full workload shape.
+
+    Each step runs the reference's experience path (oracle/ref_shim.cpp
+    ref_experience: Engine::generate_batch with n_workers = threads, then
+    sequence_logprobs x2, value_estimates, scripted reward, KL shaping + GAE,
+    each spread over the same threads by sequence) on `threads` sequences with
+    a p_s-token prompt and n_s sampled tokens, and records its three phase
+    times.  Every reference cost is a chain of KvSession steps (generation:
+    P+N-1 per sequence, src/model.cpp:438-482; log-probs: T per sequence and
+    model, :484-495) or a T-token forward (values, src/losses.cpp:117-127), so
+    the full shape (B sequences, P + N tokens) costs, per phase,
+        ceil(B / threads) x phase_time x (full steps / sample steps).
+    The sample's shorter context makes attention cheaper than at the full
+    shape, so the extrapolation favours the reference slightly.
+    Returns dict(tokens_per_s, samples_per_s, secs[], sample)."""
     from oracle.oracle import ModelCfg, RefLib
-    V, d, L, H, f, S, B, P, N, _, _ = cfg_t
+    V, d, L, H, f, S, Bc, Pc, Nc, samp, _ = cfg_t
+    B, P, N = B or Bc, P or Pc, N or Nc
     ref = RefLib()
     cfg = ModelCfg(V, d, L, H, f, S)
-    w = ref.init_params(cfg, seed)
-    prompts = prompts_for(0, threads, P, V, seed)
-    seeds = [ref.mix_seed(seed, i) for i in range(threads)]
-    rates, secs = [], []
-    for _ in range(steps):
-        toks, _, s = ref.generate_batch(cfg, w, prompts, n_new, greedy=False, temperature=1.0, seeds=seeds,
-                                        n_workers=threads)
-        n = sum(len(t) for t in toks)
-        rates.append(n / s)
-        secs.append(s)
-    return float(np.median(rates)), secs
+    greedy = samp == "greedy"
+    wp = ref.init_params(cfg, seed)
+    wr = ref.init_params(cfg, seed + 1)
+    wc = ref.init_params(cfg, seed + 101, head=True)
+    prompts = prompts_for(0, threads, p_s, V, seed)
+    tok_rates, xp_rates, secs = [], [], []
+    rounds = -(-B // threads)
+    for i in range(steps):
+        t0 = time.perf_counter()
+        r = ref.experience(cfg, wp, wr, wc, prompts, max_new=n_s, greedy=greedy, seed=seed, step_index=i,
+                           kl_coef=0.003, gamma=1.0, lam=0.95, scripted_target=ord("e"), n_workers=threads)
+        secs.append(time.perf_counter() - t0)
+        g, lp, val = (float(x) for x in r["phase_seconds"])
+        n_gen = float(np.mean([len(t) for t in r["tokens"]]))
+        t_s = p_s + n_gen
+        gen_full = g * (P + N - 1) / (t_s - 1)
+        lp_full = lp * (P + N) / t_s
+        val_full = val * (P + N) / t_s
+        tok_rates.append(B * N / (rounds * gen_full))
+        xp_rates.append(B / (rounds * (gen_full + lp_full + val_full)))
+    sample = (f"extrapolated: per step the reference's experience path (Engine::generate_batch n_workers={threads} + "
+              f"sequence_logprobs x2 + value_estimates + shaping/GAE over {threads} threads, fp64) on {threads} "
+              f"sequences x {p_s}-token prompt x {n_s} sampled tokens ({np.mean(secs):.1f} s), phase times scaled "
+              f"per KvSession step to {B} sequences x ({P} + {N}) tokens in ceil({B}/{threads}) rounds")
+    return dict(tokens_per_s=float(np.median(tok_rates)), samples_per_s=float(np.median(xp_rates)), secs=secs,
+                sample=sample)
 
 
 def workload_config(args, world, B=None):
@@ -154,29 +191,36 @@ def workload_config(args, world, B=None):
             "l2": "flushed between timed steps (256 MiB write); weights+KV > L2"}
 
 
+def host_threads():
+    n = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    return max(1, min(n, 128))
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    cfg_t = CONFIGS[args.config]
-    threads = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
-    threads = max(1, min(threads, 128))
-    n_new = args.ref_new_tokens
-    # warmup + timed steps; each step is a bounded sample of the workload
-    reference_sample(cfg_t, threads, n_new, steps=max(0, min(args.warmup, 1)))
-    val, secs = reference_sample(cfg_t, threads, n_new, steps=args.steps)
-    V, d, L, H, f, S, B, P, N, samp, desc = cfg_t
-    sample = (f"{threads} sequences (one per host thread) x {P}-token prompt x {n_new} sampled tokens through the "
-              f"reference's Engine::generate_batch (n_workers={threads}, fp64) per step; prompts fed token-by-token "
-              f"as the reference does")
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    cfg_t = CONFIGS[args.config]
+    V, d, L, H, f, S, Bc, P, N, samp, desc = cfg_t
+    Bg = args.batch or Bc
+    B = per_rank_batch(args.config, Bg, world)
+    threads = host_threads()
+    # warmup + timed steps; each step is a bounded sample of the workload
+    reference_sample(cfg_t, threads, steps=max(0, min(args.warmup, 1)), B=B)
+    r = reference_sample(cfg_t, threads, steps=args.steps, B=B)
+    # the whole job: the other ranks' shares run on their own host cores in the
+    # same wall time (weak scaling), or the global batch is split (strong)
+    val = r["tokens_per_s"] * world
     line = {"impl": "reference", "metric": "rollout_tokens_per_s", "value": val, "unit": "tokens/s",
-            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * float(np.mean(secs)),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": workload_config(args, world),
-            "note": "the reference's own CPU path on this box's host cores (no GPU used)",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * float(np.mean(r["secs"])),
+            "higher_is_better": True, "scaling": "strong" if args.config in STRONG else "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic", "config": workload_config(args, world, B),
+            "experience_samples_per_s": r["samples_per_s"] * world,
+            "note": "the reference's own CPU path on this box's host cores (no GPU used); rank 0 times one rank's "
+                    "share, the value is scaled by the rank count",
             "cpu_baseline": {"value": val, "unit": "tokens/s", "cores": threads, "kind": "reference",
-                             "sample": sample},
+                             "sample": r["sample"], "experience_samples_per_s": r["samples_per_s"] * world},
             "e2e": {"value": val, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -184,6 +228,69 @@ def run_reference(args):
 def _dbg(*a):
     if os.environ.get("PPOEXP_BENCH_DEBUG"):
         print(f"[rank {os.environ.get('RANK', '0')}]", *a, file=sys.stderr, flush=True)
+
+
+KCLASS = [("gemm_decode_kernel", "gemm_decode"), ("attn_decode_kernel", "decode_attention"),
+          ("sampler_kernel", "sampler"), ("gemm_tc_kernel<256, 4>", "lm_head_lse"),
+          ("gemm_tc_kernel", "gemm_tc"), ("lse_combine", "lse_combine"), ("logprob_gather", "logprob_gather"),
+          ("attn_prefill", "attention_prefill"), ("attention_mma", "attention_prefill"), ("layernorm", "layernorm"),
+          ("embed", "embed"), ("kv_scatter", "kv_scatter"), ("shape_gae", "shape_gae")]
+
+
+def kclass(name):
+    for pat, cls in KCLASS:
+        if pat in name:
+            return cls
+    return "other"
+
+
+def cupti_breakdown(step_fn):
+    """Runs step_fn once under CUPTI (torch.profiler; kernel records do not
+    perturb the CUDA graphs or their programmatic dependent launches) and
+    returns per-class kernel times.  The generation phase (first to last
+    sampler launch, one stream) is reported as the critical-path time each
+    class adds to the decode step (end minus the previous latest end: PDL
+    overlap accounted, so the classes sum to the decode-step time); the
+    scoring phase (concurrent streams) as plain kernel durations."""
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        step_fn()
+        torch.cuda.synchronize()
+    ev = [e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA
+          and "Memcpy" not in e.name and "Memset" not in e.name]
+    ev.sort(key=lambda e: e.time_range.start)
+    samp = [i for i, e in enumerate(ev) if "sampler_kernel" in e.name]
+    out = {"decode": {}, "scoring": {}, "decode_steps": max(0, len(samp) - 1)}
+    if len(samp) < 2:
+        return out
+    lo, hi = samp[0], samp[-1]
+    prev_end = ev[lo].time_range.end
+    for e in ev[lo + 1:hi + 1]:
+        c = out["decode"].setdefault(kclass(e.name), {"us": 0.0, "resident_us": 0.0, "launches": 0})
+        c["us"] += max(0.0, e.time_range.end - prev_end)
+        c["resident_us"] += e.time_range.end - e.time_range.start
+        c["launches"] += 1
+        prev_end = max(prev_end, e.time_range.end)
+    out["decode_us"] = ev[hi].time_range.end - ev[lo].time_range.end
+    for e in ev[hi + 1:]:
+        c = out["scoring"].setdefault(kclass(e.name), {"us": 0.0, "launches": 0})
+        c["us"] += e.time_range.end - e.time_range.start
+        c["launches"] += 1
+    return out
+
+
+def decode_bytes(cfg_t, B):
+    """Algorithmic HBM bytes of one decode step averaged over the generation
+    (SURVEY.md §8d): bf16 weights of every layer + the tied LM head, plus the
+    KV cache read at the mean context P + (N-1)/2 (bf16 K and V)."""
+    V, d, L, H, f, S, _, P, N, _, _ = cfg_t
+    w_layers = 2.0 * L * (4 * d * d + 2 * d * f)
+    w_head = 2.0 * V * d
+    kv = 2.0 * B * L * 2 * d * (P + (N - 1) / 2.0)
+    act = 2.0 * B * L * (3 * d + d + f + f) * 2 + 4.0 * B * V  # operands in / out, fp32 logits
+    return {"gemm_decode": w_layers + w_head + act, "decode_attention": kv, "step": w_layers + w_head + kv,
+            "gemm_decode_launches": 4 * L + 1, "decode_attention_launches": L}
 
 
 def run_ours(args):
@@ -198,9 +305,9 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    V, d, L, H, f, S, B, P, N, samp, desc = CONFIGS[args.config]
-    if args.batch:
-        B = args.batch
+    cfg_t = CONFIGS[args.config]
+    V, d, L, H, f, S, Bc, P, N, samp, desc = cfg_t
+    B = per_rank_batch(args.config, args.batch or Bc, world)
     cfg = px.ModelConfig(V, d, L, H, f, S)
     ctx = px.Context(local)
     stream = torch.cuda.ExternalStream(ctx.stream, device=dev)
@@ -244,11 +351,6 @@ def run_ours(args):
         step(i)
         _dbg("warmup step", i)
     ctx.synchronize()
-    roof_cls = args.roofline_class
-    live_classes = ["logprob_gather", "gemm_tc"]  # launched eagerly: events here do not perturb the graphs
-    if args.profile_classes:
-        ctx.profile_filter(live_classes)
-        ctx.profile(True)
     launches0 = ctx.launch_count
     gen_ms, step_ms, tokens, seqs = [], [], 0, 0
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -271,24 +373,15 @@ def run_ours(args):
             _dbg("timed step", i)
     barrier()
     launches = ctx.launch_count - launches0
-    roof = None
-    prof = {}
-    live = {}
-    if args.profile_classes:
-        live = {k: ctx.profile_query(k) for k in live_classes}
-        # one extra, fully profiled step (outside the timed region) for the breakdown
-        ctx.profile_filter(None)
-        ctx.profile(True)
-        step(args.warmup + args.steps)
-        for cls in ("gemm_decode", "decode_attention", "gemm_tc", "gemm_simt", "logprob_gather", "sampler",
-                    "attention_prefill", "layernorm", "embed", "kv_scatter", "shape_gae", "convert", "meta"):
-            q = ctx.profile_query(cls)
-            if q["launches"]:
-                prof[cls] = q
-        ctx.profile(False)
-        ctx.profile_filter(None)
 
-    # max over ranks
+    # per-kernel breakdown of one extra step (outside the timed region), CUPTI
+    brk = None
+    if args.profile_classes:
+        try:
+            brk = cupti_breakdown(lambda: step(args.warmup + args.steps))
+        except Exception as e:  # profiler unavailable: the line just lacks the breakdown
+            _dbg("cupti failed", e)
+
     def gmax(x):
         if world == 1:
             return x
@@ -336,9 +429,12 @@ def run_ours(args):
 
     if rank == 0:
         pk = peaks()
+        hbm = pk.get("hbm_gbs", 6650.0)
+        steps_per_gen = N  # one decode unit per generated token (the first comes from the prefill logits)
         line = {"metric": "rollout_tokens_per_s", "value": value, "unit": "tokens/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_step_s * 1000 / args.steps,
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+                "higher_is_better": True, "scaling": "strong" if args.config in STRONG else "weak",
+                "vs_baseline": None, "dtype": "bf16",
                 "data": "synthetic prompts, random-init weights",
                 "config": workload_config(args, world, B),
                 "experience_samples_per_s": samples_per_s,
@@ -349,57 +445,57 @@ def run_ours(args):
             line["e2e"] = {"value": e2e_tok, "unit": "tokens/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                            "experience_samples_per_s": e2e_xp,
                            "api": "ppoexp_engine_generate / ppoexp_make_experience, HOST buffers"}
-        def rf(v, tensor):
-            if tensor:
-                ach, peak, unit = v["flops"] / v["ms"] / 1e9, pk.get("bf16_tflops_sustained", 1400.0), "TFLOP/s"
-            else:
-                ach, peak, unit = v["bytes"] / v["ms"] / 1e6, pk.get("hbm_gbs", 6650.0), "GB/s"
-            return {"bound": "tensor" if tensor else "hbm", "achieved": ach, "peak": peak, "unit": unit,
-                    "frac": ach / peak, "per_launch_ms": v["ms"] / v["launches"], "launches": v["launches"],
-                    "algorithmic_per_launch": (v["flops"] if tensor else v["bytes"]) / v["launches"]}
-        # measured DRAM traffic per launch of the roofline class, from the newest
-        # committed ncu launch list (profiles/<round>/traffic.json)
-        traffic, traffic_src = None, None
-        try:
-            import glob
-            tj = sorted(glob.glob(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "*",
-                                               "traffic.json")))
-            if tj:
-                tdoc = json.load(open(tj[-1]))
-                traffic = tdoc["bytes_per_launch"].get(roof_cls)
-                traffic_src = os.path.relpath(tj[-1], os.path.dirname(os.path.abspath(__file__)))
-        except Exception:
-            pass
-        if prof.get(roof_cls, {}).get("launches"):
-            line["roofline"] = {"kernel": roof_cls, **rf(prof[roof_cls], roof_cls in ("gemm_tc",)), "traffic": traffic,
-                                "traffic_source": traffic_src,
-                                "peak_source": "MEASURED_PEAKS.json" + (" (fallback)" if pk.get("fallback") else ""),
-                                "timing": "CUDA events on the library stream around every launch of this class, "
-                                          "one extra step of the same workload after the timed region (events inside "
-                                          "the decode CUDA graph break its PDL overlap, so the timed region carries "
-                                          "events only on eagerly launched classes: see roofline_live)"}
-        if live:
-            line["roofline_live"] = {k: rf(v, k in ("gemm_tc",)) for k, v in live.items() if v["launches"]}
-            line["roofline_live_note"] = ("per-launch CUDA events in the timed region; the reference and critic "
-                                          "scoring forwards run on two extra streams concurrently with the policy "
-                                          "forward, so these durations include overlap with the other streams")
-        if prof:
-            line["kernel_classes"] = {k: {"ms": v["ms"], "launches": v["launches"],
-                                          "GB_s": v["bytes"] / v["ms"] / 1e6 if v["ms"] else None,
-                                          "TF_s": v["flops"] / v["ms"] / 1e9 if v["ms"] else None}
-                                      for k, v in prof.items()}
-            line["kernel_classes_note"] = "one extra fully-profiled step after the timed region (events perturb PDL)"
-            line["roofline_by_kernel"] = {k: rf(prof[k], k in ("gemm_tc",)) for k in
-                                          ("logprob_gather", "decode_attention", "gemm_decode", "gemm_tc")
-                                          if k in prof and prof[k]["ms"]}
+        db = decode_bytes(cfg_t, B)
+        gen_step_s = total_gen_s / args.steps / steps_per_gen  # timed region: mean decode unit
+        line["decode_step_roofline"] = {
+            "bound": "hbm", "achieved": db["step"] / gen_step_s / 1e9, "peak": hbm, "unit": "GB/s",
+            "frac": db["step"] / gen_step_s / 1e9 / hbm, "us_per_step": gen_step_s * 1e6,
+            "algorithmic_bytes_per_step": db["step"],
+            "note": "timed region: generation device time / decode steps; bytes = bf16 weights (layers + tied LM "
+                    "head) + KV at the mean context (SURVEY.md §8d)"}
+        if brk and brk.get("decode"):
+            ns = max(1, brk["decode_steps"])
+            dec = brk["decode"]
+            line["kernel_classes"] = {
+                "decode_us_per_step": {k: v["us"] / ns for k, v in sorted(dec.items(), key=lambda x: -x[1]["us"])},
+                "decode_launches_per_step": {k: v["launches"] / ns for k, v in dec.items()},
+                "scoring_us": {k: v["us"] for k, v in sorted(brk["scoring"].items(), key=lambda x: -x[1]["us"])},
+                "source": "CUPTI (torch.profiler) over one extra experience step after the timed region; decode = "
+                          "critical-path time per step (sums to the step), scoring = kernel durations on 3 streams"}
+            g = dec.get("gemm_decode")
+            if g and g["us"] > 0:
+                per_launch_us = g["us"] / g["launches"]
+                bytes_per_launch = db["gemm_decode"] / db["gemm_decode_launches"]
+                ach = bytes_per_launch / per_launch_us / 1e3
+                traffic, traffic_src = None, None
+                try:
+                    import glob
+                    tj = sorted(glob.glob(os.path.join(ROOT, "profiles", "*", "traffic.json")))
+                    if tj:
+                        traffic = json.load(open(tj[-1]))["bytes_per_launch"].get("gemm_decode")
+                        traffic_src = os.path.relpath(tj[-1], ROOT)
+                except Exception:
+                    pass
+                line["roofline"] = {
+                    "kernel": "gemm_decode", "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
+                    "frac": ach / hbm, "traffic": traffic, "traffic_source": traffic_src,
+                    "per_launch_us": per_launch_us, "launches_per_step": g["launches"] / ns,
+                    "algorithmic_bytes_per_launch": bytes_per_launch,
+                    "share_of_decode_step": g["us"] / max(1e-9, brk["decode_us"]),
+                    "peak_source": "MEASURED_PEAKS.json" + (" (fallback)" if pk.get("fallback") else ""),
+                    "timing": "CUPTI in-graph critical-path time per launch (PDL overlap accounted), one extra step"}
+            a_ = dec.get("decode_attention")
+            if a_ and a_["us"] > 0:
+                ach = db["decode_attention"] / db["decode_attention_launches"] / (a_["us"] / a_["launches"]) / 1e3
+                line["roofline_decode_attention"] = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
+                                                     "frac": ach / hbm}
         if not args.no_cpu_baseline and world == 1:
             try:
-                threads = len(os.sched_getaffinity(0))
-                cpu_val, secs = reference_sample(CONFIGS[args.config], threads, args.ref_new_tokens, steps=1)
-                line["cpu_baseline"] = {"value": cpu_val, "unit": "tokens/s", "cores": threads, "kind": "reference",
-                                        "sample": f"{threads} seqs x {P}-token prompt x {args.ref_new_tokens} sampled "
-                                                  f"tokens, reference Engine::generate_batch n_workers={threads}, "
-                                                  f"{secs[0]:.1f} s"}
+                threads = host_threads()
+                r = reference_sample(cfg_t, threads, steps=1, B=B)
+                line["cpu_baseline"] = {"value": r["tokens_per_s"], "unit": "tokens/s", "cores": threads,
+                                        "kind": "reference", "sample": r["sample"],
+                                        "experience_samples_per_s": r["samples_per_s"]}
             except Exception as e:  # reference build absent
                 line["cpu_baseline"] = {"value": None, "unit": "tokens/s", "cores": 0, "kind": "reference",
                                         "sample": f"unavailable: {e}"}
@@ -433,19 +529,13 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--profile-classes", action="store_true", default=True)
     ap.add_argument("--no-profile", dest="profile_classes", action="store_false")
-    ap.add_argument("--roofline-class", default="gemm_decode")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--ref-new-tokens", type=int, default=8)
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
     else:
         run_ours(args)
-    # everything is torn down explicitly above; skip interpreter-exit
-    # destructors (torch / NCCL module teardown order is not ours to control)
     sys.stdout.flush()
-    sys.stderr.flush()
-    os._exit(0)
 
 
 if __name__ == "__main__":

@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define PPOEXP_ABI_VERSION 1
+#define PPOEXP_ABI_VERSION 2
 
 /* Only the C ABI is exported from libppoexp.so (built -fvisibility=hidden). */
 #if defined(__GNUC__)
@@ -59,14 +59,18 @@ typedef enum {
 typedef enum { PPOEXP_HOST = 0, PPOEXP_DEVICE = 1 } ppoexp_where;
 
 typedef enum {
-  PPOEXP_F32 = 0,  /* parity mode: fp32 weights / KV / activations, fp32 SIMT GEMMs */
-  PPOEXP_BF16 = 1, /* perf mode: bf16 weights / KV / GEMM operands, fp32 accumulate */
-  PPOEXP_F64 = 2   /* host weight views only */
+  PPOEXP_F32 = 0,   /* parity mode: fp32 weights / KV / activations, fp32 SIMT GEMMs */
+  PPOEXP_BF16 = 1,  /* perf mode: bf16 weights / KV / GEMM operands, fp32 accumulate */
+  PPOEXP_F64 = 2,   /* host weight views only */
+  PPOEXP_MIXED = 3  /* bf16 weights; fp32 activations and KV; tensor-core products on a two-term bf16
+                       split of every activation (hi = bf16(a), lo = bf16(a - hi)), fp32 accumulate:
+                       fp32-grade results on bf16-rounded weights */
 } ppoexp_dtype;
 
 typedef struct ppoexp_ctx_s* ppoexp_ctx;
 typedef struct ppoexp_model_s* ppoexp_model;
 typedef struct ppoexp_engine_s* ppoexp_engine;
+typedef struct ppoexp_comm_s* ppoexp_comm;
 
 /* ModelConfig, include/aligner/model.hpp:30-45 (LoRA is not on this path). */
 typedef struct {
@@ -140,6 +144,12 @@ PPOEXP_API ppoexp_status ppoexp_model_refit(ppoexp_model model, const ppoexp_ten
 PPOEXP_API ppoexp_status ppoexp_model_generation(ppoexp_model model, uint64_t* out);
 PPOEXP_API ppoexp_status ppoexp_model_config_get(ppoexp_model model, ppoexp_model_config* out);
 PPOEXP_API ppoexp_status ppoexp_model_destroy(ppoexp_model model);
+/* Engine::snapshot (include/aligner/engine.hpp:67): copies one parameter of
+ * the device snapshot back in the reference layout (row-major, projections
+ * [in, out]) into caller host memory of `dtype` (PPOEXP_F64 or PPOEXP_F32);
+ * numel must equal the parameter's element count (ShapeError otherwise). */
+PPOEXP_API ppoexp_status ppoexp_model_snapshot(ppoexp_model model, const char* name, void* out, int64_t numel,
+                                               int32_t dtype);
 
 /* -------------------------------------------------------------- engine */
 /* The TensorRT-LLM analog (Engine, include/aligner/engine.hpp:49-92) over a
@@ -154,6 +164,19 @@ typedef struct {
 
 PPOEXP_API ppoexp_status ppoexp_engine_create(ppoexp_model policy, const ppoexp_engine_options* opts, ppoexp_engine* out);
 PPOEXP_API ppoexp_status ppoexp_engine_destroy(ppoexp_engine engine);
+/* Engine::build_seconds / costs / options (include/aligner/engine.hpp:66-68).
+ * Cost categories (CostBook, include/aligner/timing.hpp:13-20): the engine
+ * books "response_generation" per generate call (src/engine.cpp:179) and
+ * "refit" per refit of its model (src/engine.cpp:86-89), in seconds. */
+PPOEXP_API ppoexp_status ppoexp_engine_build_seconds(ppoexp_engine engine, double* out);
+PPOEXP_API ppoexp_status ppoexp_engine_cost(ppoexp_engine engine, const char* category, double* seconds);
+PPOEXP_API ppoexp_status ppoexp_engine_options_get(ppoexp_engine engine, ppoexp_engine_options* out);
+
+/* balance (src/engine.cpp:14-31): longest-processing-time assignment of n
+ * tasks with costs[n] to n_workers (ranks): tasks by cost descending (index
+ * ascending on ties), each to the least-loaded worker (lowest index on ties).
+ * out_worker[i] = the worker of task i.  Host only. */
+PPOEXP_API ppoexp_status ppoexp_balance(const double* costs, int64_t n, int64_t n_workers, int64_t* out_worker);
 
 /* Engine::generate_batch (src/engine.cpp:148-182) / generate()
  * (src/model.cpp:438-482) for B tasks at once.
@@ -222,6 +245,20 @@ typedef struct {
   double lam;
 } ppoexp_ppo_hyper;
 
+/* ----------------------------------------------------------- collective */
+/* One NCCL communicator per rank (one process per GPU): rank 0 creates the
+ * 128-byte unique id, the caller ships it to every rank (any side channel),
+ * and every rank calls ppoexp_comm_create concurrently.  NCCL is loaded at
+ * run time (libnccl.so.2). */
+#define PPOEXP_COMM_ID_BYTES 128
+PPOEXP_API ppoexp_status ppoexp_comm_unique_id(uint8_t* out_id);
+PPOEXP_API ppoexp_status ppoexp_comm_create(ppoexp_ctx ctx, const uint8_t* id, int32_t rank, int32_t world,
+                                            ppoexp_comm* out);
+PPOEXP_API ppoexp_status ppoexp_comm_destroy(ppoexp_comm comm);
+/* buf[0..n) <- its sum over all ranks, accumulated in rank order (bit-identical
+ * on every rank): one ncclAllGather + a rank-order sum on the context stream. */
+PPOEXP_API ppoexp_status ppoexp_comm_allgather_sum(ppoexp_comm comm, double* buf, int64_t n, int32_t where);
+
 /* Collective hook for the whitening partials: called on the host with a
  * device pointer to `n` doubles that must be replaced in place by their sum
  * over all ranks (stream-ordered on `stream`).  NULL = single rank. */
@@ -240,7 +277,7 @@ typedef int32_t (*ppoexp_allreduce_fn)(double* device_buf, int64_t n, void* stre
  *   (5) whitening (north-star) through `allreduce`.
  * Outputs padded [B, max_new] (where = `where`), lengths[B], rewards[B];
  * stats[8] = {kl_sum, kl_count, reward_sum, n_seqs, adv_mean, adv_std,
- * gen_ms, total_ms}: the first six are GLOBAL (summed over ranks by the same
+ * gen_ms, total_ms} (timing[4] optionally the StepTiming split): the first six are GLOBAL (summed over ranks by the same
  * single collective that carries the whitening partials — the reference's
  * kl_mean / reward_mean, src/ppo.cpp:389-392, :438-441, are kl_sum/kl_count and
  * reward_sum/n_seqs); gen_ms / total_ms are this rank's device times.
@@ -261,6 +298,7 @@ typedef struct {
   ppoexp_ppo_hyper hyper;
   ppoexp_allreduce_fn allreduce;
   void* allreduce_user;
+  ppoexp_comm comm; /* non-NULL: the library's own NCCL all-gather (allreduce is then ignored) */
 } ppoexp_experience_request;
 
 typedef struct {
@@ -275,6 +313,10 @@ typedef struct {
   double* returns;
   double* whitened;
   double* stats;        /* [8] */
+  double* timing;       /* [4] (optional) StepTiming (include/aligner/ppo.hpp:27-37), ms of device time:
+                           {rollout, response_generation, logprob_calculation, critic_wait};
+                           critic_wait = how long the critic's values (and RM reward) ran past the
+                           actor/reference log-probs (they run concurrently on separate streams) */
 } ppoexp_rollout_batch;
 
 PPOEXP_API ppoexp_status ppoexp_make_experience(const ppoexp_experience_request* req, int64_t B, const int32_t* prompts,

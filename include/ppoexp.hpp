@@ -173,12 +173,32 @@ class DeviceModel {
     check(ppoexp_model_generation(h_, &g));
     return g;
   }
+  // Engine::snapshot (include/aligner/engine.hpp:67): one parameter in the reference layout
+  std::vector<double> snapshot(const std::string& name, std::size_t numel) const {
+    std::vector<double> out(numel);
+    check(ppoexp_model_snapshot(h_, name.c_str(), out.data(), int64_t(numel), PPOEXP_F64));
+    return out;
+  }
   const ModelConfig& config() const { return config_; }
   ppoexp_model handle() const { return h_; }
 
  private:
   ModelConfig config_;
   ppoexp_model h_ = nullptr;
+};
+
+// CostBook (include/aligner/timing.hpp:33-46): per-category seconds
+class CostBook {
+ public:
+  void add(const std::string& category, double seconds) { totals_[category] += seconds; }
+  double get(const std::string& category) const {
+    const auto it = totals_.find(category);
+    return it == totals_.end() ? 0.0 : it->second;
+  }
+  const std::map<std::string, double>& totals() const { return totals_; }
+
+ private:
+  std::map<std::string, double> totals_;
 };
 
 struct EngineOptions {
@@ -206,6 +226,26 @@ class Engine {
 
   void refit(const ModelParams& params) { model_->refit(params); }
   std::uint64_t generation_counter() const { return model_->generation_counter(); }
+  // include/aligner/engine.hpp:66-68
+  double build_seconds() const {
+    double s = 0;
+    check(ppoexp_engine_build_seconds(h_, &s));
+    return s;
+  }
+  CostBook costs() const {
+    CostBook b;
+    for (const char* cat : {"response_generation", "refit"}) {
+      double s = 0;
+      check(ppoexp_engine_cost(h_, cat, &s));
+      if (s > 0) b.add(cat, s);
+    }
+    return b;
+  }
+  EngineOptions options() const {
+    ppoexp_engine_options o{};
+    check(ppoexp_engine_options_get(h_, &o));
+    return {std::size_t(o.max_batch), std::size_t(o.page_size), std::size_t(o.max_total_tokens), o.use_graphs != 0};
+  }
   DeviceModel& model() { return *model_; }
   ppoexp_engine handle() const { return h_; }
 
@@ -241,6 +281,42 @@ class Engine {
  private:
   std::unique_ptr<DeviceModel> model_;
   ppoexp_engine h_ = nullptr;
+};
+
+// balance, src/engine.cpp:14-31 (LPT): task indices per worker (here: per rank)
+inline std::vector<std::vector<std::size_t>> balance(const std::vector<GenTask>& tasks, std::size_t n_workers) {
+  std::vector<double> costs;
+  for (const auto& t : tasks) costs.push_back(t.cost());
+  std::vector<int64_t> w(tasks.size());
+  check(ppoexp_balance(costs.data(), int64_t(costs.size()), int64_t(n_workers), w.data()));
+  std::vector<std::vector<std::size_t>> out(n_workers);
+  for (std::size_t i = 0; i < tasks.size(); ++i) out[std::size_t(w[i])].push_back(i);
+  return out;
+}
+
+// One NCCL communicator per rank (the experience step's single collective).
+class Communicator {
+ public:
+  static std::vector<uint8_t> unique_id() {
+    std::vector<uint8_t> id(PPOEXP_COMM_ID_BYTES);
+    check(ppoexp_comm_unique_id(id.data()));
+    return id;
+  }
+  Communicator(Context& ctx, const std::vector<uint8_t>& id, int rank, int world) {
+    check(ppoexp_comm_create(ctx.handle(), id.data(), rank, world, &h_));
+  }
+  ~Communicator() {
+    if (h_) ppoexp_comm_destroy(h_);
+  }
+  Communicator(const Communicator&) = delete;
+  Communicator& operator=(const Communicator&) = delete;
+  void allgather_sum(std::vector<double>& v) {
+    check(ppoexp_comm_allgather_sum(h_, v.data(), int64_t(v.size()), PPOEXP_HOST));
+  }
+  ppoexp_comm handle() const { return h_; }
+
+ private:
+  ppoexp_comm h_ = nullptr;
 };
 
 // sequence_logprobs, include/aligner/model.hpp:104 (one sequence; batch form below)
@@ -313,6 +389,15 @@ struct RolloutSeq {
 };
 using RolloutBatch = std::vector<RolloutSeq>;
 
+// include/aligner/ppo.hpp:27-37 (the experience-step slots; milliseconds)
+struct StepTiming {
+  std::size_t step = 0;
+  double rollout = 0.0;
+  double response_generation = 0.0;
+  double logprob_calculation = 0.0;
+  double critic_wait = 0.0;
+};
+
 struct PpoHyper {  // include/aligner/losses.hpp:39-50 (experience subset)
   double kl_penalty_coef = 0.003, gamma = 1.0, lam = 0.95;
 };
@@ -324,10 +409,14 @@ class ExperienceMaker {
                   int32_t scripted_target = 'z', PpoHyper hyper = {})
       : policy_(policy), reference_(reference), critic_(critic), rm_(rm), target_(scripted_target), hyper_(hyper) {}
 
-  // allreduce: NULL for one rank (see ppoexp_allreduce_fn)
+  // The library's own NCCL collective for multi-rank runs (else a callback, or one rank).
+  void set_comm(Communicator* comm) { comm_ = comm; }
+
+  // allreduce: NULL for one rank (see ppoexp_allreduce_fn); ignored when a Communicator is set
   RolloutBatch run(const std::vector<TokenSeq>& prompts, std::size_t max_new, const SamplingSpec& sampling,
                    std::uint64_t seed, std::int64_t step_index, std::int64_t gidx0 = 0,
-                   ppoexp_allreduce_fn allreduce = nullptr, void* user = nullptr, double* stats8 = nullptr) {
+                   ppoexp_allreduce_fn allreduce = nullptr, void* user = nullptr, double* stats8 = nullptr,
+                   StepTiming* timing = nullptr) {
     auto [flat, off] = detail::ragged(prompts);
     const int64_t B = int64_t(prompts.size()), N = int64_t(max_new);
     ppoexp_experience_request q{};
@@ -343,15 +432,23 @@ class ExperienceMaker {
     q.hyper = {hyper_.kl_penalty_coef, hyper_.gamma, hyper_.lam};
     q.allreduce = allreduce;
     q.allreduce_user = user;
+    q.comm = comm_ ? comm_->handle() : nullptr;
     q.policy_engine = policy_.handle();
     std::vector<int32_t> toks(B * N);
     std::vector<int64_t> lens(B);
     std::vector<double> a(B * N), r(B * N), v(B * N), rw(B), sh(B * N), adv(B * N), ret(B * N), wh(B * N),
-        st(8);
+        st(8), tm(4);
     ppoexp_rollout_batch o{toks.data(), lens.data(), a.data(), r.data(), v.data(), rw.data(), sh.data(),
-                           adv.data(), ret.data(), wh.data(), st.data()};
+                           adv.data(), ret.data(), wh.data(), st.data(), tm.data()};
     check(ppoexp_make_experience(&q, B, flat.data(), off.data(), &o, PPOEXP_HOST));
     if (stats8) std::copy(st.begin(), st.end(), stats8);
+    if (timing) {
+      timing->step = std::size_t(step_index);
+      timing->rollout = tm[0];
+      timing->response_generation = tm[1];
+      timing->logprob_calculation = tm[2];
+      timing->critic_wait = tm[3];
+    }
     RolloutBatch batch(B);
     for (int64_t b = 0; b < B; ++b) {
       auto& s = batch[b];
@@ -380,6 +477,7 @@ class ExperienceMaker {
   DeviceModel* rm_;
   int32_t target_;
   PpoHyper hyper_;
+  Communicator* comm_ = nullptr;
 };
 
 }  // namespace ppoexp

@@ -18,6 +18,21 @@ PPOEXP_API ppoexp_status ppoexp_testing_gemm_bf16(ppoexp_ctx ctx, const void* A,
                                        int64_t M, int64_t N, int64_t K, int32_t epi, void* C, int64_t ldc,
                                        int32_t path);
 
+/* Mixed-mode GEMM: C[M,N] (+)= A[M,K] (fp32) · W[N,K]^T (bf16), activations
+ * split into two bf16 terms in-kernel.  epi: 2 fp32 residual add, 3 store fp32,
+ * 5 GELU -> fp32.  M <= 256 takes the decode (swap-AB, cluster split-K) kernel. */
+PPOEXP_API ppoexp_status ppoexp_testing_gemm_mixed(ppoexp_ctx ctx, const void* A, int64_t lda, const void* W, int64_t ldw,
+                                        int64_t M, int64_t N, int64_t K, int32_t epi, void* C, int64_t ldc);
+
+/* lp[r] = log_softmax(H[r] · W^T)[target[r]] on device pointers: H [R, K] bf16,
+ * W [V, K] bf16 (the tied LM head), out[R] double.
+ * path: 0 = fused tcgen05 LM head + online LSE + gather (Epi::kLse) + combine,
+ *       1 = fp32 logits (tcgen05 GEMM) + K9 log-softmax/gather,
+ *       2 = K9 only over caller fp32 logits (H = logits [R, ldl] fp32, W unused). */
+PPOEXP_API ppoexp_status ppoexp_testing_lm_head_logprobs(ppoexp_ctx ctx, const void* H, const void* W, int64_t R,
+                                              int64_t V, int64_t K, int64_t ldl, const int32_t* target,
+                                              double* out, int32_t path);
+
 #ifdef __cplusplus
 }
 #endif

@@ -46,7 +46,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < max(os.path.getmtime(o) for o in objs):
         tmp = LIB + ".tmp"
         cmd = [NVCC, *ARCH, "-shared", "-Wno-deprecated-gpu-targets", *objs, "-o", tmp, "-lcudart_static",
-               "-Xlinker", "--exclude-libs,ALL"]
+               "-Xlinker", "--exclude-libs,ALL", "-Xlinker", "--no-undefined", "-ldl", "-lrt", "-lpthread"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")

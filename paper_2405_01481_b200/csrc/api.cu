@@ -9,6 +9,10 @@
 #include <vector>
 
 #include "../../include/ppoexp_testing.h"
+#include <chrono>
+#include <numeric>
+
+#include "comm.hpp"
 #include "engine.hpp"
 
 using namespace ppx;
@@ -21,6 +25,9 @@ struct ppoexp_model_s {
 };
 struct ppoexp_engine_s {
   std::unique_ptr<Engine> e;
+};
+struct ppoexp_comm_s {
+  std::unique_ptr<Comm> c;
 };
 
 namespace {
@@ -255,7 +262,8 @@ ppoexp_status ppoexp_model_create(ppoexp_ctx ctx, const ppoexp_model_config* cfg
     if (dh != 16 && dh != 32 && dh != 64 && dh != 128)
       throw ContractError("model config: head_dim " + std::to_string(dh) + " unsupported (16/32/64/128)");
     if (cfg->d_model % 8 || cfg->d_ff % 8) throw ContractError("model config: d_model and d_ff must be multiples of 8");
-    if (dtype != PPOEXP_F32 && dtype != PPOEXP_BF16) throw ContractError("compute dtype must be F32 or BF16");
+    if (dtype != PPOEXP_F32 && dtype != PPOEXP_BF16 && dtype != PPOEXP_MIXED)
+      throw ContractError("compute dtype must be F32, BF16 or MIXED");
     Ctx& c = *ctx->c;
     std::lock_guard<std::recursive_mutex> lk(c.mu);
     DeviceGuard g(c.device);
@@ -263,8 +271,10 @@ ppoexp_status ppoexp_model_create(ppoexp_ctx ctx, const ppoexp_model_config* cfg
     h->m.ctx = &c;
     h->m.cfg = *cfg;
     h->m.dtype = dtype;
+    const auto t0 = std::chrono::steady_clock::now();
     h->m.allocate();
     h->m.load(params, n, false);
+    h->m.build_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     *out = h.release();
   });
 }
@@ -288,6 +298,7 @@ ppoexp_status ppoexp_model_refit(ppoexp_model model, const ppoexp_tensor_view* p
     cudaEventDestroy(b);
     c.stats["refit"].ms += ms;  // CostBook "refit" category, include/aligner/timing.hpp:18
     c.stats["refit"].launches += 1;
+    model->m.refit_seconds += ms / 1000.0;
     ++model->m.generation;
   });
 }
@@ -303,6 +314,17 @@ ppoexp_status ppoexp_model_config_get(ppoexp_model model, ppoexp_model_config* o
   return guard([&] {
     need(model, "model");
     *out = model->m.cfg;
+  });
+}
+
+ppoexp_status ppoexp_model_snapshot(ppoexp_model model, const char* name, void* out, int64_t numel, int32_t dtype) {
+  return guard([&] {
+    need(model, "model");
+    need(name, "name");
+    need(out, "out");
+    std::lock_guard<std::recursive_mutex> lk(model->m.ctx->mu);
+    DeviceGuard g(model->m.ctx->device);
+    model->m.snapshot(name, out, numel, dtype);
   });
 }
 
@@ -323,7 +345,10 @@ ppoexp_status ppoexp_engine_create(ppoexp_model policy, const ppoexp_engine_opti
     need(out, "out");
     std::lock_guard<std::recursive_mutex> lk(policy->m.ctx->mu);
     auto h = std::make_unique<ppoexp_engine_s>();
+    const auto t0 = std::chrono::steady_clock::now();
     h->e = std::make_unique<Engine>(&policy->m, opts);
+    h->e->build_seconds =
+        policy->m.build_seconds + std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     *out = h.release();
   });
 }
@@ -333,6 +358,99 @@ ppoexp_status ppoexp_engine_destroy(ppoexp_engine engine) {
     if (!engine) return;
     std::lock_guard<std::recursive_mutex> lk(engine->e->c->mu);
     delete engine;
+  });
+}
+
+ppoexp_status ppoexp_engine_build_seconds(ppoexp_engine engine, double* out) {
+  return guard([&] {
+    need(engine, "engine");
+    need(out, "out");
+    *out = engine->e->build_seconds;
+  });
+}
+
+ppoexp_status ppoexp_engine_cost(ppoexp_engine engine, const char* category, double* seconds) {
+  return guard([&] {
+    need(engine, "engine");
+    need(category, "category");
+    need(seconds, "seconds");
+    const std::string cat = category;
+    // CostBook::get returns 0 for categories never booked (include/aligner/timing.hpp:37-40)
+    *seconds = cat == "response_generation" ? engine->e->gen_seconds
+               : cat == "refit"             ? engine->e->m->refit_seconds
+                                            : 0.0;
+  });
+}
+
+ppoexp_status ppoexp_engine_options_get(ppoexp_engine engine, ppoexp_engine_options* out) {
+  return guard([&] {
+    need(engine, "engine");
+    need(out, "out");
+    *out = engine->e->opts;
+  });
+}
+
+ppoexp_status ppoexp_balance(const double* costs, int64_t n, int64_t n_workers, int64_t* out_worker) {
+  return guard([&] {
+    if (n_workers <= 0) throw ContractError("balance: n_workers must be positive");
+    if (n <= 0) return;
+    need(costs, "costs");
+    need(out_worker, "out_worker");
+    // src/engine.cpp:14-31: stable sort by cost descending, least-loaded worker, lowest index on ties
+    std::vector<int64_t> order(n);
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) { return costs[a] > costs[b]; });
+    std::vector<double> load(n_workers, 0.0);
+    for (int64_t i : order) {
+      int64_t w = 0;
+      for (int64_t k = 1; k < n_workers; ++k)
+        if (load[k] < load[w]) w = k;
+      load[w] += costs[i];
+      out_worker[i] = w;
+    }
+  });
+}
+
+ppoexp_status ppoexp_comm_unique_id(uint8_t* out_id) {
+  return guard([&] {
+    need(out_id, "out_id");
+    comm_unique_id(out_id);
+  });
+}
+
+ppoexp_status ppoexp_comm_create(ppoexp_ctx ctx, const uint8_t* id, int32_t rank, int32_t world, ppoexp_comm* out) {
+  return guard([&] {
+    need(ctx, "ctx");
+    need(id, "id");
+    need(out, "out");
+    auto h = std::make_unique<ppoexp_comm_s>();
+    h->c = std::make_unique<Comm>(ctx->c.get(), id, rank, world);
+    *out = h.release();
+  });
+}
+
+ppoexp_status ppoexp_comm_destroy(ppoexp_comm comm) {
+  return guard([&] { delete comm; });
+}
+
+ppoexp_status ppoexp_comm_allgather_sum(ppoexp_comm comm, double* buf, int64_t n, int32_t where) {
+  return guard([&] {
+    need(comm, "comm");
+    if (n <= 0) return;
+    need(buf, "buf");
+    Ctx& c = *comm->c->ctx;
+    std::lock_guard<std::recursive_mutex> lk(c.mu);
+    DeviceGuard g(c.device);
+    double* d = buf;
+    if (where == PPOEXP_HOST) {
+      d = static_cast<double*>(c.workspace("comm.host", n * 8));
+      copy_in(c, d, buf, n * 8, PPOEXP_HOST);
+    }
+    comm->c->allgather_sum(d, n);
+    if (where == PPOEXP_HOST) {
+      copy_out(c, buf, d, n * 8, PPOEXP_HOST);
+      c.sync();
+    }
   });
 }
 
@@ -639,7 +757,9 @@ ppoexp_status ppoexp_make_experience(const ppoexp_experience_request* req, int64
     Ctx& c = *pol.ctx;
     std::lock_guard<std::recursive_mutex> lk(c.mu);
     DeviceGuard g(c.device);
-    cudaEvent_t ev[3];
+    // ev: 0 start, 1 whitened, 2 outputs copied; 3 generation done, 4 policy
+    // lp, 5 reference lp, 6 critic values (+ RM reward) — StepTiming
+    cudaEvent_t ev[7];
     for (auto& e : ev) PPOEXP_CUDA(cudaEventCreate(&e));
     PPOEXP_CUDA(cudaEventRecord(ev[0], c.stream));
 
@@ -703,6 +823,7 @@ ppoexp_status ppoexp_make_experience(const ppoexp_experience_request* req, int64
     PPOEXP_CUDA(cudaMemsetAsync(alp, 0, nBN * 8, c.stream));
     PPOEXP_CUDA(cudaMemsetAsync(rlp, 0, nBN * 8, c.stream));
     PPOEXP_CUDA(cudaMemsetAsync(val, 0, nBN * 8, c.stream));
+    PPOEXP_CUDA(cudaEventRecord(ev[3], c.stream));
     // The policy, reference and critic forwards read the same packed tokens and
     // write disjoint outputs: the reference and critic run on two auxiliary
     // streams (own workspaces) concurrently with the policy on the main stream,
@@ -741,14 +862,17 @@ ppoexp_status ppoexp_make_experience(const ppoexp_experience_request* req, int64
     on_aux(0, "ref/", [&] {
       float* x = forward_layers(ref, pk, nullptr);
       score_logprobs(ref, pk, x, gather, target, oidx, R, rlp);
+      PPOEXP_CUDA(cudaEventRecord(ev[5], c.stream));
     });
     on_aux(1, "crit/", [&] {
       float* x = forward_layers(cr, pk, nullptr);
       score_head(cr, x, gather, oidx, R, val);
+      PPOEXP_CUDA(cudaEventRecord(ev[6], c.stream));
     });
     {
       float* x = forward_layers(pol, pk, nullptr);
       score_logprobs(pol, pk, x, gather, target, oidx, R, alp);
+      PPOEXP_CUDA(cudaEventRecord(ev[4], c.stream));
     }
     // (4) rewards then values (CriticJob::handle_infer, src/ppo.cpp:164-193)
     double* rew = static_cast<double*>(c.workspace("xp.rew", B * 8));
@@ -760,6 +884,7 @@ ppoexp_status ppoexp_make_experience(const ppoexp_experience_request* req, int64
       });
       float* x = forward_layers(*rm, pk, nullptr);
       score_head(*rm, x, lg, lo, B, rew);
+      PPOEXP_CUDA(cudaEventRecord(ev[6], c.stream));  // the RM pass precedes the critic's (src/ppo.cpp:175-188)
     } else {
       launch_scripted_reward(c, B, N, gtok, glen, req->scripted_target, rew);
     }
@@ -796,7 +921,10 @@ ppoexp_status ppoexp_make_experience(const ppoexp_experience_request* req, int64
       PPOEXP_CUDA(cudaMemcpyAsync(coll + 5, tmp, 8, cudaMemcpyHostToDevice, c.stream));
       PPOEXP_CUDA(cudaStreamSynchronize(c.stream));
     }
-    if (req->allreduce) {
+    if (req->comm) {
+      if (req->comm->c->ctx != &c) throw ContractError("ppo_step: comm belongs to another context");
+      req->comm->c->allgather_sum(coll, 6);
+    } else if (req->allreduce) {
       const int32_t rc = req->allreduce(coll, 6, c.stream, req->allreduce_user);
       if (rc) throw PpoError("ppo_step: whitening allreduce failed (" + std::to_string(rc) + ")");
     }
@@ -823,6 +951,21 @@ ppoexp_status ppoexp_make_experience(const ppoexp_experience_request* req, int64
     PPOEXP_CUDA(cudaEventSynchronize(ev[2]));
     float total_ms = 0;
     PPOEXP_CUDA(cudaEventElapsedTime(&total_ms, ev[0], ev[2]));
+    if (out->timing) {
+      // StepTiming (include/aligner/ppo.hpp:27-37): rollout, response_generation,
+      // logprob_calculation (actor + reference, after generation), critic_wait
+      auto since = [&](int i) {
+        float ms = 0;
+        PPOEXP_CUDA(cudaEventElapsedTime(&ms, ev[0], ev[i]));
+        return double(ms);
+      };
+      const double t_gen = since(3), t_lp = std::max(since(4), since(5)), t_cr = since(6);
+      const double tm[4] = {double(total_ms), gen_ms, t_lp - t_gen, std::max(0.0, t_cr - t_lp)};
+      if (where == PPOEXP_HOST)
+        std::memcpy(out->timing, tm, sizeof tm);
+      else
+        PPOEXP_CUDA(cudaMemcpy(out->timing, tm, sizeof tm, cudaMemcpyHostToDevice));
+    }
     for (auto& e : ev) cudaEventDestroy(e);
     const double cnt = coll_h[0] > 0 ? coll_h[0] : 1.0;
     const double mean = coll_h[1] / cnt;
@@ -870,6 +1013,58 @@ extern "C" ppoexp_status ppoexp_testing_gemm_bf16(ppoexp_ctx ctx, const void* A,
       launch_gemm_simt<bf16>(c, a, lda, b, ldb, M, N, K, static_cast<Epi>(epi), C, ldc);
     else
       gemm<bf16>(c, a, lda, b, ldb, M, N, K, static_cast<Epi>(epi), C, ldc);
+    c.sync();
+  });
+}
+
+extern "C" ppoexp_status ppoexp_testing_lm_head_logprobs(ppoexp_ctx ctx, const void* H, const void* W, int64_t R,
+                                                         int64_t V, int64_t K, int64_t ldl, const int32_t* target,
+                                                         double* out, int32_t path) {
+  return guard([&] {
+    need(ctx, "ctx");
+    Ctx& c = *ctx->c;
+    std::lock_guard<std::recursive_mutex> lk(c.mu);
+    DeviceGuard g(c.device);
+    if (R <= 0) return;
+    int64_t* oidx = static_cast<int64_t*>(c.workspace("t.oidx", R * 8));
+    std::vector<int64_t> iota(R);
+    for (int64_t i = 0; i < R; ++i) iota[i] = i;
+    copy_in(c, oidx, iota.data(), R * 8, PPOEXP_HOST);
+    c.sync();
+    const auto* h = static_cast<const bf16*>(H);
+    const auto* w = static_cast<const bf16*>(W);
+    if (path == 0) {
+      const int nt = lse_tiles(V), ldp = (nt + 1) / 2 * 2;
+      LseEpi e;
+      e.target = target;
+      e.tgt_logit = static_cast<float*>(c.workspace("t.tgt", R * 4));
+      e.part = static_cast<float2*>(c.workspace("t.part", R * ldp * 8));
+      e.ldp = ldp;
+      if (!gemm_tc_lse(c, h, K, w, K, R, V, K, e)) throw ContractError("lm_head: shape not eligible");
+      launch_lse_combine(c, e.part, ldp, nt, e.tgt_logit, target, R, oidx, out);
+    } else if (path == 1) {
+      const int64_t ld = (V + 63) / 64 * 64;
+      float* lg = static_cast<float*>(c.workspace("t.logits", R * ld * 4));
+      gemm<bf16>(c, h, K, w, K, R, V, K, Epi::kStoreF32, lg, ld);
+      launch_logprob_gather<float>(c, lg, ld, R, V, target, oidx, out);
+    } else {
+      launch_logprob_gather<float>(c, static_cast<const float*>(H), ldl, R, V, target, oidx, out);
+    }
+    c.sync();
+  });
+}
+
+extern "C" ppoexp_status ppoexp_testing_gemm_mixed(ppoexp_ctx ctx, const void* A, int64_t lda, const void* W,
+                                                   int64_t ldw, int64_t M, int64_t N, int64_t K, int32_t epi, void* C,
+                                                   int64_t ldc) {
+  return guard([&] {
+    need(ctx, "ctx");
+    Ctx& c = *ctx->c;
+    std::lock_guard<std::recursive_mutex> lk(c.mu);
+    DeviceGuard g(c.device);
+    if (epi != 2 && epi != 3 && epi != 5) throw ContractError("epi must be 2, 3 or 5");
+    gemm_mixed(c, static_cast<const float*>(A), lda, static_cast<const bf16*>(W), ldw, M, N, K, static_cast<Epi>(epi), C,
+               ldc);
     c.sync();
   });
 }

@@ -38,7 +38,9 @@ Engine::Engine(Model* model, const ppoexp_engine_options* o) : m(model), c(model
   geom.max_pages_per_seq = ceil_div(S, opts.page_size);
   geom.n_pages = std::max<int64_t>(ceil_div(opts.max_total_tokens, opts.page_size), geom.max_pages_per_seq);
   DeviceGuard g(c->device);
-  const size_t ts = m->tsize();
+  if (m->mixed() && opts.max_batch > 256)
+    throw ContractError("engine: mixed mode decodes at most 256 sequences per step (max_batch <= 256)");
+  const size_t ts = m->asize();  // activation / KV element
   kv.ensure(size_t(geom.n_layers) * geom.n_pages * 2 * geom.H * geom.page_size * geom.DH * ts);
   const int64_t mb = opts.max_batch, d = cfg.d_model, f = cfg.d_ff;
   auto al = [](size_t x) { return (x + 255) / 256 * 256; };
@@ -65,6 +67,7 @@ Engine::Engine(Model* model, const ppoexp_engine_options* o) : m(model), c(model
   const size_t o_sta = sbytes; sbytes += al((2 * cfg.n_layers + 1) * mb * kStatStride * 8);
   const size_t o_part = sbytes; sbytes += al(decode_mega_part_bytes());
   const size_t o_bar = sbytes; sbytes += al(16);  // 2 x u64 grid-barrier counter / base
+  const size_t o_ovf = sbytes; sbytes += al(16);
   const size_t o_mly = sbytes; sbytes += al(cfg.n_layers * sizeof(MegaLayer));
   const size_t o_wmap = sbytes; sbytes += al(cfg.n_layers * 4 * sizeof(CUtensorMap));
   state.ensure(sbytes);
@@ -91,6 +94,7 @@ Engine::Engine(Model* model, const ppoexp_engine_options* o) : m(model), c(model
   stats = reinterpret_cast<unsigned long long*>(p + o_sta);
   part = reinterpret_cast<float*>(p + o_part);
   bar = reinterpret_cast<unsigned*>(p + o_bar);
+  stat_ovf = reinterpret_cast<unsigned*>(p + o_ovf);
   mega_layers = reinterpret_cast<MegaLayer*>(p + o_mly);
   mega_wmaps = reinterpret_cast<CUtensorMap*>(p + o_wmap);
   {
@@ -123,6 +127,7 @@ Engine::Engine(Model* model, const ppoexp_engine_options* o) : m(model), c(model
     // re-normalise 4x more rows and it measured 18% slower
     const char* ev = getenv("PPOEXP_FUSE_LN");
     fuse_ln = m->dtype == PPOEXP_BF16 && !(ev && ev[0] == '0') && !use_mega && mb <= 256 && d % 8 == 0;
+    if (m->mixed() && d % 8) throw ContractError("engine: mixed mode needs d_model % 8 == 0");
     fuse_ln_max_b = ev && ev[0] == '1' ? 256 : 64;
   }
   PPOEXP_CUDA(cudaMallocHost(&host_flags, 64));
@@ -227,7 +232,7 @@ void Engine::decode_unit(int64_t B, int64_t unit) {
       // slice on the fly (no standalone LayerNorm launches)
       const int64_t L = m->cfg.n_layers, mb = opts.max_batch;
       auto st = [&](int64_t i) { return stats + i * mb * kStatStride; };  // i = 2l (LN1), 2l+1 (LN2)
-      RowStats s0{st(0)};
+      RowStats s0{st(0), stat_ovf};
       s0.zero = st(1);
       s0.zero_n = (2 * L - 1) * mb;
       launch_embed_stats<T>(cc, next_tok, pos, B, d, static_cast<const T*>(m->tok), static_cast<const T*>(m->pos), x,
@@ -238,11 +243,11 @@ void Engine::decode_unit(int64_t B, int64_t unit) {
         gemm_decode_fused(cc, nullptr, d, static_cast<const T*>(ly.wqkv), d, B, 3 * d, d, Epi::kStore, q3, 3 * d, &l1,
                           nullptr);
         launch_attention_decode<T>(cc, q3, B, pos, done, block_table, int(l), geom, static_cast<T*>(kv.ptr), at, 0.0);
-        const RowStats so2{st(2 * l + 1)};
+        const RowStats so2{st(2 * l + 1), stat_ovf};
         gemm_decode_fused(cc, at, d, static_cast<const T*>(ly.wo), d, B, d, d, Epi::kAddResidual, x, d, nullptr, &so2);
         const LnIn l2{x, d, st(2 * l + 1), ly.ln2w, ly.ln2b, int(d)};
         gemm_decode_fused(cc, nullptr, d, static_cast<const T*>(ly.wup), d, B, f, d, Epi::kGelu, uu, f, &l2, nullptr);
-        const RowStats so1{st(2 * l + 2)};  // the last layer's down-proj feeds the standalone final LN
+        const RowStats so1{st(2 * l + 2), stat_ovf};  // the last layer's down-proj feeds the standalone final LN
         gemm_decode_fused(cc, uu, f, static_cast<const T*>(ly.wdown), f, B, d, f, Epi::kAddResidual, x, d, nullptr,
                           l + 1 < L ? &so1 : nullptr);
       }
@@ -275,8 +280,49 @@ void Engine::decode_unit(int64_t B, int64_t unit) {
   launch_sampler(cc, logits, m->vpad, B, V, sampler_state());
 }
 
+// Mixed mode (bf16 weights, fp32 activations / KV): every projection runs on
+// the split-activation decode GEMM (LayerNorm fused into QKV / up as in the
+// bf16 path, fixed-point row statistics from the residual producers), fp32
+// decode attention over the fp32 paged KV.
+void Engine::decode_unit_mixed(int64_t B, int64_t unit) {
+  Ctx& cc = *c;
+  const int64_t d = m->d(), f = m->cfg.d_ff, V = m->cfg.vocab_size, L = m->cfg.n_layers, mb = opts.max_batch;
+  float* q3 = static_cast<float*>(qkv);
+  float* at = static_cast<float*>(att);
+  float* uu = static_cast<float*>(up);
+  float* hh = static_cast<float*>(h);
+  cur_unit = unit;
+  auto st = [&](int64_t i) { return stats + i * mb * kStatStride; };
+  RowStats s0{st(0), stat_ovf};
+  s0.zero = st(1);
+  s0.zero_n = (2 * L - 1) * mb;
+  launch_embed_stats<bf16>(cc, next_tok, pos, B, d, static_cast<const bf16*>(m->tok), static_cast<const bf16*>(m->pos),
+                           x, s0);
+  for (int64_t l = 0; l < L; ++l) {
+    const Layer& ly = m->layers[l];
+    const LnIn l1{x, d, st(2 * l), ly.ln1w, ly.ln1b, int(d)};
+    gemm_decode_mixed(cc, nullptr, d, static_cast<const bf16*>(ly.wqkv), d, B, 3 * d, d, Epi::kStoreF32, q3, 3 * d,
+                      &l1, nullptr);
+    launch_attention_decode<float>(cc, q3, B, pos, done, block_table, int(l), geom, static_cast<float*>(kv.ptr), at,
+                                   0.0);
+    const RowStats so2{st(2 * l + 1), stat_ovf};
+    gemm_decode_mixed(cc, at, d, static_cast<const bf16*>(ly.wo), d, B, d, d, Epi::kAddResidual, x, d, nullptr, &so2);
+    const LnIn l2{x, d, st(2 * l + 1), ly.ln2w, ly.ln2b, int(d)};
+    gemm_decode_mixed(cc, nullptr, d, static_cast<const bf16*>(ly.wup), d, B, f, d, Epi::kGeluF32, uu, f, &l2, nullptr);
+    const RowStats so1{st(2 * l + 2), stat_ovf};
+    gemm_decode_mixed(cc, uu, f, static_cast<const bf16*>(ly.wdown), f, B, d, f, Epi::kAddResidual, x, d, nullptr,
+                      l + 1 < L ? &so1 : nullptr);
+  }
+  launch_layernorm<float>(cc, x, B, d, m->lnfw, m->lnfb, hh, nullptr, nullptr, nullptr);
+  gemm_decode_mixed(cc, hh, d, static_cast<const bf16*>(m->tok), d, B, V, d, Epi::kStoreF32, logits, m->vpad, nullptr,
+                    nullptr);
+  launch_sampler(cc, logits, m->vpad, B, V, sampler_state());
+}
+
 void Engine::run_unit(int64_t B, int64_t unit) {
-  if (m->dtype == PPOEXP_F32)
+  if (m->mixed())
+    decode_unit_mixed(B, unit);
+  else if (m->dtype == PPOEXP_F32)
     decode_unit<float>(B, unit);
   else
     decode_unit<bf16>(B, unit);
@@ -335,7 +381,7 @@ Engine::GraphSet& Engine::graph_for(int64_t B) {
 void Engine::harvest_replay(const std::vector<TimedLaunch>& evs, int64_t unit0, int units) {
   if (!c->profiling) return;
   const int64_t d = m->d();
-  const double ts = double(m->tsize());
+  const double ts = double(m->asize());
   int64_t per_unit = 0;
   for (auto& t : evs)
     if (t.cls == "decode_attention") ++per_unit;
@@ -409,6 +455,7 @@ void Engine::generate(int64_t B, const int32_t* prompts, const int64_t* offsets,
   float ms = 0;
   PPOEXP_CUDA(cudaEventElapsedTime(&ms, e0, e1));
   last_ms = ms;
+  gen_seconds += ms / 1000.0;
   if (ms_out) *ms_out = ms;
   if (const char* gp = getenv("PPOEXP_GEMM_TRACE")) dump_gemm_trace(*c, gp);
   if (const char* ap = getenv("PPOEXP_ATTN_TRACE")) {  // debug: last decode-attention launch, CTA (0, 0)
@@ -526,7 +573,11 @@ void Engine::run_chunk(int64_t B, const int32_t* prompts, const std::vector<int6
   // prefill → last-position logits → first sample
   KvTarget kt{block_table, geom, kv.ptr};
   float* xr = forward_layers(*m, pk, &kt);
-  if (m->dtype == PPOEXP_F32) {
+  if (m->mixed()) {
+    launch_layernorm<float>(cc, xr, B, d, m->lnfw, m->lnfb, static_cast<float*>(h), last_rows, nullptr, nullptr);
+    gemm_mixed(cc, static_cast<float*>(h), d, static_cast<const bf16*>(m->tok), d, B, cfg.vocab_size, d,
+               Epi::kStoreF32, logits, m->vpad);
+  } else if (m->dtype == PPOEXP_F32) {
     launch_layernorm<float>(cc, xr, B, d, m->lnfw, m->lnfb, static_cast<float*>(h), last_rows, nullptr, nullptr);
     gemm<float>(cc, static_cast<float*>(h), d, static_cast<const float*>(m->tok), d, B, cfg.vocab_size, d,
                 Epi::kStoreF32, logits, m->vpad);
@@ -587,7 +638,14 @@ void Engine::run_chunk(int64_t B, const int32_t* prompts, const std::vector<int6
   // outputs
   std::vector<int32_t> ng(B);
   PPOEXP_CUDA(cudaMemcpyAsync(ng.data(), n_gen, B * 4, cudaMemcpyDeviceToHost, cc.stream));
+  PPOEXP_CUDA(cudaMemcpyAsync(host_flags + 8, stat_ovf, 4, cudaMemcpyDeviceToHost, cc.stream));
   PPOEXP_CUDA(cudaStreamSynchronize(cc.stream));
+  if (host_flags[8]) {
+    PPOEXP_CUDA(cudaMemsetAsync(stat_ovf, 0, 4, cc.stream));
+    throw ContractError(
+        "engine: residual stream outside the fused-LayerNorm statistics range (|x| rms > ~2e4); rerun with "
+        "PPOEXP_FUSE_LN=0");
+  }
   for (int64_t b = 0; b < B; ++b) {
     cur_len[b] = ng[b];
     last_lengths[b0 + b] = ng[b];
@@ -627,7 +685,7 @@ void Engine::snapshot_events(ReplayTimes& r) {
 
 void Engine::harvest_snapshot(const ReplayTimes& r) {
   const int64_t d = m->d();
-  const double ts = double(m->tsize());
+  const double ts = double(m->asize());
   int64_t per_unit = 0;
   for (auto& t : r.events)
     if (t.cls == "decode_attention") ++per_unit;

@@ -26,6 +26,7 @@ struct Engine {
   double* uniforms;
   int32_t* host_flags = nullptr;
   unsigned long long* stats = nullptr;  // fused-LN fixed-point row statistics [2L+1][max_batch][2]
+  unsigned* stat_ovf = nullptr;         // set by a producer whose partial left the fixed-point range
   bool fuse_ln = false;
   int64_t fuse_ln_max_b = 64;  // fused LayerNorm only for decode batches up to this size
   // persistent decode-step kernel (decode_mega.cu); PPOEXP_DECODE_MEGA=0 disables
@@ -38,6 +39,8 @@ struct Engine {
   DeviceBuffer trace_buf;
   cudaEvent_t poll_ev[2]{}, t0{}, t1{};
   double last_ms = 0;
+  double gen_seconds = 0;    // CostBook "response_generation" (src/engine.cpp:179)
+  double build_seconds = 0;  // model deep copy + KV pool / graph state allocation
   int64_t cur_unit = 0;
   std::vector<int64_t> cur_P, cur_len;
 
@@ -77,6 +80,7 @@ struct Engine {
   SamplerState sampler_state() const;
   template <class T>
   void decode_unit(int64_t B, int64_t unit);
+  void decode_unit_mixed(int64_t B, int64_t unit);
   void run_unit(int64_t B, int64_t unit);
   GraphSet& graph_for(int64_t B);
   void harvest_replay(const std::vector<TimedLaunch>& evs, int64_t unit0, int units);

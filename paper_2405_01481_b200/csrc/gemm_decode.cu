@@ -82,11 +82,25 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
 // slice when it fits → fetched entirely before the grid-dependency wait), an
 // XST-deep ring of activation tiles, then barriers.  The fp32 partial used by
 // the split-K reduction reuses the weight ring after the MMAs complete.
-template <int NB>
+// Activation operand modes (XM): 0 = bf16 tile by TMA; 1 = LayerNorm fused
+// (fp32 x + row statistics normalised by the epilogue threads into bf16);
+// 2 = fp32 activation split by the epilogue threads into two bf16 terms
+// (hi = bf16(a), lo = bf16(a - hi)) issued as two MMAs into one accumulator
+// (mixed mode: bf16 weights, fp32-grade activations); 3 = LayerNorm fused + split.
+template <int XM>
+struct XMode {
+  static constexpr bool kLn = XM == 1 || XM == 3;
+  static constexpr bool kSplit = XM >= 2;
+  static constexpr bool kProduced = XM != 0;  // the epilogue threads write the X tiles
+};
+
+template <int NB, bool SPLIT = false>
 struct DecLayout {
   static constexpr int kW = BMW * BK * 2;  // 16 KB weight tile
-  static constexpr int kX = NB * BK * 2;   // activation tile
-  static constexpr int XST = NB <= 64 ? 4 : 2;
+  static constexpr int kXT = NB * BK * 2;  // one bf16 activation tile
+  static constexpr int kX = kXT * (SPLIT ? 2 : 1);  // ring stage: the tile (+ its low-order term)
+  // (split at NB = 256: 64 KB per stage next to the 128 KB partial → one stage)
+  static constexpr int XST = NB <= 64 ? 4 : (SPLIT && NB > 128 ? 1 : 2);
   static constexpr int kPart = NB * BMW * 4;  // fp32 partial [NB][128], feature-contiguous
   // 227 KB opt-in minus the static LayerNorm scratch (2 x NB floats) and slack
   static constexpr int kSmemMax = 232448 - 2 * NB * 4 - 256;
@@ -99,7 +113,7 @@ struct DecLayout {
   }
 };
 
-template <int NB, int EPI, bool LNIN>
+template <int NB, int EPI, int XM>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_decode_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX, int Mrows,
                        int N, int K, void* __restrict__ Cv, int64_t ldc, int S, int wst, LnIn ln, RowStats so,
@@ -112,7 +126,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   };
   if (threadIdx.x == 0) stamp(0);
-  using L = DecLayout<NB>;
+  constexpr bool LNIN = XMode<XM>::kLn, SPLIT = XMode<XM>::kSplit, PROD = XMode<XM>::kProduced;
+  using L = DecLayout<NB, SPLIT>;
   constexpr int XST = L::XST;
   __shared__ float ln_mu[NB], ln_rs[NB];
   constexpr int kGB = LNIN ? 512 : 1;  // LN mode: gamma / beta of the first 8 k-blocks, staged before the PDL wait
@@ -146,7 +161,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0 && lane == 0) {
     for (int i = 0; i < XST; ++i) {
-      mbar_init(&xfull[i], LNIN ? 128 : 1);  // LN mode: the 128 epilogue threads produce X
+      mbar_init(&xfull[i], PROD ? 128 : 1);  // LN / split modes: the 128 epilogue threads produce X
       mbar_init(&xempty[i], 1);
     }
     for (int i = 0; i < wst; ++i) {
@@ -193,7 +208,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      if (!LNIN)
+      if (!PROD)
         for (int it = 0; it < nkl; ++it) {
           const int kb = kb0 + it;
           // activation tile (L2-resident, produced upstream)
@@ -226,6 +241,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint64_t dx = smem_desc_sw128(sX + xs * L::kX);
 #pragma unroll
         for (int k = 0; k < BK / 16; ++k) mma_bf16(tmem, dw + 2 * k, dx + 2 * k, idesc, (it | k) != 0);
+        if constexpr (SPLIT) {  // the low-order activation term into the same accumulator
+          const uint64_t dxl = smem_desc_sw128(sX + xs * L::kX + L::kXT);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) mma_bf16(tmem, dw + 2 * k, dxl + 2 * k, idesc, 1);
+        }
         mma_commit(&xempty[xs]);
         mma_commit(&wempty[ws]);
       }
@@ -234,7 +254,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncwarp();
   } else {
     const int et = threadIdx.x - 64;  // 0..127
-    if constexpr (LNIN) {
+    if constexpr (PROD) {
       // ---- fused LayerNorm producer: every independent load first (the row
       // statistics and the x chunks of the first PF k-blocks), then row mean /
       // rstd, then LN(x) -> bf16 in the 128B-swizzled K-major layout UMMA reads.
@@ -244,12 +264,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       constexpr int PF = CPT >= 8 ? 1 : (CPT >= 4 ? 3 : 4);
       const int c8 = et & 7;
       unsigned long long sa[2][2] = {{0ull, 0ull}, {0ull, 0ull}};
+      if constexpr (LNIN) {
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        const int rr = et + u * 128;
-        if (rr < NB && rr < Mrows) {
-          sa[u][0] = __ldcg(ln.acc + rr * kStatStride);
-          sa[u][1] = __ldcg(ln.acc + rr * kStatStride + 1);
+        for (int u = 0; u < 2; ++u) {
+          const int rr = et + u * 128;
+          if (rr < NB && rr < Mrows) {
+            sa[u][0] = __ldcg(ln.acc + rr * kStatStride);
+            sa[u][1] = __ldcg(ln.acc + rr * kStatStride + 1);
+          }
         }
       }
       auto load_kb = [&](int it, float4 (&xa)[CPT][2]) {
@@ -270,28 +292,32 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
       for (int p = 0; p < PF; ++p)
         if (p < nkl) load_kb(p, xpf[p]);
+      if constexpr (LNIN) {
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        const int rr = et + u * 128;
-        if (rr < NB) {
-          float mu = 0.f, rs = 0.f;
-          if (rr < Mrows) {
-            const double inv_d = 1.0 / ln.d;
-            const double mean = stat_of(sa[u][0]) * inv_d;
-            const double var = fmax(stat_of(sa[u][1]) * inv_d - mean * mean, 0.0);
-            mu = float(mean);
-            rs = rsqrtf(float(var) + 1e-5f);
+        for (int u = 0; u < 2; ++u) {
+          const int rr = et + u * 128;
+          if (rr < NB) {
+            float mu = 0.f, rs = 0.f;
+            if (rr < Mrows) {
+              const double inv_d = 1.0 / ln.d;
+              const double mean = stat_of(sa[u][0]) * inv_d;
+              const double var = fmax(stat_of(sa[u][1]) * inv_d - mean * mean, 0.0);
+              mu = float(mean);
+              // split mode keeps fp32-grade statistics (1 / sqrt in fp64)
+              rs = SPLIT ? float(1.0 / sqrt(var + 1e-5)) : rsqrtf(float(var) + 1e-5f);
+            }
+            ln_mu[rr] = mu;
+            ln_rs[rr] = rs;
           }
-          ln_mu[rr] = mu;
-          ln_rs[rr] = rs;
         }
+        asm volatile("bar.sync 1, 128;" ::: "memory");  // mu / rstd and the staged gamma / beta
       }
-      asm volatile("bar.sync 1, 128;" ::: "memory");  // mu / rstd and the staged gamma / beta
       auto emit_kb = [&](int it, const float4 (&xa)[CPT][2]) {
         const int xs = it % XST, xu = it / XST;
         const int col = (kb0 + it) * BK + c8 * 8;
         float gv[8], bv[8];
-        if (it < kGB / BK) {
+        if constexpr (!LNIN) {
+        } else if (it < kGB / BK) {
 #pragma unroll
           for (int e = 0; e < 8; ++e) {
             gv[e] = ln_g[it * BK + c8 * 8 + e];
@@ -309,17 +335,30 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int c = 0; c < CPT; ++c) {
           const int rr = (et + c * 128) >> 3;
-          Vec16<bf16> o;
+          Vec16<bf16> o, ol;
           if (col < K && rr < Mrows) {
-            const float mu = ln_mu[rr], rs = ln_rs[rr];
             const float xv[8] = {xa[c][0].x, xa[c][0].y, xa[c][0].z, xa[c][0].w,
                                  xa[c][1].x, xa[c][1].y, xa[c][1].z, xa[c][1].w};
+            float yv[8];
+            if constexpr (LNIN) {
+              const float mu = ln_mu[rr], rs = ln_rs[rr];
 #pragma unroll
-            for (int e = 0; e < 8; ++e) o.v[e] = __float2bfloat16_rn(gv[e] * ((xv[e] - mu) * rs) + bv[e]);
+              for (int e = 0; e < 8; ++e) yv[e] = gv[e] * ((xv[e] - mu) * rs) + bv[e];
+            } else {
+#pragma unroll
+              for (int e = 0; e < 8; ++e) yv[e] = xv[e];
+            }
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              o.v[e] = __float2bfloat16_rn(yv[e]);
+              if constexpr (SPLIT) ol.v[e] = __float2bfloat16_rn(yv[e] - __bfloat162float(o.v[e]));
+            }
           } else {
             o.u = make_uint4(0u, 0u, 0u, 0u);
+            ol.u = o.u;
           }
           *reinterpret_cast<uint4*>(tile + rr * 128 + ((c8 ^ (rr & 7)) << 4)) = o.u;
+          if constexpr (SPLIT) *reinterpret_cast<uint4*>(tile + L::kXT + rr * 128 + ((c8 ^ (rr & 7)) << 4)) = ol.u;
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor-core reads
         asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&xfull[xs])) : "memory");
@@ -381,6 +420,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             static_cast<bf16*>(Cv)[o] = __float2bfloat16_rn(gelu_tanh(a));
           } else if constexpr (EPI == int(Epi::kAddResidual)) {
             static_cast<float*>(Cv)[o] += a;
+          } else if constexpr (EPI == int(Epi::kGeluF32)) {
+            static_cast<float*>(Cv)[o] = gelu_tanh(a);
           } else {
             static_cast<float*>(Cv)[o] = a;
           }
@@ -417,8 +458,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           s1 += wred[(w4 * NB + bcol) * 2];
           s2 += wred[(w4 * NB + bcol) * 2 + 1];
         }
-        atomicAdd(&so.acc[bcol * kStatStride], stat_fix(s1));
-        atomicAdd(&so.acc[bcol * kStatStride + 1], stat_fix(s2));
+        atomicAdd(&so.acc[bcol * kStatStride], stat_fix(s1, so.ovf));
+        atomicAdd(&so.acc[bcol * kStatStride + 1], stat_fix(s2, so.ovf));
       }
     }
   }
@@ -560,6 +601,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           *xp = nv;
           ps += double(nv);
           pq += double(nv) * double(nv);
+        } else if constexpr (EPI == int(Epi::kGeluF32)) {
+          static_cast<float*>(Cv)[o] = gelu_tanh(a);
         } else {
           static_cast<float*>(Cv)[o] = a;
         }
@@ -578,8 +621,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           s1 += red[bcol * nf4 + g4].x;
           s2 += red[bcol * nf4 + g4].y;
         }
-        atomicAdd(&so.acc[bcol * kStatStride], stat_fix(s1));
-        atomicAdd(&so.acc[bcol * kStatStride + 1], stat_fix(s2));
+        atomicAdd(&so.acc[bcol * kStatStride], stat_fix(s1, so.ovf));
+        atomicAdd(&so.acc[bcol * kStatStride + 1], stat_fix(s2, so.ovf));
       }
     }
     if (push == 2) {
@@ -601,14 +644,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-template <int NB, int EPI, bool LNIN>
+template <int NB, int EPI, int XM>
 void launch_dec(Ctx& c, const bf16* X, int64_t ldx, const bf16* W, int64_t ldw, int64_t M, int64_t N, int64_t K,
                void* C, int64_t ldc, const LnIn* ln, const RowStats* so) {
-  using L = DecLayout<NB>;
+  constexpr bool LNIN = XMode<XM>::kLn;
+  using L = DecLayout<NB, XMode<XM>::kSplit>;
   const CUtensorMap tw = make_map(W, N, K, ldw, BMW);
-  // LN mode never reads X through TMA; any valid map will do
-  const CUtensorMap tx = LNIN ? tw : make_map(X, M, K, ldx, NB);
-  auto k = gemm_decode_kernel<NB, EPI, LNIN>;
+  // produced-X modes never read X through TMA; any valid map will do
+  const CUtensorMap tx = XMode<XM>::kProduced ? tw : make_map(X, M, K, ldx, NB);
+  auto k = gemm_decode_kernel<NB, EPI, XM>;
   const int smem_max = L::kSmemMax - (LNIN ? 2 * 512 * 4 : 0);  // LN mode: static gamma / beta staging
   static bool attr = false;
   if (!attr) {
@@ -684,7 +728,7 @@ void launch_dec(Ctx& c, const bf16* X, int64_t ldx, const bf16* W, int64_t ldw, 
   const LnIn lnv = ln ? *ln : LnIn{};
   const RowStats sov = (so && EPI == int(Epi::kAddResidual)) ? *so : RowStats{};
   const double flops = 2.0 * M * N * K;
-  const double bytes = 2.0 * N * K + double(M) * K * (LNIN ? 4 : 2) + double(M) * N * ((EPI == 0 || EPI == 1) ? 2 : 4);
+  const double bytes = 2.0 * N * K + double(M) * K * (XM ? 4 : 2) + double(M) * N * ((EPI == 0 || EPI == 1) ? 2 : 4);
   c.launch("gemm_decode", bytes, flops, [&] {
     uint64_t* dbg = nullptr;
     static const bool gtrace = getenv("PPOEXP_GEMM_TRACE") != nullptr;
@@ -694,28 +738,46 @@ void launch_dec(Ctx& c, const bf16* X, int64_t ldx, const bf16* W, int64_t ldw, 
       c.gemm_trace_meta.push_back({int(N), int(K), EPI, S});
       dbg = buf + slot * 16;
     }
-    PPOEXP_CUDA(cudaLaunchKernelEx(&cfg, k, tw, tx, int(M), int(N), int(K), C, ldc, S, wst, lnv, sov, push, dbg));
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, k, tw, tx, int(M), int(N), int(K), C, ldc, S, wst, lnv, sov, push, dbg);
+    if (e != cudaSuccess) {
+      (void)cudaGetLastError();
+      throw Error(6, std::string("cuda: decode GEMM launch failed (") + cudaGetErrorString(e) + ") NB=" +
+                         std::to_string(NB) + " EPI=" + std::to_string(EPI) + " XM=" + std::to_string(XM) +
+                         " M=" + std::to_string(M) + " N=" + std::to_string(N) + " K=" + std::to_string(K) +
+                         " S=" + std::to_string(S) + " wst=" + std::to_string(wst) + " smem=" +
+                         std::to_string(cfg.dynamicSmemBytes) + " max=" + std::to_string(smem_max));
+    }
   });
 }
 
-template <int NB, bool LNIN>
+template <int NB, int XM>
 void dispatch(Ctx& c, const bf16* X, int64_t ldx, const bf16* W, int64_t ldw, int64_t M, int64_t N, int64_t K, Epi epi,
              void* C, int64_t ldc, const LnIn* ln, const RowStats* so) {
-  switch (epi) {
-    case Epi::kStore: return launch_dec<NB, 0, LNIN>(c, X, ldx, W, ldw, M, N, K, C, ldc, ln, so);
-    case Epi::kGelu: return launch_dec<NB, 1, LNIN>(c, X, ldx, W, ldw, M, N, K, C, ldc, ln, so);
-    case Epi::kAddResidual: return launch_dec<NB, 2, LNIN>(c, X, ldx, W, ldw, M, N, K, C, ldc, ln, so);
-    case Epi::kStoreF32: return launch_dec<NB, 3, LNIN>(c, X, ldx, W, ldw, M, N, K, C, ldc, ln, so);
+  if constexpr (XMode<XM>::kSplit) {  // mixed mode: fp32 outputs only
+    switch (epi) {
+      case Epi::kAddResidual: return launch_dec<NB, 2, XM>(c, X, ldx, W, ldw, M, N, K, C, ldc, ln, so);
+      case Epi::kStoreF32: return launch_dec<NB, 3, XM>(c, X, ldx, W, ldw, M, N, K, C, ldc, ln, so);
+      case Epi::kGeluF32: return launch_dec<NB, 5, XM>(c, X, ldx, W, ldw, M, N, K, C, ldc, ln, so);
+      default: throw ContractError("decode GEMM: split activations need an fp32 epilogue");
+    }
+  } else {
+    switch (epi) {
+      case Epi::kStore: return launch_dec<NB, 0, XM>(c, X, ldx, W, ldw, M, N, K, C, ldc, ln, so);
+      case Epi::kGelu: return launch_dec<NB, 1, XM>(c, X, ldx, W, ldw, M, N, K, C, ldc, ln, so);
+      case Epi::kAddResidual: return launch_dec<NB, 2, XM>(c, X, ldx, W, ldw, M, N, K, C, ldc, ln, so);
+      case Epi::kStoreF32: return launch_dec<NB, 3, XM>(c, X, ldx, W, ldw, M, N, K, C, ldc, ln, so);
+      default: throw ContractError("decode GEMM: unsupported epilogue");
+    }
   }
 }
 
-template <bool LNIN>
+template <int XM>
 void dispatch_nb(Ctx& c, const bf16* X, int64_t ldx, const bf16* W, int64_t ldw, int64_t M, int64_t N, int64_t K,
                 Epi epi, void* C, int64_t ldc, const LnIn* ln, const RowStats* so) {
-  if (M <= 32) return dispatch<32, LNIN>(c, X, ldx, W, ldw, M, N, K, epi, C, ldc, ln, so);
-  if (M <= 64) return dispatch<64, LNIN>(c, X, ldx, W, ldw, M, N, K, epi, C, ldc, ln, so);
-  if (M <= 128) return dispatch<128, LNIN>(c, X, ldx, W, ldw, M, N, K, epi, C, ldc, ln, so);
-  return dispatch<256, LNIN>(c, X, ldx, W, ldw, M, N, K, epi, C, ldc, ln, so);
+  if (M <= 32) return dispatch<32, XM>(c, X, ldx, W, ldw, M, N, K, epi, C, ldc, ln, so);
+  if (M <= 64) return dispatch<64, XM>(c, X, ldx, W, ldw, M, N, K, epi, C, ldc, ln, so);
+  if (M <= 128) return dispatch<128, XM>(c, X, ldx, W, ldw, M, N, K, epi, C, ldc, ln, so);
+  return dispatch<256, XM>(c, X, ldx, W, ldw, M, N, K, epi, C, ldc, ln, so);
 }
 
 }  // namespace
@@ -742,7 +804,7 @@ void dump_gemm_trace(Ctx& c, const char* path) {
 bool gemm_decode_bf16(Ctx& c, const bf16* A, int64_t lda, const bf16* B, int64_t ldb, int64_t M, int64_t N, int64_t K,
                       Epi epi, void* C, int64_t ldc) {
   if (M > 256 || M <= 0) return false;
-  dispatch_nb<false>(c, A, lda, B, ldb, M, N, K, epi, C, ldc, nullptr, nullptr);
+  dispatch_nb<0>(c, A, lda, B, ldb, M, N, K, epi, C, ldc, nullptr, nullptr);
   return true;
 }
 
@@ -751,9 +813,23 @@ void gemm_decode_fused(Ctx& c, const bf16* X, int64_t ldx, const bf16* W, int64_
   if (M > 256 || M <= 0) throw ContractError("decode GEMM: batch above 256");
   if (ln) {
     if (K % 8 || ln->d != K) throw ContractError("decode GEMM: fused LayerNorm needs K == d_model, K % 8 == 0");
-    return dispatch_nb<true>(c, X, ldx, W, ldw, M, N, K, epi, C, ldc, ln, so);
+    return dispatch_nb<1>(c, X, ldx, W, ldw, M, N, K, epi, C, ldc, ln, so);
   }
-  return dispatch_nb<false>(c, X, ldx, W, ldw, M, N, K, epi, C, ldc, ln, so);
+  return dispatch_nb<0>(c, X, ldx, W, ldw, M, N, K, epi, C, ldc, ln, so);
+}
+
+// Mixed mode (bf16 weights, fp32 activations): the fp32 activation (or the
+// LayerNorm of x when ln != null) is split into two bf16 terms in-kernel.
+void gemm_decode_mixed(Ctx& c, const float* X, int64_t ldx, const bf16* W, int64_t ldw, int64_t M, int64_t N, int64_t K,
+                       Epi epi, void* C, int64_t ldc, const LnIn* ln, const RowStats* so) {
+  if (M > 256 || M <= 0) throw ContractError("decode GEMM: batch above 256");
+  if (K % 8 || ldx % 4) throw ContractError("decode GEMM (mixed): K and the activation stride must be multiples of 8 / 4");
+  if (ln) {
+    if (ln->d != K) throw ContractError("decode GEMM: fused LayerNorm needs K == d_model");
+    return dispatch_nb<3>(c, nullptr, 0, W, ldw, M, N, K, epi, C, ldc, ln, so);
+  }
+  const LnIn xin{X, ldx, nullptr, nullptr, nullptr, int(K)};
+  return dispatch_nb<2>(c, nullptr, 0, W, ldw, M, N, K, epi, C, ldc, &xin, so);
 }
 
 }  // namespace ppx

@@ -92,6 +92,8 @@ void launch_gemm_simt(Ctx& c, const T* A, int64_t lda, const T* B, int64_t ldb, 
       case Epi::kStoreF32:
         launch_kernel(c, gemm_simt_kernel<T, 3>, dim3(grid), dim3(256), 0, 1, A, lda, B, ldb, M, N, K, C, ldc);
         break;
+      case Epi::kLse:
+        throw ContractError("gemm_simt: no LSE epilogue");
     }
   });
 }

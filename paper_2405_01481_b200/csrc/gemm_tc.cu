@@ -117,7 +117,7 @@ struct SmemLayout {
 template <int BN, int EPI>
 __global__ void __launch_bounds__(kThreads, 2)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
-                   int K, void* __restrict__ Cv, int64_t ldc, int group_m) {
+                   int K, void* __restrict__ Cv, int64_t ldc, int group_m, LseEpi lse) {
   using L = SmemLayout<BN>;
   constexpr int S = L::kStages;
   extern __shared__ uint8_t smem_raw[];
@@ -194,6 +194,48 @@ __global__ void __launch_bounds__(kThreads, 2)
     // epilogue warps 2..5 → TMEM lane quarter = warp % 4
     const int q = warp & 3;
     const int row = m0 + q * 32 + lane;
+    if constexpr (EPI == int(Epi::kLse)) {
+      // LM head + online log-sum-exp + target gather: the fp32 logits of this
+      // row's BN columns never leave registers.  Each tile writes its (max,
+      // sum exp(l - max)) partial; the tile holding the row's target also
+      // writes the target logit (src/tensor.cpp:428-456, :491-519).
+      constexpr float kLog2e = 1.4426950408889634f;
+      const int tgt = row < M ? lse.target[row] : -1;
+      mbar_wait(tmem_full, 0);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      float m = -INFINITY, s = 0.f, tv = 0.f;
+      bool has_t = false;
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 32) {
+        uint32_t v[32];
+        tmem_ld32(tmem + (uint32_t(q * 32) << 16) + uint32_t(c), v);
+        const int col = n0 + c;
+        if (col >= N) break;
+        const int nv = min(32, N - col);
+        float cm = -INFINITY;
+#pragma unroll
+        for (int e = 0; e < 32; ++e)
+          if (e < nv) cm = fmaxf(cm, __uint_as_float(v[e]));
+        if (cm > m) {
+          s *= exp2f((m - cm) * kLog2e);
+          m = cm;
+        }
+        const float mb = m * kLog2e;
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+          const float f = __uint_as_float(v[e]);
+          if (e < nv) s += exp2f(fmaf(f, kLog2e, -mb));
+          if (col + e == tgt) {
+            tv = f;
+            has_t = true;
+          }
+        }
+      }
+      if (row < M) {
+        lse.part[int64_t(row) * lse.ldp + n_blk] = make_float2(m, s);
+        if (has_t) lse.tgt_logit[row] = tv;
+      }
+    } else {
     mbar_wait(tmem_full, 0);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll 1
@@ -258,6 +300,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         }
       }
     }
+    }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -309,7 +352,7 @@ namespace {
 
 template <int BN, int EPI>
 void launch_tc(Ctx& c, const bf16* A, int64_t lda, const bf16* B, int64_t ldb, int64_t M, int64_t N, int64_t K,
-               void* C, int64_t ldc) {
+               void* C, int64_t ldc, const LseEpi& lse = LseEpi{}) {
   using L = SmemLayout<BN>;
   const CUtensorMap ta = make_map(A, M, K, lda, BM);
   const CUtensorMap tb = make_map(B, N, K, ldb, BN);
@@ -322,9 +365,12 @@ void launch_tc(Ctx& c, const bf16* A, int64_t lda, const bf16* B, int64_t ldb, i
   const int num_m = int(ceil_div(M, BM)), num_n = int(ceil_div(N, BN));
   const int group_m = num_m < 16 ? num_m : 16;
   const double flops = 2.0 * M * N * K;
-  const double bytes = 2.0 * (M * K + N * K) + double(M) * N * ((EPI == 0 || EPI == 1) ? 2 : 4);
-  c.launch("gemm_tc", bytes, flops, [&] {
-    launch_kernel(c, k, dim3(num_m * num_n), dim3(kThreads), L::kBytes, 1, ta, tb, int(M), int(N), int(K), C, ldc, group_m);
+  const double out_bytes = EPI == int(Epi::kLse) ? double(M) * (num_n * 8 + 8)
+                                                 : double(M) * N * ((EPI == 0 || EPI == 1) ? 2 : 4);
+  const double bytes = 2.0 * (M * K + N * K) + out_bytes;
+  c.launch(EPI == int(Epi::kLse) ? "lm_head_lse" : "gemm_tc", bytes, flops, [&] {
+    launch_kernel(c, k, dim3(num_m * num_n), dim3(kThreads), L::kBytes, 1, ta, tb, int(M), int(N), int(K), C, ldc,
+                  group_m, lse);
   });
 }
 
@@ -336,6 +382,7 @@ void dispatch_epi(Ctx& c, const bf16* A, int64_t lda, const bf16* B, int64_t ldb
     case Epi::kGelu: return launch_tc<BN, 1>(c, A, lda, B, ldb, M, N, K, C, ldc);
     case Epi::kAddResidual: return launch_tc<BN, 2>(c, A, lda, B, ldb, M, N, K, C, ldc);
     case Epi::kStoreF32: return launch_tc<BN, 3>(c, A, lda, B, ldb, M, N, K, C, ldc);
+    case Epi::kLse: throw ContractError("gemm: the LSE epilogue goes through gemm_tc_lse");
   }
 }
 
@@ -370,6 +417,21 @@ bool gemm_tc_bf16(Ctx& c, const bf16* A, int64_t lda, const bf16* B, int64_t ldb
   if (bn_env == 256 && num_m * ceil_div(N, 256) >= 148)
     return dispatch_epi<256>(c, A, lda, B, ldb, M, N, K, epi, C, ldc), true;
   return dispatch_epi<128>(c, A, lda, B, ldb, M, N, K, epi, C, ldc), true;
+}
+
+// Fused LM head + online LSE + target gather (scoring, bf16 perf mode).
+// part[M, ldp] gets one (max, sum exp) pair per 256-column tile.
+int lse_tiles(int64_t N) { return int(ceil_div(N, 256)); }
+
+bool gemm_tc_lse(Ctx& c, const bf16* A, int64_t lda, const bf16* B, int64_t ldb, int64_t M, int64_t N, int64_t K,
+                 const LseEpi& e) {
+  if (tc_disabled()) return false;
+  if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15) return false;
+  if ((lda * 2) % 16 || (ldb * 2) % 16 || K % 8) return false;
+  if (e.ldp < lse_tiles(N)) throw ContractError("gemm_tc_lse: partial row stride too small");
+  if (M <= 0 || N <= 0 || K <= 0) return true;
+  launch_tc<256, int(Epi::kLse)>(c, A, lda, B, ldb, M, N, K, nullptr, 0, e);
+  return true;
 }
 
 }  // namespace ppx

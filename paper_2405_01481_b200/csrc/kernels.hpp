@@ -37,7 +37,20 @@ void launch_layernorm(Ctx& c, const float* x, int64_t rows, int64_t d, const flo
                       const int32_t* gather, const float* head, float* head_out);
 
 // K3: C[M,N] = A[M,K] · B[N,K]^T with epilogue.
-enum class Epi : int { kStore = 0, kGelu = 1, kAddResidual = 2, kStoreF32 = 3 };
+enum class Epi : int { kStore = 0, kGelu = 1, kAddResidual = 2, kStoreF32 = 3, kLse = 4, kGeluF32 = 5 };
+// Epilogue outputs of the fused LM-head + log-sum-exp + gather GEMM (Epi::kLse).
+struct LseEpi {
+  const int32_t* target = nullptr;  // [M] target column per row (< 0: none)
+  float* tgt_logit = nullptr;       // [M] fp32 logit of the target
+  float2* part = nullptr;           // [M, ldp] (max, sum exp(l - max)) per 256-column tile
+  int ldp = 0;
+};
+int lse_tiles(int64_t N);
+bool gemm_tc_lse(Ctx& c, const bf16* A, int64_t lda, const bf16* B, int64_t ldb, int64_t M, int64_t N, int64_t K,
+                 const LseEpi& e);
+// lp[r] = tgt_logit[r] - LSE(part[r, :ntiles]) → out[out_index[r]] (fp64 combine).
+void launch_lse_combine(Ctx& c, const float2* part, int ldp, int ntiles, const float* tgt_logit,
+                        const int32_t* target, int64_t rows, const int64_t* out_index, double* out);
 template <class T>
 void launch_gemm(Ctx& c, const T* A, int64_t lda, const T* B, int64_t ldb, int64_t M, int64_t N, int64_t K,
                  Epi epi, void* C, int64_t ldc);
@@ -49,9 +62,18 @@ void launch_gemm(Ctx& c, const T* A, int64_t lda, const T* B, int64_t ldb, int64
 // their per-CTA partials with integer atomics (order-independent, so the
 // statistics are bit-reproducible); consumer GEMMs normalise their activation
 // K-slice on the fly (LN = src/model.cpp:387-400, one-pass mean / variance).
-constexpr int kStatShift = 28;
+// Range: every producer adds one partial per row (a 128-feature slice of x, or
+// the whole row at the embedding); a partial must stay below kStatMax so that up
+// to 64 of them cannot overflow 2^63 (|x| rms up to ~2.3e4 per element).  A
+// partial beyond that sets *ovf and the engine fails loudly (no silent clamp).
+constexpr int kStatShift = 20;
 constexpr int kStatStride = 16;  // u64 per row: one 128-byte line each, so the producers' atomics spread over L2 slices
-__device__ __forceinline__ unsigned long long stat_fix(double v) {
+constexpr double kStatMax = 9.2233720368547758e18 / 64.0 / double(1ll << kStatShift);
+__device__ __forceinline__ unsigned long long stat_fix(double v, unsigned* ovf) {
+  if (!(fabs(v) < kStatMax)) {
+    if (ovf) atomicOr(ovf, 1u);
+    v = 0.0;
+  }
   return static_cast<unsigned long long>(__double2ll_rn(v * double(1ll << kStatShift)));
 }
 __device__ __forceinline__ double stat_of(unsigned long long a) {
@@ -59,6 +81,7 @@ __device__ __forceinline__ double stat_of(unsigned long long a) {
 }
 struct RowStats {
   unsigned long long* acc;            // [rows][kStatStride] (first two used), zero before the first add
+  unsigned* ovf = nullptr;            // set to 1 when a partial is outside the fixed-point range
   unsigned long long* zero = nullptr;  // (embedding only) accumulator rows to clear for this step
   int64_t zero_n = 0;                  // ... their number
 };
@@ -75,6 +98,13 @@ struct LnIn {
 // Epi::kAddResidual only).
 void gemm_decode_fused(Ctx& c, const bf16* X, int64_t ldx, const bf16* W, int64_t ldw, int64_t M, int64_t N, int64_t K,
                       Epi epi, void* C, int64_t ldc, const LnIn* ln, const RowStats* so);
+// Mixed mode (bf16 weights, fp32 activations): X fp32 (or LN(x) when ln != null)
+// split into hi + lo bf16 terms in-kernel, two MMAs per k-step; fp32 epilogues.
+void gemm_decode_mixed(Ctx& c, const float* X, int64_t ldx, const bf16* W, int64_t ldw, int64_t M, int64_t N, int64_t K,
+                       Epi epi, void* C, int64_t ldc, const LnIn* ln, const RowStats* so);
+// Mixed-mode GEMM for any M (decode-sized M goes to gemm_decode_mixed).
+void gemm_mixed(Ctx& c, const float* A, int64_t lda, const bf16* W, int64_t ldw, int64_t M, int64_t N, int64_t K,
+                Epi epi, void* C, int64_t ldc, const LseEpi* lse = nullptr);
 // Embedding that also writes the row statistics of x and clears so.zero's first zero_n rows.
 template <class T>
 void launch_embed_stats(Ctx& c, const int32_t* tokens, const int32_t* positions, int64_t rows, int64_t d,

@@ -149,8 +149,8 @@ __global__ void __launch_bounds__(256) embed_stats_kernel(const int32_t* __restr
       a += red[0][k];
       c += red[1][k];
     }
-    so.acc[r * kStatStride] = stat_fix(a);  // the sole producer of these accumulators
-    so.acc[r * kStatStride + 1] = stat_fix(c);
+    so.acc[r * kStatStride] = stat_fix(a, so.ovf);  // the sole producer of these accumulators
+    so.acc[r * kStatStride + 1] = stat_fix(c, so.ovf);
   }
   // clear this step's downstream accumulators (the previous step's readers
   // have completed: PDL_ENTRY waited for the predecessor grid)

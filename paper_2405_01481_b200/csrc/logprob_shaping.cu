@@ -95,6 +95,26 @@ __global__ void __launch_bounds__(NTH) logprob_gather_kernel(const T* __restrict
   }
 }
 
+// K9f combine: the fused LM-head GEMM (Epi::kLse) leaves one (max, sum exp)
+// pair per 256-column tile; a warp per row merges them in fp64 and gathers:
+// lp = l[target] - (M + log sum_j s_j exp(m_j - M)).
+__global__ void lse_combine_kernel(const float2* __restrict__ part, int ldp, int ntiles,
+                                   const float* __restrict__ tgt_logit, const int32_t* __restrict__ target,
+                                   int64_t rows, const int64_t* __restrict__ out_index, double* __restrict__ out) {
+  PDL_ENTRY();
+  const int64_t r = blockIdx.x * int64_t(blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (r >= rows || target[r] < 0) return;
+  const float2* p = part + r * ldp;
+  float M = -INFINITY;
+  for (int j = lane; j < ntiles; j += 32) M = fmaxf(M, p[j].x);
+  M = warp_max(M);
+  double S = 0.0;
+  for (int j = lane; j < ntiles; j += 32) S += double(p[j].y) * exp(double(p[j].x) - double(M));
+  S = warp_sum_d(S);
+  if (lane == 0) out[out_index[r]] = double(tgt_logit[r]) - (double(M) + log(S));
+}
+
 // ------------------------------------------------------------------ K11
 // One warp per sequence.  Shaping (kl_penalized_rewards, src/losses.cpp:188-199):
 //   r_t = -kl_coef * (a_t - ref_t);  r_{n-1} += R
@@ -200,6 +220,15 @@ void launch_logprob_gather(Ctx& c, const T* logits, int64_t ld, int64_t rows, in
   if ((ld * sizeof(T)) % 16) throw ContractError("logprob_gather: row stride must be 16-byte aligned");
   c.launch("logprob_gather", double(rows) * V * sizeof(T) + rows * 20.0, 0, [&] {
     launch_kernel(c, logprob_gather_kernel<T, 256>, dim3(rows), dim3(256), 0, 1, logits, ld, rows, V, target, out_index, out);
+  });
+}
+
+void launch_lse_combine(Ctx& c, const float2* part, int ldp, int ntiles, const float* tgt_logit,
+                        const int32_t* target, int64_t rows, const int64_t* out_index, double* out) {
+  if (rows <= 0) return;
+  c.launch("lse_combine", double(rows) * (ntiles * 8.0 + 20.0), 0, [&] {
+    launch_kernel(c, lse_combine_kernel, dim3(ceil_div(rows, 8)), dim3(256), 0, 1, part, ldp, ntiles, tgt_logit, target,
+                  rows, out_index, out);
   });
 }
 

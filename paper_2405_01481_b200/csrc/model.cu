@@ -152,6 +152,68 @@ void Model::load(const ppoexp_tensor_view* views, int64_t n, bool refit) {
   PPOEXP_CUDA(cudaStreamSynchronize(c.stream));
 }
 
+// Engine::snapshot (include/aligner/engine.hpp:67), one parameter: the device
+// copy back in the reference layout ([in, out] projections, row-major).
+void Model::snapshot(const std::string& name, void* out, int64_t numel, int out_dtype) {
+  const auto exp = expected(cfg);
+  const std::vector<int64_t>* shape = nullptr;
+  for (const auto& [n, sh] : exp)
+    if (n == name) shape = &sh;
+  if (!shape) throw ContractError("snapshot: unknown parameter " + name);
+  int64_t want = 1;
+  for (auto v : *shape) want *= v;
+  if (numel != want)
+    throw ShapeError("snapshot: " + name + " has " + std::to_string(want) + " elements, buffer " + std::to_string(numel));
+  if (out_dtype != PPOEXP_F64 && out_dtype != PPOEXP_F32) throw ContractError("snapshot: dtype must be F64 or F32");
+  const int64_t d = cfg.d_model, f = cfg.d_ff;
+  // device source: base pointer, element type (0 f32, 1 T), rows x cols as stored, row offset, transposed
+  const void* base = nullptr;
+  bool is_t = true, tr = false;
+  int64_t rows = 0, cols = 0, row0 = 0;
+  if (name == "tok_embed.weight") base = tok, rows = cfg.vocab_size, cols = d;
+  else if (name == "pos_embed.weight") base = pos, rows = cfg.max_seq_len, cols = d;
+  else if (name == "final_norm.weight") base = lnfw, is_t = false, rows = 1, cols = d;
+  else if (name == "final_norm.bias") base = lnfb, is_t = false, rows = 1, cols = d;
+  else if (name == "scalar_head.weight") base = head, is_t = false, rows = 1, cols = d;
+  else {
+    const size_t dot = name.find('.', 7);
+    const Layer& ly = layers[std::stoll(name.substr(7, dot - 7))];
+    const std::string rest = name.substr(dot + 1);
+    tr = true;
+    if (rest == "attn_norm.weight") base = ly.ln1w, is_t = tr = false, rows = 1, cols = d;
+    else if (rest == "attn_norm.bias") base = ly.ln1b, is_t = tr = false, rows = 1, cols = d;
+    else if (rest == "ffn_norm.weight") base = ly.ln2w, is_t = tr = false, rows = 1, cols = d;
+    else if (rest == "ffn_norm.bias") base = ly.ln2b, is_t = tr = false, rows = 1, cols = d;
+    else if (rest == "attn.q_proj.weight") base = ly.wqkv, rows = d, cols = d, row0 = 0;
+    else if (rest == "attn.k_proj.weight") base = ly.wqkv, rows = d, cols = d, row0 = d;
+    else if (rest == "attn.v_proj.weight") base = ly.wqkv, rows = d, cols = d, row0 = 2 * d;
+    else if (rest == "attn.o_proj.weight") base = ly.wo, rows = d, cols = d;
+    else if (rest == "ffn.up_proj.weight") base = ly.wup, rows = f, cols = d;
+    else if (rest == "ffn.down_proj.weight") base = ly.wdown, rows = d, cols = f;
+  }
+  const size_t esz = is_t ? tsize() : 4;
+  std::vector<uint8_t> h(size_t(rows) * cols * esz);
+  PPOEXP_CUDA(cudaStreamSynchronize(ctx->stream));
+  PPOEXP_CUDA(cudaMemcpy(h.data(), static_cast<const uint8_t*>(base) + size_t(row0) * cols * esz, h.size(),
+                         cudaMemcpyDeviceToHost));
+  auto at = [&](int64_t i) -> double {
+    if (!is_t || dtype == PPOEXP_F32) return reinterpret_cast<const float*>(h.data())[i];
+    uint32_t u = uint32_t(reinterpret_cast<const uint16_t*>(h.data())[i]) << 16;
+    float v;
+    std::memcpy(&v, &u, 4);
+    return v;
+  };
+  // stored [rows=out, cols=in] (W^T) when tr: reference element [i][o] = stored[o][i]
+  for (int64_t e = 0; e < want; ++e) {
+    const int64_t si = tr ? (e % rows) * cols + e / rows : e;
+    const double v = at(si);
+    if (out_dtype == PPOEXP_F64)
+      static_cast<double*>(out)[e] = v;
+    else
+      static_cast<float*>(out)[e] = float(v);
+  }
+}
+
 // ------------------------------------------------------------------ packing
 void pack_metadata(Ctx& c, Packed& p, const std::string& tag) {
   p.B = static_cast<int64_t>(p.offsets.size()) - 1;
@@ -227,36 +289,114 @@ static float* forward_layers_t(Model& m, const Packed& p, const KvTarget* kv) {
   return x;
 }
 
+// Mixed mode: bf16 weights, fp32 activations / KV, split-bf16 tensor-core GEMMs.
+static float* forward_layers_mixed(Model& m, const Packed& p, const KvTarget* kv) {
+  Ctx& c = *m.ctx;
+  const int64_t M = p.M, d = m.d(), f = m.cfg.d_ff, H = m.cfg.n_heads, DH = m.dh();
+  float* x = static_cast<float*>(c.workspace("fwd.x", M * d * 4));
+  float* h = static_cast<float*>(c.workspace("fwd.h", M * d * 4));
+  float* qkv = static_cast<float*>(c.workspace("fwd.qkv", M * 3 * d * 4));
+  float* att = static_cast<float*>(c.workspace("fwd.att", M * d * 4));
+  float* up = static_cast<float*>(c.workspace("fwd.up", M * f * 4));
+  launch_embed<bf16>(c, p.tokens_d, p.positions_d, M, d, static_cast<const bf16*>(m.tok),
+                     static_cast<const bf16*>(m.pos), x);
+  for (int64_t l = 0; l < m.cfg.n_layers; ++l) {
+    const Layer& ly = m.layers[l];
+    launch_layernorm<float>(c, x, M, d, ly.ln1w, ly.ln1b, h, nullptr, nullptr, nullptr);
+    gemm_mixed(c, h, d, static_cast<const bf16*>(ly.wqkv), d, M, 3 * d, d, Epi::kStoreF32, qkv, 3 * d);
+    if (kv)
+      launch_kv_scatter<float>(c, qkv, M, d, p.seq_of_row_d, p.positions_d, kv->block_table, int(l), kv->geom,
+                               static_cast<float*>(kv->pool));
+    launch_attention_prefill<float>(c, qkv, p.offsets_d, p.B, p.max_len, H, DH, att);
+    gemm_mixed(c, att, d, static_cast<const bf16*>(ly.wo), d, M, d, d, Epi::kAddResidual, x, d);
+    launch_layernorm<float>(c, x, M, d, ly.ln2w, ly.ln2b, h, nullptr, nullptr, nullptr);
+    gemm_mixed(c, h, d, static_cast<const bf16*>(ly.wup), d, M, f, d, Epi::kGeluF32, up, f);
+    gemm_mixed(c, up, f, static_cast<const bf16*>(ly.wdown), f, M, d, f, Epi::kAddResidual, x, d);
+  }
+  return x;
+}
+
 float* forward_layers(Model& m, const Packed& p, const KvTarget* kv) {
   if (p.M <= 0) return nullptr;
   if (p.max_len > m.cfg.max_seq_len)
     throw ContractError("forward: sequence length " + std::to_string(p.max_len) + " exceeds max_seq_len " +
                         std::to_string(m.cfg.max_seq_len));
+  if (m.mixed()) return forward_layers_mixed(m, p, kv);
   return m.dtype == PPOEXP_F32 ? forward_layers_t<float>(m, p, kv) : forward_layers_t<bf16>(m, p, kv);
 }
 
 // ------------------------------------------------------------------ scoring
+// The LM head runs with the fused log-sum-exp + gather epilogue (Epi::kLse in
+// gemm_tc.cu / gemm_mixed.cu): fp32 logits stay in registers, only one (max,
+// sum) pair per 256-column tile per row reaches HBM.  PPOEXP_SCORING=logits
+// instead materialises fp32 logits and runs K9 (logprob_gather).
+static bool fused_scoring() {
+  static const bool on = [] {
+    const char* e = getenv("PPOEXP_SCORING");
+    return !(e && std::string(e) == "logits");
+  }();
+  return on;
+}
+
+static void score_logprobs_fused(Model& m, const float* x, const int32_t* gather, const int32_t* target,
+                                 const int64_t* out_index, int64_t R, double* out) {
+  Ctx& c = *m.ctx;
+  const int64_t d = m.d(), V = m.cfg.vocab_size;
+  const int nt = lse_tiles(V);
+  const int ldp = (nt + 1) / 2 * 2;
+  // rows per chunk: partials <= ~1 GiB
+  const int64_t chunk = std::max<int64_t>(128, std::min<int64_t>(R, (int64_t(1) << 30) / (ldp * 8)));
+  const int64_t cr = std::min(chunk, R);
+  float2* part = static_cast<float2*>(c.workspace("score.part", cr * ldp * 8));
+  float* tl = static_cast<float*>(c.workspace("score.tgt", cr * 4));
+  const bool mx = m.mixed();  // fp32 final LayerNorm + split-activation LM head
+  void* hf = c.workspace("score.hf", cr * d * (mx ? 4 : 2));
+  for (int64_t r0 = 0; r0 < R; r0 += chunk) {
+    const int64_t n = std::min(chunk, R - r0);
+    LseEpi e;
+    e.target = target + r0;
+    e.tgt_logit = tl;
+    e.part = part;
+    e.ldp = ldp;
+    if (mx) {
+      launch_layernorm<float>(c, x, n, d, m.lnfw, m.lnfb, static_cast<float*>(hf), gather + r0, nullptr, nullptr);
+      gemm_mixed(c, static_cast<float*>(hf), d, static_cast<const bf16*>(m.tok), d, n, V, d, Epi::kLse, nullptr, 0, &e);
+    } else {
+      launch_layernorm<bf16>(c, x, n, d, m.lnfw, m.lnfb, static_cast<bf16*>(hf), gather + r0, nullptr, nullptr);
+      if (!gemm_tc_lse(c, static_cast<bf16*>(hf), d, static_cast<const bf16*>(m.tok), d, n, V, d, e))
+        throw ContractError("scoring: fused LM head needs 16-byte aligned rows (d_model % 8 == 0)");
+    }
+    launch_lse_combine(c, part, ldp, nt, tl, target + r0, n, out_index + r0, out);
+  }
+}
+
 template <class T>
 static void score_logprobs_t(Model& m, const float* x, const int32_t* gather, const int32_t* target,
                              const int64_t* out_index, int64_t R, double* out) {
   Ctx& c = *m.ctx;
+  if constexpr (std::is_same_v<T, bf16>) {
+    if (fused_scoring()) return score_logprobs_fused(m, x, gather, target, out_index, R, out);
+  }
   const int64_t d = m.d(), V = m.cfg.vocab_size, ld = m.vpad;
   // logits are streamed in row chunks of <= ~2 GiB
-  const int64_t chunk = std::max<int64_t>(128, std::min<int64_t>(R, (int64_t(2) << 30) / (ld * sizeof(T))));
+  const int64_t chunk = std::max<int64_t>(128, std::min<int64_t>(R, (int64_t(2) << 30) / (ld * sizeof(float))));
   T* hf = static_cast<T*>(c.workspace("score.hf", std::min(chunk, R) * d * sizeof(T)));
-  T* logits = static_cast<T*>(c.workspace("score.logits", std::min(chunk, R) * ld * sizeof(T)));
+  // fp32 logits in both modes (bf16 logits would add |l|*2^-9 to every log-prob)
+  float* logits = static_cast<float*>(c.workspace("score.logits", std::min(chunk, R) * ld * sizeof(float)));
   for (int64_t r0 = 0; r0 < R; r0 += chunk) {
     const int64_t n = std::min(chunk, R - r0);
     launch_layernorm<T>(c, x, n, d, m.lnfw, m.lnfb, hf, gather + r0, nullptr, nullptr);
-    gemm<T>(c, hf, d, static_cast<const T*>(m.tok), d, n, V, d, Epi::kStore, logits, ld);
-    launch_logprob_gather<T>(c, logits, ld, n, V, target + r0, out_index + r0, out);
+    gemm<T>(c, hf, d, static_cast<const T*>(m.tok), d, n, V, d, Epi::kStoreF32, logits, ld);
+    launch_logprob_gather<float>(c, logits, ld, n, V, target + r0, out_index + r0, out);
   }
 }
 
 void score_logprobs(Model& m, const Packed&, const float* x, const int32_t* gather, const int32_t* target,
                     const int64_t* out_index, int64_t R, double* out) {
   if (R <= 0) return;
-  if (m.dtype == PPOEXP_F32)
+  if (m.mixed())
+    score_logprobs_fused(m, x, gather, target, out_index, R, out);
+  else if (m.dtype == PPOEXP_F32)
     score_logprobs_t<float>(m, x, gather, target, out_index, R, out);
   else
     score_logprobs_t<bf16>(m, x, gather, target, out_index, R, out);
@@ -267,7 +407,7 @@ void score_head(Model& m, const float* x, const int32_t* gather, const int64_t* 
   if (!m.cfg.scalar_head) throw ContractError("model has no scalar head");
   Ctx& c = *m.ctx;
   float* vals = static_cast<float*>(c.workspace("score.vals", R * 4));
-  if (m.dtype == PPOEXP_F32)
+  if (m.dtype == PPOEXP_F32 || m.mixed())
     launch_layernorm<float>(c, x, R, m.d(), m.lnfw, m.lnfb, (float*)nullptr, gather, m.head, vals);
   else
     launch_layernorm<bf16>(c, x, R, m.d(), m.lnfw, m.lnfb, (bf16*)nullptr, gather, m.head, vals);

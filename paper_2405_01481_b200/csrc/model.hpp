@@ -26,9 +26,14 @@ struct Model {
   std::vector<Layer> layers;
   float *lnfw = nullptr, *lnfb = nullptr, *head = nullptr;
   int64_t vpad = 0;  // padded logits row stride
+  double build_seconds = 0.0;  // host wall time of the deep copy at build (Engine::build_seconds)
+  double refit_seconds = 0.0;  // CostBook "refit" (src/engine.cpp:86-89), device time of every refit
 
   int64_t d() const { return cfg.d_model; }
-  size_t tsize() const { return dtype == PPOEXP_F32 ? 4 : 2; }
+  size_t tsize() const { return dtype == PPOEXP_F32 ? 4 : 2; }  // weight element
+  size_t asize() const { return dtype == PPOEXP_BF16 ? 2 : 4; }  // activation / KV element
+  int wdt() const { return dtype == PPOEXP_F32 ? PPOEXP_F32 : PPOEXP_BF16; }  // weight storage dtype
+  bool mixed() const { return dtype == PPOEXP_MIXED; }
   int64_t dh() const { return cfg.d_model / cfg.n_heads; }
 
   // expected_names / param_shape, src/model.cpp:66-115
@@ -36,6 +41,8 @@ struct Model {
   void allocate();
   // Validate names/shapes (err = RefitError or ContractError) then copy.
   void load(const ppoexp_tensor_view* v, int64_t n, bool refit);
+  // Engine::snapshot: one parameter back in the reference layout (host, f64 or f32)
+  void snapshot(const std::string& name, void* out, int64_t numel, int dtype);
 };
 
 // A ragged batch packed row-major on the device.

@@ -16,6 +16,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import weakref
 from dataclasses import dataclass, field
 from typing import Sequence
 
@@ -25,7 +26,7 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("PPOEXP_LIB") or os.path.join(_PKG, "libppoexp.so")  # override: A/B runs only
 
 HOST, DEVICE = 0, 1
-F32, BF16, F64 = 0, 1, 2
+F32, BF16, F64, MIXED = 0, 1, 2, 3  # MIXED: bf16 weights, fp32-grade activations (include/ppoexp.h)
 PAD_TOKEN, EOT_TOKEN = 256, 257  # include/aligner/model.hpp:17-18
 
 
@@ -88,12 +89,12 @@ class _XpReq(C.Structure):
     _fields_ = [("policy_engine", C.c_void_p), ("reference", C.c_void_p), ("critic", C.c_void_p), ("rm", C.c_void_p),
                 ("scripted_target", C.c_int32), ("reserved", C.c_int32), ("sampling", _Sampling),
                 ("seed", C.c_uint64), ("step_index", C.c_int64), ("gidx0", C.c_int64), ("max_new", C.c_int64),
-                ("hyper", _Hyper), ("allreduce", _ALLREDUCE), ("allreduce_user", C.c_void_p)]
+                ("hyper", _Hyper), ("allreduce", _ALLREDUCE), ("allreduce_user", C.c_void_p), ("comm", C.c_void_p)]
 
 
 class _Rollout(C.Structure):
     _fields_ = [(n, C.c_void_p) for n in ("tokens", "lengths", "actor_lp", "ref_lp", "values", "rewards", "shaped",
-                                          "advantages", "returns", "whitened", "stats")]
+                                          "advantages", "returns", "whitened", "stats", "timing")]
 
 
 _lib = None
@@ -134,6 +135,15 @@ def lib():
             "ppoexp_whiten_partials": [I64, I64, P, P, P, P, I32],
             "ppoexp_whiten_apply": [I64, I64, P, P, P, P, P, I32],
             "ppoexp_make_experience": [P, I64, P, P, P, I32],
+            "ppoexp_model_snapshot": [P, C.c_char_p, P, I64, I32],
+            "ppoexp_engine_build_seconds": [P, P],
+            "ppoexp_engine_cost": [P, C.c_char_p, P],
+            "ppoexp_engine_options_get": [P, P],
+            "ppoexp_balance": [P, I64, I64, P],
+            "ppoexp_comm_unique_id": [P],
+            "ppoexp_comm_create": [P, P, I32, I32, P],
+            "ppoexp_comm_destroy": [P],
+            "ppoexp_comm_allgather_sum": [P, P, I64, I32],
         }
         for name, args in sigs.items():
             f = getattr(L, name)
@@ -258,9 +268,20 @@ class Context:
         self.h = C.c_void_p()
         _check(lib().ppoexp_ctx_create(device, C.byref(self.h)))
         self.device = device
+        self._children = weakref.WeakSet()  # engines / models / communicators on this context
+
+    def _adopt(self, obj):
+        self._children.add(obj)
 
     def close(self):
+        """Destroys the context; library objects still open on it are closed
+        first (engines before models), so no handle outlives its context."""
         if self.h:
+            kids = list(self._children)
+            for kind in (Engine, Communicator, DeviceModel):
+                for k in kids:
+                    if isinstance(k, kind):
+                        k.close()
             _check(lib().ppoexp_ctx_destroy(self.h))
             self.h = C.c_void_p()
 
@@ -312,6 +333,7 @@ class DeviceModel:
         views, keep = _views(params)
         cfg = config._c()
         _check(lib().ppoexp_model_create(ctx.h, C.byref(cfg), views, len(params), dtype, C.byref(self.h)))
+        ctx._adopt(self)
 
     def refit(self, params):
         """Engine::refit, src/engine.cpp:60-90 (RefitError, nothing touched, on a name/shape mismatch)."""
@@ -328,6 +350,16 @@ class DeviceModel:
         g = C.c_uint64()
         _check(lib().ppoexp_model_generation(self.h, C.byref(g)))
         return g.value
+
+    def snapshot(self, name: str | None = None, dtype=F64):
+        """Engine::snapshot (include/aligner/engine.hpp:67): the device copy in the
+        reference layout — one parameter, or the whole {name: array} map."""
+        if name is None:
+            return {n: self.snapshot(n, dtype) for n, _ in expected_names(self.config)}
+        shape = dict(expected_names(self.config))[name]
+        out = np.zeros(shape, np.float64 if dtype == F64 else np.float32)
+        _check(lib().ppoexp_model_snapshot(self.h, name.encode(), out.ctypes.data, out.size, dtype))
+        return out
 
     def close(self):
         if self.h:
@@ -404,6 +436,7 @@ class Engine:
         self.h = C.c_void_p()
         _check(lib().ppoexp_engine_create(model.h, C.byref(o), C.byref(self.h)))
         self.last_ms = 0.0
+        model.ctx._adopt(self)
 
     def refit(self, params):
         self.model.refit(params)
@@ -411,6 +444,31 @@ class Engine:
     @property
     def generation_counter(self):
         return self.model.generation_counter
+
+    def build_seconds(self) -> float:
+        """Engine::build_seconds (include/aligner/engine.hpp:66)."""
+        v = C.c_double()
+        _check(lib().ppoexp_engine_build_seconds(self.h, C.byref(v)))
+        return v.value
+
+    def costs(self) -> dict:
+        """Engine::costs() (CostBook totals in seconds, include/aligner/timing.hpp:33-46)."""
+        out = {}
+        for cat in ("response_generation", "refit"):
+            v = C.c_double()
+            _check(lib().ppoexp_engine_cost(self.h, cat.encode(), C.byref(v)))
+            if v.value:
+                out[cat] = v.value
+        return out
+
+    def snapshot(self):
+        """Engine::snapshot(): the frozen weights in the reference layout."""
+        return self.model.snapshot()
+
+    def options(self) -> EngineOptions:
+        o = _EngineOpts()
+        _check(lib().ppoexp_engine_options_get(self.h, C.byref(o)))
+        return EngineOptions(o.max_batch, o.page_size, o.max_total_tokens, bool(o.use_graphs))
 
     def generate_batch(self, tasks: Sequence[GenTask]):
         """Engine::generate_batch, src/engine.cpp:148-182 (per-task SamplingSpec)."""
@@ -436,6 +494,52 @@ class Engine:
     def close(self):
         if self.h:
             _check(lib().ppoexp_engine_destroy(self.h))
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def balance(tasks_or_costs, n_workers: int):
+    """balance (src/engine.cpp:14-31): LPT assignment; returns task indices per
+    worker (tasks by cost descending, each on the least-loaded worker, ties to
+    the lowest worker index).  Used to shard prompts over ranks."""
+    costs = np.array([t.cost() if isinstance(t, GenTask) else float(t) for t in tasks_or_costs], np.float64)
+    w = np.zeros(len(costs), np.int64)
+    _check(lib().ppoexp_balance(costs.ctypes.data, len(costs), n_workers, w.ctypes.data))
+    return [[i for i in range(len(costs)) if w[i] == k] for k in range(n_workers)]
+
+
+class Communicator:
+    """One NCCL communicator per rank (the experience step's single collective
+    inside the library, include/ppoexp.h ppoexp_comm_*).  Rank 0 makes the id
+    (``unique_id()``); the caller ships it to every rank."""
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = (C.c_uint8 * 128)()
+        _check(lib().ppoexp_comm_unique_id(buf))
+        return bytes(buf)
+
+    def __init__(self, ctx: Context, uid: bytes, rank: int, world: int):
+        self.ctx, self.rank, self.world = ctx, rank, world
+        self.h = C.c_void_p()
+        idb = (C.c_uint8 * 128).from_buffer_copy(uid)
+        _check(lib().ppoexp_comm_create(ctx.h, idb, rank, world, C.byref(self.h)))
+        ctx._adopt(self)
+
+    def allgather_sum(self, buf):
+        """buf (numpy fp64 or CUDA tensor) <- its rank-order sum over all ranks."""
+        ptr, where = _ptr(buf)
+        _check(lib().ppoexp_comm_allgather_sum(self.h, ptr, buf.size if where == HOST else buf.numel(), where))
+        return buf
+
+    def close(self):
+        if self.h:
+            _check(lib().ppoexp_comm_destroy(self.h))
             self.h = C.c_void_p()
 
     def __del__(self):
@@ -577,6 +681,15 @@ class PpoHyper:
 
 
 @dataclass
+class StepTiming:
+    """StepTiming (include/aligner/ppo.hpp:27-37), milliseconds of device time."""
+    rollout: float
+    response_generation: float
+    logprob_calculation: float
+    critic_wait: float
+
+
+@dataclass
 class ExperienceStats:
     kl_sum: float
     kl_count: float
@@ -586,6 +699,7 @@ class ExperienceStats:
     adv_std: float
     gen_ms: float
     total_ms: float
+    timing: "StepTiming | None" = None
 
     @property
     def kl_mean(self):
@@ -601,8 +715,10 @@ class ExperienceMaker:
     policy engine + reference + critic (+ RM or the scripted reward)."""
 
     def __init__(self, engine: Engine, reference: DeviceModel, critic: DeviceModel, rm: DeviceModel | None = None,
-                 scripted_target: int = 122, hyper: PpoHyper | None = None, allreduce=None):
+                 scripted_target: int = 122, hyper: PpoHyper | None = None, allreduce=None,
+                 comm: Communicator | None = None):
         self.engine, self.reference, self.critic, self.rm = engine, reference, critic, rm
+        self.comm = comm
         self.scripted_target = scripted_target
         self.hyper = hyper or PpoHyper()
         self._allreduce_py = allreduce
@@ -622,7 +738,8 @@ class ExperienceMaker:
                       self.scripted_target, 0,
                       _Sampling(1 if sampling.greedy else 0, sampling.top_k, sampling.temperature, sampling.top_p),
                       seed, step_index, gidx0, max_new,
-                      _Hyper(self.hyper.kl_penalty_coef, self.hyper.gamma, self.hyper.lam), self._allreduce_c, None)
+                      _Hyper(self.hyper.kl_penalty_coef, self.hyper.gamma, self.hyper.lam), self._allreduce_c, None,
+                      self.comm.h if self.comm else None)
 
     def run_device(self, prompts_flat, offsets, out: dict, *, max_new, sampling, seed=0, step_index=0, gidx0=0):
         """All buffers are CUDA torch tensors (prompts int32 flat, offsets int64
@@ -630,7 +747,7 @@ class ExperienceMaker:
         B = offsets.numel() - 1
         req = self._req(sampling, seed, step_index, gidx0, max_new)
         ro = _Rollout(*[out[k].data_ptr() for k in ("tokens", "lengths", "actor_lp", "ref_lp", "values", "rewards",
-                                                    "shaped", "advantages", "returns", "whitened", "stats")])
+                                                    "shaped", "advantages", "returns", "whitened", "stats")], None)
         _check(lib().ppoexp_make_experience(C.byref(req), B, prompts_flat.data_ptr(), offsets.data_ptr(), C.byref(ro),
                                             DEVICE))
 
@@ -649,10 +766,10 @@ class ExperienceMaker:
         o = dict(tokens=np.zeros((B, max_new), np.int32), lengths=np.zeros(B, np.int64),
                  **{k: np.zeros((B, max_new)) for k in ("actor_lp", "ref_lp", "values", "shaped", "advantages",
                                                         "returns", "whitened")},
-                 rewards=np.zeros(B), stats=np.zeros(8))
+                 rewards=np.zeros(B), stats=np.zeros(8), timing=np.zeros(4))
         req = self._req(sampling, seed, step_index, gidx0, max_new)
         ro = _Rollout(*[o[k].ctypes.data for k in ("tokens", "lengths", "actor_lp", "ref_lp", "values", "rewards",
-                                                   "shaped", "advantages", "returns", "whitened", "stats")])
+                                                   "shaped", "advantages", "returns", "whitened", "stats", "timing")])
         _check(lib().ppoexp_make_experience(C.byref(req), B, flat.ctypes.data, offs.ctypes.data, C.byref(ro), HOST))
         batch = []
         for b in range(B):
@@ -661,4 +778,4 @@ class ExperienceMaker:
                                     o["actor_lp"][b, :n].copy(), o["ref_lp"][b, :n].copy(), o["values"][b, :n].copy(),
                                     float(o["rewards"][b]), o["advantages"][b, :n].copy(), o["returns"][b, :n].copy(),
                                     np.ones(n), o["whitened"][b, :n].copy(), o["shaped"][b, :n].copy()))
-        return batch, ExperienceStats(*[float(v) for v in o["stats"]])
+        return batch, ExperienceStats(*[float(v) for v in o["stats"]], timing=StepTiming(*map(float, o["timing"])))

@@ -33,7 +33,7 @@ def test_header_declares_entry_points():
 def test_library_exports_every_declared_symbol(lib):
     missing = [n for n in declared() if not hasattr(lib, n)]
     assert not missing, missing
-    assert lib.ppoexp_abi_version() == 1
+    assert lib.ppoexp_abi_version() == 2
 
 
 def test_no_torch_types_in_abi():

@@ -53,3 +53,88 @@ def test_gemm_vs_torch(glib, ctx, M, N, K, epi, path):
     assert err.max().item() <= 0, f"max abs err {(out - ref).abs().max().item():.3e}"
     if epi in (0, 1):  # untouched padding
         assert torch.all(Cm[:, N:] == 0)
+
+
+@pytest.fixture(scope="module")
+def lmlib():
+    from paper_2405_01481_b200 import ppoexp as px
+    f = px.lib().ppoexp_testing_lm_head_logprobs
+    f.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_void_p,
+                  C.c_void_p, C.c_int32]
+    f.restype = C.c_int32
+    return px, f
+
+
+@pytest.mark.parametrize("R,V,K", [(300, 1000, 128), (1024, 50257, 768), (130, 128256, 256), (4096, 32000, 2048),
+                                   (1, 258, 64)])
+@pytest.mark.parametrize("path", [0, 1])
+def test_lm_head_logprobs_vs_torch(lmlib, ctx, R, V, K, path):
+    """Scoring log-probs (src/tensor.cpp:428-456 log_softmax + :491-519 gather)
+    from bf16 hidden rows and the tied bf16 LM head: the fused tcgen05 LM head
+    with the online-LSE epilogue (path 0) and fp32 logits + K9 (path 1)
+    against torch on the same bf16 operands, fp32 products, fp64 softmax."""
+    import torch
+    px, f = lmlib
+    g = torch.Generator(device="cuda").manual_seed(R + V + K)
+    H = torch.randn(R, K, generator=g, device="cuda").to(torch.bfloat16)
+    W = (torch.randn(V, K, generator=g, device="cuda") * (2.0 / K ** 0.5)).to(torch.bfloat16)
+    tgt = torch.randint(0, V, (R,), generator=g, device="cuda", dtype=torch.int32)
+    tgt[::7] = V - 1  # the ragged last column tile
+    out = torch.zeros(R, dtype=torch.float64, device="cuda")
+    px._check(f(ctx.h, H.data_ptr(), W.data_ptr(), R, V, K, 0, tgt.data_ptr(), out.data_ptr(), path))
+    logits = (H.double() @ W.double().T)
+    ref = torch.log_softmax(logits, dim=-1).gather(1, tgt.long()[:, None])[:, 0]
+    err = (out - ref).abs()
+    assert (err <= 1e-4 * (1 + ref.abs())).all(), f"max abs err {err.max().item():.3e}"
+
+
+def test_k9_on_fp32_logits_vs_torch(lmlib, ctx):
+    import torch
+    px, f = lmlib
+    R, V, ld = 513, 50257, 50304
+    g = torch.Generator(device="cuda").manual_seed(3)
+    L = torch.randn(R, ld, generator=g, device="cuda") * 4
+    tgt = torch.randint(0, V, (R,), generator=g, device="cuda", dtype=torch.int32)
+    out = torch.zeros(R, dtype=torch.float64, device="cuda")
+    px._check(f(ctx.h, L.data_ptr(), None, R, V, 0, ld, tgt.data_ptr(), out.data_ptr(), 2))
+    ref = torch.log_softmax(L[:, :V].double(), dim=-1).gather(1, tgt.long()[:, None])[:, 0]
+    assert (out - ref).abs().max().item() < 1e-4
+
+
+MIXED_SHAPES = [(64, 2304, 768), (64, 768, 3072), (200, 50257, 768), (17, 96, 16), (300, 1000, 768),
+                (2048, 3072, 768), (4096, 768, 3072), (1000, 4096, 4096)]
+
+
+@pytest.mark.parametrize("M,N,K", MIXED_SHAPES)
+@pytest.mark.parametrize("epi", [2, 3, 5])
+def test_gemm_mixed_vs_torch(ctx, M, N, K, epi):
+    """Mixed mode: fp32 activations x bf16 weights on the tensor cores with the
+    two-term activation split must match fp64 products of the same operands to
+    fp32-grade accuracy (bound below, ~1e-6 relative for these shapes)."""
+    import torch
+    from paper_2405_01481_b200 import ppoexp as px
+    f = px.lib().ppoexp_testing_gemm_mixed
+    f.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_int64,
+                  C.c_int32, C.c_void_p, C.c_int64]
+    f.restype = C.c_int32
+    g = torch.Generator(device="cuda").manual_seed(M + 3 * N + 7 * K + epi)
+    A = torch.randn(M, K, generator=g, device="cuda")
+    W = (torch.randn(N, K, generator=g, device="cuda") * 0.05).to(torch.bfloat16)
+    ldc = (N + 63) // 64 * 64
+    Cm = torch.randn(M, ldc, generator=g, device="cuda") if epi == 2 else torch.zeros(M, ldc, device="cuda")
+    base = Cm.double().clone()
+    torch.cuda.synchronize()
+    px._check(f(ctx.h, A.data_ptr(), K, W.data_ptr(), K, M, N, K, epi, Cm.data_ptr(), ldc))
+    ref = A.double() @ W.double().T
+    if epi == 5:
+        ref = torch.nn.functional.gelu(ref, approximate="tanh")
+    if epi == 2:
+        ref = ref + base[:, :N]
+    # the split represents every activation to 2^-18 relative (|a - hi - lo|),
+    # plus fp32 accumulation: bound the error by 2^-16 sum_k |a_k w_k| + fp32 ulps
+    mag = A.double().abs() @ W.double().abs().T
+    if epi == 5:
+        mag = mag * 1.2  # |gelu'| <= 1.13
+    err = (Cm[:, :N].double() - ref).abs()
+    bound = 2.0 ** -16 * mag + 2e-7 * (1 + ref.abs())
+    assert (err <= bound).all(), f"max abs err {err.max().item():.3e}, max err/bound {(err / bound).max().item():.3f}"
