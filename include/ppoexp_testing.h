@@ -18,6 +18,10 @@ PPOEXP_API ppoexp_status ppoexp_testing_gemm_bf16(ppoexp_ctx ctx, const void* A,
                                        int64_t M, int64_t N, int64_t K, int32_t epi, void* C, int64_t ldc,
                                        int32_t path);
 
+/* How often the host chose kernel variant `name` on this context (e.g.
+ * "sampler:pair_uncached"); graph-captured launches count once per capture. */
+PPOEXP_API ppoexp_status ppoexp_testing_variant_count(ppoexp_ctx ctx, const char* name, int64_t* out);
+
 /* Mixed-mode GEMM: C[M,N] (+)= A[M,K] (fp32) · W[N,K]^T (bf16), activations
  * split into two bf16 terms in-kernel.  epi: 2 fp32 residual add, 3 store fp32,
  * 5 GELU -> fp32.  M <= 256 takes the decode (swap-AB, cluster split-K) kernel. */

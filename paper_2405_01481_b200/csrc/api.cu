@@ -85,13 +85,6 @@ void check_offsets(const std::vector<int64_t>& off, int64_t B) {
     if (off[b + 1] < off[b]) throw ContractError("offsets must be non-decreasing");
 }
 
-void check_tokens_host(const int32_t* t, int64_t n, int64_t V) {
-  for (int64_t i = 0; i < n; ++i)
-    if (t[i] < 0 || t[i] >= V)
-      throw IndexError("token id " + std::to_string(t[i]) + " at position " + std::to_string(i) + " out of range [0," +
-                       std::to_string(V) + ")");
-}
-
 // packs caller tokens into the device workspace and uploads the metadata
 Packed pack_tokens(Ctx& c, const int32_t* tokens, const std::vector<int64_t>& off, int where, const std::string& tag) {
   Packed p;
@@ -486,7 +479,7 @@ ppoexp_status ppoexp_sequence_logprobs(ppoexp_model model, int64_t B, const int3
     const auto off = to_host(c, offsets, B + 1, where);
     check_offsets(off, B);
     const int64_t M = off[B];
-    if (where == PPOEXP_HOST) check_tokens_host(tokens, M, m.cfg.vocab_size);
+    check_tokens(c, tokens, M, m.cfg.vocab_size, where, "sequence_logprobs");
     Packed p = pack_tokens(c, tokens, off, where, "lp");
     double* out_d = static_cast<double*>(c.workspace("lp.out", std::max<int64_t>(M, 1) * 8));
     PPOEXP_CUDA(cudaMemsetAsync(out_d, 0, M * 8, c.stream));  // out[start] = 0 (src/model.cpp:487)
@@ -527,7 +520,7 @@ ppoexp_status ppoexp_response_logprob_sums(ppoexp_model model, int64_t B, const 
       roff[b + 1] = roff[b] + T - rs[b];
     }
     const int64_t R = roff[B];
-    if (where == PPOEXP_HOST) check_tokens_host(tokens, off[B], m.cfg.vocab_size);
+    check_tokens(c, tokens, off[B], m.cfg.vocab_size, where, "scoring");
     Packed p = pack_tokens(c, tokens, off, where, "rsum");
     int64_t* rs_d = upload(c, "rsum.rs", rs);
     int64_t* roff_d = upload(c, "rsum.roff", roff);
@@ -577,7 +570,7 @@ ppoexp_status ppoexp_value_estimates(ppoexp_model critic, int64_t B, const int32
       }
       R += T - rs[b];
     }
-    if (where == PPOEXP_HOST) check_tokens_host(tokens, off[B], m.cfg.vocab_size);
+    check_tokens(c, tokens, off[B], m.cfg.vocab_size, where, "scoring");
     int32_t* gd = upload(c, "val.gather", gather);
     int64_t* od = upload(c, "val.oidx", oidx);
     Packed p = pack_tokens(c, tokens, off, where, "val");
@@ -603,7 +596,7 @@ ppoexp_status ppoexp_reward_head(ppoexp_model rm, int64_t B, const int32_t* toke
     check_offsets(off, B);
     for (int64_t b = 0; b < B; ++b)
       if (off[b + 1] == off[b]) throw ContractError("last_content_index: empty sequence");
-    if (where == PPOEXP_HOST) check_tokens_host(tokens, off[B], m.cfg.vocab_size);
+    check_tokens(c, tokens, off[B], m.cfg.vocab_size, where, "scoring");
     Packed p = pack_tokens(c, tokens, off, where, "rw");
     int32_t* gd = static_cast<int32_t*>(c.workspace("rw.gather", B * 4));
     int64_t* od = static_cast<int64_t*>(c.workspace("rw.oidx", B * 8));
@@ -790,7 +783,6 @@ ppoexp_status ppoexp_make_experience(const ppoexp_experience_request* req, int64
     copy_in(c, pd, prompts, off[B] * 4, where);
     int64_t* poff_d = upload(c, "xp.poff", off);
     double gen_ms = 0;
-    if (where == PPOEXP_HOST) check_tokens_host(prompts, off[B], pol.cfg.vocab_size);
     const std::vector<ppoexp_sampling> sps(B, req->sampling);
     E.generate(B, pd, off.data(), mx.data(), sps.data(), seeds.data(), N, gtok, glp, glen, PPOEXP_HOST, &gen_ms,
                PPOEXP_DEVICE, PPOEXP_DEVICE);
@@ -1066,5 +1058,16 @@ extern "C" ppoexp_status ppoexp_testing_gemm_mixed(ppoexp_ctx ctx, const void* A
     gemm_mixed(c, static_cast<const float*>(A), lda, static_cast<const bf16*>(W), ldw, M, N, K, static_cast<Epi>(epi), C,
                ldc);
     c.sync();
+  });
+}
+
+extern "C" ppoexp_status ppoexp_testing_variant_count(ppoexp_ctx ctx, const char* name, int64_t* out) {
+  return guard([&] {
+    need(ctx, "ctx");
+    need(name, "name");
+    need(out, "out");
+    std::lock_guard<std::recursive_mutex> lk(ctx->c->mu);
+    const auto it = ctx->c->variants.find(name);
+    *out = it == ctx->c->variants.end() ? 0 : it->second;
   });
 }

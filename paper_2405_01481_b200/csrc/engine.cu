@@ -436,12 +436,8 @@ void Engine::generate(int64_t B, const int32_t* prompts, const int64_t* offsets,
     if (P > S) throw ContractError("generate: sequence length exceeds max_seq_len " + std::to_string(S));
     if (mx[b] < 0) throw ContractError("generate: max_new must be >= 0");
   }
-  if (where_tokens == PPOEXP_HOST) {
-    for (int64_t i = 0; i < off[B]; ++i)
-      if (prompts[i] < 0 || prompts[i] >= cfg.vocab_size)
-        throw IndexError("generate: token id " + std::to_string(prompts[i]) + " out of range [0," +
-                         std::to_string(cfg.vocab_size) + ")");
-  }
+  // host ids scanned here; device ids by a validation kernel (IndexError before any use)
+  check_tokens(*c, prompts, off[B], cfg.vocab_size, where_tokens < 0 ? where : where_tokens, "generate");
   last_lengths.assign(B, 0);
   cudaEvent_t e0 = t0, e1 = t1;
   PPOEXP_CUDA(cudaEventRecord(e0, c->stream));

@@ -203,6 +203,9 @@ void decode_mega_weight_maps(const MegaLayer* layers_host, int L, int d, int f, 
 void launch_decode_mega(Ctx& c, const MegaArgs& a, double bytes);
 
 // misc
+// IndexError (the reference's wording, src/model.cpp:284-287) for any id outside
+// [0, V): a host scan (where = 0) or a device validation kernel (where = 1).
+void check_tokens(Ctx& c, const int32_t* tokens, int64_t n, int64_t V, int where, const char* what);
 void launch_convert(Ctx& c, const void* src, int src_dtype, void* dst, int dst_dtype, int64_t rows, int64_t cols,
                     bool transpose, int64_t dst_ld, int64_t dst_row0);
 void launch_scripted_reward(Ctx& c, int64_t B, int64_t stride, const int32_t* tokens, const int64_t* lengths,

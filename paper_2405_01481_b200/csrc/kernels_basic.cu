@@ -568,6 +568,43 @@ __global__ void convert_kernel(const void* src, int sdt, void* dst, int ddt, int
   }
 }
 
+// IndexError check for device-resident token ids: the first position whose id is
+// outside [0, V) (atomicMin over positions; n when all are valid).
+__global__ void validate_tokens_kernel(const int32_t* __restrict__ t, int64_t n, int64_t V,
+                                       unsigned long long* __restrict__ first_bad) {
+  PDL_ENTRY();
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    if (t[i] < 0 || t[i] >= V) atomicMin(first_bad, static_cast<unsigned long long>(i));
+}
+
+void check_tokens(Ctx& c, const int32_t* tokens, int64_t n, int64_t V, int where, const char* what) {
+  auto fail = [&](int64_t i, int32_t v) {
+    throw IndexError(std::string(what) + ": token id " + std::to_string(v) + " at position " + std::to_string(i) +
+                     " out of range [0," + std::to_string(V) + ")");
+  };
+  if (n <= 0) return;
+  if (where == 0) {
+    for (int64_t i = 0; i < n; ++i)
+      if (tokens[i] < 0 || tokens[i] >= V) fail(i, tokens[i]);
+    return;
+  }
+  auto* fb = static_cast<unsigned long long*>(c.workspace("validate.first_bad", 16));
+  const unsigned long long init = static_cast<unsigned long long>(n);
+  PPOEXP_CUDA(cudaMemcpyAsync(fb, &init, 8, cudaMemcpyHostToDevice, c.stream));
+  c.launch("validate", 4.0 * n, 0, [&] {
+    launch_kernel(c, validate_tokens_kernel, dim3(std::min<int64_t>(ceil_div(n, 256), 592)), dim3(256), 0, 1, tokens, n,
+                  V, fb);
+  });
+  unsigned long long first = 0;
+  PPOEXP_CUDA(cudaMemcpyAsync(&first, fb, 8, cudaMemcpyDeviceToHost, c.stream));
+  PPOEXP_CUDA(cudaStreamSynchronize(c.stream));
+  if (first < init) {
+    int32_t v = 0;
+    PPOEXP_CUDA(cudaMemcpy(&v, tokens + first, 4, cudaMemcpyDeviceToHost));
+    fail(int64_t(first), v);
+  }
+}
+
 void launch_convert(Ctx& c, const void* src, int src_dtype, void* dst, int dst_dtype, int64_t rows, int64_t cols,
                     bool transpose, int64_t dst_ld, int64_t dst_row0) {
   if (rows * cols <= 0) return;

@@ -67,6 +67,7 @@ struct Ctx {
   int64_t launches = 0;          // eager launches + graph-replayed kernel nodes
   int64_t capture_launches = 0;  // kernels recorded into the graph being captured
   std::map<std::string, ClassStats> stats;
+  std::map<std::string, int64_t> variants;  // kernel-variant choices made on the host (tests assert the branch ran)
   std::vector<TimedLaunch> pending;          // eager timed launches to harvest
   std::vector<TimedLaunch>* capture_events = nullptr;  // events recorded while capturing
   std::vector<cudaEvent_t> event_pool;

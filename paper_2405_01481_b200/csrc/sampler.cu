@@ -802,6 +802,7 @@ void launch_sampler(Ctx& c, const float* logits, int64_t ld, int64_t B, int64_t 
   if (pair_ok && !pair) {
     // vocabularies too large for the per-CTA logit cache (e.g. 128k): still a
     // CTA pair per row, each streaming its half of the row from L2 every pass
+    ++c.variants["sampler:pair_uncached"];
     c.launch("sampler", double(B) * V * 4, 0, [&] {
       cudaLaunchConfig_t cfg{};
       cfg.gridDim = dim3(unsigned(2 * B));
@@ -820,6 +821,7 @@ void launch_sampler(Ctx& c, const float* logits, int64_t ld, int64_t B, int64_t 
       PPOEXP_CUDA(cudaLaunchKernelEx(&cfg, sampler_kernel<false, 2>, logits, ld, V, s));
     });
   } else if (pair) {
+    ++c.variants["sampler:pair_cached"];
     const int64_t half = (V + 7) / 8 * 4;
     const size_t smem = size_t(half) * sizeof(float);
     static bool attr = false;
@@ -846,6 +848,7 @@ void launch_sampler(Ctx& c, const float* logits, int64_t ld, int64_t B, int64_t 
       PPOEXP_CUDA(cudaLaunchKernelEx(&cfg, sampler_kernel<true, 2>, logits, ld, V, s));
     });
   } else if (V <= kCacheMaxV) {
+    ++c.variants["sampler:single_cached"];
     const size_t smem = size_t(V) * sizeof(float);
     static bool attr = false;
     if (!attr) {
@@ -856,6 +859,7 @@ void launch_sampler(Ctx& c, const float* logits, int64_t ld, int64_t B, int64_t 
     c.launch("sampler", double(B) * V * 4, 0,
              [&] { launch_kernel(c, sampler_kernel<true, 1>, dim3(B), dim3(NT), smem, 1, logits, ld, V, s); });
   } else {
+    ++c.variants["sampler:single_uncached"];
     c.launch("sampler", double(B) * V * 4, 0,
              [&] { launch_kernel(c, sampler_kernel<false, 1>, dim3(B), dim3(NT), 0, 1, logits, ld, V, s); });
   }

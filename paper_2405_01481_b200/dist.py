@@ -16,10 +16,12 @@ class _CudaArray:
                                          "strides": None, "stream": None}
 
 
-def allgather_sum_fn(group=None, device=None):
+def allgather_sum_fn(group=None, device=None, stage_on_host=False):
     """fn(ptr, n, stream) for ExperienceMaker(allreduce=...): replaces the n
     doubles at ptr (device memory on `device`, or host memory when device is
-    None/cpu) by their sum over the ranks of `group`, in rank order."""
+    None/cpu) by their sum over the ranks of `group`, in rank order.
+    stage_on_host: gather through host tensors (a gloo group over device
+    buffers, e.g. several ranks sharing one GPU in the tests)."""
     import torch
     import torch.distributed as dist
 
@@ -31,12 +33,13 @@ def allgather_sum_fn(group=None, device=None):
             buf = torch.from_numpy(host)
         else:
             buf = torch.as_tensor(_CudaArray(ptr, n), device=device)
-        parts = [torch.empty_like(buf) for _ in range(world)]
-        dist.all_gather(parts, buf.clone(), group=group)
+        src = buf.cpu() if stage_on_host else buf.clone()
+        parts = [torch.empty_like(src) for _ in range(world)]
+        dist.all_gather(parts, src, group=group)
         total = parts[0].clone()
         for p in parts[1:]:  # fixed rank order
             total += p
-        buf.copy_(total)
+        buf.copy_(total.to(buf.device))
         if buf.is_cuda:
             torch.cuda.current_stream(buf.device).synchronize()
 

@@ -101,3 +101,17 @@ def test_build_sft_sequence_layout():
         px.build_sft_sequence(cfg, [], [1])
     with pytest.raises(px.ContractError, match="leaves no room for a response"):
         px.build_sft_sequence(cfg, list(range(9)), [1, 2, 3])
+
+
+@pytest.mark.gpu
+def test_cpp_facade_two_ranks_nccl(lib):
+    """Compiled C++ caller, two processes, one GPU each, the library's own NCCL
+    collective (ppoexp_comm_*): identical global statistics on both ranks."""
+    import subprocess
+
+    import torch
+    n = torch.cuda.device_count()
+    if n < 2:
+        pytest.skip("needs two GPUs")
+    r = subprocess.run([_build_facade_test(), "--ranks2", str(n)], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "RANKS2 OK" in r.stdout, (r.returncode, r.stdout, r.stderr)

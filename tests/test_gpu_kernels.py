@@ -81,6 +81,7 @@ def test_lm_head_logprobs_vs_torch(lmlib, ctx, R, V, K, path):
     tgt = torch.randint(0, V, (R,), generator=g, device="cuda", dtype=torch.int32)
     tgt[::7] = V - 1  # the ragged last column tile
     out = torch.zeros(R, dtype=torch.float64, device="cuda")
+    torch.cuda.synchronize()  # the library runs on its own stream
     px._check(f(ctx.h, H.data_ptr(), W.data_ptr(), R, V, K, 0, tgt.data_ptr(), out.data_ptr(), path))
     logits = (H.double() @ W.double().T)
     ref = torch.log_softmax(logits, dim=-1).gather(1, tgt.long()[:, None])[:, 0]
@@ -96,6 +97,7 @@ def test_k9_on_fp32_logits_vs_torch(lmlib, ctx):
     L = torch.randn(R, ld, generator=g, device="cuda") * 4
     tgt = torch.randint(0, V, (R,), generator=g, device="cuda", dtype=torch.int32)
     out = torch.zeros(R, dtype=torch.float64, device="cuda")
+    torch.cuda.synchronize()
     px._check(f(ctx.h, L.data_ptr(), None, R, V, 0, ld, tgt.data_ptr(), out.data_ptr(), 2))
     ref = torch.log_softmax(L[:, :V].double(), dim=-1).gather(1, tgt.long()[:, None])[:, 0]
     assert (out - ref).abs().max().item() < 1e-4

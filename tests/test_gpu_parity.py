@@ -464,3 +464,180 @@ def test_bf16_decode_is_deterministic(px, ctx, oracle, monkeypatch, fuse_ln):
         for a, b in zip(runs[0], r):
             assert np.array_equal(a.tokens, b.tokens)
             assert np.array_equal(a.logprobs, b.logprobs)
+
+
+# ----------------------------------------------------------------- mixed mode (the parity-grade fast path)
+# bf16 weights (the same bf16-rounded weights on both sides: "identical weights"),
+# fp32 activations / KV, tensor-core products on a two-term bf16 split of every
+# activation.  Held to the north_star bar exactly: greedy / sampled tokens and
+# sample counts bit-exact, log-probs / KL / values / advantages within
+# 1e-3 abs + 1e-3 rel (ATOL, RTOL above).
+
+def _mixed_experience_check(px, ctx, oracle, cfg, prompts, N, seed=3, kl=0.003, tol_scale=1.0):
+    wp = bf16_round(oracle.init_params(cfg, seed))
+    wr = bf16_round(oracle.init_params(cfg, seed + 1))
+    wc = bf16_round(oracle.init_params(cfg, seed + 2, head=True, head_seed=seed + 3))
+    pc = to_px_cfg(cfg)
+    eng = px.Engine(px.DeviceModel(ctx, pc, wp, px.MIXED))
+    ref = px.DeviceModel(ctx, pc, wr, px.MIXED)
+    crit = px.DeviceModel(ctx, pc.with_head(), wc, px.MIXED)
+    xm = px.ExperienceMaker(eng, ref, crit, scripted_target=ord("e"), hyper=px.PpoHyper(kl, 1.0, 0.95))
+    batch, st = xm.run(prompts, max_new=N, sampling=px.SamplingSpec.greedy_spec(), seed=seed)
+    exp = oracle.experience(cfg, wp, wr, wc, prompts, max_new=N, greedy=True, kl_coef=kl, scripted_target=ord("e"))
+    worst = {}
+    for i, s in enumerate(batch):
+        assert np.array_equal(s.response, exp["tokens"][i]), f"greedy rollout {i} differs from the oracle"
+        for k, got, want in (("actor_lp", s.actor_logprobs, exp["actor_logprobs"][i]),
+                             ("ref_lp", s.ref_logprobs, exp["ref_logprobs"][i]),
+                             ("kl", s.actor_logprobs - s.ref_logprobs,
+                              exp["actor_logprobs"][i] - exp["ref_logprobs"][i]),
+                             ("values", s.values, exp["values"][i]), ("advantages", s.advantages, exp["advantages"][i]),
+                             ("returns", s.returns, exp["returns"][i]), ("whitened", s.whitened_advantages,
+                                                                         exp["whitened"][i])):
+            worst[k] = max(worst.get(k, 0.0), close(got, want, ATOL * tol_scale, RTOL * tol_scale))
+    close([s.reward for s in batch], exp["rewards"], 0, 0)  # scripted counts: exact
+    close(st.kl_mean, exp["kl_mean"])
+    close(st.reward_mean, exp["reward_mean"], 0, 0)
+    eng.close()
+    return worst
+
+
+def test_mixed_experience_c1(px, ctx, oracle):
+    cfg = ModelCfg(V=1024, d=128, L=2, H=4, f=512, S=128)
+    _mixed_experience_check(px, ctx, oracle, cfg, synthetic_prompts(7, 8, 9, ragged_lengths=True), 64)
+
+
+def test_mixed_experience_c2_full_depth(px, ctx, oracle):
+    """The benchmarked C2 shape at full depth (12 layers, d 768, vocab 50257)."""
+    cfg = ModelCfg(V=50257, d=768, L=12, H=12, f=3072, S=512)
+    w = _mixed_experience_check(px, ctx, oracle, cfg, synthetic_prompts(5, 4, 16, ragged_lengths=True), 24)
+    print("c2 worst abs errors", w)
+
+
+@pytest.mark.parametrize("shape", ["c3", "c4"])
+def test_mixed_experience_wide(px, ctx, oracle, shape):
+    """C3 width (d 2048, vocab 32000) and C4 width (d 4096, vocab 128256, the
+    uncached large-vocab sampler), one layer to keep the fp64 oracle short."""
+    cfg = (ModelCfg(V=32000, d=2048, L=1, H=16, f=8192, S=1024) if shape == "c3"
+           else ModelCfg(V=128256, d=4096, L=1, H=32, f=14336, S=2048))
+    _mixed_experience_check(px, ctx, oracle, cfg, synthetic_prompts(9, 2, 8, ragged_lengths=True), 8)
+
+
+@pytest.mark.parametrize("top_k,top_p,tau", [(0, 1.0, 0.7), (0, 0.9, 1.0), (40, 0.95, 1.3)])
+def test_mixed_sampled_tokens_exact(px, ctx, oracle, top_k, top_p, tau):
+    """Temperature / top-k / top-p sampling (one mt19937_64 uniform per token):
+    tokens and sample counts bit-exact against the oracle on the same weights."""
+    cfg = ModelCfg(V=1024, d=128, L=2, H=4, f=512, S=128)
+    w = bf16_round(oracle.init_params(cfg, 13))
+    w[:cfg.V * cfg.d] *= 20.0  # sharpen the distribution so the filters cut inside the row
+    w = bf16_round(w)
+    prompts = synthetic_prompts(17, 8, 9, ragged_lengths=True)
+    N = 40
+    eng = engine(px, ctx, cfg, w, px.MIXED)
+    seeds = [oracle.mix_seed(29, i) for i in range(len(prompts))]
+    res = eng.generate_batch([px.GenTask(p, N, px.SamplingSpec.temperature_spec(tau, s, top_k, top_p))
+                              for p, s in zip(prompts, seeds)])
+    u = np.stack([oracle.uniforms(s, N) for s in seeds])
+    t_o, l_o = oracle.generate(cfg, w, prompts, N, greedy=False, temperature=tau, top_k=top_k, top_p=top_p,
+                               uniforms=u)
+    for r, t, l in zip(res, t_o, l_o):
+        assert np.array_equal(r.tokens, t)
+        close(r.logprobs, l)
+
+
+def test_mixed_response_logprob_sums(px, ctx, oracle):
+    """DPO scoring sums (frozen_response_logprob_sum, src/trainers.cpp:24-29) at
+    the C2 width / vocab through the fused LM-head + LSE epilogue."""
+    cfg = ModelCfg(V=50257, d=768, L=2, H=12, f=3072, S=512)
+    w = bf16_round(oracle.init_params(cfg, 31))
+    m = px.DeviceModel(ctx, to_px_cfg(cfg), w, px.MIXED)
+    rng = np.random.default_rng(3)
+    seqs, rs = [], []
+    for i in range(6):
+        full, r = px.build_sft_sequence(to_px_cfg(cfg), rng.integers(0, 256, 5 + 3 * i).tolist(),
+                                        rng.integers(0, 256, 4 + 5 * i).tolist())
+        seqs.append(full)
+        rs.append(r)
+    got = px.response_logprob_sums(m, seqs, rs)
+    lps = oracle.sequence_logprobs(cfg, w, seqs)
+    close(got, [float(sum(lp[r:])) for lp, r in zip(lps, rs)])
+    close(np.concatenate(px.sequence_logprobs(m, seqs)), np.concatenate(lps))
+
+
+@pytest.mark.parametrize("dtype", ["mixed", "bf16"])
+def test_fused_ln_statistics_with_outliers(px, ctx, oracle, dtype):
+    """1e3-magnitude outlier features at d = 4096 (massive activations): the
+    fused-LayerNorm fixed-point row statistics stay in range and the decode
+    matches the oracle teacher-forced (mixed: within the north_star bar)."""
+    cfg = ModelCfg(V=2048, d=4096, L=1, H=32, f=1024, S=64)
+    w = oracle.init_params(cfg, 37)
+    pos0 = cfg.V * cfg.d
+    for p_ in range(cfg.S):  # 8 outlier features of magnitude ~1e3 in every position
+        w[pos0 + p_ * cfg.d + np.arange(0, 4096, 512)] = 1000.0 * (1 + 0.01 * p_)
+    w = bf16_round(w)
+    prompts = synthetic_prompts(41, 4, 6, ragged_lengths=True)
+    eng = engine(px, ctx, cfg, w, px.MIXED if dtype == "mixed" else px.BF16)
+    res = eng.generate_batch([px.GenTask(p, 12) for p in prompts])
+    for r, p in zip(res, prompts):
+        lp = oracle.sequence_logprobs(cfg, w, [np.concatenate([p, r.tokens])])[0][len(p):]
+        if dtype == "mixed":
+            close(r.logprobs, lp)
+        else:
+            close(r.logprobs, lp, atol=5e-2, rtol=5e-3)
+
+
+def test_fused_ln_statistics_overflow_is_an_error(px, ctx, oracle):
+    """A residual stream beyond the fixed-point range fails loudly (no silent clamp)."""
+    cfg = ModelCfg(V=512, d=256, L=1, H=4, f=512, S=32)
+    w = oracle.init_params(cfg, 43)
+    pos0 = cfg.V * cfg.d
+    w[pos0:pos0 + cfg.S * cfg.d] = 3.0e5
+    eng = engine(px, ctx, cfg, bf16_round(w), px.BF16)
+    with pytest.raises(px.ContractError, match="statistics range"):
+        eng.generate_batch([px.GenTask([1, 2, 3], 4)])
+
+
+def test_large_vocab_uncached_sampler_branch(px, ctx, oracle):
+    """Vocab 128256 > 2 x the per-CTA logit cache: the uncached CTA-pair sampler
+    (sampler_kernel<false, 2>, the config-4 path), token-exact vs the oracle."""
+    cfg = ModelCfg(V=128256, d=32, L=1, H=2, f=64, S=48)
+    w = oracle.init_params(cfg, 17).astype(np.float32).astype(np.float64)
+    w[:cfg.V * cfg.d] *= 40.0
+    prompts = synthetic_prompts(19, 6, 8, ragged_lengths=True)
+    N = 6
+    import ctypes
+    f = px.lib().ppoexp_testing_variant_count
+    f.argtypes = [ctypes.c_void_p, ctypes.c_char_p, ctypes.c_void_p]
+    n0 = ctypes.c_int64()
+    px._check(f(ctx.h, b"sampler:pair_uncached", ctypes.byref(n0)))
+    eng = engine(px, ctx, cfg, w, px.F32)
+    for top_k, top_p in ((0, 0.9), (50, 0.95), (0, 1.0)):
+        seeds = [oracle.mix_seed(23 + top_k, i) for i in range(len(prompts))]
+        res = eng.generate_batch([px.GenTask(p, N, px.SamplingSpec.temperature_spec(1.0, s, top_k, top_p))
+                                  for p, s in zip(prompts, seeds)])
+        u = np.stack([oracle.uniforms(s, N) for s in seeds])
+        t_o, l_o = oracle.generate(cfg, w, prompts, N, greedy=False, top_k=top_k, top_p=top_p, uniforms=u)
+        for r, t, l in zip(res, t_o, l_o):
+            assert np.array_equal(r.tokens, t)
+            close(r.logprobs, l)
+    n1 = ctypes.c_int64()
+    px._check(f(ctx.h, b"sampler:pair_uncached", ctypes.byref(n1)))
+    assert n1.value > n0.value, "the uncached CTA-pair sampler branch did not run"
+
+
+def test_device_token_ids_are_validated(px, ctx, oracle):
+    """Out-of-range ids in DEVICE-resident inputs raise IndexError (a device
+    validation kernel) instead of reading out of bounds (the reference throws
+    IndexError, src/model.cpp:284-287)."""
+    import torch
+    cfg = ModelCfg(258, 32, 1, 2, 64, 32)
+    m = px.DeviceModel(ctx, to_px_cfg(cfg), oracle.init_params(cfg, 5), px.BF16)
+    toks = torch.tensor([1, 2, 3, 300, 4], dtype=torch.int32, device="cuda")
+    offs = torch.tensor([0, 5], dtype=torch.int64, device="cuda")
+    out = torch.zeros(5, dtype=torch.float64, device="cuda")
+    torch.cuda.synchronize()
+    rc = px.lib().ppoexp_sequence_logprobs(m.h, 1, toks.data_ptr(), offs.data_ptr(), out.data_ptr(), px.DEVICE)
+    with pytest.raises(px.IndexError_, match="position 3"):
+        px._check(rc)
+    # the context stays usable
+    assert len(px.sequence_logprobs(m, [[1, 2, 3]])[0]) == 3
