@@ -7,8 +7,14 @@ experience samples/s, 1/2/4/8 B200 vs the host-CPU reference).
 A step = one experience step (ppo_step's experience half, src/ppo.cpp:302-393,
 + advantage whitening) for this rank's prompts: batched rollout decode,
 policy + reference log-probs, critic values, scripted reward, KL shaping, GAE
-and whitening through ONE all-gather of 6 fp64 partials.  Weak scaling: every
-rank owns B prompts (global indices rank*B ...).
+and whitening through ONE all-gather of 6 fp64 partials (the library's own
+NCCL communicator).  Weak scaling (c1, c2, c4): every rank owns B prompts
+(global indices rank*B ...); strong scaling (c3): 256 prompts split over ranks.
+
+dtype: the headline runs the mixed mode (bf16 weights, fp32-grade activations
+and KV: the mode that meets the north_star parity bar, tests/test_gpu_parity.py
+test_mixed_*); the bf16-activation variant is measured the same way and
+reported inside the line as `bf16_variant`.
 
 value        = rollout tokens/s (generated tokens incl. EOT / generation-phase
                device time, CUDA events, max over ranks), inputs resident in HBM.
@@ -297,6 +303,35 @@ def decode_bytes(cfg_t, B, act_bytes=2):
 
 
 def run_ours(args):
+    """The headline line (args.dtype, default mixed) plus, for mixed, the bf16
+    variant measured the same way and reported inside the line."""
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    line = bench_mode(args, args.dtype, primary=True)
+    if args.dtype == "mixed" and args.variant:
+        v = bench_mode(args, "bf16", primary=False)
+        if line is not None and v is not None:
+            line["bf16_variant"] = {
+                k: v[k] for k in ("value", "ms_per_step", "experience_samples_per_s", "gen_ms_per_step", "e2e",
+                                  "decode_step_roofline", "roofline") if k in v}
+            line["bf16_variant"]["dtype"] = DTYPE_LABEL["bf16"]
+            line["bf16_variant"]["note"] = ("bf16 activations / KV: faster, but values and advantages miss the "
+                                            "1e-3 + 1e-3|x| bar by up to ~15x (tools/parity_probe.py); the headline "
+                                            "`value` is the parity-grade mixed mode")
+    if line is not None:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def bench_mode(args, dtype, primary):
     import torch
     import torch.distributed as dist
     from paper_2405_01481_b200 import ppoexp as px
@@ -304,9 +339,6 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     cfg_t = CONFIGS[args.config]
     V, d, L, H, f, S, Bc, P, N, samp, desc = cfg_t
@@ -317,7 +349,7 @@ def run_ours(args):
     w_pol = init_weights(cfg, SEED, dev)
     w_ref = init_weights(cfg, SEED + 1, dev)
     w_crit = init_weights(cfg, SEED + 101, dev, head=True)
-    DT = {"mixed": px.MIXED, "bf16": px.BF16}[args.dtype]
+    DT = {"mixed": px.MIXED, "bf16": px.BF16}[dtype]
     policy = px.DeviceModel(ctx, cfg, w_pol, DT)
     engine = px.Engine(policy, px.EngineOptions(max_batch=max(B, 1), page_size=64,
                                                  max_total_tokens=B * (-(-(P + N) // 64)) * 64))
@@ -326,13 +358,17 @@ def run_ours(args):
     del w_pol, w_ref, w_crit
     torch.cuda.synchronize()
 
-    # the single collective: all-gather of the 6 fp64 partials, summed in rank
-    # order on every rank (paper_2405_01481_b200/dist.py)
-    from paper_2405_01481_b200.dist import allgather_sum_fn
-    allreduce = allgather_sum_fn(device=dev) if world > 1 else None
+    # the single collective: the library's own NCCL communicator all-gathers the
+    # 6 fp64 partials and sums them in rank order on every rank (ppoexp_comm_*);
+    # torch.distributed only ships the 128-byte NCCL id
+    comm = None
+    if world > 1:
+        uid = [px.Communicator.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = px.Communicator(ctx, uid[0], rank, world)
 
     xm = px.ExperienceMaker(engine, reference, critic, scripted_target=ord("e"),
-                            hyper=px.PpoHyper(0.003, 1.0, 0.95), allreduce=allreduce)
+                            hyper=px.PpoHyper(0.003, 1.0, 0.95), comm=comm)
     sampling = (px.SamplingSpec.greedy_spec() if samp == "greedy"
                 else px.SamplingSpec.temperature_spec(1.0, 0, 0, TOP_P))
     prompts = prompts_for(rank, B, P, V, SEED)
@@ -410,7 +446,7 @@ def run_ours(args):
 
     # ---- e2e through the C ABI with HOST buffers (pinned staging inside the library)
     e2e_tok, e2e_xp, h2d, d2h = None, None, 0, 0
-    if args.e2e_steps > 0:
+    if args.e2e_steps > 0 and primary:
         tasks = [px.GenTask(p, N, px.SamplingSpec.temperature_spec(1.0, 1000 + rank * B + i, 0, TOP_P)
                             if samp != "greedy" else px.SamplingSpec.greedy_spec()) for i, p in enumerate(prompts)]
         walls, ntok = [], 0
@@ -438,7 +474,7 @@ def run_ours(args):
         line = {"metric": "rollout_tokens_per_s", "value": value, "unit": "tokens/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_step_s * 1000 / args.steps,
                 "higher_is_better": True, "scaling": "strong" if args.config in STRONG else "weak",
-                "vs_baseline": None, "dtype": DTYPE_LABEL[args.dtype],
+                "vs_baseline": None, "dtype": DTYPE_LABEL[dtype],
                 "data": "synthetic prompts, random-init weights",
                 "config": workload_config(args, world, B),
                 "experience_samples_per_s": samples_per_s,
@@ -449,7 +485,7 @@ def run_ours(args):
             line["e2e"] = {"value": e2e_tok, "unit": "tokens/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                            "experience_samples_per_s": e2e_xp,
                            "api": "ppoexp_engine_generate / ppoexp_make_experience, HOST buffers"}
-        db = decode_bytes(cfg_t, B, 4 if args.dtype == "mixed" else 2)
+        db = decode_bytes(cfg_t, B, 4 if dtype == "mixed" else 2)
         gen_step_s = total_gen_s / args.steps / steps_per_gen  # timed region: mean decode unit
         line["decode_step_roofline"] = {
             "bound": "hbm", "achieved": db["step"] / gen_step_s / 1e9, "peak": hbm, "unit": "GB/s",
@@ -493,7 +529,7 @@ def run_ours(args):
                 ach = db["decode_attention"] / db["decode_attention_launches"] / (a_["us"] / a_["launches"]) / 1e3
                 line["roofline_decode_attention"] = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
                                                      "frac": ach / hbm}
-        if not args.no_cpu_baseline and world == 1:
+        if not args.no_cpu_baseline and world == 1 and primary:
             try:
                 threads = host_threads()
                 r = reference_sample(cfg_t, threads, steps=1, B=B)
@@ -503,7 +539,6 @@ def run_ours(args):
             except Exception as e:  # reference build absent
                 line["cpu_baseline"] = {"value": None, "unit": "tokens/s", "cores": 0, "kind": "reference",
                                         "sample": f"unavailable: {e}"}
-        print(json.dumps(line), flush=True)
     # Ordered teardown: torch tensors that lived on the library stream, then the
     # library objects (engine before its models, models before the context),
     # then the process group.
@@ -512,14 +547,14 @@ def run_ours(args):
     torch.cuda.synchronize()
     torch.cuda.empty_cache()
     xm = None
+    if comm is not None:
+        comm.close()
     engine.close()
     policy.close()
     reference.close()
     critic.close()
     ctx.close()
-    if world > 1:
-        dist.barrier()
-        dist.destroy_process_group()
+    return line if rank == 0 else None
 
 
 def main():
@@ -534,6 +569,8 @@ def main():
     ap.add_argument("--profile-classes", action="store_true", default=True)
     ap.add_argument("--no-profile", dest="profile_classes", action="store_false")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-variant", dest="variant", action="store_false",
+                    help="mixed headline only (skip the bf16-activation variant)")
     ap.add_argument("--dtype", default="mixed", choices=["mixed", "bf16"],
                     help="mixed: bf16 weights + fp32-grade activations/KV (meets the 1e-3 parity bar); "
                          "bf16: bf16 activations/KV (faster, outside the bar for values)")
