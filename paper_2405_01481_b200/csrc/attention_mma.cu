@@ -219,6 +219,222 @@ __global__ void __launch_bounds__(128) attn_prefill_mma_kernel(const bf16* __res
   }
 }
 
+// ---------------------------------------------------------------- mixed mode
+// The same FlashAttention-2 structure with fp32-grade products for mixed mode:
+// q, k, v arrive in fp32; each tile is split into two bf16 terms (x = hi + lo,
+// |x - hi - lo| <= 2^-18 |x|) and every product takes three MMAs
+// (hi*hi + hi*lo + lo*hi; the lo*lo term is below fp32 rounding): S = Q K^T and
+// O += P V with P split the same way after the fp32 online softmax.  K / V
+// tiles are staged as fp32 by cp.async one tile ahead and split in shared memory.
+__device__ __forceinline__ void split2(float x0, float x1, uint32_t& hi, uint32_t& lo) {
+  const __nv_bfloat162 h = __floats2bfloat162_rn(x0, x1);
+  const float2 hf = __bfloat1622float2(h);
+  const __nv_bfloat162 l = __floats2bfloat162_rn(x0 - hf.x, x1 - hf.y);
+  hi = *reinterpret_cast<const uint32_t*>(&h);
+  lo = *reinterpret_cast<const uint32_t*>(&l);
+}
+
+template <int DH>
+struct SplitSmem {
+  static constexpr int LD = DH + 8;                 // bf16 row (conflict-free ldmatrix)
+  static constexpr int kTile = 64 * LD;             // elements of one 64-row bf16 tile
+  static constexpr int kStage = 64 * DH;            // fp32 elements of one staged 64-row tile
+  // bf16: Qh Ql Kh Kl Vh Vl; fp32 staging: K, V
+  static constexpr size_t kBytes = size_t(6) * kTile * 2 + size_t(2) * kStage * 4;
+};
+
+template <int DH>
+__global__ void __launch_bounds__(128) attn_prefill_split_kernel(const float* __restrict__ qkv,
+                                                                 const int64_t* __restrict__ seq_offsets, int64_t H,
+                                                                 float* __restrict__ out) {
+  PDL_ENTRY();
+  using SL = SplitSmem<DH>;
+  constexpr int LD = SL::LD, KC = DH / 16, NO = DH / 8, CH4 = DH / 4;
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  bf16* sb = reinterpret_cast<bf16*>(smem_raw);
+  bf16 *sQh = sb, *sQl = sb + SL::kTile, *sKh = sb + 2 * SL::kTile, *sKl = sb + 3 * SL::kTile;
+  bf16 *sVh = sb + 4 * SL::kTile, *sVl = sb + 5 * SL::kTile;
+  float* stK = reinterpret_cast<float*>(sb + 6 * SL::kTile);
+  float* stV = stK + SL::kStage;
+  const int64_t b = blockIdx.z, h = blockIdx.y, q0 = int64_t(blockIdx.x) * QT;
+  const int64_t start = seq_offsets[b], len = seq_offsets[b + 1] - start;
+  if (q0 >= len) return;
+  const int64_t d = H * DH, ld3 = 3 * d;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t4 = lane & 3;
+
+  // fp32 rows -> staging (cp.async, zero-filled past the end)
+  auto stage_rows = [&](float* dst, int64_t row0, int64_t col0) {
+    for (int e = tid; e < 64 * CH4; e += 128) {
+      const int r = e / CH4, c = e % CH4;
+      const int64_t rr = row0 + r;
+      const bool ok = rr < len;
+      cp_async16(dst + r * DH + c * 4, qkv + (start + (ok ? rr : 0)) * ld3 + col0 + c * 4, ok);
+    }
+  };
+  // staging (or registers for Q) -> hi / lo bf16 tiles
+  auto split_tile = [&](const float* src, bf16* hi, bf16* lo) {
+    for (int e = tid; e < 64 * CH4; e += 128) {
+      const int r = e / CH4, c = e % CH4;
+      const float4 v = *reinterpret_cast<const float4*>(src + r * DH + c * 4);
+      uint32_t h0, l0, h1, l1;
+      split2(v.x, v.y, h0, l0);
+      split2(v.z, v.w, h1, l1);
+      *reinterpret_cast<uint2*>(hi + r * LD + c * 4) = make_uint2(h0, h1);
+      *reinterpret_cast<uint2*>(lo + r * LD + c * 4) = make_uint2(l0, l1);
+    }
+  };
+  const int64_t kend = min(len, q0 + QT);
+  const int ntiles = int((kend + KT - 1) / KT);
+  // Q through the K staging buffer, then the first K / V tile
+  stage_rows(stK, q0, h * DH);
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncthreads();
+  split_tile(stK, sQh, sQl);
+  __syncthreads();
+  stage_rows(stK, 0, d + h * DH);
+  stage_rows(stV, 0, 2 * d + h * DH);
+  cp_async_commit();
+
+  uint32_t qh[KC][4], ql[KC][4];
+  float o[NO][4];
+#pragma unroll
+  for (int i = 0; i < NO; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+  float m_r[2] = {-FLT_MAX, -FLT_MAX}, l_r[2] = {0.f, 0.f};
+  const float scale = 1.0f / sqrtf(float(DH));
+  const int64_t qrow0 = q0 + warp * 16 + g, qrow1 = qrow0 + 8;
+#pragma unroll
+  for (int kc = 0; kc < KC; ++kc) {
+    const int r = warp * 16 + (lane & 15), c = kc * 16 + (lane >> 4) * 8;
+    ldsm_x4(qh[kc][0], qh[kc][1], qh[kc][2], qh[kc][3], sQh + r * LD + c);
+    ldsm_x4(ql[kc][0], ql[kc][1], ql[kc][2], ql[kc][3], sQl + r * LD + c);
+  }
+
+  for (int it = 0; it < ntiles; ++it) {
+    cp_async_wait<0>();
+    __syncthreads();  // staged tile landed; the previous tile's MMAs are done with the split tiles
+    split_tile(stK, sKh, sKl);
+    split_tile(stV, sVh, sVl);
+    __syncthreads();  // split tiles visible; staging free
+    if (it + 1 < ntiles) {
+      stage_rows(stK, int64_t(it + 1) * KT, d + h * DH);
+      stage_rows(stV, int64_t(it + 1) * KT, 2 * d + h * DH);
+      cp_async_commit();
+    }
+    const int64_t k0 = int64_t(it) * KT;
+    float s[KT / 8][4];
+#pragma unroll
+    for (int j = 0; j < KT / 8; ++j) s[j][0] = s[j][1] = s[j][2] = s[j][3] = 0.f;
+#pragma unroll
+    for (int kc = 0; kc < KC; ++kc) {
+#pragma unroll
+      for (int j = 0; j < KT / 8; j += 2) {
+        uint32_t b0, b1, b2, b3, c0, c1, c2, c3;
+        const int r = j * 8 + (lane & 7) + ((lane >> 4) << 3), c = kc * 16 + ((lane >> 3) & 1) * 8;
+        ldsm_x4(b0, b1, b2, b3, sKh + r * LD + c);
+        ldsm_x4(c0, c1, c2, c3, sKl + r * LD + c);
+        mma16816(s[j], ql[kc], b0, b1);  // small terms first
+        mma16816(s[j + 1], ql[kc], b2, b3);
+        mma16816(s[j], qh[kc], c0, c1);
+        mma16816(s[j + 1], qh[kc], c2, c3);
+        mma16816(s[j], qh[kc], b0, b1);
+        mma16816(s[j + 1], qh[kc], b2, b3);
+      }
+    }
+    // scale, causal / length mask, online softmax (fp32, exp in the natural domain)
+    float mx[2] = {-FLT_MAX, -FLT_MAX};
+#pragma unroll
+    for (int j = 0; j < KT / 8; ++j)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int64_t key = k0 + j * 8 + 2 * t4 + (e & 1);
+        const int64_t qr = e < 2 ? qrow0 : qrow1;
+        float v = s[j][e] * scale;
+        if (key > qr || key >= len) v = -FLT_MAX;
+        s[j][e] = v;
+        mx[e >> 1] = fmaxf(mx[e >> 1], v);
+      }
+    float corr[2];
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 1));
+      mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 2));
+      const float mn = fmaxf(m_r[r], mx[r]);
+      corr[r] = m_r[r] == -FLT_MAX ? 0.f : expf(m_r[r] - mn);
+      m_r[r] = mn;
+    }
+    float rs[2] = {0.f, 0.f};
+#pragma unroll
+    for (int j = 0; j < KT / 8; ++j)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int r = e >> 1;
+        const float p = s[j][e] == -FLT_MAX ? 0.f : expf(s[j][e] - m_r[r]);
+        s[j][e] = p;
+        rs[r] += p;
+      }
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      rs[r] += __shfl_xor_sync(0xffffffffu, rs[r], 1);
+      rs[r] += __shfl_xor_sync(0xffffffffu, rs[r], 2);
+      l_r[r] = l_r[r] * corr[r] + rs[r];
+    }
+#pragma unroll
+    for (int i = 0; i < NO; ++i) {
+      o[i][0] *= corr[0];
+      o[i][1] *= corr[0];
+      o[i][2] *= corr[1];
+      o[i][3] *= corr[1];
+    }
+#pragma unroll
+    for (int kk = 0; kk < KT / 16; ++kk) {
+      uint32_t ph[4], pl[4];
+      split2(s[2 * kk][0], s[2 * kk][1], ph[0], pl[0]);
+      split2(s[2 * kk][2], s[2 * kk][3], ph[1], pl[1]);
+      split2(s[2 * kk + 1][0], s[2 * kk + 1][1], ph[2], pl[2]);
+      split2(s[2 * kk + 1][2], s[2 * kk + 1][3], ph[3], pl[3]);
+#pragma unroll
+      for (int i = 0; i < NO; i += 2) {
+        uint32_t b0, b1, b2, b3, c0, c1, c2, c3;
+        const int r = kk * 16 + (lane & 7) + ((lane >> 3) & 1) * 8, c = i * 8 + (lane >> 4) * 8;
+        ldsm_x4_t(b0, b1, b2, b3, sVh + r * LD + c);
+        ldsm_x4_t(c0, c1, c2, c3, sVl + r * LD + c);
+        mma16816(o[i], pl, b0, b1);
+        mma16816(o[i + 1], pl, b2, b3);
+        mma16816(o[i], ph, c0, c1);
+        mma16816(o[i + 1], ph, c2, c3);
+        mma16816(o[i], ph, b0, b1);
+        mma16816(o[i + 1], ph, b2, b3);
+      }
+    }
+  }
+  const float inv0 = 1.0f / l_r[0], inv1 = 1.0f / l_r[1];
+#pragma unroll
+  for (int i = 0; i < NO; ++i) {
+    const int64_t col = h * DH + i * 8 + 2 * t4;
+    if (qrow0 < len) *reinterpret_cast<float2*>(out + (start + qrow0) * d + col) = make_float2(o[i][0] * inv0, o[i][1] * inv0);
+    if (qrow1 < len) *reinterpret_cast<float2*>(out + (start + qrow1) * d + col) = make_float2(o[i][2] * inv1, o[i][3] * inv1);
+  }
+}
+
+template <int DH>
+void launch_split(Ctx& c, const float* qkv, const int64_t* seq_offsets, int64_t B, int64_t max_len, int64_t H,
+                  float* out) {
+  constexpr size_t smem = SplitSmem<DH>::kBytes;
+  static bool attr = false;
+  if (!attr) {
+    PPOEXP_CUDA(cudaFuncSetAttribute(attn_prefill_split_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(smem)));
+    attr = true;
+  }
+  dim3 grid(ceil_div(max_len, QT), H, B);
+  const double flops = 2.0 * 2.0 * B * H * double(max_len) * max_len / 2 * DH;
+  c.launch("attention_prefill", 0, flops, [&] {
+    launch_kernel(c, attn_prefill_split_kernel<DH>, grid, dim3(128), smem, 1, qkv, seq_offsets, H, out);
+  });
+}
+
 // bf16 prefill attention on tensor cores; false if the head size is unsupported.
 template <int DH>
 void launch_mma(Ctx& c, const bf16* qkv, const int64_t* seq_offsets, int64_t B, int64_t max_len, int64_t H,
@@ -238,6 +454,19 @@ void launch_mma(Ctx& c, const bf16* qkv, const int64_t* seq_offsets, int64_t B, 
 }
 
 }  // namespace
+
+// Mixed-mode prefill attention (fp32 q/k/v/out, split-bf16 tensor-core products).
+void attention_prefill_split(Ctx& c, const float* qkv, const int64_t* seq_offsets, int64_t B, int64_t max_len,
+                             int64_t H, int64_t DH, float* out) {
+  if (B <= 0 || max_len <= 0) return;
+  switch (DH) {
+    case 16: return launch_split<16>(c, qkv, seq_offsets, B, max_len, H, out);
+    case 32: return launch_split<32>(c, qkv, seq_offsets, B, max_len, H, out);
+    case 64: return launch_split<64>(c, qkv, seq_offsets, B, max_len, H, out);
+    case 128: return launch_split<128>(c, qkv, seq_offsets, B, max_len, H, out);
+    default: throw ContractError("attention: head_dim " + std::to_string(DH) + " unsupported (16/32/64/128)");
+  }
+}
 
 // bf16 prefill attention on tensor cores; false if the head size is unsupported.
 bool attention_prefill_mma(Ctx& c, const bf16* qkv, const int64_t* seq_offsets, int64_t B, int64_t max_len,

@@ -122,6 +122,11 @@ template <class T>
 void launch_attention_prefill(Ctx& c, const T* qkv, const int64_t* seq_offsets, int64_t B, int64_t max_len,
                               int64_t H, int64_t DH, T* out);
 
+// K5a in mixed mode: fp32 q/k/v in, fp32 out, tensor-core products on the
+// two-term bf16 split (three MMAs per product).
+void attention_prefill_split(Ctx& c, const float* qkv, const int64_t* seq_offsets, int64_t B, int64_t max_len,
+                             int64_t H, int64_t DH, float* out);
+
 // K5b: one decode step: append this step's K/V (row b of qkv at position
 // pos[b]) to the paged pool, then attend over positions 0..pos[b].
 // Sequences with done[b] != 0 are skipped.

@@ -307,7 +307,7 @@ static float* forward_layers_mixed(Model& m, const Packed& p, const KvTarget* kv
     if (kv)
       launch_kv_scatter<float>(c, qkv, M, d, p.seq_of_row_d, p.positions_d, kv->block_table, int(l), kv->geom,
                                static_cast<float*>(kv->pool));
-    launch_attention_prefill<float>(c, qkv, p.offsets_d, p.B, p.max_len, H, DH, att);
+    attention_prefill_split(c, qkv, p.offsets_d, p.B, p.max_len, H, DH, att);
     gemm_mixed(c, att, d, static_cast<const bf16*>(ly.wo), d, M, d, d, Epi::kAddResidual, x, d);
     launch_layernorm<float>(c, x, M, d, ly.ln2w, ly.ln2b, h, nullptr, nullptr, nullptr);
     gemm_mixed(c, h, d, static_cast<const bf16*>(ly.wup), d, M, f, d, Epi::kGeluF32, up, f);
