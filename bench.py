@@ -46,6 +46,11 @@ CONFIGS = {
     "c3": (32000, 2048, 24, 16, 8192, 1024, 256, 128, 512, "top_p", "1.3B policy/critic, 256 prompts x 512 tokens global (strong scaling: 256/N per rank), vocab 32k"),
     "c4": (128256, 4096, 32, 32, 14336, 2048, 64, 128, 1024, "top_p", "8B-shape reference block, paged KV, 64 prompts x 1024 per GPU"),
 }
+# c5 (DPO-style scoring sweep, BASELINE config 5): the C4-shaped model scores
+# chosen + rejected sequences of 4096 tokens (build_sft_sequence layout: a
+# 1024-token prompt + 3071 response tokens + EOT) through
+# ppoexp_response_logprob_sums (frozen_response_logprob_sum, src/trainers.cpp:24-29)
+C5 = dict(V=128256, d=4096, L=32, H=32, f=14336, S=4096, P=1024, T=4096)
 TOP_P = 0.9
 SEED = 20240809
 STRONG = {"c3"}
@@ -558,13 +563,96 @@ def bench_mode(args, dtype, primary):
     return line if rank == 0 else None
 
 
+def c5_flops(B_pairs):
+    """Algorithmic flops of scoring B pairs (2B sequences of T tokens): every
+    layer GEMM over all T positions, causal attention (QK^T and PV over T^2/2
+    pairs), the tied LM head over the response rows only."""
+    c = C5
+    T, R = c["T"], c["T"] - c["P"]
+    per_seq = (2.0 * T * (4 * c["d"] ** 2 + 2 * c["d"] * c["f"]) * c["L"] + 2.0 * 2.0 * T * T / 2 * c["d"] * c["L"]
+               + 2.0 * R * c["d"] * c["V"])
+    return 2 * B_pairs * per_seq
+
+
+def run_c5(args):
+    """DPO scoring sweep: dpo pairs/s (and scored tokens/s) at each B of
+    --c5-batches, with the tensor roofline of the whole scoring pass."""
+    import torch
+    from paper_2405_01481_b200 import ppoexp as px
+    dev = torch.device("cuda", 0)
+    c = C5
+    cfg = px.ModelConfig(c["V"], c["d"], c["L"], c["H"], c["f"], c["S"])
+    DT = {"mixed": px.MIXED, "bf16": px.BF16}[args.dtype]
+    ctx = px.Context(0)
+    model = px.DeviceModel(ctx, cfg, init_weights(cfg, SEED + 1, dev), DT)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(SEED)
+    pk = peaks()
+    sweep = []
+    batches = [int(x) for x in args.c5_batches.split(",") if x]
+    chunk = 16  # sequences per call (65,536 rows): bounds the activation workspaces
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    stream = torch.cuda.ExternalStream(ctx.stream, device=dev)
+    with Clocks(0) as clk:
+        for B in batches:
+            seqs, rs = [], []
+            for i in range(B):
+                prompt = rng.integers(0, 256, c["P"]).tolist()
+                for _ in range(2):  # chosen, rejected
+                    full, r = px.build_sft_sequence(cfg, prompt, rng.integers(0, 256, c["T"] - c["P"] - 1).tolist())
+                    seqs.append(full)
+                    rs.append(r)
+
+            def step():
+                out = []
+                for k in range(0, len(seqs), chunk):
+                    out.append(px.response_logprob_sums(model, seqs[k:k + chunk], rs[k:k + chunk]))
+                return np.concatenate(out)
+
+            for _ in range(max(1, min(args.warmup, 1))):
+                sums = step()
+            ms = []
+            for _ in range(max(1, args.c5_steps)):
+                ctx.synchronize()
+                ev0.record(stream)
+                sums = step()
+                ev1.record(stream)
+                ev1.synchronize()
+                ms.append(ev0.elapsed_time(ev1))
+            t = float(np.median(ms)) / 1000.0
+            fl = c5_flops(B)
+            sweep.append({"pairs": B, "sequences": 2 * B, "tokens": 2 * B * c["T"], "ms": t * 1000,
+                          "pairs_per_s": B / t, "scored_tokens_per_s": 2 * B * c["T"] / t,
+                          "tflops": fl / t / 1e12, "frac": fl / t / 1e12 / pk.get("bf16_tflops_sustained", 1400.0),
+                          "sum_mean": float(np.mean(sums))})
+            _dbg("c5", sweep[-1])
+    top = max(sweep, key=lambda x: x["pairs"])
+    line = {"metric": "dpo_scored_pairs_per_s", "value": top["pairs_per_s"], "unit": "pairs/s", "n_gpus": 1,
+            "steps": args.c5_steps, "warmup": 1, "ms_per_step": top["ms"], "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": DTYPE_LABEL[args.dtype], "data": "synthetic pairs, random-init weights",
+            "config": {"workload": "c5", "description": "DPO scoring sweep: chosen/rejected log-prob sums, vocab 128256, "
+                                                        "seq 4096, C4-shaped model (d 4096, 32 layers)",
+                       **{k: v for k, v in C5.items()}, "batches": batches},
+            "sweep": sweep,
+            "roofline": {"bound": "tensor", "achieved": top["tflops"], "peak": pk.get("bf16_tflops_sustained", 1400.0),
+                         "unit": "TFLOP/s", "frac": top["frac"], "traffic": None,
+                         "note": "whole scoring pass (all kernels) at the largest B; algorithmic flops = layer GEMMs "
+                                 "over all positions + causal attention + LM head over response rows"},
+            "clocks": clk.summary()}
+    print(json.dumps(line), flush=True)
+    model.close()
+    ctx.close()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS) + ["c5"])
+    ap.add_argument("--c5-batches", default="1,8,64")
+    ap.add_argument("--c5-steps", type=int, default=1)
     ap.add_argument("--batch", type=int, default=0)
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--profile-classes", action="store_true", default=True)
@@ -576,7 +664,13 @@ def main():
                     help="mixed: bf16 weights + fp32-grade activations/KV (meets the 1e-3 parity bar); "
                          "bf16: bf16 activations/KV (faster, outside the bar for values)")
     args = ap.parse_args()
-    if args.impl == "reference":
+    if args.config == "c5":
+        if args.impl == "reference":
+            print(json.dumps({"impl": "reference", "unavailable": "c5 (4096-token, 8B-shape fp64 forward) is not "
+                                                                  "timed on the host; see DESIGN.md"}))
+            return
+        run_c5(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_ours(args)

@@ -71,6 +71,7 @@ typedef struct ppoexp_ctx_s* ppoexp_ctx;
 typedef struct ppoexp_model_s* ppoexp_model;
 typedef struct ppoexp_engine_s* ppoexp_engine;
 typedef struct ppoexp_comm_s* ppoexp_comm;
+typedef struct ppoexp_trainer_s* ppoexp_trainer;
 
 /* ModelConfig, include/aligner/model.hpp:30-45 (LoRA is not on this path). */
 typedef struct {
@@ -321,6 +322,53 @@ typedef struct {
 
 PPOEXP_API ppoexp_status ppoexp_make_experience(const ppoexp_experience_request* req, int64_t B, const int32_t* prompts,
                                      const int64_t* offsets, const ppoexp_rollout_batch* out, int32_t where);
+
+/* ------------------------------------------------------------ train side */
+/* The updates that consume the experience: a device trainer
+ * per model holding fp32 master weights (initialised from `params`, the
+ * reference's ModelParams), AdamW state and a recorded forward/backward.
+ * After a step, ppoexp_trainer_refit copies the weights into `serving` in
+ * place (Engine::refit, src/engine.cpp:60-90; generation counter + 1). */
+typedef struct { /* AdamW::Options, include/aligner/optim.hpp:38-43 */
+  double beta1, beta2, eps, weight_decay;
+} ppoexp_adamw_options;
+
+PPOEXP_API ppoexp_status ppoexp_trainer_create(ppoexp_ctx ctx, const ppoexp_model_config* config,
+                                               const ppoexp_tensor_view* params, int64_t n_params,
+                                               ppoexp_model serving, const ppoexp_adamw_options* opts,
+                                               ppoexp_trainer* out);
+PPOEXP_API ppoexp_status ppoexp_trainer_destroy(ppoexp_trainer trainer);
+/* PPO actor update (src/ppo.cpp:395-424): B sequences prompt ++ response
+ * (ragged tokens/offsets), response_start[B]; old_logprobs / advantages / mask
+ * flat over the response tokens in sequence order (mask NULL = all ones);
+ * ppo_actor_loss (src/losses.cpp:201-214) then AdamW at `lr`.  loss_out gets
+ * the loss before the update. */
+PPOEXP_API ppoexp_status ppoexp_trainer_ppo_actor_step(ppoexp_trainer trainer, int64_t B, const int32_t* tokens,
+                                                       const int64_t* offsets, const int64_t* response_start,
+                                                       const double* old_logprobs, const double* advantages,
+                                                       const double* mask, double clip_eps, double lr,
+                                                       double* loss_out, int32_t where);
+/* Critic update (CriticJob::handle_train, src/ppo.cpp:195-231): per-sequence
+ * ppo_critic_loss (src/losses.cpp:216-231), mean over sequences, AdamW.
+ * The trainer's config must have the scalar head. */
+PPOEXP_API ppoexp_status ppoexp_trainer_critic_step(ppoexp_trainer trainer, int64_t B, const int32_t* tokens,
+                                                    const int64_t* offsets, const int64_t* response_start,
+                                                    const double* old_values, const double* returns,
+                                                    double value_clip, double lr, double* loss_out, int32_t where);
+/* DPO-family update (dpo_micro_loss, src/trainers.cpp:54-80): 2*n_pairs
+ * sequences in build_sft_sequence layout, chosen then rejected per pair;
+ * policy sums from the trainer, frozen sums from `reference`
+ * (frozen_response_logprob_sum); variant 0 dpo, 1 ipo, 2 cdpo, 3 kto
+ * (dpo_family_loss, src/losses.cpp:129-166).  margin_out (optional): the
+ * mean implicit-reward margin beta * mean((pc - rc) - (pr - rr)). */
+PPOEXP_API ppoexp_status ppoexp_trainer_dpo_step(ppoexp_trainer trainer, ppoexp_model reference, int64_t n_pairs,
+                                                 const int32_t* tokens, const int64_t* offsets,
+                                                 const int64_t* response_start, int32_t variant, double beta,
+                                                 double cdpo_eps, double lr, double* loss_out, double* margin_out,
+                                                 int32_t where);
+PPOEXP_API ppoexp_status ppoexp_trainer_refit(ppoexp_trainer trainer);
+/* One master parameter in the reference layout (fp64 host buffer of numel). */
+PPOEXP_API ppoexp_status ppoexp_trainer_get(ppoexp_trainer trainer, const char* name, double* out, int64_t numel);
 
 #ifdef __cplusplus
 }

@@ -294,6 +294,14 @@ class RefLib:
         L.ref_reward_head.argtypes = [C.POINTER(I64), C.POINTER(D), C.POINTER(I32), I64, C.POINTER(D)]
         L.ref_kl_penalized_rewards.argtypes = [D, C.POINTER(D), C.POINTER(D), I64, D, C.POINTER(D)]
         L.ref_gae.argtypes = [C.POINTER(D), C.POINTER(D), I64, D, D, C.POINTER(D), C.POINTER(D)]
+        L.ref_ppo_actor_step.argtypes = [C.POINTER(I64), C.POINTER(D), I64, C.POINTER(I32), C.POINTER(I64),
+                                         C.POINTER(I64), C.POINTER(D), C.POINTER(D), D, D, C.POINTER(D), I64,
+                                         C.POINTER(D)]
+        L.ref_critic_step.argtypes = [C.POINTER(I64), C.POINTER(D), I64, C.POINTER(I32), C.POINTER(I64),
+                                      C.POINTER(I64), C.POINTER(D), C.POINTER(D), D, D, C.POINTER(D), I64,
+                                      C.POINTER(D)]
+        L.ref_dpo_step.argtypes = [C.POINTER(I64), C.POINTER(D), C.POINTER(D), I64, C.POINTER(I32), C.POINTER(I64),
+                                   C.POINTER(I64), I32, D, D, D, C.POINTER(D), I64, C.POINTER(D)]
         L.ref_experience.argtypes = [C.POINTER(I64), C.POINTER(D), C.POINTER(D), C.POINTER(D), C.POINTER(D), I32,
                                      C.POINTER(I32), C.POINTER(I64), I64, I64, I64, I32, D, C.c_uint64, I64, D, D,
                                      D, I64, C.POINTER(I32), C.POINTER(I64), C.POINTER(D), C.POINTER(D),
@@ -368,6 +376,48 @@ class RefLib:
         ret = np.zeros(len(rw), np.float64)
         self._chk(self.lib.ref_gae(_p(rw, D), _p(v, D), len(rw), gamma, lam, _p(adv, D), _p(ret, D)))
         return adv, ret
+
+    # ---- train-side steps on the reference's tape + AdamW (checkers for the GPU trainer)
+    def ppo_actor_step(self, cfg, w, seqs, rs, old_lp, adv, clip_eps, lr, adam=(0.9, 0.999, 1e-8, 0.0), n_steps=1):
+        flat, offs = ragged(seqs)
+        w = np.array(w, np.float64)
+        rs = np.asarray(rs, np.int64)
+        old_lp, adv = np.ascontiguousarray(old_lp, np.float64), np.ascontiguousarray(adv, np.float64)
+        a4 = np.asarray(adam, np.float64)
+        losses = np.zeros(n_steps, np.float64)
+        self._chk(self.lib.ref_ppo_actor_step(cfg.as6(), _p(w, D), len(seqs), _p(flat, I32), _p(offs, I64), _p(rs, I64),
+                                              _p(old_lp, D), _p(adv, D), clip_eps, lr, _p(a4, D), n_steps,
+                                              _p(losses, D)))
+        return w, losses
+
+    def critic_step(self, cfg, w, seqs, rs, old_values, returns, value_clip, lr, adam=(0.9, 0.999, 1e-8, 0.0),
+                    n_steps=1):
+        flat, offs = ragged(seqs)
+        w = np.array(w, np.float64)
+        rs = np.asarray(rs, np.int64)
+        ov, rt = np.ascontiguousarray(old_values, np.float64), np.ascontiguousarray(returns, np.float64)
+        a4 = np.asarray(adam, np.float64)
+        losses = np.zeros(n_steps, np.float64)
+        self._chk(self.lib.ref_critic_step(cfg.as6(), _p(w, D), len(seqs), _p(flat, I32), _p(offs, I64), _p(rs, I64),
+                                           _p(ov, D), _p(rt, D), value_clip, lr, _p(a4, D), n_steps, _p(losses, D)))
+        return w, losses
+
+    def dpo_step(self, cfg, w_policy, w_ref, pairs, variant, beta, cdpo_eps, lr, adam=(0.9, 0.999, 1e-8, 0.0),
+                 n_steps=1):
+        """pairs: list of (chosen_full, rejected_full, response_start_chosen, response_start_rejected)."""
+        seqs, rs = [], []
+        for c, r, rc, rr in pairs:
+            seqs += [c, r]
+            rs += [rc, rr]
+        flat, offs = ragged(seqs)
+        w = np.array(w_policy, np.float64)
+        wr = np.ascontiguousarray(w_ref, np.float64)
+        rs = np.asarray(rs, np.int64)
+        a4 = np.asarray(adam, np.float64)
+        losses = np.zeros(n_steps, np.float64)
+        self._chk(self.lib.ref_dpo_step(cfg.as6(), _p(w, D), _p(wr, D), len(pairs), _p(flat, I32), _p(offs, I64),
+                                        _p(rs, I64), variant, beta, cdpo_eps, lr, _p(a4, D), n_steps, _p(losses, D)))
+        return w, losses
 
     def experience(self, cfg, w_policy, w_ref, w_critic, prompts, *, max_new, greedy, temperature=1.0, seed=0,
                    step_index=0, gidx0=0, kl_coef=0.003, gamma=1.0, lam=0.95, scripted_target=122, w_rm=None,

@@ -21,6 +21,7 @@
 #include "aligner/engine.hpp"
 #include "aligner/losses.hpp"
 #include "aligner/model.hpp"
+#include "aligner/optim.hpp"
 #include "aligner/rng.hpp"
 
 using namespace aligner;
@@ -306,6 +307,161 @@ int ref_experience(const int64_t* c6, const double* w_policy, const double* w_re
       phase_seconds[1] = std::chrono::duration<double>(t2 - t1).count();
       phase_seconds[2] = std::chrono::duration<double>(t3 - t2).count();
     }
+  });
+}
+
+
+// ---------------------------------------------------------------- training
+// The train-side steps that consume the experience, on the reference's own
+// tape autodiff and AdamW (checkers for the GPU trainer).  Each runs n_steps
+// optimizer steps on the same batch (the reference's AdamW state persists
+// across them) and returns the loss of every step; weights in/out in the flat
+// canonical layout.  adam4 = {beta1, beta2, eps, weight_decay}.
+
+static AdamW make_adam(const double* adam4) {
+  AdamW::Options o;
+  o.beta1 = adam4[0];
+  o.beta2 = adam4[1];
+  o.eps = adam4[2];
+  o.weight_decay = adam4[3];
+  return AdamW(o);
+}
+
+// PPO actor update, src/ppo.cpp:395-424 (+ ppo_actor_loss, src/losses.cpp:201-214).
+// tokens: prompt ++ response per sequence (ragged, offsets[B+1]); the
+// response of sequence b starts at rs[b]; old_lp / adv are flat over all
+// response tokens in sequence order; mask = 1 everywhere (src/ppo.cpp:385).
+int ref_ppo_actor_step(const int64_t* c6, double* w, int64_t B, const int32_t* tokens, const int64_t* offsets,
+                       const int64_t* rs, const double* old_lp, const double* adv, double clip_eps, double lr,
+                       const double* adam4, int64_t n_steps, double* losses) {
+  return guarded([&] {
+    const auto cfg = make_cfg(c6, 0);
+    auto params = from_flat(cfg, w);
+    params.set_requires_grad_on_trainable();
+    AdamW opt = make_adam(adam4);
+    int64_t n_tok = 0;
+    for (int64_t b = 0; b < B; ++b) n_tok += offsets[b + 1] - offsets[b] - rs[b];
+    const std::vector<double> flat_old(old_lp, old_lp + n_tok), flat_adv(adv, adv + n_tok), mask(n_tok, 1.0);
+    for (int64_t s = 0; s < n_steps; ++s) {
+      Tape tape;
+      {
+        TapeScope scope(tape);
+        std::vector<Tensor> rows;
+        for (int64_t b = 0; b < B; ++b) {
+          TokenSeq full(tokens + offsets[b], tokens + offsets[b + 1]);
+          TokenSeq resp(full.begin() + rs[b], full.end());
+          Tensor logits = forward_one(params, full);
+          Tensor lp = log_softmax(slice_rows(logits, std::size_t(rs[b]) - 1, full.size() - 1));
+          Tensor part = gather_token_logprobs(lp, resp);
+          rows.push_back(reshape(part, {part.size(), 1}));
+        }
+        Tensor new_lp = reshape(concat_rows(rows), {std::size_t(n_tok)});
+        Tensor loss = ppo_actor_loss(new_lp, flat_old, flat_adv, clip_eps, mask);
+        losses[s] = loss.item();
+        params.zero_grad();
+        backward(loss);
+      }
+      opt.step(params, lr);
+      params.zero_grad();
+    }
+    to_flat(params, w);
+  });
+}
+
+// Critic update, CriticJob::handle_train (src/ppo.cpp:195-231): per sequence
+// ppo_critic_loss (src/losses.cpp:216-231) over its response values, mean over
+// sequences.  old_values / returns flat over the response tokens.
+int ref_critic_step(const int64_t* c6, double* w, int64_t B, const int32_t* tokens, const int64_t* offsets,
+                    const int64_t* rs, const double* old_values, const double* returns, double value_clip, double lr,
+                    const double* adam4, int64_t n_steps, double* losses) {
+  return guarded([&] {
+    const auto cfg = make_cfg(c6, 1);
+    auto params = from_flat(cfg, w);
+    params.set_requires_grad_on_trainable();
+    AdamW opt = make_adam(adam4);
+    for (int64_t s = 0; s < n_steps; ++s) {
+      Tape tape;
+      {
+        TapeScope scope(tape);
+        Tensor total = Tensor::scalar(0.0);
+        int64_t o = 0;
+        for (int64_t b = 0; b < B; ++b) {
+          TokenSeq full(tokens + offsets[b], tokens + offsets[b + 1]);
+          const int64_t n = int64_t(full.size()) - rs[b];
+          Tensor values = value_estimates(params, params.at("scalar_head.weight"), full, std::size_t(rs[b]));
+          std::vector<double> mask(n, 1.0);
+          Tensor loss = ppo_critic_loss(values, std::span<const double>(old_values + o, n),
+                                        std::span<const double>(returns + o, n), value_clip, mask);
+          total = add(total, loss);
+          o += n;
+        }
+        Tensor mean_loss = mul_scalar(total, 1.0 / double(B));
+        losses[s] = mean_loss.item();
+        params.zero_grad();
+        backward(mean_loss);
+      }
+      opt.step(params, lr);
+      params.zero_grad();
+    }
+    to_flat(params, w);
+  });
+}
+
+// DPO-family update (dpo_micro_loss, src/trainers.cpp:54-80; dpo_family_loss,
+// src/losses.cpp:129-166): policy sums on the tape (forward_one + log_softmax +
+// gather + masked sum over the response, src/trainers.cpp:17-21), frozen
+// reference sums from sequence_logprobs.  Pairs: chosen b = sequence 2b,
+// rejected b = sequence 2b+1.  variant: 0 dpo, 1 ipo, 2 cdpo, 3 kto.
+int ref_dpo_step(const int64_t* c6, double* w_policy, const double* w_ref, int64_t n_pairs, const int32_t* tokens,
+                 const int64_t* offsets, const int64_t* rs, int32_t variant, double beta, double cdpo_eps,
+                 double lr, const double* adam4, int64_t n_steps, double* losses) {
+  return guarded([&] {
+    const auto cfg = make_cfg(c6, 0);
+    auto policy = from_flat(cfg, w_policy);
+    const auto refm = from_flat(cfg, w_ref);
+    policy.set_requires_grad_on_trainable();
+    AdamW opt = make_adam(adam4);
+    DpoHyper h;
+    h.beta = beta;
+    h.variant = static_cast<DpoVariant>(variant);
+    h.cdpo_eps = cdpo_eps;
+    auto seq = [&](int64_t i) { return TokenSeq(tokens + offsets[i], tokens + offsets[i + 1]); };
+    std::vector<double> rc, rr;
+    for (int64_t p = 0; p < n_pairs; ++p)
+      for (int k = 0; k < 2; ++k) {
+        const auto full = seq(2 * p + k);
+        const auto lps = sequence_logprobs(refm, full);
+        double acc = 0.0;
+        for (std::size_t t = std::size_t(rs[2 * p + k]); t < full.size(); ++t) acc += lps[t];
+        (k ? rr : rc).push_back(acc);
+      }
+    for (int64_t s = 0; s < n_steps; ++s) {
+      Tape tape;
+      {
+        TapeScope scope(tape);
+        std::vector<Tensor> pc, pr;
+        for (int64_t p = 0; p < n_pairs; ++p)
+          for (int k = 0; k < 2; ++k) {
+            const auto full = seq(2 * p + k);
+            const std::size_t r0 = std::size_t(rs[2 * p + k]);
+            TokenSeq inputs(full.begin(), full.end() - 1), targets(full.begin() + 1, full.end());
+            std::vector<double> mask(targets.size(), 0.0);
+            for (std::size_t t = r0 - 1; t < targets.size(); ++t) mask[t] = 1.0;
+            Tensor lp = gather_token_logprobs(log_softmax(forward_one(policy, inputs)), targets);
+            Tensor sum_t = masked_sum(lp, mask);
+            (k ? pr : pc).push_back(reshape(sum_t, {1, 1}));
+          }
+        Tensor policy_chosen = reshape(concat_rows(pc), {std::size_t(n_pairs)});
+        Tensor policy_rejected = reshape(concat_rows(pr), {std::size_t(n_pairs)});
+        Tensor loss = dpo_family_loss(policy_chosen, policy_rejected, Tensor({rc.size()}, rc), Tensor({rr.size()}, rr), h);
+        losses[s] = loss.item();
+        policy.zero_grad();
+        backward(loss);
+      }
+      opt.step(policy, lr);
+      policy.zero_grad();
+    }
+    to_flat(policy, w_policy);
   });
 }
 

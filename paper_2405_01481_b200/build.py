@@ -17,6 +17,7 @@ CSRC = os.path.join(PKG, "csrc")
 OBJ = os.path.join(ROOT, "build", "obj")
 LIB = os.path.join(PKG, "libppoexp.so")
 NVCC = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
+CUDA_LIB = os.path.join(os.path.dirname(os.path.dirname(os.path.realpath(NVCC))), "lib64")  # cuBLAS (train-side GEMMs)
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hidden,-fvisibility-inlines-hidden", "-Xptxas", "-O3", "--expt-relaxed-constexpr",
          "-Wno-deprecated-gpu-targets", f"-I{os.path.join(ROOT, 'include')}"]
@@ -46,7 +47,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < max(os.path.getmtime(o) for o in objs):
         tmp = LIB + ".tmp"
         cmd = [NVCC, *ARCH, "-shared", "-Wno-deprecated-gpu-targets", *objs, "-o", tmp, "-lcudart_static",
-               "-Xlinker", "--exclude-libs,ALL", "-Xlinker", "--no-undefined", "-ldl", "-lrt", "-lpthread"]
+               "-Xlinker", "--exclude-libs,ALL", "-Xlinker", "--no-undefined", "-ldl", "-lrt", "-lpthread",
+               f"-L{CUDA_LIB}", "-lcublas", "-Xlinker", f"-rpath,{CUDA_LIB}"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")

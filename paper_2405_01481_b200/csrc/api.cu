@@ -14,6 +14,7 @@
 
 #include "comm.hpp"
 #include "engine.hpp"
+#include "train.hpp"
 
 using namespace ppx;
 
@@ -28,6 +29,9 @@ struct ppoexp_engine_s {
 };
 struct ppoexp_comm_s {
   std::unique_ptr<Comm> c;
+};
+struct ppoexp_trainer_s {
+  std::unique_ptr<Trainer> t;
 };
 
 namespace {
@@ -978,6 +982,114 @@ ppoexp_status ppoexp_make_experience(const ppoexp_experience_request* req, int64
         PPOEXP_CUDA(cudaMemcpy(out->stats, stats_h, sizeof stats_h, cudaMemcpyHostToDevice));
     }
     c.harvest();
+  });
+}
+
+// ------------------------------------------------------------------ train side
+ppoexp_status ppoexp_trainer_create(ppoexp_ctx ctx, const ppoexp_model_config* config, const ppoexp_tensor_view* params,
+                                    int64_t n, ppoexp_model serving, const ppoexp_adamw_options* opts,
+                                    ppoexp_trainer* out) {
+  return guard([&] {
+    need(ctx, "ctx");
+    need(config, "config");
+    need(params, "params");
+    need(out, "out");
+    if (serving && serving->m.ctx != ctx->c.get()) throw ContractError("trainer: serving model on another context");
+    AdamOpts o;
+    if (opts) o = AdamOpts{opts->beta1, opts->beta2, opts->eps, opts->weight_decay};
+    std::lock_guard<std::recursive_mutex> lk(ctx->c->mu);
+    auto h = std::make_unique<ppoexp_trainer_s>();
+    h->t = std::make_unique<Trainer>(ctx->c.get(), *config, params, n, serving ? &serving->m : nullptr, o);
+    *out = h.release();
+  });
+}
+
+ppoexp_status ppoexp_trainer_destroy(ppoexp_trainer trainer) {
+  return guard([&] { delete trainer; });
+}
+
+ppoexp_status ppoexp_trainer_ppo_actor_step(ppoexp_trainer trainer, int64_t B, const int32_t* tokens,
+                                            const int64_t* offsets, const int64_t* response_start,
+                                            const double* old_lp, const double* adv, const double* mask,
+                                            double clip_eps, double lr, double* loss_out, int32_t where) {
+  return guard([&] {
+    need(trainer, "trainer");
+    if (B <= 0) throw PpoError("ppo_step: empty prompt batch");
+    need(tokens, "tokens");
+    need(old_lp, "old_logprobs");
+    need(adv, "advantages");
+    Trainer& t = *trainer->t;
+    std::lock_guard<std::recursive_mutex> lk(t.c->mu);
+    DeviceGuard g(t.c->device);
+    const double l = t.ppo_actor_step(B, tokens, offsets, response_start, old_lp, adv, mask, clip_eps, lr, where);
+    if (loss_out) *loss_out = l;
+  });
+}
+
+ppoexp_status ppoexp_trainer_critic_step(ppoexp_trainer trainer, int64_t B, const int32_t* tokens,
+                                         const int64_t* offsets, const int64_t* response_start,
+                                         const double* old_values, const double* returns, double value_clip, double lr,
+                                         double* loss_out, int32_t where) {
+  return guard([&] {
+    need(trainer, "trainer");
+    if (B <= 0) throw PpoError("critic job: empty training batch");
+    need(tokens, "tokens");
+    need(old_values, "old_values");
+    need(returns, "returns");
+    Trainer& t = *trainer->t;
+    std::lock_guard<std::recursive_mutex> lk(t.c->mu);
+    DeviceGuard g(t.c->device);
+    const double l = t.critic_step(B, tokens, offsets, response_start, old_values, returns, value_clip, lr, where);
+    if (loss_out) *loss_out = l;
+  });
+}
+
+ppoexp_status ppoexp_trainer_dpo_step(ppoexp_trainer trainer, ppoexp_model reference, int64_t n_pairs,
+                                      const int32_t* tokens, const int64_t* offsets, const int64_t* response_start,
+                                      int32_t variant, double beta, double cdpo_eps, double lr, double* loss_out,
+                                      double* margin_out, int32_t where) {
+  return guard([&] {
+    need(trainer, "trainer");
+    need(reference, "reference");
+    if (n_pairs <= 0) throw ContractError("dpo_family_loss: mismatched sequence counts");
+    need(tokens, "tokens");
+    Trainer& t = *trainer->t;
+    std::lock_guard<std::recursive_mutex> lk(t.c->mu);
+    DeviceGuard g(t.c->device);
+    // frozen reference sums through the public scoring path (fused LM head)
+    std::vector<double> ref_sums(2 * n_pairs);
+    double* dst = ref_sums.data();
+    if (where == PPOEXP_DEVICE) dst = static_cast<double*>(t.c->workspace("dpo.ref_sums", 2 * n_pairs * 8));
+    const ppoexp_status rc =
+        ppoexp_response_logprob_sums(reference, 2 * n_pairs, tokens, offsets, response_start, dst, where);
+    if (rc != PPOEXP_OK) throw Error(int(rc), g_err);
+    if (where == PPOEXP_DEVICE) {
+      PPOEXP_CUDA(cudaStreamSynchronize(t.c->stream));
+      PPOEXP_CUDA(cudaMemcpy(ref_sums.data(), dst, 2 * n_pairs * 8, cudaMemcpyDeviceToHost));
+    }
+    const double l = t.dpo_step(n_pairs, tokens, offsets, response_start, ref_sums, variant, beta, cdpo_eps, lr, where,
+                                margin_out);
+    if (loss_out) *loss_out = l;
+  });
+}
+
+ppoexp_status ppoexp_trainer_refit(ppoexp_trainer trainer) {
+  return guard([&] {
+    need(trainer, "trainer");
+    std::lock_guard<std::recursive_mutex> lk(trainer->t->c->mu);
+    DeviceGuard g(trainer->t->c->device);
+    trainer->t->refit();
+  });
+}
+
+ppoexp_status ppoexp_trainer_get(ppoexp_trainer trainer, const char* name, double* out, int64_t numel) {
+  return guard([&] {
+    need(trainer, "trainer");
+    need(name, "name");
+    need(out, "out");
+    std::lock_guard<std::recursive_mutex> lk(trainer->t->c->mu);
+    DeviceGuard g(trainer->t->c->device);
+    trainer->t->get(name, out, numel);
   });
 }
 

@@ -144,6 +144,13 @@ def lib():
             "ppoexp_comm_create": [P, P, I32, I32, P],
             "ppoexp_comm_destroy": [P],
             "ppoexp_comm_allgather_sum": [P, P, I64, I32],
+            "ppoexp_trainer_create": [P, P, P, I64, P, P, P],
+            "ppoexp_trainer_destroy": [P],
+            "ppoexp_trainer_ppo_actor_step": [P, I64, P, P, P, P, P, P, D, D, P, I32],
+            "ppoexp_trainer_critic_step": [P, I64, P, P, P, P, P, D, D, P, I32],
+            "ppoexp_trainer_dpo_step": [P, P, I64, P, P, P, I32, D, D, D, P, P, I32],
+            "ppoexp_trainer_refit": [P],
+            "ppoexp_trainer_get": [P, C.c_char_p, P, I64],
         }
         for name, args in sigs.items():
             f = getattr(L, name)
@@ -278,7 +285,7 @@ class Context:
         first (engines before models), so no handle outlives its context."""
         if self.h:
             kids = list(self._children)
-            for kind in (Engine, Communicator, DeviceModel):
+            for kind in (Engine, Communicator, Trainer, DeviceModel):
                 for k in kids:
                     if isinstance(k, kind):
                         k.close()
@@ -540,6 +547,107 @@ class Communicator:
     def close(self):
         if self.h:
             _check(lib().ppoexp_comm_destroy(self.h))
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class _Adam(C.Structure):
+    _fields_ = [("beta1", C.c_double), ("beta2", C.c_double), ("eps", C.c_double), ("weight_decay", C.c_double)]
+
+
+@dataclass
+class AdamWOptions:
+    """AdamW::Options, include/aligner/optim.hpp:38-43."""
+    beta1: float = 0.9
+    beta2: float = 0.999
+    eps: float = 1e-8
+    weight_decay: float = 0.0
+
+
+DPO_VARIANTS = {"dpo": 0, "ipo": 1, "cdpo": 2, "kto": 3}  # DpoVariant, include/aligner/losses.hpp:26
+
+
+class Trainer:
+    """The train side that consumes the experience: fp32 master
+    weights + AdamW on the device, the PPO actor update (src/ppo.cpp:395-424),
+    the critic update (src/ppo.cpp:195-231) and the DPO family
+    (src/trainers.cpp:54-80); ``refit()`` pushes the weights into the serving
+    model in place (Engine::refit)."""
+
+    def __init__(self, ctx: Context, config: ModelConfig, params, serving: DeviceModel | None = None,
+                 adamw: AdamWOptions | None = None):
+        if isinstance(params, np.ndarray):
+            params = flat_to_params(config, params)
+        self.ctx, self.config = ctx, config
+        views, keep = _views(params)
+        a = adamw or AdamWOptions()
+        self.h = C.c_void_p()
+        _check(lib().ppoexp_trainer_create(ctx.h, C.byref(config._c()), views, len(params),
+                                           serving.h if serving else None,
+                                           C.byref(_Adam(a.beta1, a.beta2, a.eps, a.weight_decay)), C.byref(self.h)))
+        ctx._adopt(self)
+
+    @staticmethod
+    def _seqs(seqs, rs):
+        flat, offs = ragged(seqs)
+        return flat, offs, np.ascontiguousarray(rs, np.int64)
+
+    def ppo_actor_step(self, seqs, response_starts, old_logprobs, advantages, clip_eps=0.2, lr=1e-7, mask=None):
+        flat, offs, rs = self._seqs(seqs, response_starts)
+        old = np.ascontiguousarray(np.concatenate([np.asarray(x, np.float64) for x in old_logprobs]))
+        adv = np.ascontiguousarray(np.concatenate([np.asarray(x, np.float64) for x in advantages]))
+        mk = None if mask is None else np.ascontiguousarray(np.concatenate(mask), np.float64)
+        loss = C.c_double()
+        _check(lib().ppoexp_trainer_ppo_actor_step(self.h, len(seqs), flat.ctypes.data, offs.ctypes.data, rs.ctypes.data,
+                                                   old.ctypes.data, adv.ctypes.data,
+                                                   mk.ctypes.data if mk is not None else None, clip_eps, lr,
+                                                   C.byref(loss), HOST))
+        return loss.value
+
+    def critic_step(self, seqs, response_starts, old_values, returns, value_clip=0.2, lr=1e-7):
+        flat, offs, rs = self._seqs(seqs, response_starts)
+        ov = np.ascontiguousarray(np.concatenate([np.asarray(x, np.float64) for x in old_values]))
+        rt = np.ascontiguousarray(np.concatenate([np.asarray(x, np.float64) for x in returns]))
+        loss = C.c_double()
+        _check(lib().ppoexp_trainer_critic_step(self.h, len(seqs), flat.ctypes.data, offs.ctypes.data, rs.ctypes.data,
+                                                ov.ctypes.data, rt.ctypes.data, value_clip, lr, C.byref(loss), HOST))
+        return loss.value
+
+    def dpo_step(self, reference: DeviceModel, pairs, variant="dpo", beta=0.1, cdpo_eps=0.0, lr=1e-7):
+        """pairs: [(chosen_full, rejected_full, rs_chosen, rs_rejected)] (build_sft_sequence layouts)."""
+        seqs, rs = [], []
+        for c_, r_, a_, b_ in pairs:
+            seqs += [c_, r_]
+            rs += [a_, b_]
+        flat, offs, rs = self._seqs(seqs, rs)
+        loss, margin = C.c_double(), C.c_double()
+        _check(lib().ppoexp_trainer_dpo_step(self.h, reference.h, len(pairs), flat.ctypes.data, offs.ctypes.data,
+                                             rs.ctypes.data, DPO_VARIANTS[variant], beta, cdpo_eps, lr,
+                                             C.byref(loss), C.byref(margin), HOST))
+        return loss.value, margin.value
+
+    def refit(self):
+        _check(lib().ppoexp_trainer_refit(self.h))
+
+    def get(self, name=None):
+        if name is None:
+            return {n: self.get(n) for n, _ in expected_names(self.config)}
+        shape = dict(expected_names(self.config))[name]
+        out = np.zeros(shape, np.float64)
+        _check(lib().ppoexp_trainer_get(self.h, name.encode(), out.ctypes.data, out.size))
+        return out
+
+    def flat(self):
+        return np.concatenate([self.get(n).ravel() for n, _ in expected_names(self.config)])
+
+    def close(self):
+        if self.h:
+            _check(lib().ppoexp_trainer_destroy(self.h))
             self.h = C.c_void_p()
 
     def __del__(self):

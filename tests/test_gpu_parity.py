@@ -641,3 +641,24 @@ def test_device_token_ids_are_validated(px, ctx, oracle):
         px._check(rc)
     # the context stays usable
     assert len(px.sequence_logprobs(m, [[1, 2, 3]])[0]) == 3
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "mixed"])
+def test_dpo_sums_c5_width(px, ctx, oracle, dtype):
+    """DPO chosen / rejected sums at the C5 width and vocab (d 4096, V 128256),
+    one layer: both compute modes within 1e-3 + 1e-3 |sum| of the oracle
+    (the sums are what the DPO loss consumes, src/trainers.cpp:54-80)."""
+    cfg = ModelCfg(V=128256, d=4096, L=1, H=32, f=14336, S=64)
+    w = bf16_round(oracle.init_params(cfg, 47))
+    m = px.DeviceModel(ctx, to_px_cfg(cfg), w, px.MIXED if dtype == "mixed" else px.BF16)
+    rng = np.random.default_rng(8)
+    seqs, rs = [], []
+    for i in range(2):
+        prompt = rng.integers(0, 256, 12).tolist()
+        for _ in range(2):  # chosen, rejected
+            full, r = px.build_sft_sequence(to_px_cfg(cfg), prompt, rng.integers(0, 256, 20).tolist())
+            seqs.append(full)
+            rs.append(r)
+    got = px.response_logprob_sums(m, seqs, rs)
+    lps = oracle.sequence_logprobs(cfg, w, seqs)
+    close(got, [float(sum(lp[r:])) for lp, r in zip(lps, rs)])

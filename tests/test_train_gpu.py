@@ -1,0 +1,134 @@
+"""The train side against the reference itself: the
+unmodified reference sources compiled in place (oracle/_ref, its tape autodiff
+and AdamW) run the same update on the same fp32-rounded weights.  Losses of
+every step and the weights after the steps must agree within 1e-3 abs + 1e-3
+rel (north_star).  GPU only; needs oracle/_ref (built by oracle/Makefile)."""
+import os
+
+import numpy as np
+import pytest
+
+from oracle.oracle import REF_SO, ModelCfg, synthetic_prompts
+from tests.golden_util import to_px_cfg
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not os.path.exists(REF_SO), reason="oracle/_ref not built")]
+
+CFG = ModelCfg(V=1024, d=128, L=2, H=4, f=512, S=128)  # C1 (BASELINE config 1)
+ADAM = (0.9, 0.999, 1e-8, 0.01)
+TOL = 1e-3
+
+
+def close(a, b, atol=TOL, rtol=TOL):
+    a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+    err = np.abs(a - b) - (atol + rtol * np.abs(b))
+    assert (err <= 0).all(), f"max excess {err.max():.3e}, max abs diff {np.abs(a - b).max():.3e}"
+    return float(np.abs(a - b).max())
+
+
+@pytest.fixture(scope="module")
+def ref():
+    from oracle.oracle import RefLib
+    return RefLib()
+
+
+@pytest.fixture(scope="module")
+def px():
+    from paper_2405_01481_b200 import ppoexp
+    return ppoexp
+
+
+def f32(w):
+    return np.asarray(w, np.float32).astype(np.float64)
+
+
+def rollout(oracle, seed, n=6):
+    prompts = synthetic_prompts(seed, n, 9, ragged_lengths=True)
+    rng = np.random.default_rng(seed)
+    seqs = [np.concatenate([p, rng.integers(0, 256, 5 + 3 * i)]).astype(np.int32) for i, p in enumerate(prompts)]
+    return seqs, [len(p) for p in prompts]
+
+
+def test_ppo_actor_step_matches_reference(px, ctx, oracle, ref):
+    w = f32(ref.init_params(CFG, 5))
+    seqs, rs = rollout(oracle, 3)
+    lps = oracle.sequence_logprobs(CFG, w, seqs)
+    rng = np.random.default_rng(1)
+    # old log-probs a little off the current ones: some ratios fall outside the clip range
+    old = [lp[r:] + rng.normal(0, 0.15, len(lp) - r) for lp, r in zip(lps, rs)]
+    adv = [rng.normal(0, 1, len(lp) - r) for lp, r in zip(lps, rs)]
+    lr, steps = 3e-4, 3
+    w_ref, l_ref = ref.ppo_actor_step(CFG, w, seqs, rs, np.concatenate(old), np.concatenate(adv), 0.2, lr,
+                                      adam=ADAM, n_steps=steps)
+    tr = px.Trainer(ctx, to_px_cfg(CFG), w, adamw=px.AdamWOptions(*ADAM))
+    losses = [tr.ppo_actor_step(seqs, rs, old, adv, clip_eps=0.2, lr=lr) for _ in range(steps)]
+    close(losses, l_ref)
+    close(tr.flat(), w_ref)
+    assert np.abs(w_ref - w).max() > lr  # the weights moved
+
+
+def test_critic_step_matches_reference(px, ctx, oracle, ref):
+    cfg = CFG
+    w = f32(ref.init_params(cfg, 6, head=True))
+    w[-cfg.d:] = f32(np.random.default_rng(2).normal(0, 0.1, cfg.d))  # a non-zero scalar head
+    seqs, rs = rollout(oracle, 4)
+    rng = np.random.default_rng(3)
+    n = [len(s) - r for s, r in zip(seqs, rs)]
+    old_v = [rng.normal(0, 0.5, k) for k in n]
+    rets = [rng.normal(0, 1, k) for k in n]
+    lr, steps = 3e-4, 3
+    w_ref, l_ref = ref.critic_step(cfg, w, seqs, rs, np.concatenate(old_v), np.concatenate(rets), 0.2, lr, adam=ADAM,
+                                   n_steps=steps)
+    tr = px.Trainer(ctx, to_px_cfg(cfg, True), w, adamw=px.AdamWOptions(*ADAM))
+    losses = [tr.critic_step(seqs, rs, old_v, rets, value_clip=0.2, lr=lr) for _ in range(steps)]
+    close(losses, l_ref)
+    close(tr.flat(), w_ref)
+
+
+@pytest.mark.parametrize("variant", ["dpo", "ipo", "cdpo", "kto"])
+def test_dpo_step_matches_reference(px, ctx, oracle, ref, variant):
+    w_pol = f32(ref.init_params(CFG, 7))
+    w_ref = f32(ref.init_params(CFG, 8))
+    rng = np.random.default_rng(4)
+    pc = to_px_cfg(CFG)
+    pairs = []
+    for i in range(4):
+        prompt = rng.integers(0, 256, 6 + i).tolist()
+        c, rc = px.build_sft_sequence(pc, prompt, rng.integers(0, 256, 7 + i).tolist())
+        r, rr = px.build_sft_sequence(pc, prompt, rng.integers(0, 256, 5 + 2 * i).tolist())
+        pairs.append((c, r, rc, rr))
+    lr, steps, beta, eps = 3e-4, 2, 0.5, 0.1
+    var = {"dpo": 0, "ipo": 1, "cdpo": 2, "kto": 3}[variant]
+    w_out, l_ref = ref.dpo_step(CFG, w_pol, w_ref, pairs, var, beta, eps, lr, adam=ADAM, n_steps=steps)
+    frozen = px.DeviceModel(ctx, pc, w_ref, px.F32)
+    tr = px.Trainer(ctx, pc, w_pol, adamw=px.AdamWOptions(*ADAM))
+    losses = [tr.dpo_step(frozen, pairs, variant, beta, eps, lr)[0] for _ in range(steps)]
+    close(losses, l_ref)
+    close(tr.flat(), w_out)
+
+
+def test_trainer_refit_updates_the_engine(px, ctx, oracle, ref):
+    """After an actor update, refit pushes the weights into the serving engine
+    in place: the generation counter advances and the engine's snapshot is the
+    trainer's weights (Engine::refit, src/engine.cpp:60-90)."""
+    w = f32(ref.init_params(CFG, 9))
+    pc = to_px_cfg(CFG)
+    eng = px.Engine(px.DeviceModel(ctx, pc, w, px.F32))
+    tr = px.Trainer(ctx, pc, w, serving=eng.model)
+    seqs, rs = rollout(oracle, 5, n=3)
+    lps = oracle.sequence_logprobs(CFG, w, seqs)
+    old = [lp[r:] for lp, r in zip(lps, rs)]
+    adv = [np.ones(len(o)) for o in old]
+    tr.ppo_actor_step(seqs, rs, old, adv, lr=1e-3)
+    g0 = eng.generation_counter
+    tr.refit()
+    assert eng.generation_counter == g0 + 1
+    snap = eng.model.snapshot()
+    got = tr.get()
+    for k in ("tok_embed.weight", "layers.1.attn.q_proj.weight", "layers.0.ffn.down_proj.weight", "final_norm.bias"):
+        assert np.array_equal(snap[k], got[k]), k
+    # the refitted engine generates what a freshly built engine on those weights generates
+    flat = tr.flat()
+    fresh = px.Engine(px.DeviceModel(ctx, pc, flat, px.F32))
+    task = [px.GenTask(list(seqs[0][:rs[0]]), 8)]
+    a, b = eng.generate_batch(task)[0], fresh.generate_batch(task)[0]
+    assert np.array_equal(a.tokens, b.tokens) and np.array_equal(a.logprobs, b.logprobs)

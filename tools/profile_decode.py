@@ -16,12 +16,13 @@ ap.add_argument("--config", default="c2")
 ap.add_argument("--new", type=int, default=24)
 ap.add_argument("--graphs", type=int, default=1)
 ap.add_argument("--score", type=int, default=0)
+ap.add_argument("--dtype", default="mixed", choices=["mixed", "bf16"])
 a = ap.parse_args()
 V, d, L, H, f, S, B, P, N, samp, _ = bench.CONFIGS[a.config]
 cfg = px.ModelConfig(V, d, L, H, f, S)
 ctx = px.Context(0)
 dev = torch.device("cuda", 0)
-m = px.DeviceModel(ctx, cfg, bench.init_weights(cfg, 1, dev), px.BF16)
+m = px.DeviceModel(ctx, cfg, bench.init_weights(cfg, 1, dev), px.MIXED if a.dtype == "mixed" else px.BF16)
 eng = px.Engine(m, px.EngineOptions(max_batch=B, use_graphs=bool(a.graphs)))
 prompts = bench.prompts_for(0, B, P, V, 1)
 tasks = [px.GenTask(p, a.new, px.SamplingSpec.temperature_spec(1.0, i, 0, 0.9)) for i, p in enumerate(prompts)]

@@ -1,0 +1,31 @@
+#!/bin/bash
+# Round-2 profiles (run on the GPU box through gpurun).  Produces gpurun_out/prof2/*
+# for profiles/round2/.  Every ncu command profiles a workload that first ran
+# clean without ncu; --clock-control none throughout (B200_PROFILING.md).
+set -x
+O=gpurun_out/prof2
+mkdir -p $O
+BENCH="python bench.py --steps 2 --warmup 1 --e2e-steps 0 --no-cpu-baseline --no-profile --no-variant"
+$BENCH > $O/bench_plain.log 2>&1 || exit 1
+DEC="python tools/profile_decode.py --new 88 --dtype mixed"
+$DEC > $O/decode_plain.log 2>&1 || exit 1
+SCORE="python tools/profile_decode.py --new 24 --dtype mixed --score 1"
+$SCORE > $O/score_plain.log 2>&1 || exit 1
+# 1. the contract's launch list of the bench command (per-launch device times, cold, serialised)
+ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-file $O/launches_bench.csv $BENCH > $O/ncu0.log 2>&1
+# 2. warm-L2 launch list of steady-state mixed decode with DRAM bytes per launch
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
+    --cache-control none -s 1500 -c 900 --csv --log-file $O/launches_decode.csv $DEC > $O/ncu1.log 2>&1
+# 3. scoring-phase kernels with DRAM bytes
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
+    -k regex:"gemm_mixed|attn_prefill_split|layernorm|lse_combine" -s 100 -c 300 --csv \
+    --log-file $O/launches_scoring.csv $SCORE > $O/ncu2.log 2>&1
+# 4. full captures of the top kernels
+ncu --set full --import-source on --clock-control none -k regex:gemm_decode_kernel -s 202 -c 1 -o $O/full_gemm_decode_a $DEC > $O/ncu3.log 2>&1
+ncu --set full --import-source on --clock-control none -k regex:gemm_decode_kernel -s 201 -c 1 -o $O/full_gemm_decode_b $DEC > $O/ncu4.log 2>&1
+ncu --set full --import-source on --clock-control none -k regex:attn_decode -s 100 -c 1 -o $O/full_attn_decode $DEC > $O/ncu5.log 2>&1
+ncu --set full --import-source on --clock-control none -k regex:sampler -s 30 -c 1 -o $O/full_sampler $DEC > $O/ncu6.log 2>&1
+ncu --set full --import-source on --clock-control none -k regex:"gemm_mixed_kernel" -s 40 -c 1 -o $O/full_gemm_mixed $SCORE > $O/ncu7.log 2>&1
+ncu --set full --import-source on --clock-control none -k regex:"attn_prefill_split" -s 10 -c 1 -o $O/full_attn_prefill_split $SCORE > $O/ncu8.log 2>&1
+ncu --set full --import-source on --clock-control none -k regex:"gemm_mixed_kernel<4>" -s 0 -c 1 -o $O/full_lm_head_lse $SCORE > $O/ncu9.log 2>&1
+ls -la $O
