@@ -139,6 +139,7 @@ __global__ void __launch_bounds__(128, 6) attn_decode_kernel(const T* __restrict
   constexpr int EPT = DH;                     // lane-per-token: whole row
   constexpr int DPL = DH >= 32 ? DH / 32 : 1; // dims per lane (P·V)
   constexpr int DLANES = DH / DPL;
+  constexpr bool HALF = TT == 16 && sizeof(T) == 4 && CPR % 2 == 0;  // fp32 KV: 16-token tiles, half rows per lane
   extern __shared__ __align__(16) uint8_t smem_dec[];
   __shared__ float sm_m[NW], sm_l[NW];
   __shared__ float sm_acc[NW][DH];
@@ -222,9 +223,25 @@ __global__ void __launch_bounds__(128, 6) attn_decode_kernel(const T* __restrict
     }
     __syncwarp();
     const int nt = int((ctx - t0) < TT ? (ctx - t0) : TT);
-    // ---- scores: lane = token
+    // ---- scores: lane = token (HALF: 16-token fp32 tiles, lanes 0-15 and
+    // 16-31 take the two halves of the same token's row, one shuffle joins them)
     float s = -FLT_MAX;
-    if (lane < nt) {
+    if constexpr (HALF) {
+      const int tk = lane & 15, hv = lane >> 4;
+      float dot = 0.f;
+      if (tk < nt) {
+        const uint8_t* kt = tile_ptr(buf, 0);
+#pragma unroll
+        for (int c = hv * (CPR / 2); c < (hv + 1) * (CPR / 2); ++c) {
+          Vec16<T> v4;
+          v4.u = *reinterpret_cast<const uint4*>(kt + chunk(tk, c));
+#pragma unroll
+          for (int e = 0; e < Vec16<T>::N; ++e) dot = fmaf(to_f(v4.v[e]), q[c * Vec16<T>::N + e], dot);
+        }
+      }
+      dot += __shfl_xor_sync(0xffffffffu, dot, 16);
+      if (lane < nt) s = dot * inv_sqrt_dh;
+    } else if (lane < nt) {
       const uint8_t* kt = tile_ptr(buf, 0);
       float dot = 0.f;
 #pragma unroll
@@ -343,8 +360,16 @@ void decode_impl(Ctx& c, const T* qkv, int64_t B, const int32_t* pos, const int3
     const char* e = getenv("PPOEXP_ATTN_TILE");
     return e ? atoi(e) : 32;
   }();
+  // fp32 KV (mixed / F32 modes): a 32-token fp32 tile set is 64 KB per CTA (3 CTAs/SM, 1.7 waves at
+  // C2); 16-token tiles with two lanes per token row keep 6 CTAs/SM (one wave)
+  static const int f32_tile = [] {
+    const char* e = getenv("PPOEXP_ATTN_TILE_F32");
+    return e ? atoi(e) : 16;
+  }();
   if (tile == 16 && DH * sizeof(T) == 128)
     decode_launch<T, DH, 2, 16>(c, qkv, B, pos, done, block_table, layer, g, kv, out, bytes);
+  else if (sizeof(T) == 4 && f32_tile == 16 && DH >= 32)
+    decode_launch<T, DH, 1, 16>(c, qkv, B, pos, done, block_table, layer, g, kv, out, bytes);
   else
     decode_launch<T, DH, 1, 32>(c, qkv, B, pos, done, block_table, layer, g, kv, out, bytes);
 }
