@@ -626,6 +626,22 @@ def run_c5(args):
                           "tflops": fl / t / 1e12, "frac": fl / t / 1e12 / pk.get("bf16_tflops_sustained", 1400.0),
                           "sum_mean": float(np.mean(sums))})
             _dbg("c5", sweep[-1])
+    breakdown = None
+    if args.profile_classes:  # CUPTI kernel durations of one more B=1 scoring call (after the timed sweep)
+        try:
+            from torch.profiler import ProfilerActivity, profile
+            seqs1 = seqs[:2]
+            with profile(activities=[ProfilerActivity.CUDA]) as prof:
+                px.response_logprob_sums(model, seqs1, rs[:2])
+                torch.cuda.synchronize()
+            agg = {}
+            for e in prof.events():
+                if e.device_type == torch.autograd.DeviceType.CUDA and "Memcpy" not in e.name:
+                    k = kclass(e.name)
+                    agg[k] = agg.get(k, 0.0) + (e.time_range.end - e.time_range.start)
+            breakdown = {k: v / 1000.0 for k, v in sorted(agg.items(), key=lambda x: -x[1])}
+        except Exception as e:  # profiler unavailable
+            _dbg("cupti failed", e)
     top = max(sweep, key=lambda x: x["pairs"])
     line = {"metric": "dpo_scored_pairs_per_s", "value": top["pairs_per_s"], "unit": "pairs/s", "n_gpus": 1,
             "steps": args.c5_steps, "warmup": 1, "ms_per_step": top["ms"], "higher_is_better": True, "scaling": "weak",
@@ -639,6 +655,8 @@ def run_c5(args):
                          "note": "whole scoring pass (all kernels) at the largest B; algorithmic flops = layer GEMMs "
                                  "over all positions + causal attention + LM head over response rows"},
             "clocks": clk.summary()}
+    if breakdown:
+        line["kernel_ms_one_pair"] = breakdown
     print(json.dumps(line), flush=True)
     model.close()
     ctx.close()

@@ -22,6 +22,17 @@ PPOEXP_API ppoexp_status ppoexp_testing_gemm_bf16(ppoexp_ctx ctx, const void* A,
  * "sampler:pair_uncached"); graph-captured launches count once per capture. */
 PPOEXP_API ppoexp_status ppoexp_testing_variant_count(ppoexp_ctx ctx, const char* name, int64_t* out);
 
+/* Causal prefill attention over packed ragged sequences (bf16 qkv [M, 3 d],
+ * out [M, d]); path 0 = tcgen05 flash attention, 1 = mma.sync. */
+PPOEXP_API ppoexp_status ppoexp_testing_attention_prefill(ppoexp_ctx ctx, const void* qkv, const int64_t* offsets,
+                                               int64_t B, int64_t max_len, int64_t H, int64_t DH, int64_t M,
+                                               void* out, int32_t path);
+
+/* D[128, N] = A[128, 64] (K-major) x B[64, N] (row-major: MN-major operand), one
+ * tcgen05 MMA chain; pins the MN-major 128B-swizzle descriptor (variant 0 / 1). */
+PPOEXP_API ppoexp_status ppoexp_testing_umma_probe(ppoexp_ctx ctx, const void* A, const void* B, int32_t N, float* out,
+                                        int32_t variant);
+
 /* Mixed-mode GEMM: C[M,N] (+)= A[M,K] (fp32) · W[N,K]^T (bf16), activations
  * split into two bf16 terms in-kernel.  epi: 2 fp32 residual add, 3 store fp32,
  * 5 GELU -> fp32.  M <= 256 takes the decode (swap-AB, cluster split-K) kernel. */

@@ -1183,3 +1183,40 @@ extern "C" ppoexp_status ppoexp_testing_variant_count(ppoexp_ctx ctx, const char
     *out = it == ctx->c->variants.end() ? 0 : it->second;
   });
 }
+
+namespace ppx {
+void umma_probe(Ctx& c, const bf16* A, const bf16* B, int N, float* out, int variant);
+}
+extern "C" ppoexp_status ppoexp_testing_umma_probe(ppoexp_ctx ctx, const void* A, const void* B, int32_t N, float* out,
+                                                   int32_t variant) {
+  return guard([&] {
+    need(ctx, "ctx");
+    Ctx& c = *ctx->c;
+    std::lock_guard<std::recursive_mutex> lk(c.mu);
+    DeviceGuard g(c.device);
+    if (N != 64 && N != 128) throw ContractError("N must be 64 or 128");
+    umma_probe(c, static_cast<const bf16*>(A), static_cast<const bf16*>(B), N, out, variant);
+    c.sync();
+  });
+}
+
+namespace ppx {
+bool attention_prefill_mma(Ctx& c, const bf16* qkv, const int64_t* seq_offsets, int64_t B, int64_t max_len,
+                           int64_t H, int64_t DH, bf16* out);
+}
+extern "C" ppoexp_status ppoexp_testing_attention_prefill(ppoexp_ctx ctx, const void* qkv, const int64_t* offsets,
+                                                          int64_t B, int64_t max_len, int64_t H, int64_t DH,
+                                                          int64_t M, void* out, int32_t path) {
+  return guard([&] {
+    need(ctx, "ctx");
+    Ctx& c = *ctx->c;
+    std::lock_guard<std::recursive_mutex> lk(c.mu);
+    DeviceGuard g(c.device);
+    const auto* q = static_cast<const bf16*>(qkv);
+    auto* o = static_cast<bf16*>(out);
+    bool ok = path == 0 ? attention_prefill_tc(c, q, offsets, B, max_len, H, DH, M, o)
+                        : attention_prefill_mma(c, q, offsets, B, max_len, H, DH, o);
+    if (!ok) throw ContractError("attention path not eligible for this shape");
+    c.sync();
+  });
+}

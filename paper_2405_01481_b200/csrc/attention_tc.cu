@@ -1,0 +1,353 @@
+// attention_tc.cu — K5a on the 5th-generation tensor cores: causal flash
+// attention over packed ragged sequences (bf16 scoring / critic / RM forwards
+// and the engine's batched prefill; src/model.cpp:230-236 semantics: scores
+// scaled by 1/sqrt(dh) before the max, causal, exp(s - max) / sum).
+//
+// CTA = 128 queries of one (sequence, head), 6 warps:
+//   warp 0    : TMA producer — the Q tile once, then K / V tiles of 64 keys
+//               (128B-swizzled boxes of the packed qkv buffer) into a 3-stage ring;
+//   warp 1    : TMEM allocator + MMA issuer — S_j = Q K_j^T into one of two TMEM
+//               score buffers (issued one tile ahead), O += P_j V_j into the TMEM
+//               output accumulator (V is the MN-major B operand, straight from TMA);
+//   warps 2-5 : softmax — thread r owns query row r (TMEM lane r): tcgen05.ld of
+//               the score row, mask, online max / sum in the log2 domain, the
+//               O-row rescale in TMEM when the max moves, P_j (bf16) written in
+//               the UMMA K-major swizzle; epilogue O / l -> global.
+#include <cuda.h>
+
+#include <cfloat>
+
+#include "kernels.hpp"
+
+namespace ppx {
+
+CUtensorMap make_map(const void* ptr, int64_t rows, int64_t cols, int64_t ld, int box_rows);  // gemm_tc.cu
+
+namespace {
+
+constexpr int BQ = 128, BKV = 64, NST = 3, kThr = 192;
+
+__device__ __forceinline__ uint32_t su32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void bar_init(uint64_t* b, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(n));
+}
+__device__ __forceinline__ void bar_expect(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ void bar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\nWAIT_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t@!P1 bra WAIT_%=;\n\t}" ::"r"(
+          su32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma2d(const CUtensorMap* m, uint64_t* bar, void* dst, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          su32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(su32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+// K-major, 128B swizzle, 8-row atoms 1024 B apart
+__device__ __forceinline__ uint64_t desc_k(const void* p) {
+  const uint64_t a = su32(p);
+  return ((a >> 4) & 0x3FFFull) | (1ull << 16) | (64ull << 32) | (1ull << 46) | (2ull << 61);
+}
+// MN-major, 128B swizzle: 8 K-rows x 128 B atoms, 1024 B apart along K; the next
+// 64 N-elements (the next TMA box of 64 rows x 128 B) 8192 B further (pinned by
+// tools/umma_probe.py / umma_probe.cu)
+__device__ __forceinline__ uint64_t desc_mn(const void* p) {
+  const uint64_t a = su32(p);
+  return ((a >> 4) & 0x3FFFull) | ((8192ull >> 4) << 16) | ((1024ull >> 4) << 32) | (1ull << 46) | (2ull << 61);
+}
+constexpr uint32_t idesc(int M, int N, bool b_mn) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | (b_mn ? (1u << 16) : 0u) | (uint32_t(N >> 3) << 17) |
+         (uint32_t(M >> 4) << 24);
+}
+__device__ __forceinline__ void mma(uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\ttcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+      "l"(a), "l"(b), "r"(id), "r"(acc));
+}
+__device__ __forceinline__ void commit(uint64_t* b) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ void tld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,"
+      "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tst32(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,"
+      "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
+      "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
+      "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+
+template <int DH>
+struct FaSmem {
+  static constexpr int kQ = BQ * DH * 2;      // Q: DH/64 boxes of 128 rows x 128 B
+  static constexpr int kKV = BKV * DH * 2;    // one K (or V) tile: DH/64 boxes of 64 rows x 128 B
+  static constexpr int kP = BQ * BKV * 2;     // P tile: 128 rows x 128 B
+  static constexpr int kBytes = kQ + NST * 2 * kKV + 2 * kP + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int kTmem = 256;           // S0 (64) | S1 (64) | O (DH <= 128)
+};
+
+template <int DH>
+__global__ void __launch_bounds__(kThr, 1)
+    attn_prefill_tc_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tkv,
+                           const int64_t* __restrict__ seq_offsets, int H, bf16* __restrict__ out) {
+  using L = FaSmem<DH>;
+  constexpr int NB = DH / 64;  // 64-column boxes per row
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = sm;
+  auto sK = [&](int s) { return sm + L::kQ + s * 2 * L::kKV; };
+  auto sV = [&](int s) { return sm + L::kQ + s * 2 * L::kKV + L::kKV; };
+  auto sP = [&](int b) { return sm + L::kQ + NST * 2 * L::kKV + b * L::kP; };
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L::kQ + NST * 2 * L::kKV + 2 * L::kP);
+  uint64_t* q_full = bars;
+  uint64_t* kv_full = bars + 1;         // [NST]
+  uint64_t* kv_empty = kv_full + NST;   // [NST]
+  uint64_t* s_full = kv_empty + NST;    // [2]
+  uint64_t* s_free = s_full + 2;        // [2]
+  uint64_t* p_full = s_free + 2;        // [2]
+  uint64_t* o_done = p_full + 2;        // one completion per P V product
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(o_done + 1);
+
+  PDL_ENTRY();
+  const int64_t b = blockIdx.z;
+  const int h = blockIdx.y;
+  const int64_t q0 = int64_t(blockIdx.x) * BQ;
+  const int64_t start = seq_offsets[b], len = seq_offsets[b + 1] - start;
+  if (q0 >= len) return;
+  const int64_t d = int64_t(H) * DH;
+  const int64_t kend = min(len, q0 + BQ);
+  const int nt = int((kend + BKV - 1) / BKV);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    bar_init(q_full, 1);
+    for (int s = 0; s < NST; ++s) {
+      bar_init(&kv_full[s], 1);
+      bar_init(&kv_empty[s], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      bar_init(&s_full[i], 1);
+      bar_init(&s_free[i], 128);
+      bar_init(&p_full[i], 128);
+    }
+    bar_init(o_done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tq)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tkv)) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tslot)), "r"(L::kTmem));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tslot;
+  const uint32_t tO = tmem + 128;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      bar_expect(q_full, L::kQ);
+      for (int c = 0; c < NB; ++c) tma2d(&tq, q_full, sQ + c * (BQ * 128), int(h * DH + c * 64), int(start + q0));
+      for (int j = 0; j < nt; ++j) {
+        const int s = j % NST, r = j / NST;
+        if (r > 0) bar_wait(&kv_empty[s], (r - 1) & 1);
+        bar_expect(&kv_full[s], 2 * L::kKV);
+        const int row = int(start + int64_t(j) * BKV);
+        for (int c = 0; c < NB; ++c) {
+          tma2d(&tkv, &kv_full[s], sK(s) + c * (BKV * 128), int(d + h * DH + c * 64), row);
+          tma2d(&tkv, &kv_full[s], sV(s) + c * (BKV * 128), int(2 * d + h * DH + c * 64), row);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t id_s = idesc(BQ, BKV, false), id_o = idesc(BQ, DH, true);
+      auto issue_s = [&](int j) {
+        const int s = j % NST, bf = j & 1;
+        bar_wait(&kv_full[s], (j / NST) & 1);
+        if (j >= 2) bar_wait(&s_free[bf], ((j >> 1) - 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+        for (int kk = 0; kk < DH / 16; ++kk) {
+          const uint64_t a = desc_k(sQ + (kk >> 2) * (BQ * 128)) + 2 * (kk & 3);
+          const uint64_t bb = desc_k(sK(s) + (kk >> 2) * (BKV * 128)) + 2 * (kk & 3);
+          mma(tmem + bf * 64, a, bb, id_s, kk > 0);
+        }
+        commit(&s_full[bf]);
+      };
+      bar_wait(q_full, 0);
+      issue_s(0);
+      for (int j = 0; j < nt; ++j) {
+        if (j + 1 < nt) issue_s(j + 1);
+        const int bf = j & 1, s = j % NST;
+        bar_wait(&p_full[bf], (j >> 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+        for (int kk = 0; kk < BKV / 16; ++kk) {
+          const uint64_t a = desc_k(sP(bf)) + 2 * kk;
+          const uint64_t bb = desc_mn(sV(s)) + ((2048 * kk) >> 4);
+          mma(tO, a, bb, id_o, (j | kk) != 0);
+        }
+        commit(o_done);
+        commit(&kv_empty[s]);
+      }
+    }
+    __syncwarp();
+  } else {
+    // ---- softmax: thread r <-> query q0 + r <-> TMEM lane r
+    const int q = warp & 3, r = q * 32 + lane;
+    const uint32_t lane_off = uint32_t(q * 32) << 16;
+    const int64_t qi = q0 + r;
+    const float scale = 1.4426950408889634f / sqrtf(float(DH));  // log2 domain
+    float m = -FLT_MAX, l = 0.f;
+    for (int j = 0; j < nt; ++j) {
+      const int bf = j & 1;
+      bar_wait(&s_full[bf], (j >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      uint32_t sa[32], sb[32];
+      tld32(tmem + lane_off + bf * 64, sa);
+      tld32(tmem + lane_off + bf * 64 + 32, sb);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      bar_arrive(&s_free[bf]);
+      const int64_t k0 = int64_t(j) * BKV;
+      float sv[64];
+      float mx = -FLT_MAX;
+#pragma unroll
+      for (int c = 0; c < 64; ++c) {
+        const int64_t key = k0 + c;
+        float v = __uint_as_float(c < 32 ? sa[c] : sb[c - 32]) * scale;
+        if (key > qi || key >= len) v = -FLT_MAX;
+        sv[c] = v;
+        mx = fmaxf(mx, v);
+      }
+      const float mn = fmaxf(m, mx);
+      const float corr = m == -FLT_MAX ? 0.f : exp2f(m - mn);
+      float rs = 0.f;
+#pragma unroll
+      for (int c = 0; c < 64; ++c) {
+        const float p = sv[c] == -FLT_MAX ? 0.f : exp2f(sv[c] - mn);
+        sv[c] = p;
+        rs += p;
+      }
+      l = l * corr + rs;
+      if (j > 0) {
+        // O holds P_{j-1} V_{j-1}: wait for it, then rescale rows whose max moved
+        bar_wait(o_done, (j - 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        if (__any_sync(0xffffffffu, mn > m)) {
+#pragma unroll 1
+          for (int c = 0; c < DH; c += 32) {
+            uint32_t o[32];
+            tld32(tO + lane_off + c, o);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+            for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * corr);
+            tst32(tO + lane_off + c, o);
+          }
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        }
+      }
+      m = mn;
+      // P_j row (bf16) in the K-major 128B swizzle: row r at r * 128, chunk c ^ (r & 7)
+      uint8_t* prow = sP(bf) + r * 128;
+#pragma unroll
+      for (int c8 = 0; c8 < 8; ++c8) {
+        Vec16<bf16> pv;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) pv.v[e] = __float2bfloat16_rn(sv[c8 * 8 + e]);
+        *reinterpret_cast<uint4*>(prow + ((c8 ^ (r & 7)) << 4)) = pv.u;
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      bar_arrive(&p_full[bf]);
+    }
+    // ---- epilogue: O / l
+    bar_wait(o_done, (nt - 1) & 1);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const float inv = 1.0f / l;
+#pragma unroll 1
+    for (int c = 0; c < DH; c += 32) {
+      uint32_t o[32];
+      tld32(tO + lane_off + c, o);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      if (qi < len) {
+        bf16* dst = out + (start + qi) * d + h * DH + c;
+#pragma unroll
+        for (int e8 = 0; e8 < 32; e8 += 8) {
+          Vec16<bf16> ov;
+#pragma unroll
+          for (int e = 0; e < 8; ++e) ov.v[e] = __float2bfloat16_rn(__uint_as_float(o[e8 + e]) * inv);
+          *reinterpret_cast<uint4*>(dst + e8) = ov.u;
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(L::kTmem));
+  }
+}
+
+template <int DH>
+void launch_fa(Ctx& c, const bf16* qkv, const int64_t* seq_offsets, int64_t B, int64_t max_len, int64_t H,
+               int64_t M_total, bf16* out) {
+  using L = FaSmem<DH>;
+  const int64_t d = H * DH;
+  const CUtensorMap tq = make_map(qkv, M_total, 3 * d, 3 * d, BQ);
+  const CUtensorMap tkv = make_map(qkv, M_total, 3 * d, 3 * d, BKV);
+  static bool attr = false;
+  if (!attr) {
+    PPOEXP_CUDA(cudaFuncSetAttribute(attn_prefill_tc_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     L::kBytes));
+    attr = true;
+  }
+  dim3 grid(unsigned(ceil_div(max_len, BQ)), unsigned(H), unsigned(B));
+  const double flops = 2.0 * 2.0 * B * H * double(max_len) * max_len / 2 * DH;
+  c.launch("attention_prefill", 0, flops, [&] {
+    launch_kernel(c, attn_prefill_tc_kernel<DH>, grid, dim3(kThr), L::kBytes, 1, tq, tkv, seq_offsets, int(H), out);
+  });
+}
+
+}  // namespace
+
+// bf16 prefill attention on tcgen05; false when the shape is not supported
+// (head_dim 64 / 128, 16-byte aligned qkv rows).
+bool attention_prefill_tc(Ctx& c, const bf16* qkv, const int64_t* seq_offsets, int64_t B, int64_t max_len, int64_t H,
+                          int64_t DH, int64_t M_total, bf16* out) {
+  static const bool off = [] {
+    const char* e = getenv("PPOEXP_ATTN_TC");
+    return e && e[0] == '0';
+  }();
+  if (off || M_total <= 0 || (reinterpret_cast<uintptr_t>(qkv) & 15)) return false;
+  switch (DH) {
+    case 64: return launch_fa<64>(c, qkv, seq_offsets, B, max_len, H, M_total, out), true;
+    case 128: return launch_fa<128>(c, qkv, seq_offsets, B, max_len, H, M_total, out), true;
+    default: return false;
+  }
+}
+
+}  // namespace ppx

@@ -355,6 +355,63 @@ __global__ void __launch_bounds__(256) layernorm_warp_kernel(const float* __rest
   }
 }
 
+// Wide rows (1024 < d <= 8192, d % 1024 == 0 via VPT float4 per thread): CTA
+// of 256 threads per row, every load issued before the first reduction,
+// two-pass statistics from registers, 8- / 16-byte stores.
+template <class T, int VPT>
+__global__ void __launch_bounds__(256) layernorm_wide_kernel(const float* __restrict__ x, int64_t d,
+                                                             const float* __restrict__ g, const float* __restrict__ b,
+                                                             T* __restrict__ y, const int32_t* __restrict__ gather,
+                                                             const float* __restrict__ head,
+                                                             float* __restrict__ head_out) {
+  PDL_ENTRY();
+  __shared__ float red[32];
+  const int64_t r = blockIdx.x;
+  const int64_t src = gather ? gather[r] : r;
+  const float4* xr = reinterpret_cast<const float4*>(x + src * d);
+  float4 v[VPT];
+#pragma unroll
+  for (int i = 0; i < VPT; ++i) v[i] = __ldg(xr + threadIdx.x + i * 256);
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < VPT; ++i) s += (v[i].x + v[i].y) + (v[i].z + v[i].w);
+  const float mu = block_sum<256>(s, red) / float(d);
+  float q = 0.f;
+#pragma unroll
+  for (int i = 0; i < VPT; ++i) {
+    const float a = v[i].x - mu, bq = v[i].y - mu, c = v[i].z - mu, e = v[i].w - mu;
+    q += (a * a + bq * bq) + (c * c + e * e);
+  }
+  const float is = 1.0f / sqrtf(block_sum<256>(q, red) / float(d) + 1e-5f);
+  float hd = 0.f;
+#pragma unroll
+  for (int i = 0; i < VPT; ++i) {
+    const int j = (threadIdx.x + i * 256) * 4;
+    const float4 gg = __ldg(reinterpret_cast<const float4*>(g + j)), bb = __ldg(reinterpret_cast<const float4*>(b + j));
+    const float o0 = gg.x * ((v[i].x - mu) * is) + bb.x, o1 = gg.y * ((v[i].y - mu) * is) + bb.y;
+    const float o2 = gg.z * ((v[i].z - mu) * is) + bb.z, o3 = gg.w * ((v[i].w - mu) * is) + bb.w;
+    if (y) {
+      if constexpr (sizeof(T) == 2) {
+        __nv_bfloat162 p0 = __floats2bfloat162_rn(o0, o1), p1 = __floats2bfloat162_rn(o2, o3);
+        uint2 u;
+        u.x = *reinterpret_cast<uint32_t*>(&p0);
+        u.y = *reinterpret_cast<uint32_t*>(&p1);
+        *reinterpret_cast<uint2*>(y + r * d + j) = u;
+      } else {
+        *reinterpret_cast<float4*>(y + r * d + j) = make_float4(o0, o1, o2, o3);
+      }
+    }
+    if (head) {
+      const float4 hh = __ldg(reinterpret_cast<const float4*>(head + j));
+      hd += o0 * hh.x + o1 * hh.y + o2 * hh.z + o3 * hh.w;
+    }
+  }
+  if (head) {
+    hd = block_sum<256>(hd, red);
+    if (threadIdx.x == 0) head_out[r] = hd;
+  }
+}
+
 // CTA-per-row float4 variant for few rows (decode): one float4 per thread,
 // two barrier-reductions — short dependency chains on many SMs.
 template <class T>
@@ -489,6 +546,19 @@ void launch_layernorm(Ctx& c, const float* x, int64_t rows, int64_t d, const flo
       } else {
         launch_kernel(c, layernorm_warp_kernel<T>, dim3(ceil_div(rows, 8)), dim3(256), 0, 1, x, rows, d, g, b, y,
                       gather, head, head_out);
+      }
+    } else if (d % 1024 == 0 && d <= 8192) {
+      auto go = [&](auto kern) {
+        launch_kernel(c, kern, dim3(rows), dim3(256), 0, 1, x, d, g, b, y, gather, head, head_out);
+      };
+      switch (d / 1024) {
+        case 2: go(layernorm_wide_kernel<T, 2>); break;
+        case 3: go(layernorm_wide_kernel<T, 3>); break;
+        case 4: go(layernorm_wide_kernel<T, 4>); break;
+        case 5: go(layernorm_wide_kernel<T, 5>); break;
+        case 6: go(layernorm_wide_kernel<T, 6>); break;
+        case 7: go(layernorm_wide_kernel<T, 7>); break;
+        default: go(layernorm_wide_kernel<T, 8>); break;
       }
     } else {
       launch_kernel(c, layernorm_kernel<T>, dim3(rows), dim3(256), 0, 1, x, rows, d, g, b, y, gather, head, head_out);

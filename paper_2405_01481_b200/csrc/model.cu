@@ -280,7 +280,9 @@ static float* forward_layers_t(Model& m, const Packed& p, const KvTarget* kv) {
     if (kv)
       launch_kv_scatter<T>(c, qkv, M, d, p.seq_of_row_d, p.positions_d, kv->block_table, int(l), kv->geom,
                            static_cast<T*>(kv->pool));
-    launch_attention_prefill<T>(c, qkv, p.offsets_d, p.B, p.max_len, H, DH, att);
+    bool done = false;
+    if constexpr (std::is_same_v<T, bf16>) done = attention_prefill_tc(c, qkv, p.offsets_d, p.B, p.max_len, H, DH, M, att);
+    if (!done) launch_attention_prefill<T>(c, qkv, p.offsets_d, p.B, p.max_len, H, DH, att);
     gemm<T>(c, att, d, static_cast<const T*>(ly.wo), d, M, d, d, Epi::kAddResidual, x, d);
     launch_layernorm<T>(c, x, M, d, ly.ln2w, ly.ln2b, h, nullptr, nullptr, nullptr);
     gemm<T>(c, h, d, static_cast<const T*>(ly.wup), d, M, f, d, Epi::kGelu, up, f);

@@ -140,3 +140,39 @@ def test_gemm_mixed_vs_torch(ctx, M, N, K, epi):
     err = (Cm[:, :N].double() - ref).abs()
     bound = 2.0 ** -16 * mag + 2e-7 * (1 + ref.abs())
     assert (err <= bound).all(), f"max abs err {err.max().item():.3e}, max err/bound {(err / bound).max().item():.3f}"
+
+
+@pytest.mark.parametrize("DH,H,lens", [(64, 12, [320, 37, 1, 129, 64]), (128, 4, [4096]), (128, 8, [200, 513, 7]),
+                                       (64, 2, [2048, 2048])])
+@pytest.mark.parametrize("path", [0, 1])
+def test_attention_prefill_vs_torch(ctx, DH, H, lens, path):
+    """Causal prefill attention over packed ragged sequences (src/model.cpp:230-236):
+    the tcgen05 flash attention (path 0: TMA K/V, S and O in TMEM, V as the
+    MN-major operand) and the mma.sync kernel (path 1) against torch fp32."""
+    import torch
+    from paper_2405_01481_b200 import ppoexp as px
+    f = px.lib().ppoexp_testing_attention_prefill
+    f.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_int64,
+                  C.c_void_p, C.c_int32]
+    f.restype = C.c_int32
+    d = H * DH
+    M = sum(lens)
+    g = torch.Generator(device="cuda").manual_seed(M + DH)
+    qkv = (torch.randn(M, 3 * d, generator=g, device="cuda") * 1.5).to(torch.bfloat16)
+    offs = torch.tensor([0] + list(np.cumsum(lens)), dtype=torch.int64, device="cuda")
+    out = torch.zeros(M, d, dtype=torch.bfloat16, device="cuda")
+    torch.cuda.synchronize()
+    px._check(f(ctx.h, qkv.data_ptr(), offs.data_ptr(), len(lens), max(lens), H, DH, M, out.data_ptr(), path))
+    ref = torch.empty(M, d, device="cuda")
+    q, k, v = qkv.float().split(d, dim=1)
+    o = 0
+    for T in lens:
+        qs = q[o:o + T].view(T, H, DH).transpose(0, 1)
+        ks = k[o:o + T].view(T, H, DH).transpose(0, 1)
+        vs = v[o:o + T].view(T, H, DH).transpose(0, 1)
+        s = qs @ ks.transpose(1, 2) / DH ** 0.5
+        s = s.masked_fill(torch.triu(torch.ones(T, T, dtype=torch.bool, device="cuda"), 1), float("-inf"))
+        ref[o:o + T] = (torch.softmax(s, -1) @ vs).transpose(0, 1).reshape(T, d)
+        o += T
+    err = (out.float() - ref).abs()
+    assert err.max().item() < 2e-2, f"max abs err {err.max().item():.3e}"
