@@ -337,12 +337,17 @@ void launch_fa(Ctx& c, const bf16* qkv, const int64_t* seq_offsets, int64_t B, i
 // bf16 prefill attention on tcgen05; false when the shape is not supported
 // (head_dim 64 / 128, 16-byte aligned qkv rows).
 bool attention_prefill_tc(Ctx& c, const bf16* qkv, const int64_t* seq_offsets, int64_t B, int64_t max_len, int64_t H,
-                          int64_t DH, int64_t M_total, bf16* out) {
-  static const bool off = [] {
+                          int64_t DH, int64_t M_total, bf16* out, bool force) {
+  // PPOEXP_ATTN_TC: 0 = never, 1 = always, default = sequences longer than 512
+  // (C2's 320-token rows: the 64-query mma.sync kernel measured 99 vs 119 us per
+  // launch — short key loops leave the tcgen05 pipeline mostly in its prologue;
+  // C5's 4096-token rows: 49.5 -> 36.0 ms per pair)
+  static const int mode = [] {
     const char* e = getenv("PPOEXP_ATTN_TC");
-    return e && e[0] == '0';
+    return e ? atoi(e) : -1;
   }();
-  if (off || M_total <= 0 || (reinterpret_cast<uintptr_t>(qkv) & 15)) return false;
+  if (!force && (mode == 0 || (mode < 0 && max_len <= 512))) return false;
+  if (M_total <= 0 || (reinterpret_cast<uintptr_t>(qkv) & 15)) return false;
   switch (DH) {
     case 64: return launch_fa<64>(c, qkv, seq_offsets, B, max_len, H, M_total, out), true;
     case 128: return launch_fa<128>(c, qkv, seq_offsets, B, max_len, H, M_total, out), true;

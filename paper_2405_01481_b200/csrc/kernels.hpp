@@ -124,7 +124,7 @@ void launch_attention_prefill(Ctx& c, const T* qkv, const int64_t* seq_offsets, 
 
 // K5a on tcgen05 (bf16, head_dim 64 / 128): false when not eligible.
 bool attention_prefill_tc(Ctx& c, const bf16* qkv, const int64_t* seq_offsets, int64_t B, int64_t max_len, int64_t H,
-                          int64_t DH, int64_t M_total, bf16* out);
+                          int64_t DH, int64_t M_total, bf16* out, bool force = false);
 // K5a in mixed mode: fp32 q/k/v in, fp32 out, tensor-core products on the
 // two-term bf16 split (three MMAs per product).
 void attention_prefill_split(Ctx& c, const float* qkv, const int64_t* seq_offsets, int64_t B, int64_t max_len,
