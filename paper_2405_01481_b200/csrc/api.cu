@@ -828,7 +828,20 @@ ppoexp_status ppoexp_make_experience(const ppoexp_experience_request* req, int64
       const char* e = getenv("PPOEXP_SCORE_STREAMS");
       return !(e && e[0] == '0');
     }();
-    const bool conc = concurrent && !rm;
+    // concurrent forwards hold one set of activation workspaces each: fall back
+    // to one stream when two more sets would not fit comfortably in free HBM
+    // (e.g. config 4 in mixed mode: 74k rows x (6 d + f) fp32 = 11.5 GB per set)
+    bool roomy = true;
+    {
+      size_t free_b = 0, total_b = 0;
+      if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
+        const double per_set = double(foff[B]) * double(6 * pol.cfg.d_model + pol.cfg.d_ff) * double(pol.asize());
+        roomy = 2.0 * per_set < 0.6 * double(free_b);
+      } else {
+        (void)cudaGetLastError();
+      }
+    }
+    const bool conc = concurrent && !rm && roomy;
     cudaStream_t main_stream = c.stream;
     auto on_aux = [&](int i, const char* prefix, auto&& body) {
       if (!conc) {

@@ -115,7 +115,7 @@ __global__ void __launch_bounds__(128, 6) attn_decode_kernel(const T* __restrict
                                                           const int32_t* __restrict__ done,
                                                           const int32_t* __restrict__ block_table, int layer,
                                                           KvGeom g, T* __restrict__ kv, T* __restrict__ out,
-                                                          unsigned long long* dbg) {
+                                                          unsigned long long* dbg, bf16* __restrict__ split_out) {
   // debug (PPOEXP_ATTN_TRACE): CTA (0, 0) thread 0 stage clocks
   auto stamp = [&](int k) {
     if (dbg && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) dbg[k] = clock64();
@@ -304,7 +304,14 @@ __global__ void __launch_bounds__(128, 6) attn_decode_kernel(const T* __restrict
     float o = 0.f;
 #pragma unroll
     for (int k = 0; k < NW; ++k) o += sm_acc[k][i] * sc[k];
-    out[b * d + h * DH + i] = from_f<T>(o * inv);
+    if (split_out) {  // mixed decode: the O projection TMAs the two bf16 terms
+      const float v = o * inv;
+      const bf16 hi = __float2bfloat16_rn(v);
+      split_out[b * 2 * d + h * DH + i] = hi;
+      split_out[b * 2 * d + d + h * DH + i] = __float2bfloat16_rn(v - __bfloat162float(hi));
+    } else {
+      out[b * d + h * DH + i] = from_f<T>(o * inv);
+    }
   }
   stamp(5);
   if (dbg && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) dbg[6] = ctx;
@@ -323,7 +330,8 @@ void prefill_impl(Ctx& c, const T* qkv, const int64_t* seq_offsets, int64_t B, i
 
 template <class T, int DH, int NS, int TT>
 void decode_launch(Ctx& c, const T* qkv, int64_t B, const int32_t* pos, const int32_t* done,
-                   const int32_t* block_table, int layer, const KvGeom& g, T* kv, T* out, double bytes) {
+                   const int32_t* block_table, int layer, const KvGeom& g, T* kv, T* out, double bytes,
+                   bf16* split_out) {
   auto k = attn_decode_kernel<T, DH, NS, TT>;
   const size_t row = DH * sizeof(T) == 128 ? 128 : DH * sizeof(T) + 16;  // kernel's LDB
   const size_t smem = size_t(4) * NS * 2 * TT * row;                     // 4 warps x NS x (K, V) x TT rows
@@ -343,12 +351,12 @@ void decode_launch(Ctx& c, const T* qkv, int64_t B, const int32_t* pos, const in
   if (getenv("PPOEXP_ATTN_TRACE"))  // debug: stamps of the last launch
     dbg = static_cast<unsigned long long*>(c.workspace("attn.trace", 16 * 8));
   c.launch("decode_attention", bytes, 0, [&] { launch_kernel(c, k, grid, dim3(128), smem, 1, qkv, pos, done,
-                                                              block_table, layer, g, kv, out, dbg); });
+                                                              block_table, layer, g, kv, out, dbg, split_out); });
 }
 
 template <class T, int DH>
 void decode_impl(Ctx& c, const T* qkv, int64_t B, const int32_t* pos, const int32_t* done, const int32_t* block_table,
-                 int layer, const KvGeom& g, T* kv, T* out, double bytes) {
+                 int layer, const KvGeom& g, T* kv, T* out, double bytes, bf16* split_out) {
   if (g.page_size % 32) throw ContractError("engine: page_size must be a multiple of 32");
   // single-stage tiles halve the CTA's shared memory (6 resident CTAs/SM for dh 64 bf16: one wave of
   // 768 (sequence, head) CTAs at C2); other warps on the SM hide each warp's tile latency
@@ -367,11 +375,11 @@ void decode_impl(Ctx& c, const T* qkv, int64_t B, const int32_t* pos, const int3
     return e ? atoi(e) : 16;
   }();
   if (tile == 16 && DH * sizeof(T) == 128)
-    decode_launch<T, DH, 2, 16>(c, qkv, B, pos, done, block_table, layer, g, kv, out, bytes);
+    decode_launch<T, DH, 2, 16>(c, qkv, B, pos, done, block_table, layer, g, kv, out, bytes, split_out);
   else if (sizeof(T) == 4 && f32_tile == 16 && DH >= 32)
-    decode_launch<T, DH, 1, 16>(c, qkv, B, pos, done, block_table, layer, g, kv, out, bytes);
+    decode_launch<T, DH, 1, 16>(c, qkv, B, pos, done, block_table, layer, g, kv, out, bytes, split_out);
   else
-    decode_launch<T, DH, 1, 32>(c, qkv, B, pos, done, block_table, layer, g, kv, out, bytes);
+    decode_launch<T, DH, 1, 32>(c, qkv, B, pos, done, block_table, layer, g, kv, out, bytes, split_out);
 }
 
 }  // namespace
@@ -398,13 +406,14 @@ void launch_attention_prefill(Ctx& c, const T* qkv, const int64_t* seq_offsets, 
 template <class T>
 void launch_attention_decode(Ctx& c, const T* qkv, int64_t B, const int32_t* pos, const int32_t* done,
                              const int32_t* block_table, int layer, const KvGeom& g, T* kv, T* out,
-                             double algorithmic_bytes) {
+                             double algorithmic_bytes, bf16* split_out) {
   if (B <= 0) return;
+  const double ab = algorithmic_bytes;
   switch (g.DH) {
-    case 16: return decode_impl<T, 16>(c, qkv, B, pos, done, block_table, layer, g, kv, out, algorithmic_bytes);
-    case 32: return decode_impl<T, 32>(c, qkv, B, pos, done, block_table, layer, g, kv, out, algorithmic_bytes);
-    case 64: return decode_impl<T, 64>(c, qkv, B, pos, done, block_table, layer, g, kv, out, algorithmic_bytes);
-    case 128: return decode_impl<T, 128>(c, qkv, B, pos, done, block_table, layer, g, kv, out, algorithmic_bytes);
+    case 16: return decode_impl<T, 16>(c, qkv, B, pos, done, block_table, layer, g, kv, out, ab, split_out);
+    case 32: return decode_impl<T, 32>(c, qkv, B, pos, done, block_table, layer, g, kv, out, ab, split_out);
+    case 64: return decode_impl<T, 64>(c, qkv, B, pos, done, block_table, layer, g, kv, out, ab, split_out);
+    case 128: return decode_impl<T, 128>(c, qkv, B, pos, done, block_table, layer, g, kv, out, ab, split_out);
     default: throw ContractError("attention: head_dim " + std::to_string(g.DH) + " unsupported (16/32/64/128)");
   }
 }
@@ -414,8 +423,8 @@ template void launch_attention_prefill<float>(Ctx&, const float*, const int64_t*
 template void launch_attention_prefill<bf16>(Ctx&, const bf16*, const int64_t*, int64_t, int64_t, int64_t, int64_t,
                                              bf16*);
 template void launch_attention_decode<float>(Ctx&, const float*, int64_t, const int32_t*, const int32_t*,
-                                             const int32_t*, int, const KvGeom&, float*, float*, double);
+                                             const int32_t*, int, const KvGeom&, float*, float*, double, bf16*);
 template void launch_attention_decode<bf16>(Ctx&, const bf16*, int64_t, const int32_t*, const int32_t*,
-                                            const int32_t*, int, const KvGeom&, bf16*, bf16*, double);
+                                            const int32_t*, int, const KvGeom&, bf16*, bf16*, double, bf16*);
 
 }  // namespace ppx

@@ -128,6 +128,14 @@ Engine::Engine(Model* model, const ppoexp_engine_options* o) : m(model), c(model
     const char* ev = getenv("PPOEXP_FUSE_LN");
     fuse_ln = m->dtype == PPOEXP_BF16 && !(ev && ev[0] == '0') && !use_mega && mb <= 256 && d % 8 == 0;
     if (m->mixed() && d % 8) throw ContractError("engine: mixed mode needs d_model % 8 == 0");
+    // mixed decode: split-plane activations TMA'd by the GEMMs (standalone split
+    // LayerNorm, attention / GELU epilogues writing hi|lo planes) — measured
+    // 754 -> 674 us per C2 step and 16.0 -> 13.2 ms per C4 step against the
+    // in-kernel split (PPOEXP_MIXED_PLANES=0: LayerNorm fused into the consumers,
+    // 2: planes for the O / down operands only)
+    const char* pe = getenv("PPOEXP_MIXED_PLANES");
+    mixed_planes = m->mixed() && (pe ? pe[0] == '1' : true) && d <= 4096;
+    mixed_oplanes = m->mixed() && !mixed_planes && pe && pe[0] == '2';
     fuse_ln_max_b = ev && ev[0] == '1' ? 256 : 64;
   }
   PPOEXP_CUDA(cudaMallocHost(&host_flags, 64));
@@ -292,6 +300,34 @@ void Engine::decode_unit_mixed(int64_t B, int64_t unit) {
   float* uu = static_cast<float*>(up);
   float* hh = static_cast<float*>(h);
   cur_unit = unit;
+  if (mixed_planes) {
+    // activations reach the GEMMs as two bf16 planes [B, 2K] TMA'd by the consumers:
+    // a standalone split LayerNorm (normalised once, not per weight tile), the
+    // attention writing its output split, the up projection's GELU epilogue split
+    bf16* hp = static_cast<bf16*>(h);   // [mb, 2d] in the fp32 [mb, d] buffer
+    bf16* ap = static_cast<bf16*>(att);
+    bf16* upp = static_cast<bf16*>(up);  // [mb, 2f]
+    launch_embed<bf16>(cc, next_tok, pos, B, d, static_cast<const bf16*>(m->tok), static_cast<const bf16*>(m->pos), x);
+    for (int64_t l = 0; l < L; ++l) {
+      const Layer& ly = m->layers[l];
+      launch_layernorm_split(cc, x, B, d, ly.ln1w, ly.ln1b, hp);
+      gemm_decode_planes(cc, hp, 2 * d, static_cast<const bf16*>(ly.wqkv), d, B, 3 * d, d, Epi::kStoreF32, q3, 3 * d,
+                         nullptr);
+      launch_attention_decode<float>(cc, q3, B, pos, done, block_table, int(l), geom, static_cast<float*>(kv.ptr), at,
+                                     0.0, ap);
+      gemm_decode_planes(cc, ap, 2 * d, static_cast<const bf16*>(ly.wo), d, B, d, d, Epi::kAddResidual, x, d, nullptr);
+      launch_layernorm_split(cc, x, B, d, ly.ln2w, ly.ln2b, hp);
+      gemm_decode_planes(cc, hp, 2 * d, static_cast<const bf16*>(ly.wup), d, B, f, d, Epi::kGeluSplit, upp, 2 * f,
+                         nullptr);
+      gemm_decode_planes(cc, upp, 2 * f, static_cast<const bf16*>(ly.wdown), f, B, d, f, Epi::kAddResidual, x, d,
+                         nullptr);
+    }
+    launch_layernorm_split(cc, x, B, d, m->lnfw, m->lnfb, hp);
+    gemm_decode_planes(cc, hp, 2 * d, static_cast<const bf16*>(m->tok), d, B, V, d, Epi::kStoreF32, logits, m->vpad,
+                       nullptr);
+    launch_sampler(cc, logits, m->vpad, B, V, sampler_state());
+    return;
+  }
   auto st = [&](int64_t i) { return stats + i * mb * kStatStride; };
   RowStats s0{st(0), stat_ovf};
   s0.zero = st(1);
@@ -303,13 +339,25 @@ void Engine::decode_unit_mixed(int64_t B, int64_t unit) {
     const LnIn l1{x, d, st(2 * l), ly.ln1w, ly.ln1b, int(d)};
     gemm_decode_mixed(cc, nullptr, d, static_cast<const bf16*>(ly.wqkv), d, B, 3 * d, d, Epi::kStoreF32, q3, 3 * d,
                       &l1, nullptr);
+    const RowStats so2{st(2 * l + 1), stat_ovf};
+    const LnIn l2{x, d, st(2 * l + 1), ly.ln2w, ly.ln2b, int(d)};
+    const RowStats so1{st(2 * l + 2), stat_ovf};
+    if (mixed_oplanes) {  // O / down operands as bf16 planes from the attention / GELU epilogues
+      bf16* ap = static_cast<bf16*>(att);
+      bf16* upp = static_cast<bf16*>(up);
+      launch_attention_decode<float>(cc, q3, B, pos, done, block_table, int(l), geom, static_cast<float*>(kv.ptr), at,
+                                     0.0, ap);
+      gemm_decode_planes(cc, ap, 2 * d, static_cast<const bf16*>(ly.wo), d, B, d, d, Epi::kAddResidual, x, d, &so2);
+      gemm_decode_mixed(cc, nullptr, d, static_cast<const bf16*>(ly.wup), d, B, f, d, Epi::kGeluSplit, upp, 2 * f, &l2,
+                        nullptr);
+      gemm_decode_planes(cc, upp, 2 * f, static_cast<const bf16*>(ly.wdown), f, B, d, f, Epi::kAddResidual, x, d,
+                         l + 1 < L ? &so1 : nullptr);
+      continue;
+    }
     launch_attention_decode<float>(cc, q3, B, pos, done, block_table, int(l), geom, static_cast<float*>(kv.ptr), at,
                                    0.0);
-    const RowStats so2{st(2 * l + 1), stat_ovf};
     gemm_decode_mixed(cc, at, d, static_cast<const bf16*>(ly.wo), d, B, d, d, Epi::kAddResidual, x, d, nullptr, &so2);
-    const LnIn l2{x, d, st(2 * l + 1), ly.ln2w, ly.ln2b, int(d)};
     gemm_decode_mixed(cc, nullptr, d, static_cast<const bf16*>(ly.wup), d, B, f, d, Epi::kGeluF32, uu, f, &l2, nullptr);
-    const RowStats so1{st(2 * l + 2), stat_ovf};
     gemm_decode_mixed(cc, uu, f, static_cast<const bf16*>(ly.wdown), f, B, d, f, Epi::kAddResidual, x, d, nullptr,
                       l + 1 < L ? &so1 : nullptr);
   }

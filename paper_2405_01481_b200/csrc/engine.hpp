@@ -28,6 +28,8 @@ struct Engine {
   unsigned long long* stats = nullptr;  // fused-LN fixed-point row statistics [2L+1][max_batch][2]
   unsigned* stat_ovf = nullptr;         // set by a producer whose partial left the fixed-point range
   bool fuse_ln = false;
+  bool mixed_planes = false;   // mixed decode through bf16 hi/lo activation planes (decode_unit_mixed)
+  bool mixed_oplanes = false;  // ... planes for the O / down operands only (LayerNorm stays fused)
   int64_t fuse_ln_max_b = 64;  // fused LayerNorm only for decode batches up to this size
   // persistent decode-step kernel (decode_mega.cu); PPOEXP_DECODE_MEGA=0 disables
   bool use_mega = false;

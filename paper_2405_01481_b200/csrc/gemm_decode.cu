@@ -86,12 +86,14 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
 // (fp32 x + row statistics normalised by the epilogue threads into bf16);
 // 2 = fp32 activation split by the epilogue threads into two bf16 terms
 // (hi = bf16(a), lo = bf16(a - hi)) issued as two MMAs into one accumulator
-// (mixed mode: bf16 weights, fp32-grade activations); 3 = LayerNorm fused + split.
+// (mixed mode: bf16 weights, fp32-grade activations); 3 = LayerNorm fused + split;
+// 4 = split terms that arrive as two bf16 planes [rows, 2K] (hi | lo, written
+// by the producer kernel), both TMA'd.
 template <int XM>
 struct XMode {
   static constexpr bool kLn = XM == 1 || XM == 3;
   static constexpr bool kSplit = XM >= 2;
-  static constexpr bool kProduced = XM != 0;  // the epilogue threads write the X tiles
+  static constexpr bool kProduced = XM == 1 || XM == 2 || XM == 3;  // the epilogue threads write the X tiles
 };
 
 template <int NB, bool SPLIT = false>
@@ -115,7 +117,8 @@ struct DecLayout {
 
 template <int NB, int EPI, int XM>
 __global__ void __launch_bounds__(kThreads, 1)
-    gemm_decode_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX, int Mrows,
+    gemm_decode_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
+                       const __grid_constant__ CUtensorMap tmX2, int Mrows,
                        int N, int K, void* __restrict__ Cv, int64_t ldc, int S, int wst, LnIn ln, RowStats so,
                        int push, uint64_t* dbg) {
   // debug timeline (PPOEXP_GEMM_TRACE): CTA (0, 0) stamps clock64 at each stage
@@ -216,6 +219,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (xu > 0) mbar_wait(&xempty[xs], (xu - 1) & 1);
           mbar_expect_tx(&xfull[xs], L::kX);
           tma_load_2d(&tmX, &xfull[xs], sX + xs * L::kX, kb * BK, 0);
+          if constexpr (SPLIT) tma_load_2d(&tmX2, &xfull[xs], sX + xs * L::kX + L::kXT, kb * BK, 0);
         }
     } else if (lane == 1) {
       // refill the weight ring for slices larger than the ring
@@ -422,6 +426,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             static_cast<float*>(Cv)[o] += a;
           } else if constexpr (EPI == int(Epi::kGeluF32)) {
             static_cast<float*>(Cv)[o] = gelu_tanh(a);
+          } else if constexpr (EPI == int(Epi::kGeluSplit)) {
+            const float gv = gelu_tanh(a);
+            const bf16 hi = __float2bfloat16_rn(gv);
+            static_cast<bf16*>(Cv)[o] = hi;
+            static_cast<bf16*>(Cv)[o + N] = __float2bfloat16_rn(gv - __bfloat162float(hi));
           } else {
             static_cast<float*>(Cv)[o] = a;
           }
@@ -603,6 +612,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           pq += double(nv) * double(nv);
         } else if constexpr (EPI == int(Epi::kGeluF32)) {
           static_cast<float*>(Cv)[o] = gelu_tanh(a);
+        } else if constexpr (EPI == int(Epi::kGeluSplit)) {
+          const float gv = gelu_tanh(a);
+          const bf16 hi = __float2bfloat16_rn(gv);
+          static_cast<bf16*>(Cv)[o] = hi;
+          static_cast<bf16*>(Cv)[o + N] = __float2bfloat16_rn(gv - __bfloat162float(hi));
         } else {
           static_cast<float*>(Cv)[o] = a;
         }
@@ -650,8 +664,10 @@ void launch_dec(Ctx& c, const bf16* X, int64_t ldx, const bf16* W, int64_t ldw, 
   constexpr bool LNIN = XMode<XM>::kLn;
   using L = DecLayout<NB, XMode<XM>::kSplit>;
   const CUtensorMap tw = make_map(W, N, K, ldw, BMW);
-  // produced-X modes never read X through TMA; any valid map will do
+  // produced-X modes never read X through TMA; any valid map will do.  Planes
+  // (XM 4): hi = X[:, 0:K), lo = X[:, K:2K) with row stride ldx (= 2K)
   const CUtensorMap tx = XMode<XM>::kProduced ? tw : make_map(X, M, K, ldx, NB);
+  const CUtensorMap tx2 = XM == 4 ? make_map(X + K, M, K, ldx, NB) : tx;
   auto k = gemm_decode_kernel<NB, EPI, XM>;
   const int smem_max = L::kSmemMax - (LNIN ? 2 * 512 * 4 : 0);  // LN mode: static gamma / beta staging
   static bool attr = false;
@@ -738,7 +754,8 @@ void launch_dec(Ctx& c, const bf16* X, int64_t ldx, const bf16* W, int64_t ldw, 
       c.gemm_trace_meta.push_back({int(N), int(K), EPI, S});
       dbg = buf + slot * 16;
     }
-    const cudaError_t e = cudaLaunchKernelEx(&cfg, k, tw, tx, int(M), int(N), int(K), C, ldc, S, wst, lnv, sov, push, dbg);
+    const cudaError_t e =
+        cudaLaunchKernelEx(&cfg, k, tw, tx, tx2, int(M), int(N), int(K), C, ldc, S, wst, lnv, sov, push, dbg);
     if (e != cudaSuccess) {
       (void)cudaGetLastError();
       throw Error(6, std::string("cuda: decode GEMM launch failed (") + cudaGetErrorString(e) + ") NB=" +
@@ -758,6 +775,7 @@ void dispatch(Ctx& c, const bf16* X, int64_t ldx, const bf16* W, int64_t ldw, in
       case Epi::kAddResidual: return launch_dec<NB, 2, XM>(c, X, ldx, W, ldw, M, N, K, C, ldc, ln, so);
       case Epi::kStoreF32: return launch_dec<NB, 3, XM>(c, X, ldx, W, ldw, M, N, K, C, ldc, ln, so);
       case Epi::kGeluF32: return launch_dec<NB, 5, XM>(c, X, ldx, W, ldw, M, N, K, C, ldc, ln, so);
+      case Epi::kGeluSplit: return launch_dec<NB, 6, XM>(c, X, ldx, W, ldw, M, N, K, C, ldc, ln, so);
       default: throw ContractError("decode GEMM: split activations need an fp32 epilogue");
     }
   } else {
@@ -816,6 +834,15 @@ void gemm_decode_fused(Ctx& c, const bf16* X, int64_t ldx, const bf16* W, int64_
     return dispatch_nb<1>(c, X, ldx, W, ldw, M, N, K, epi, C, ldc, ln, so);
   }
   return dispatch_nb<0>(c, X, ldx, W, ldw, M, N, K, epi, C, ldc, ln, so);
+}
+
+// Mixed mode, activation as two bf16 planes [M, 2K] (hi | lo) from the producer
+// kernel (split LayerNorm / attention / GELU epilogue): both TMA'd, two MMAs.
+void gemm_decode_planes(Ctx& c, const bf16* X, int64_t ldx, const bf16* W, int64_t ldw, int64_t M, int64_t N, int64_t K,
+                        Epi epi, void* C, int64_t ldc, const RowStats* so) {
+  if (M > 256 || M <= 0) throw ContractError("decode GEMM: batch above 256");
+  if (K % 8 || ldx % 8 || ldx < 2 * K) throw ContractError("decode GEMM (planes): K % 8 and a [M, 2K] operand required");
+  return dispatch_nb<4>(c, X, ldx, W, ldw, M, N, K, epi, C, ldc, nullptr, so);
 }
 
 // Mixed mode (bf16 weights, fp32 activations): the fp32 activation (or the

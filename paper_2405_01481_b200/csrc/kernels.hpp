@@ -37,7 +37,8 @@ void launch_layernorm(Ctx& c, const float* x, int64_t rows, int64_t d, const flo
                       const int32_t* gather, const float* head, float* head_out);
 
 // K3: C[M,N] = A[M,K] · B[N,K]^T with epilogue.
-enum class Epi : int { kStore = 0, kGelu = 1, kAddResidual = 2, kStoreF32 = 3, kLse = 4, kGeluF32 = 5 };
+// kGeluSplit: GELU output written as two bf16 planes (hi at [row, col], lo at [row, N + col]; ldc >= 2N)
+enum class Epi : int { kStore = 0, kGelu = 1, kAddResidual = 2, kStoreF32 = 3, kLse = 4, kGeluF32 = 5, kGeluSplit = 6 };
 // Epilogue outputs of the fused LM-head + log-sum-exp + gather GEMM (Epi::kLse).
 struct LseEpi {
   const int32_t* target = nullptr;  // [M] target column per row (< 0: none)
@@ -102,6 +103,10 @@ void gemm_decode_fused(Ctx& c, const bf16* X, int64_t ldx, const bf16* W, int64_
 // split into hi + lo bf16 terms in-kernel, two MMAs per k-step; fp32 epilogues.
 void gemm_decode_mixed(Ctx& c, const float* X, int64_t ldx, const bf16* W, int64_t ldw, int64_t M, int64_t N, int64_t K,
                        Epi epi, void* C, int64_t ldc, const LnIn* ln, const RowStats* so);
+void gemm_decode_planes(Ctx& c, const bf16* X, int64_t ldx, const bf16* W, int64_t ldw, int64_t M, int64_t N, int64_t K,
+                        Epi epi, void* C, int64_t ldc, const RowStats* so);
+// LayerNorm written as two bf16 planes y[r, 0:d) = hi, y[r, d:2d) = lo (mixed decode).
+void launch_layernorm_split(Ctx& c, const float* x, int64_t rows, int64_t d, const float* g, const float* b, bf16* y);
 // Mixed-mode GEMM for any M (decode-sized M goes to gemm_decode_mixed).
 void gemm_mixed(Ctx& c, const float* A, int64_t lda, const bf16* W, int64_t ldw, int64_t M, int64_t N, int64_t K,
                 Epi epi, void* C, int64_t ldc, const LseEpi* lse = nullptr);
@@ -133,10 +138,11 @@ void attention_prefill_split(Ctx& c, const float* qkv, const int64_t* seq_offset
 // K5b: one decode step: append this step's K/V (row b of qkv at position
 // pos[b]) to the paged pool, then attend over positions 0..pos[b].
 // Sequences with done[b] != 0 are skipped.
+// split_out (fp32 KV only, nullable): the output as two bf16 planes [B, 2d] instead of `out`.
 template <class T>
 void launch_attention_decode(Ctx& c, const T* qkv, int64_t B, const int32_t* pos, const int32_t* done,
                              const int32_t* block_table, int layer, const KvGeom& g, T* kv, T* out,
-                             double algorithmic_bytes);
+                             double algorithmic_bytes, bf16* split_out = nullptr);
 
 // K8: fused sampler over logits [B, ld] fp32 (src/model.cpp:450-477 + top-k/p).
 struct SampleParams {

@@ -412,6 +412,54 @@ __global__ void __launch_bounds__(256) layernorm_wide_kernel(const float* __rest
   }
 }
 
+// Mixed decode: LayerNorm of a row (fp32, two-pass statistics in fp64) written as
+// two bf16 planes, y[r, j] = hi, y[r, d + j] = lo (the consumer GEMM TMAs both).
+__global__ void layernorm_split_kernel(const float* __restrict__ x, int64_t d, const float* __restrict__ g,
+                                       const float* __restrict__ b, bf16* __restrict__ y) {
+  PDL_ENTRY();
+  __shared__ double red[32];
+  const int64_t r = blockIdx.x;
+  const int nw = (blockDim.x + 31) >> 5, w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int j = threadIdx.x * 4;
+  const bool act = j < d;
+  const float4 v = act ? *reinterpret_cast<const float4*>(x + r * d + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+  double s = warp_sum_d(double(v.x) + v.y + v.z + v.w);
+  if (lane == 0) red[w] = s;
+  __syncthreads();
+  double mu = 0.0;
+  for (int k = 0; k < nw; ++k) mu += red[k];
+  mu /= double(d);
+  __syncthreads();
+  const double c0 = v.x - mu, c1 = v.y - mu, c2 = v.z - mu, c3 = v.w - mu;
+  double q = warp_sum_d(act ? c0 * c0 + c1 * c1 + c2 * c2 + c3 * c3 : 0.0);
+  if (lane == 0) red[w] = q;
+  __syncthreads();
+  double var = 0.0;
+  for (int k = 0; k < nw; ++k) var += red[k];
+  const double is = 1.0 / sqrt(var / double(d) + 1e-5);
+  if (!act) return;
+  const float4 gg = *reinterpret_cast<const float4*>(g + j), bb = *reinterpret_cast<const float4*>(b + j);
+  const float o[4] = {float(gg.x * (c0 * is) + bb.x), float(gg.y * (c1 * is) + bb.y), float(gg.z * (c2 * is) + bb.z),
+                      float(gg.w * (c3 * is) + bb.w)};
+  bf16 hi[4], lo[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    hi[e] = __float2bfloat16_rn(o[e]);
+    lo[e] = __float2bfloat16_rn(o[e] - __bfloat162float(hi[e]));
+  }
+  *reinterpret_cast<uint2*>(y + r * 2 * d + j) = *reinterpret_cast<const uint2*>(hi);
+  *reinterpret_cast<uint2*>(y + r * 2 * d + d + j) = *reinterpret_cast<const uint2*>(lo);
+}
+
+void launch_layernorm_split(Ctx& c, const float* x, int64_t rows, int64_t d, const float* g, const float* b, bf16* y) {
+  if (rows <= 0) return;
+  if (d % 4 || d > 4096) throw ContractError("layernorm (split planes): d % 4 == 0 and d <= 4096 required");
+  const int th = int((d / 4 + 31) / 32 * 32);
+  c.launch("layernorm", double(rows) * d * 8, 0, [&] {
+    launch_kernel(c, layernorm_split_kernel, dim3(rows), dim3(th), 0, 1, x, d, g, b, y);
+  });
+}
+
 // CTA-per-row float4 variant for few rows (decode): one float4 per thread,
 // two barrier-reductions — short dependency chains on many SMs.
 template <class T>

@@ -662,3 +662,14 @@ def test_dpo_sums_c5_width(px, ctx, oracle, dtype):
     got = px.response_logprob_sums(m, seqs, rs)
     lps = oracle.sequence_logprobs(cfg, w, seqs)
     close(got, [float(sum(lp[r:])) for lp, r in zip(lps, rs)])
+
+
+@pytest.mark.parametrize("planes", ["0", "1"])
+def test_mixed_decode_activation_paths(px, ctx, oracle, monkeypatch, planes):
+    """Mixed decode with the LayerNorm fused into the consumer GEMMs (planes=0,
+    the narrow-model default) and with split LayerNorm / attention / GELU
+    producers writing bf16 hi|lo planes that the GEMMs TMA (planes=1, the
+    wide-model default): both meet the bar at the C2 width."""
+    monkeypatch.setenv("PPOEXP_MIXED_PLANES", planes)
+    cfg = ModelCfg(V=50257, d=768, L=2, H=12, f=3072, S=512)
+    _mixed_experience_check(px, ctx, oracle, cfg, synthetic_prompts(3, 4, 12, ragged_lengths=True), 16)
