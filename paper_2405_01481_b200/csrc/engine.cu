@@ -65,11 +65,7 @@ Engine::Engine(Model* model, const ppoexp_engine_options* o) : m(model), c(model
   const size_t o_last = sbytes; sbytes += al(mb * 4);
   // fused-LN row statistics: one accumulator pair per row for each LayerNorm of a step
   const size_t o_sta = sbytes; sbytes += al((2 * cfg.n_layers + 1) * mb * kStatStride * 8);
-  const size_t o_part = sbytes; sbytes += al(decode_mega_part_bytes());
-  const size_t o_bar = sbytes; sbytes += al(16);  // 2 x u64 grid-barrier counter / base
   const size_t o_ovf = sbytes; sbytes += al(16);
-  const size_t o_mly = sbytes; sbytes += al(cfg.n_layers * sizeof(MegaLayer));
-  const size_t o_wmap = sbytes; sbytes += al(cfg.n_layers * 4 * sizeof(CUtensorMap));
   state.ensure(sbytes);
   PPOEXP_CUDA(cudaMemset(state.ptr, 0, sbytes));
   char* p = static_cast<char*>(state.ptr);
@@ -92,41 +88,14 @@ Engine::Engine(Model* model, const ppoexp_engine_options* o) : m(model), c(model
   uniforms = reinterpret_cast<double*>(p + o_uni);
   last_rows = reinterpret_cast<int32_t*>(p + o_last);
   stats = reinterpret_cast<unsigned long long*>(p + o_sta);
-  part = reinterpret_cast<float*>(p + o_part);
-  bar = reinterpret_cast<unsigned*>(p + o_bar);
   stat_ovf = reinterpret_cast<unsigned*>(p + o_ovf);
-  mega_layers = reinterpret_cast<MegaLayer*>(p + o_mly);
-  mega_wmaps = reinterpret_cast<CUtensorMap*>(p + o_wmap);
-  {
-    trace_path = getenv("PPOEXP_MEGA_TRACE");
-    // opt-in (PPOEXP_DECODE_MEGA=1): measured at parity with / slightly behind
-    // the per-op graph at the C2 shape on B200
-    const char* ev = getenv("PPOEXP_DECODE_MEGA");
-    use_mega = m->dtype == PPOEXP_BF16 && ev && ev[0] == '1';
-    if (use_mega) {
-      std::vector<MegaLayer> ml(cfg.n_layers);
-      for (int64_t l = 0; l < cfg.n_layers; ++l) {
-        const Layer& ly = m->layers[l];
-        ml[l] = {static_cast<const bf16*>(ly.wqkv), static_cast<const bf16*>(ly.wo), static_cast<const bf16*>(ly.wup),
-                 static_cast<const bf16*>(ly.wdown), ly.ln1w, ly.ln1b, ly.ln2w, ly.ln2b};
-      }
-      PPOEXP_CUDA(cudaMemcpy(mega_layers, ml.data(), ml.size() * sizeof(MegaLayer), cudaMemcpyHostToDevice));
-      if (d % 128 == 0 && f % 128 == 0) {
-        std::vector<CUtensorMap> wm(cfg.n_layers * 4);
-        decode_mega_weight_maps(ml.data(), int(cfg.n_layers), int(d), int(f), wm.data());
-        PPOEXP_CUDA(cudaMemcpy(mega_wmaps, wm.data(), wm.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
-      } else {
-        use_mega = false;
-      }
-    }
-  }
   {
     // default for bf16 decode batches <= 64 (PPOEXP_FUSE_LN=0 disables, =1
     // forces it up to 256): removes 24 of the 25 LN launches of a decode step,
     // -6% step time at C2 on B200; at batch 256 every weight tile would
     // re-normalise 4x more rows and it measured 18% slower
     const char* ev = getenv("PPOEXP_FUSE_LN");
-    fuse_ln = m->dtype == PPOEXP_BF16 && !(ev && ev[0] == '0') && !use_mega && mb <= 256 && d % 8 == 0;
+    fuse_ln = m->dtype == PPOEXP_BF16 && !(ev && ev[0] == '0') && mb <= 256 && d % 8 == 0;
     if (m->mixed() && d % 8) throw ContractError("engine: mixed mode needs d_model % 8 == 0");
     // mixed decode: split-plane activations TMA'd by the GEMMs (standalone split
     // LayerNorm, attention / GELU epilogues writing hi|lo planes) — measured
@@ -195,44 +164,6 @@ void Engine::decode_unit(int64_t B, int64_t unit) {
   T* uu = static_cast<T*>(up);
   cur_unit = unit;
   if constexpr (std::is_same_v<T, bf16>) {
-    if (use_mega) {
-      MegaArgs a{};
-      a.B = int(B);
-      a.d = int(d);
-      a.f = int(f);
-      a.L = int(m->cfg.n_layers);
-      a.next_tok = next_tok;
-      a.pos = pos;
-      a.done = done;
-      a.block_table = block_table;
-      a.g = geom;
-      a.kv = static_cast<bf16*>(kv.ptr);
-      a.tok = static_cast<const bf16*>(m->tok);
-      a.posemb = static_cast<const bf16*>(m->pos);
-      a.layers = mega_layers;
-      a.wmaps = mega_wmaps;
-      a.lnfw = m->lnfw;
-      a.lnfb = m->lnfb;
-      a.x = x;
-      a.h = hh;
-      a.att = at;
-      a.up = uu;
-      a.part = part;
-      a.bar = bar;
-      if (const char* e = getenv("PPOEXP_MEGA_PREFETCH")) a.prefetch = atoi(e);
-      if (decode_mega_plan(a)) {
-        decode_mega_act_maps(a, opts.max_batch);
-        if (trace_path) {
-          trace_buf.ensure(size_t(8 * a.L) * a.grid * 2 * 8 + size_t(a.L) * a.grid * 8 * 4 * 8);
-          a.trace = static_cast<uint64_t*>(trace_buf.ptr);
-        }
-        const double wbytes = double(m->cfg.n_layers) * (4.0 * d * d + 2.0 * d * f) * 2.0;
-        launch_decode_mega(cc, a, wbytes);
-        gemm<T>(cc, hh, d, static_cast<const T*>(m->tok), d, B, V, d, Epi::kStoreF32, logits, m->vpad);
-        launch_sampler(cc, logits, m->vpad, B, V, sampler_state());
-        return;
-      }
-    }
     if (fuse_ln && B <= fuse_ln_max_b) {
       // bf16 path with LayerNorm fused into the consumer GEMMs: embed / O-proj /
       // down-proj accumulate fixed-point row statistics of x (one buffer per
@@ -521,14 +452,6 @@ void Engine::generate(int64_t B, const int32_t* prompts, const int64_t* offsets,
       for (int k = 1; k < 8; ++k)
         fprintf(fp, "%-14s %8.2f us\n", nm[k], h[k] > h[k - 1] ? (h[k] - h[k - 1]) / 1965.0 : 0.0);
       fprintf(fp, "total %.2f us, crossing-bucket members %llu\n", (h[7] - h[0]) / 1965.0, h[8]);
-      fclose(fp);
-    }
-  }
-  if (trace_path && trace_buf.ptr) {  // debug: raw stamps of the last decode step
-    std::vector<uint64_t> h(trace_buf.bytes / 8);
-    PPOEXP_CUDA(cudaMemcpy(h.data(), trace_buf.ptr, trace_buf.bytes, cudaMemcpyDeviceToHost));
-    if (FILE* fp = fopen(trace_path, "wb")) {
-      fwrite(h.data(), 8, h.size(), fp);
       fclose(fp);
     }
   }

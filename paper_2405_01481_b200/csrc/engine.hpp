@@ -31,14 +31,6 @@ struct Engine {
   bool mixed_planes = false;   // mixed decode through bf16 hi/lo activation planes (decode_unit_mixed)
   bool mixed_oplanes = false;  // ... planes for the O / down operands only (LayerNorm stays fused)
   int64_t fuse_ln_max_b = 64;  // fused LayerNorm only for decode batches up to this size
-  // persistent decode-step kernel (decode_mega.cu); PPOEXP_DECODE_MEGA=0 disables
-  bool use_mega = false;
-  float* part = nullptr;
-  unsigned* bar = nullptr;
-  MegaLayer* mega_layers = nullptr;
-  CUtensorMap* mega_wmaps = nullptr;
-  const char* trace_path = nullptr;  // PPOEXP_MEGA_TRACE: dump per-barrier stamps of the last step
-  DeviceBuffer trace_buf;
   cudaEvent_t poll_ev[2]{}, t0{}, t1{};
   double last_ms = 0;
   double gen_seconds = 0;    // CostBook "response_generation" (src/engine.cpp:179)

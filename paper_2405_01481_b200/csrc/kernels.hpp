@@ -184,37 +184,6 @@ void launch_reduce_partials(Ctx& c, int64_t B, const double* part, double* out5)
 void launch_whiten_apply(Ctx& c, int64_t B, int64_t stride, const int64_t* lengths, const double* adv,
                          const double* stats3, double* out);
 
-// Persistent cooperative decode step (bf16, batch <= 64, head_dim 32/64,
-// d_model and d_ff multiples of 128): embedding + all layers + final LN into h,
-// see decode_mega.cu.
-struct MegaLayer {
-  const bf16 *wqkv, *wo, *wup, *wdown;
-  const float *ln1w, *ln1b, *ln2w, *ln2b;
-};
-struct MegaArgs {
-  CUtensorMap tm_h, tm_att, tm_up;  // activation operands, box 64 rows x 64
-  int B, d, f, L;
-  int grid, split[4];               // filled by decode_mega_plan: K splits of qkv / o / up / down
-  const int32_t *next_tok, *pos, *done, *block_table;
-  KvGeom g;
-  bf16* kv;
-  const bf16 *tok, *posemb;
-  const MegaLayer* layers;   // device [L]
-  const CUtensorMap* wmaps;  // device [L][4] weight maps (qkv, o, up, down), box 128 rows x 64
-  const float *lnfw, *lnfb;
-  float* x;
-  bf16 *h, *att, *up;
-  float* part;    // split-K partials, decode_mega_part_bytes()
-  unsigned* bar;  // [2] grid barrier (zero-initialised)
-  int prefetch = 1;           // L2-prefetch layer l+1's weights during layer l
-  uint64_t* trace = nullptr;  // debug: [8L][grid][2] globaltimer stamps
-};
-size_t decode_mega_part_bytes();
-// Fills the launch plan; false when the shape is not supported.
-bool decode_mega_plan(MegaArgs& a);
-void decode_mega_act_maps(MegaArgs& a, int64_t rows);
-void decode_mega_weight_maps(const MegaLayer* layers_host, int L, int d, int f, CUtensorMap* out);
-void launch_decode_mega(Ctx& c, const MegaArgs& a, double bytes);
 
 // misc
 // IndexError (the reference's wording, src/model.cpp:284-287) for any id outside

@@ -23,7 +23,7 @@ from typing import Sequence
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.environ.get("PPOEXP_LIB") or os.path.join(_PKG, "libppoexp.so")  # override: A/B runs only
+LIB_PATH = os.path.join(_PKG, "libppoexp.so")
 
 HOST, DEVICE = 0, 1
 F32, BF16, F64, MIXED = 0, 1, 2, 3  # MIXED: bf16 weights, fp32-grade activations (include/ppoexp.h)

@@ -400,32 +400,6 @@ def test_bf16_fused_layernorm_matches_unfused(px, ctx, oracle, monkeypatch):
     assert same >= len(prompts) // 2
 
 
-@pytest.mark.parametrize("heads", [4, 8])  # head_dim 64 and 32
-def test_bf16_persistent_decode_matches_per_op(px, ctx, oracle, monkeypatch, heads):
-    """The persistent cooperative decode kernel (decode_mega.cu: grid barriers,
-    tcgen05 split-K GEMM phases, partial reductions in the consumers) against
-    the per-op graph path, and teacher-forced against the oracle."""
-    cfg = ModelCfg(V=4096, d=256, L=3, H=heads, f=1024, S=128)
-    wb = bf16_round(oracle.init_params(cfg, 23))
-    prompts = synthetic_prompts(40, 24, 12, ragged_lengths=True)
-    outs = {}
-    for flag in ("0", "1"):
-        monkeypatch.setenv("PPOEXP_DECODE_MEGA", flag)
-        eng = engine(px, ctx, cfg, wb, px.BF16)
-        outs[flag] = eng.generate_batch([px.GenTask(p, 48) for p in prompts])
-    same = 0
-    for a, b, p in zip(outs["0"], outs["1"], prompts):
-        n = 0
-        while n < min(len(a.tokens), len(b.tokens)) and a.tokens[n] == b.tokens[n]:
-            n += 1
-        same += n == len(a.tokens)
-        close(b.logprobs[:n], a.logprobs[:n], atol=2e-2, rtol=2e-3)
-        full = np.concatenate([p, b.tokens])
-        lp = oracle.sequence_logprobs(cfg, wb, [full])[0][len(p):]
-        close(b.logprobs, lp, atol=3e-2, rtol=3e-3)
-    assert same >= len(prompts) // 2
-
-
 def test_bf16_decode_batch_above_fused_ln_limit(px, ctx, oracle):
     """Decode batches above 64 take the standalone-LayerNorm path (the fused
     LayerNorm is the default only up to 64 rows): teacher-forced against the

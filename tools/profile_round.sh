@@ -9,7 +9,7 @@ DEC="python tools/profile_decode.py --new 88"
 $DEC > gpurun_out/prof/decode_plain.log 2>&1 || exit 1
 # in-graph timeline of the decode step (CUPTI via torch.profiler): critical-path share per kernel
 python tools/timeline.py --new 88 > gpurun_out/prof/timeline_decode.txt 2>&1
-PPOEXP_DECODE_MEGA=1 python tools/timeline.py --new 88 --mega > gpurun_out/prof/timeline_decode_mega.txt 2>&1
+
 # per-stage trace of the decode GEMMs (clock64 inside CTA (0,0))
 PPOEXP_GEMM_TRACE=gpurun_out/prof/gemm_trace.bin python tools/profile_decode.py --new 24 > /dev/null 2>&1
 python tools/gemm_trace.py gpurun_out/prof/gemm_trace.bin > gpurun_out/prof/gemm_trace.txt 2>&1
@@ -29,5 +29,4 @@ ncu --set full --import-source on --clock-control none -k regex:attn_decode -s 1
 ncu --set full --import-source on --clock-control none -k regex:logprob_gather -s 2 -c 1 -o gpurun_out/prof/full_logprob $CMD > gpurun_out/prof/ncu5.log 2>&1
 ncu --set full --import-source on --clock-control none -k regex:gemm_tc_kernel -s 100 -c 1 -o gpurun_out/prof/full_gemm_tc $CMD > gpurun_out/prof/ncu6.log 2>&1
 ncu --set full --import-source on --clock-control none -k regex:sampler -s 30 -c 1 -o gpurun_out/prof/full_sampler $DEC > gpurun_out/prof/ncu7.log 2>&1
-PPOEXP_DECODE_MEGA=1 ncu --set full --import-source on --clock-control none -k regex:decode_mega -s 30 -c 1 -o gpurun_out/prof/full_decode_mega $DEC > gpurun_out/prof/ncu8.log 2>&1
 ls -la gpurun_out/prof

@@ -5,7 +5,7 @@ and prints, for a window of consecutive decode steps in steady state, each
 kernel's duration and the gap since the previous kernel ended (negative =
 overlap through programmatic dependent launch), aggregated per kernel class.
 
-    python tools/timeline.py [--new 88] [--mega]
+    python tools/timeline.py [--new 88]
 """
 import argparse
 import collections
@@ -22,13 +22,10 @@ from paper_2405_01481_b200 import ppoexp as px  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--new", type=int, default=88)
-ap.add_argument("--mega", action="store_true")
 ap.add_argument("--steps", type=int, default=8, help="decode steps to aggregate (from the middle)")
 ap.add_argument("--config", default="c2")
 ap.add_argument("--batch", type=int, default=0)
 a = ap.parse_args()
-if a.mega:
-    os.environ["PPOEXP_DECODE_MEGA"] = "1"
 V, d, L, H, f, S, B, P, N, samp, _ = bench.CONFIGS[a.config]
 B = a.batch or B
 cfg = px.ModelConfig(V, d, L, H, f, S)
