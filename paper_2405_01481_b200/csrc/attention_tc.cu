@@ -231,23 +231,36 @@ __global__ void __launch_bounds__(kThr, 1)
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       bar_arrive(&s_free[bf]);
-      const int64_t k0 = int64_t(j) * BKV;
+      const int k0 = j * BKV;
       float sv[64];
       float mx = -FLT_MAX;
+      // masks only on tiles that reach the diagonal or the end of the sequence
+      // (block-uniform test): the others are raw scaled scores
+      if (k0 + BKV - 1 <= int(q0) && k0 + BKV <= int(len)) {
 #pragma unroll
-      for (int c = 0; c < 64; ++c) {
-        const int64_t key = k0 + c;
-        float v = __uint_as_float(c < 32 ? sa[c] : sb[c - 32]) * scale;
-        if (key > qi || key >= len) v = -FLT_MAX;
-        sv[c] = v;
-        mx = fmaxf(mx, v);
+        for (int c = 0; c < 64; ++c) {
+          sv[c] = __uint_as_float(c < 32 ? sa[c] : sb[c - 32]) * scale;
+          mx = fmaxf(mx, sv[c]);
+        }
+      } else {
+        const int lim = min(int(qi), int(len) - 1) - k0;  // keys k0 + c with c <= lim are visible
+#pragma unroll
+        for (int c = 0; c < 64; ++c) {
+          const float v = c <= lim ? __uint_as_float(c < 32 ? sa[c] : sb[c - 32]) * scale : -FLT_MAX;
+          sv[c] = v;
+          mx = fmaxf(mx, v);
+        }
       }
-      const float mn = fmaxf(m, mx);
+      // lazy rescale (log2 domain): keep the running max unless some row of the
+      // warp grew by more than 2^8 — p <= 256 stays exact in fp32 / bf16 and the
+      // final O / l uses the same max, so the result is unchanged
+      const bool grow = __any_sync(0xffffffffu, m == -FLT_MAX || mx > m + 8.f);
+      const float mn = grow ? fmaxf(m, mx) : m;
       const float corr = m == -FLT_MAX ? 0.f : exp2f(m - mn);
       float rs = 0.f;
 #pragma unroll
-      for (int c = 0; c < 64; ++c) {
-        const float p = sv[c] == -FLT_MAX ? 0.f : exp2f(sv[c] - mn);
+      for (int c = 0; c < 64; ++c) {  // masked scores (-FLT_MAX) underflow to exactly 0
+        const float p = exp2f(sv[c] - mn);
         sv[c] = p;
         rs += p;
       }
@@ -256,7 +269,7 @@ __global__ void __launch_bounds__(kThr, 1)
         // O holds P_{j-1} V_{j-1}: wait for it, then rescale rows whose max moved
         bar_wait(o_done, (j - 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        if (__any_sync(0xffffffffu, mn > m)) {
+        if (grow) {
 #pragma unroll 1
           for (int c = 0; c < DH; c += 32) {
             uint32_t o[32];
@@ -274,10 +287,13 @@ __global__ void __launch_bounds__(kThr, 1)
       uint8_t* prow = sP(bf) + r * 128;
 #pragma unroll
       for (int c8 = 0; c8 < 8; ++c8) {
-        Vec16<bf16> pv;
+        uint32_t w4[4];
 #pragma unroll
-        for (int e = 0; e < 8; ++e) pv.v[e] = __float2bfloat16_rn(sv[c8 * 8 + e]);
-        *reinterpret_cast<uint4*>(prow + ((c8 ^ (r & 7)) << 4)) = pv.u;
+        for (int e = 0; e < 4; ++e) {
+          const __nv_bfloat162 p2 = __floats2bfloat162_rn(sv[c8 * 8 + 2 * e], sv[c8 * 8 + 2 * e + 1]);
+          w4[e] = *reinterpret_cast<const uint32_t*>(&p2);
+        }
+        *reinterpret_cast<uint4*>(prow + ((c8 ^ (r & 7)) << 4)) = make_uint4(w4[0], w4[1], w4[2], w4[3]);
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
