@@ -354,15 +354,13 @@ void launch_fa(Ctx& c, const bf16* qkv, const int64_t* seq_offsets, int64_t B, i
 // (head_dim 64 / 128, 16-byte aligned qkv rows).
 bool attention_prefill_tc(Ctx& c, const bf16* qkv, const int64_t* seq_offsets, int64_t B, int64_t max_len, int64_t H,
                           int64_t DH, int64_t M_total, bf16* out, bool force) {
-  // PPOEXP_ATTN_TC: 0 = never, 1 = always, default = sequences longer than 512
-  // (C2's 320-token rows: the 64-query mma.sync kernel measured 99 vs 119 us per
-  // launch — short key loops leave the tcgen05 pipeline mostly in its prologue;
-  // C5's 4096-token rows: 49.5 -> 36.0 ms per pair)
+  // PPOEXP_ATTN_TC=0 falls back to the mma.sync kernel (measured slower: C2 scoring
+  // 3.94 vs 3.17 ms per step, C5 shape 1.44 vs 0.50 ms per launch)
   static const int mode = [] {
     const char* e = getenv("PPOEXP_ATTN_TC");
-    return e ? atoi(e) : -1;
+    return e ? atoi(e) : 1;
   }();
-  if (!force && (mode == 0 || (mode < 0 && max_len <= 512))) return false;
+  if (!force && mode == 0) return false;
   if (M_total <= 0 || (reinterpret_cast<uintptr_t>(qkv) & 15)) return false;
   switch (DH) {
     case 64: return launch_fa<64>(c, qkv, seq_offsets, B, max_len, H, M_total, out), true;
