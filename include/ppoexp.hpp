@@ -294,6 +294,22 @@ inline std::vector<std::vector<std::size_t>> balance(const std::vector<GenTask>&
   return out;
 }
 
+// spin_make_pairs (src/losses.cpp:277-295): chosen = dataset response, rejected =
+// the frozen reference's greedy generation (one batched device generate);
+// degenerate pairs are dropped and counted.
+struct SftExample {
+  TokenSeq prompt, response;
+};
+struct PreferenceExample {
+  TokenSeq prompt, chosen, rejected;
+};
+struct SpinPairs {
+  std::vector<PreferenceExample> pairs;
+  std::size_t dropped = 0;
+};
+class Engine;
+SpinPairs spin_make_pairs(const std::vector<SftExample>& examples, Engine& reference, std::size_t max_new);
+
 // One NCCL communicator per rank (the experience step's single collective).
 class Communicator {
  public:
@@ -479,5 +495,26 @@ class ExperienceMaker {
   PpoHyper hyper_;
   Communicator* comm_ = nullptr;
 };
+
+inline SpinPairs spin_make_pairs(const std::vector<SftExample>& examples, Engine& reference, std::size_t max_new) {
+  std::vector<GenTask> tasks;
+  for (const auto& ex : examples) {
+    GenTask t;
+    t.prompt = ex.prompt;
+    t.max_new = max_new;
+    tasks.push_back(t);  // greedy (SamplingSpec default)
+  }
+  const auto gens = reference.generate_batch(tasks);
+  SpinPairs out;
+  for (std::size_t i = 0; i < examples.size(); ++i) {
+    const TokenSeq& rej = gens[i].tokens;
+    if (rej.empty() || rej == examples[i].response) {
+      ++out.dropped;
+      continue;
+    }
+    out.pairs.push_back({examples[i].prompt, examples[i].response, rej});
+  }
+  return out;
+}
 
 }  // namespace ppoexp

@@ -657,6 +657,36 @@ class Trainer:
             pass
 
 
+@dataclass
+class SpinPairs:
+    """SpinPairs (include/aligner/losses.hpp:140-143)."""
+    pairs: list  # (prompt, chosen, rejected) token arrays
+    dropped: int = 0
+
+
+def spin_make_pairs(reference_engine: "Engine", examples, max_new: int, strip_eot: bool = False) -> SpinPairs:
+    """spin_make_pairs (src/losses.cpp:277-295): chosen = the dataset response,
+    rejected = the frozen reference's greedy generation for the prompt — all
+    prompts in one batched device generate; degenerate pairs (rejected empty or
+    equal to the response) are dropped and counted.  strip_eot drops a trailing
+    EOT from the generation first, as the SPIN trainer does before rebuilding
+    the sequence (src/trainers.cpp:104-111)."""
+    examples = list(examples)
+    res = reference_engine.generate_batch([GenTask(np.asarray(p, np.int32), max_new, SamplingSpec.greedy_spec())
+                                           for p, _ in examples])
+    out = SpinPairs([], 0)
+    for (prompt, response), r in zip(examples, res):
+        rej = np.asarray(r.tokens, np.int32)
+        if strip_eot and len(rej) and rej[-1] == EOT_TOKEN:
+            rej = rej[:-1]
+        resp = np.asarray(response, np.int32)
+        if len(rej) == 0 or (len(rej) == len(resp) and np.array_equal(rej, resp)):
+            out.dropped += 1
+            continue
+        out.pairs.append((np.asarray(prompt, np.int32), resp, rej))
+    return out
+
+
 def build_engine(ctx: Context, params, config: ModelConfig, opts: EngineOptions | None = None, dtype=BF16):
     """build_engine, include/aligner/engine.hpp:91-92."""
     return Engine(DeviceModel(ctx, config, params, dtype), opts)

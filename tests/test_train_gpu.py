@@ -132,3 +132,21 @@ def test_trainer_refit_updates_the_engine(px, ctx, oracle, ref):
     task = [px.GenTask(list(seqs[0][:rs[0]]), 8)]
     a, b = eng.generate_batch(task)[0], fresh.generate_batch(task)[0]
     assert np.array_equal(a.tokens, b.tokens) and np.array_equal(a.logprobs, b.logprobs)
+
+
+def test_spin_make_pairs_matches_reference_generation(px, ctx, oracle, ref):
+    """spin_make_pairs (src/losses.cpp:277-295) on the device engine: the
+    rejected side is the reference model's greedy generation (equal to the
+    oracle's), degenerate pairs (rejected == response) are dropped and counted."""
+    w = f32(ref.init_params(CFG, 12))
+    eng = px.Engine(px.DeviceModel(ctx, to_px_cfg(CFG), w, px.F32))
+    prompts = synthetic_prompts(13, 5, 7, ragged_lengths=True)
+    t_o, _ = oracle.generate(CFG, w, prompts, 6)
+    rng = np.random.default_rng(2)
+    examples = [(p, rng.integers(0, 256, 6)) for p in prompts]
+    examples[2] = (prompts[2], t_o[2])  # the reference would generate exactly the response: dropped
+    sp = px.spin_make_pairs(eng, examples, 6)
+    assert sp.dropped == 1 and len(sp.pairs) == 4
+    kept = [i for i in range(5) if i != 2]
+    for (p, c, r), i in zip(sp.pairs, kept):
+        assert np.array_equal(r, t_o[i]) and np.array_equal(c, examples[i][1])
