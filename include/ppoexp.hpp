@@ -152,7 +152,7 @@ inline std::pair<std::vector<int32_t>, std::vector<int64_t>> ragged(const std::v
 // A device-resident weight snapshot (Engine's deep copy, src/engine.cpp:33-48).
 class DeviceModel {
  public:
-  DeviceModel(Context& ctx, const ModelParams& params, const ModelConfig& config, int dtype = PPOEXP_BF16)
+  DeviceModel(Context& ctx, const ModelParams& params, const ModelConfig& config, int dtype = PPOEXP_MIXED)
       : config_(config) {
     const auto v = detail::views(params);
     const auto c = config.c();
@@ -212,7 +212,7 @@ struct EngineOptions {
 class Engine {
  public:
   Engine(Context& ctx, const ModelParams& params, const ModelConfig& config, EngineOptions opts = {},
-         int dtype = PPOEXP_BF16)
+         int dtype = PPOEXP_MIXED)
       : model_(std::make_unique<DeviceModel>(ctx, params, config, dtype)) {
     ppoexp_engine_options o{int64_t(opts.max_batch), int64_t(opts.page_size), int64_t(opts.max_total_tokens),
                             opts.use_graphs ? 1 : 0, 0};

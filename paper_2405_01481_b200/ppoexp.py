@@ -329,7 +329,7 @@ class Context:
 class DeviceModel:
     """A device-resident ModelParams snapshot (build = deep copy, src/engine.cpp:33-48)."""
 
-    def __init__(self, ctx: Context, config: ModelConfig, params, dtype: int = BF16):
+    def __init__(self, ctx: Context, config: ModelConfig, params, dtype: int = MIXED):
         if isinstance(params, np.ndarray):
             try:
                 params = flat_to_params(config, params)
@@ -687,7 +687,7 @@ def spin_make_pairs(reference_engine: "Engine", examples, max_new: int, strip_eo
     return out
 
 
-def build_engine(ctx: Context, params, config: ModelConfig, opts: EngineOptions | None = None, dtype=BF16):
+def build_engine(ctx: Context, params, config: ModelConfig, opts: EngineOptions | None = None, dtype=MIXED):
     """build_engine, include/aligner/engine.hpp:91-92."""
     return Engine(DeviceModel(ctx, config, params, dtype), opts)
 
