@@ -302,6 +302,10 @@ class RefLib:
                                       C.POINTER(D)]
         L.ref_dpo_step.argtypes = [C.POINTER(I64), C.POINTER(D), C.POINTER(D), I64, C.POINTER(I32), C.POINTER(I64),
                                    C.POINTER(I64), I32, D, D, D, C.POINTER(D), I64, C.POINTER(D)]
+        L.ref_ppo_loop.argtypes = [C.POINTER(I64), C.POINTER(D), C.POINTER(D), C.POINTER(D), I32, C.POINTER(I32),
+                                   C.POINTER(I64), I64, I64, C.c_uint64, D, D, D, D, D, D, C.POINTER(D), I64,
+                                   C.POINTER(I32), C.POINTER(I64), C.POINTER(D), C.POINTER(D), C.POINTER(D),
+                                   C.POINTER(D)]
         L.ref_experience.argtypes = [C.POINTER(I64), C.POINTER(D), C.POINTER(D), C.POINTER(D), C.POINTER(D), I32,
                                      C.POINTER(I32), C.POINTER(I64), I64, I64, I64, I32, D, C.c_uint64, I64, D, D,
                                      D, I64, C.POINTER(I32), C.POINTER(I64), C.POINTER(D), C.POINTER(D),
@@ -418,6 +422,29 @@ class RefLib:
         self._chk(self.lib.ref_dpo_step(cfg.as6(), _p(w, D), _p(wr, D), len(pairs), _p(flat, I32), _p(offs, I64),
                                         _p(rs, I64), variant, beta, cdpo_eps, lr, _p(a4, D), n_steps, _p(losses, D)))
         return w, losses
+
+    def ppo_loop(self, cfg, w_policy, w_ref, w_critic, prompts, *, max_new, n_iters, kl_coef, lr, clip_eps=0.2,
+                 value_clip=0.2, gamma=1.0, lam=0.95, scripted_target=122, adam=(0.9, 0.999, 1e-8, 0.0)):
+        """n_iters greedy PPO iterations on the reference (experience, actor and
+        critic updates with persistent AdamW, engine refit)."""
+        flat, offs = ragged(prompts)
+        B = len(prompts)
+        wp, wc = np.array(w_policy, np.float64), np.array(w_critic, np.float64)
+        wr = np.ascontiguousarray(w_ref, np.float64)
+        shp = (n_iters, B, max_new)
+        toks = np.zeros(shp, np.int32)
+        n = np.zeros((n_iters, B), np.int64)
+        a, v, adv = (np.zeros(shp, np.float64) for _ in range(3))
+        losses = np.zeros((n_iters, 2), np.float64)
+        a4 = np.asarray(adam, np.float64)
+        self._chk(self.lib.ref_ppo_loop(cfg.as6(), _p(wp, D), _p(wr, D), _p(wc, D), scripted_target, _p(flat, I32),
+                                        _p(offs, I64), B, max_new, 0, kl_coef, gamma, lam, clip_eps, value_clip, lr,
+                                        _p(a4, D), n_iters, _p(toks, I32), _p(n, I64), _p(a, D), _p(v, D), _p(adv, D),
+                                        _p(losses, D)))
+        cut = lambda m, it: [m[it, b, :n[it, b]].copy() for b in range(B)]
+        iters = [dict(tokens=cut(toks, it), actor_logprobs=cut(a, it), values=cut(v, it), advantages=cut(adv, it),
+                      actor_loss=losses[it, 0], critic_loss=losses[it, 1]) for it in range(n_iters)]
+        return iters, wp, wc
 
     def experience(self, cfg, w_policy, w_ref, w_critic, prompts, *, max_new, greedy, temperature=1.0, seed=0,
                    step_index=0, gidx0=0, kl_coef=0.003, gamma=1.0, lam=0.95, scripted_target=122, w_rm=None,

@@ -465,4 +465,114 @@ int ref_dpo_step(const int64_t* c6, double* w_policy, const double* w_ref, int64
   });
 }
 
+
+// n_iters PPO iterations on the reference (ppo_step, src/ppo.cpp:302-441, with the
+// critic in-process): greedy experience (ref_experience's stages), the actor
+// update on the tape + AdamW (:395-424), the critic update (handle_train,
+// :195-231), the engine refit (:431-432); AdamW moments persist across
+// iterations (one optimizer per job).  Per iteration i: tokens / lengths /
+// actor_lp / values / advantages [n_iters, B, max_new] and losses[i] =
+// {actor, critic}; final weights written back.
+int ref_ppo_loop(const int64_t* c6, double* w_policy, const double* w_ref, double* w_critic, int32_t scripted_target,
+                 const int32_t* prompts, const int64_t* offsets, int64_t B, int64_t max_new, uint64_t seed,
+                 double kl_coef, double gamma, double lam, double clip_eps, double value_clip, double lr,
+                 const double* adam4, int64_t n_iters, int32_t* out_tokens, int64_t* out_n, double* out_actor_lp,
+                 double* out_values, double* out_adv, double* losses) {
+  return guarded([&] {
+    const auto cfg = make_cfg(c6, 0);
+    auto ccfg = cfg;
+    ccfg.scalar_head = true;
+    auto policy = from_flat(cfg, w_policy);
+    const auto refm = from_flat(cfg, w_ref);
+    auto critic = from_flat(ccfg, w_critic);
+    policy.set_requires_grad_on_trainable();
+    critic.set_requires_grad_on_trainable();
+    AdamW actor_opt = make_adam(adam4), critic_opt = make_adam(adam4);
+    auto engine = build_engine(policy, cfg, EngineOptions{});
+    const int64_t BN = B * max_new;
+    for (int64_t it = 0; it < n_iters; ++it) {
+      std::vector<GenTask> tasks(B);
+      for (int64_t i = 0; i < B; ++i) {
+        tasks[i].prompt.assign(prompts + offsets[i], prompts + offsets[i + 1]);
+        tasks[i].max_new = std::size_t(max_new);
+        tasks[i].sampling = SamplingSpec::greedy_spec();
+      }
+      (void)seed;
+      const auto gens = engine->generate_batch(tasks);
+      std::vector<TokenSeq> full(B);
+      std::vector<std::size_t> P(B);
+      std::vector<double> flat_old, flat_adv, flat_vals, flat_ret;
+      std::vector<std::vector<double>> vals_b(B), ret_b(B);
+      for (int64_t i = 0; i < B; ++i) {
+        P[i] = tasks[i].prompt.size();
+        full[i] = tasks[i].prompt;
+        full[i].insert(full[i].end(), gens[i].tokens.begin(), gens[i].tokens.end());
+        const std::size_t n = gens[i].tokens.size();
+        out_n[it * B + i] = int64_t(n);
+        const auto a = sequence_logprobs(policy, full[i]);
+        const auto r = sequence_logprobs(refm, full[i]);
+        std::vector<double> al(a.begin() + P[i], a.end()), rl(r.begin() + P[i], r.end());
+        double R = 0.0;
+        for (std::size_t t = P[i]; t < full[i].size(); ++t) R += full[i][t] == scripted_target ? 1.0 : 0.0;
+        const auto v = value_estimates(critic, critic.at("scalar_head.weight"), full[i], P[i]);
+        std::vector<double> vv(v.values().begin(), v.values().end());
+        const auto shaped = kl_penalized_rewards(R, al, rl, kl_coef);
+        const auto est = gae(shaped, vv, gamma, lam);
+        for (std::size_t t = 0; t < n; ++t) {
+          out_tokens[it * BN + i * max_new + int64_t(t)] = gens[i].tokens[t];
+          out_actor_lp[it * BN + i * max_new + int64_t(t)] = al[t];
+          out_values[it * BN + i * max_new + int64_t(t)] = vv[t];
+          out_adv[it * BN + i * max_new + int64_t(t)] = est.advantages[t];
+        }
+        flat_old.insert(flat_old.end(), al.begin(), al.end());
+        flat_adv.insert(flat_adv.end(), est.advantages.begin(), est.advantages.end());
+        vals_b[i] = vv;
+        ret_b[i] = est.returns;
+      }
+      {  // actor update (src/ppo.cpp:395-424)
+        Tape tape;
+        {
+          TapeScope scope(tape);
+          std::vector<Tensor> rows;
+          for (int64_t i = 0; i < B; ++i) {
+            TokenSeq resp(full[i].begin() + P[i], full[i].end());
+            Tensor logits = forward_one(policy, full[i]);
+            Tensor lp = log_softmax(slice_rows(logits, P[i] - 1, full[i].size() - 1));
+            Tensor part = gather_token_logprobs(lp, resp);
+            rows.push_back(reshape(part, {part.size(), 1}));
+          }
+          Tensor new_lp = reshape(concat_rows(rows), {flat_old.size()});
+          Tensor loss = ppo_actor_loss(new_lp, flat_old, flat_adv, clip_eps, std::vector<double>(flat_old.size(), 1.0));
+          losses[it * 2] = loss.item();
+          policy.zero_grad();
+          backward(loss);
+        }
+        actor_opt.step(policy, lr);
+        policy.zero_grad();
+      }
+      {  // critic update (src/ppo.cpp:195-231)
+        Tape tape;
+        {
+          TapeScope scope(tape);
+          Tensor total = Tensor::scalar(0.0);
+          for (int64_t i = 0; i < B; ++i) {
+            Tensor values = value_estimates(critic, critic.at("scalar_head.weight"), full[i], P[i]);
+            std::vector<double> mask(values.size(), 1.0);
+            total = add(total, ppo_critic_loss(values, vals_b[i], ret_b[i], value_clip, mask));
+          }
+          Tensor mean_loss = mul_scalar(total, 1.0 / double(B));
+          losses[it * 2 + 1] = mean_loss.item();
+          critic.zero_grad();
+          backward(mean_loss);
+        }
+        critic_opt.step(critic, lr);
+        critic.zero_grad();
+      }
+      engine->refit(policy);  // src/ppo.cpp:431-432
+    }
+    to_flat(policy, w_policy);
+    to_flat(critic, w_critic);
+  });
+}
+
 }  // extern "C"

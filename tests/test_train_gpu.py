@@ -150,3 +150,47 @@ def test_spin_make_pairs_matches_reference_generation(px, ctx, oracle, ref):
     kept = [i for i in range(5) if i != 2]
     for (p, c, r), i in zip(sp.pairs, kept):
         assert np.array_equal(r, t_o[i]) and np.array_equal(c, examples[i][1])
+
+
+
+def test_ppo_iterations_match_reference(px, ctx, oracle, ref):
+    """Three full PPO iterations (ppo_step, src/ppo.cpp:302-441): greedy
+    experience → actor update → critic update → refit of the serving engine and
+    the critic → the next experience on the refitted models, against the same
+    loop run by the reference itself (its tape autodiff and persistent AdamW;
+    oracle/ref_shim.cpp ref_ppo_loop).  Rollouts identical, experience and
+    losses within the bar in every iteration, final weights within the bar."""
+    cfg = ModelCfg(V=258, d=32, L=2, H=2, f=64, S=48)
+    pc = to_px_cfg(cfg)
+    w_pol = f32(ref.init_params(cfg, 21))
+    w_ref = f32(ref.init_params(cfg, 22))
+    w_crit = f32(ref.init_params(cfg, 23, head=True))
+    w_crit[-cfg.d:] = f32(np.random.default_rng(5).normal(0, 0.1, cfg.d))
+    prompts = synthetic_prompts(31, 4, 6, ragged_lengths=True)
+    N, lr, kl, iters = 8, 3e-4, 0.01, 3
+    ref_iters, w_pol_ref, w_crit_ref = ref.ppo_loop(cfg, w_pol, w_ref, w_crit, prompts, max_new=N, n_iters=iters,
+                                                     kl_coef=kl, lr=lr, scripted_target=ord("e"), adam=ADAM)
+    eng = px.Engine(px.DeviceModel(ctx, pc, w_pol, px.F32))
+    refm = px.DeviceModel(ctx, pc, w_ref, px.F32)
+    crit = px.DeviceModel(ctx, pc.with_head(), w_crit, px.F32)
+    actor = px.Trainer(ctx, pc, w_pol, serving=eng.model, adamw=px.AdamWOptions(*ADAM))
+    critic = px.Trainer(ctx, pc.with_head(), w_crit, serving=crit, adamw=px.AdamWOptions(*ADAM))
+    xm = px.ExperienceMaker(eng, refm, crit, scripted_target=ord("e"), hyper=px.PpoHyper(kl, 1.0, 0.95))
+    for it, r in enumerate(ref_iters):
+        batch, _ = xm.run(prompts, max_new=N, sampling=px.SamplingSpec.greedy_spec(), seed=7, step_index=it)
+        for i, s in enumerate(batch):
+            assert np.array_equal(s.response, r["tokens"][i]), f"iteration {it}: rollout {i} differs"
+            close(s.actor_logprobs, r["actor_logprobs"][i])
+            close(s.values, r["values"][i])
+            close(s.advantages, r["advantages"][i])
+        seqs = [np.concatenate([p, s.response]).astype(np.int32) for p, s in zip(prompts, batch)]
+        rs = [len(p) for p in prompts]
+        la = actor.ppo_actor_step(seqs, rs, [s.actor_logprobs for s in batch], [s.advantages for s in batch],
+                                  clip_eps=0.2, lr=lr)
+        lc = critic.critic_step(seqs, rs, [s.values for s in batch], [s.returns for s in batch], value_clip=0.2,
+                                lr=lr)
+        close([la, lc], [r["actor_loss"], r["critic_loss"]])
+        actor.refit()
+        critic.refit()
+    close(actor.flat(), w_pol_ref)
+    close(critic.flat(), w_crit_ref)
