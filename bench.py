@@ -244,7 +244,10 @@ def _dbg(*a):
 
 
 KCLASS = [("gemm_decode_kernel", "gemm_decode"), ("attn_decode_kernel", "decode_attention"),
-          ("sampler_kernel", "sampler"), ("gemm_tc_kernel<256, 4>", "lm_head_lse"),
+          ("sampler_kernel", "sampler"), ("gemm_tc_kernel<256, 4", "lm_head_lse"), ("gemm_tc_kernel<128, 3, true", "gemm_mixed"),
+          ("gemm_tc_kernel<128, 2, true", "gemm_mixed"), ("gemm_tc_kernel<128, 6, true", "gemm_mixed"),
+          ("gemm_tc_kernel<256, 3, true", "gemm_mixed"), ("gemm_tc_kernel<256, 2, true", "gemm_mixed"),
+          ("gemm_tc_kernel<256, 6, true", "gemm_mixed"),
           ("gemm_mixed_kernel<4>", "lm_head_lse"), ("gemm_mixed_kernel", "gemm_mixed"),
           ("gemm_tc_kernel", "gemm_tc"), ("lse_combine", "lse_combine"), ("logprob_gather", "logprob_gather"),
           ("attn_prefill", "attention_prefill"), ("attention_mma", "attention_prefill"), ("layernorm", "layernorm"),

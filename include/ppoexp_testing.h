@@ -33,6 +33,11 @@ PPOEXP_API ppoexp_status ppoexp_testing_attention_prefill(ppoexp_ctx ctx, const 
 PPOEXP_API ppoexp_status ppoexp_testing_umma_probe(ppoexp_ctx ctx, const void* A, const void* B, int32_t N, float* out,
                                         int32_t variant);
 
+/* Mixed-mode GEMM over activation planes A[M, 2K] (hi | lo bf16): epi 2 residual add,
+ * 3 store fp32, 6 GELU -> hi | lo planes (C [M, 2N] bf16, ldc = row stride). */
+PPOEXP_API ppoexp_status ppoexp_testing_gemm_planes(ppoexp_ctx ctx, const void* A, const void* W, int64_t M, int64_t N,
+                                         int64_t K, int32_t epi, void* C, int64_t ldc);
+
 /* Mixed-mode GEMM: C[M,N] (+)= A[M,K] (fp32) · W[N,K]^T (bf16), activations
  * split into two bf16 terms in-kernel.  epi: 2 fp32 residual add, 3 store fp32,
  * 5 GELU -> fp32.  M <= 256 takes the decode (swap-AB, cluster split-K) kernel. */

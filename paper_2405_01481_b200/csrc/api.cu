@@ -1233,3 +1233,17 @@ extern "C" ppoexp_status ppoexp_testing_attention_prefill(ppoexp_ctx ctx, const 
     c.sync();
   });
 }
+
+extern "C" ppoexp_status ppoexp_testing_gemm_planes(ppoexp_ctx ctx, const void* A, const void* W, int64_t M, int64_t N,
+                                                    int64_t K, int32_t epi, void* C, int64_t ldc) {
+  return guard([&] {
+    need(ctx, "ctx");
+    Ctx& c = *ctx->c;
+    std::lock_guard<std::recursive_mutex> lk(c.mu);
+    DeviceGuard g(c.device);
+    if (epi != 2 && epi != 3 && epi != 6) throw ContractError("epi must be 2, 3 or 6");
+    gemm_tc_planes(c, static_cast<const bf16*>(A), 2 * K, static_cast<const bf16*>(W), K, M, N, K, static_cast<Epi>(epi),
+                   C, ldc);
+    c.sync();
+  });
+}

@@ -246,7 +246,7 @@ struct SplitSmem {
 template <int DH>
 __global__ void __launch_bounds__(128) attn_prefill_split_kernel(const float* __restrict__ qkv,
                                                                  const int64_t* __restrict__ seq_offsets, int64_t H,
-                                                                 float* __restrict__ out) {
+                                                                 float* __restrict__ out, bf16* __restrict__ planes) {
   PDL_ENTRY();
   using SL = SplitSmem<DH>;
   constexpr int LD = SL::LD, KC = DH / 16, NO = DH / 8, CH4 = DH / 4;
@@ -413,6 +413,20 @@ __global__ void __launch_bounds__(128) attn_prefill_split_kernel(const float* __
 #pragma unroll
   for (int i = 0; i < NO; ++i) {
     const int64_t col = h * DH + i * 8 + 2 * t4;
+    if (planes) {  // the O projection reads the output as hi | lo bf16 planes [M, 2d]
+      uint32_t h, l;
+      if (qrow0 < len) {
+        split2(o[i][0] * inv0, o[i][1] * inv0, h, l);
+        *reinterpret_cast<uint32_t*>(planes + (start + qrow0) * 2 * d + col) = h;
+        *reinterpret_cast<uint32_t*>(planes + (start + qrow0) * 2 * d + d + col) = l;
+      }
+      if (qrow1 < len) {
+        split2(o[i][2] * inv1, o[i][3] * inv1, h, l);
+        *reinterpret_cast<uint32_t*>(planes + (start + qrow1) * 2 * d + col) = h;
+        *reinterpret_cast<uint32_t*>(planes + (start + qrow1) * 2 * d + d + col) = l;
+      }
+      continue;
+    }
     if (qrow0 < len) *reinterpret_cast<float2*>(out + (start + qrow0) * d + col) = make_float2(o[i][0] * inv0, o[i][1] * inv0);
     if (qrow1 < len) *reinterpret_cast<float2*>(out + (start + qrow1) * d + col) = make_float2(o[i][2] * inv1, o[i][3] * inv1);
   }
@@ -420,7 +434,7 @@ __global__ void __launch_bounds__(128) attn_prefill_split_kernel(const float* __
 
 template <int DH>
 void launch_split(Ctx& c, const float* qkv, const int64_t* seq_offsets, int64_t B, int64_t max_len, int64_t H,
-                  float* out) {
+                  float* out, bf16* planes) {
   constexpr size_t smem = SplitSmem<DH>::kBytes;
   static bool attr = false;
   if (!attr) {
@@ -431,7 +445,7 @@ void launch_split(Ctx& c, const float* qkv, const int64_t* seq_offsets, int64_t 
   dim3 grid(ceil_div(max_len, QT), H, B);
   const double flops = 2.0 * 2.0 * B * H * double(max_len) * max_len / 2 * DH;
   c.launch("attention_prefill", 0, flops, [&] {
-    launch_kernel(c, attn_prefill_split_kernel<DH>, grid, dim3(128), smem, 1, qkv, seq_offsets, H, out);
+    launch_kernel(c, attn_prefill_split_kernel<DH>, grid, dim3(128), smem, 1, qkv, seq_offsets, H, out, planes);
   });
 }
 
@@ -457,13 +471,13 @@ void launch_mma(Ctx& c, const bf16* qkv, const int64_t* seq_offsets, int64_t B, 
 
 // Mixed-mode prefill attention (fp32 q/k/v/out, split-bf16 tensor-core products).
 void attention_prefill_split(Ctx& c, const float* qkv, const int64_t* seq_offsets, int64_t B, int64_t max_len,
-                             int64_t H, int64_t DH, float* out) {
+                             int64_t H, int64_t DH, float* out, bf16* planes) {
   if (B <= 0 || max_len <= 0) return;
   switch (DH) {
-    case 16: return launch_split<16>(c, qkv, seq_offsets, B, max_len, H, out);
-    case 32: return launch_split<32>(c, qkv, seq_offsets, B, max_len, H, out);
-    case 64: return launch_split<64>(c, qkv, seq_offsets, B, max_len, H, out);
-    case 128: return launch_split<128>(c, qkv, seq_offsets, B, max_len, H, out);
+    case 16: return launch_split<16>(c, qkv, seq_offsets, B, max_len, H, out, planes);
+    case 32: return launch_split<32>(c, qkv, seq_offsets, B, max_len, H, out, planes);
+    case 64: return launch_split<64>(c, qkv, seq_offsets, B, max_len, H, out, planes);
+    case 128: return launch_split<128>(c, qkv, seq_offsets, B, max_len, H, out, planes);
     default: throw ContractError("attention: head_dim " + std::to_string(DH) + " unsupported (16/32/64/128)");
   }
 }

@@ -107,15 +107,18 @@ __device__ __forceinline__ void store_split(const AChunks& a, uint8_t* hi, uint8
     const int q = et + c * 128, r = q >> 3, c8 = q & 7;
     const float x[8] = {a.v[c][0].x, a.v[c][0].y, a.v[c][0].z, a.v[c][0].w,
                         a.v[c][1].x, a.v[c][1].y, a.v[c][1].z, a.v[c][1].w};
-    Vec16<bf16> h, l;
+    uint32_t h[4], l[4];
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      h.v[e] = __float2bfloat16_rn(x[e]);
-      l.v[e] = __float2bfloat16_rn(x[e] - __bfloat162float(h.v[e]));
+    for (int e = 0; e < 4; ++e) {  // packed cvt.rn.bf16x2.f32: one conversion per pair
+      const __nv_bfloat162 hp = __floats2bfloat162_rn(x[2 * e], x[2 * e + 1]);
+      const float2 hf = __bfloat1622float2(hp);
+      const __nv_bfloat162 lp = __floats2bfloat162_rn(x[2 * e] - hf.x, x[2 * e + 1] - hf.y);
+      h[e] = *reinterpret_cast<const uint32_t*>(&hp);
+      l[e] = *reinterpret_cast<const uint32_t*>(&lp);
     }
     const int off = r * 128 + ((c8 ^ (r & 7)) << 4);
-    *reinterpret_cast<uint4*>(hi + off) = h.u;
-    *reinterpret_cast<uint4*>(lo + off) = l.u;
+    *reinterpret_cast<uint4*>(hi + off) = make_uint4(h[0], h[1], h[2], h[3]);
+    *reinterpret_cast<uint4*>(lo + off) = make_uint4(l[0], l[1], l[2], l[3]);
   }
 }
 

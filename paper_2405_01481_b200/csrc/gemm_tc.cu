@@ -101,24 +101,28 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-template <int BN>
+template <int BN, bool SPLIT = false>
 struct SmemLayout {
-  static constexpr int kA = BM * BK * 2;   // 16 KB
+  static constexpr int kAT = BM * BK * 2;  // 16 KB: one bf16 A tile
+  static constexpr int kA = kAT * (SPLIT ? 2 : 1);  // mixed mode: hi and lo planes of the activation
   static constexpr int kB = BN * BK * 2;
   static constexpr int kStage = kA + kB;
   // ~110 KB of stages: two CTAs share an SM (TMEM: 2 x BN <= 512 columns), so
   // one CTA's epilogue (TMEM -> registers -> global, fp32 residual RMW)
-  // overlaps the other's TMA/MMA main loop
-  static constexpr int kStages = (110 * 1024) / kStage > 8 ? 8 : (110 * 1024) / kStage;
+  // overlaps the other's TMA/MMA main loop.  Split 128 x 256 tiles (the LM
+  // head's LSE) take one CTA per SM with three 64 KB stages instead.
+  static constexpr int kBudget = (SPLIT && BN == 256) ? 200 * 1024 : 110 * 1024;
+  static constexpr int kStages = kBudget / kStage > 8 ? 8 : kBudget / kStage;
   static constexpr int kBytes = kStages * kStage + 1024 /*align*/ + 256 /*barriers*/;
   static constexpr int kTmemCols = BN < 32 ? 32 : BN;
 };
 
-template <int BN, int EPI>
+template <int BN, int EPI, bool SPLIT = false>
 __global__ void __launch_bounds__(kThreads, 2)
-    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
-                   int K, void* __restrict__ Cv, int64_t ldc, int group_m, LseEpi lse) {
-  using L = SmemLayout<BN>;
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmA2,
+                   const __grid_constant__ CUtensorMap tmB, int M, int N, int K, void* __restrict__ Cv, int64_t ldc,
+                   int group_m, LseEpi lse) {
+  using L = SmemLayout<BN, SPLIT>;
   constexpr int S = L::kStages;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -170,6 +174,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         if (r > 0) mbar_wait(&empty[s], (r - 1) & 1);
         mbar_expect_tx(&full[s], L::kStage);
         tma_load_2d(&tmA, &full[s], sA + s * L::kA, kb * BK, m0);
+        if constexpr (SPLIT) tma_load_2d(&tmA2, &full[s], sA + s * L::kA + L::kAT, kb * BK, m0);
         tma_load_2d(&tmB, &full[s], sB + s * L::kB, kb * BK, n0);
       }
     }
@@ -185,6 +190,11 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll
         for (int k = 0; k < BK / 16; ++k)  // UMMA_K = 16 (32 bytes): +2 in the >>4 address field
           mma_bf16(tmem, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
+        if constexpr (SPLIT) {  // the activation's low-order bf16 term into the same accumulator
+          const uint64_t dal = smem_desc_sw128(sA + s * L::kA + L::kAT);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) mma_bf16(tmem, dal + 2 * k, db + 2 * k, idesc, 1);
+        }
         mma_commit(&empty[s]);
       }
       mma_commit(tmem_full);
@@ -245,7 +255,25 @@ __global__ void __launch_bounds__(kThreads, 2)
       const int col = n0 + c;
       if (row >= M || col >= N) continue;
       const bool full_cols = col + 32 <= N;
-      if constexpr (EPI == int(Epi::kStore) || EPI == int(Epi::kGelu)) {
+      if constexpr (EPI == int(Epi::kGeluSplit)) {
+        // GELU output as two bf16 planes: hi at [row, col], lo at [row, N + col]
+        bf16* dst = static_cast<bf16*>(Cv) + int64_t(row) * ldc + col;
+#pragma unroll
+        for (int e = 0; e < 32; e += 2) {
+          if (col + e + 1 < N || full_cols) {
+            const float g0 = gelu_tanh(__uint_as_float(v[e])), g1 = gelu_tanh(__uint_as_float(v[e + 1]));
+            const __nv_bfloat162 h = __floats2bfloat162_rn(g0, g1);
+            const float2 hf = __bfloat1622float2(h);
+            *reinterpret_cast<__nv_bfloat162*>(dst + e) = h;
+            *reinterpret_cast<__nv_bfloat162*>(dst + N + e) = __floats2bfloat162_rn(g0 - hf.x, g1 - hf.y);
+          } else if (col + e < N) {
+            const float g0 = gelu_tanh(__uint_as_float(v[e]));
+            const bf16 h = __float2bfloat16_rn(g0);
+            dst[e] = h;
+            dst[N + e] = __float2bfloat16_rn(g0 - __bfloat162float(h));
+          }
+        }
+      } else if constexpr (EPI == int(Epi::kStore) || EPI == int(Epi::kGelu)) {
         bf16* dst = static_cast<bf16*>(Cv) + int64_t(row) * ldc + col;
         if (full_cols) {
 #pragma unroll
@@ -350,13 +378,15 @@ CUtensorMap make_map(const void* ptr, int64_t rows, int64_t cols, int64_t ld, in
 
 namespace {
 
-template <int BN, int EPI>
+template <int BN, int EPI, bool SPLIT = false>
 void launch_tc(Ctx& c, const bf16* A, int64_t lda, const bf16* B, int64_t ldb, int64_t M, int64_t N, int64_t K,
                void* C, int64_t ldc, const LseEpi& lse = LseEpi{}) {
-  using L = SmemLayout<BN>;
+  using L = SmemLayout<BN, SPLIT>;
   const CUtensorMap ta = make_map(A, M, K, lda, BM);
+  // split planes: the activation is [M, 2K] (hi | lo) with row stride lda
+  const CUtensorMap ta2 = SPLIT ? make_map(A + K, M, K, lda, BM) : ta;
   const CUtensorMap tb = make_map(B, N, K, ldb, BN);
-  auto k = gemm_tc_kernel<BN, EPI>;
+  auto k = gemm_tc_kernel<BN, EPI, SPLIT>;
   static bool attr = false;
   if (!attr) {
     PPOEXP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kBytes));
@@ -367,10 +397,10 @@ void launch_tc(Ctx& c, const bf16* A, int64_t lda, const bf16* B, int64_t ldb, i
   const double flops = 2.0 * M * N * K;
   const double out_bytes = EPI == int(Epi::kLse) ? double(M) * (num_n * 8 + 8)
                                                  : double(M) * N * ((EPI == 0 || EPI == 1) ? 2 : 4);
-  const double bytes = 2.0 * (M * K + N * K) + out_bytes;
-  c.launch(EPI == int(Epi::kLse) ? "lm_head_lse" : "gemm_tc", bytes, flops, [&] {
-    launch_kernel(c, k, dim3(num_m * num_n), dim3(kThreads), L::kBytes, 1, ta, tb, int(M), int(N), int(K), C, ldc,
-                  group_m, lse);
+  const double bytes = 2.0 * ((SPLIT ? 2 : 1) * M * K + N * K) + out_bytes;
+  c.launch(EPI == int(Epi::kLse) ? "lm_head_lse" : (SPLIT ? "gemm_mixed" : "gemm_tc"), bytes, flops, [&] {
+    launch_kernel(c, k, dim3(num_m * num_n), dim3(kThreads), L::kBytes, 1, ta, ta2, tb, int(M), int(N), int(K), C,
+                  ldc, group_m, lse);
   });
 }
 
@@ -383,6 +413,7 @@ void dispatch_epi(Ctx& c, const bf16* A, int64_t lda, const bf16* B, int64_t ldb
     case Epi::kAddResidual: return launch_tc<BN, 2>(c, A, lda, B, ldb, M, N, K, C, ldc);
     case Epi::kStoreF32: return launch_tc<BN, 3>(c, A, lda, B, ldb, M, N, K, C, ldc);
     case Epi::kLse: throw ContractError("gemm: the LSE epilogue goes through gemm_tc_lse");
+    default: throw ContractError("gemm: fp32-activation epilogues go through the mixed-mode GEMMs");
   }
 }
 
@@ -422,6 +453,41 @@ bool gemm_tc_bf16(Ctx& c, const bf16* A, int64_t lda, const bf16* B, int64_t ldb
 // Fused LM head + online LSE + target gather (scoring, bf16 perf mode).
 // part[M, ldp] gets one (max, sum exp) pair per 256-column tile.
 int lse_tiles(int64_t N) { return int(ceil_div(N, 256)); }
+
+// Mixed mode with the activation as two bf16 planes A[M, 2K] (hi | lo, row
+// stride lda >= 2K, written by the producer: split LayerNorm / attention /
+// GELU epilogue): both TMA'd, two MMAs per k16 step; 128 x 128 tiles (two
+// CTAs per SM), the LSE epilogue on 128 x 256 tiles.
+void gemm_tc_planes(Ctx& c, const bf16* A, int64_t lda, const bf16* W, int64_t ldw, int64_t M, int64_t N, int64_t K,
+                    Epi epi, void* C, int64_t ldc, const LseEpi* lse) {
+  if (M <= 0 || N <= 0 || K <= 0) return;
+  if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(W)) & 15 || (lda * 2) % 16 || (ldw * 2) % 16 ||
+      K % 8 || lda < 2 * K)
+    throw ContractError("gemm (planes): 16-byte aligned rows, K % 8 and a [M, 2K] activation required");
+  if (epi == Epi::kLse) {
+    if (!lse || lse->ldp < lse_tiles(N)) throw ContractError("gemm (planes): LSE outputs missing");
+    return launch_tc<256, int(Epi::kLse), true>(c, A, lda, W, ldw, M, N, K, nullptr, 0, *lse);
+  }
+  if (M <= 128) return gemm_decode_planes(c, A, lda, W, ldw, M, N, K, epi, C, ldc, nullptr);
+  static const int bn = [] {  // 256: one CTA per SM, three 64 KB stages; 128: two CTAs per SM
+    const char* e = getenv("PPOEXP_PLANES_BN");
+    return e ? atoi(e) : 256;
+  }();
+  if (bn == 128) {
+    switch (epi) {
+      case Epi::kStoreF32: return launch_tc<128, int(Epi::kStoreF32), true>(c, A, lda, W, ldw, M, N, K, C, ldc);
+      case Epi::kAddResidual: return launch_tc<128, int(Epi::kAddResidual), true>(c, A, lda, W, ldw, M, N, K, C, ldc);
+      case Epi::kGeluSplit: return launch_tc<128, int(Epi::kGeluSplit), true>(c, A, lda, W, ldw, M, N, K, C, ldc);
+      default: throw ContractError("gemm (planes): unsupported epilogue");
+    }
+  }
+  switch (epi) {
+    case Epi::kStoreF32: return launch_tc<256, int(Epi::kStoreF32), true>(c, A, lda, W, ldw, M, N, K, C, ldc);
+    case Epi::kAddResidual: return launch_tc<256, int(Epi::kAddResidual), true>(c, A, lda, W, ldw, M, N, K, C, ldc);
+    case Epi::kGeluSplit: return launch_tc<256, int(Epi::kGeluSplit), true>(c, A, lda, W, ldw, M, N, K, C, ldc);
+    default: throw ContractError("gemm (planes): unsupported epilogue");
+  }
+}
 
 bool gemm_tc_lse(Ctx& c, const bf16* A, int64_t lda, const bf16* B, int64_t ldb, int64_t M, int64_t N, int64_t K,
                  const LseEpi& e) {

@@ -106,7 +106,11 @@ void gemm_decode_mixed(Ctx& c, const float* X, int64_t ldx, const bf16* W, int64
 void gemm_decode_planes(Ctx& c, const bf16* X, int64_t ldx, const bf16* W, int64_t ldw, int64_t M, int64_t N, int64_t K,
                         Epi epi, void* C, int64_t ldc, const RowStats* so);
 // LayerNorm written as two bf16 planes y[r, 0:d) = hi, y[r, d:2d) = lo (mixed decode).
-void launch_layernorm_split(Ctx& c, const float* x, int64_t rows, int64_t d, const float* g, const float* b, bf16* y);
+void launch_layernorm_split(Ctx& c, const float* x, int64_t rows, int64_t d, const float* g, const float* b, bf16* y,
+                            const int32_t* gather = nullptr);
+// Mixed-mode GEMM over a [M, 2K] hi|lo bf16 plane activation (tcgen05, both planes TMA'd).
+void gemm_tc_planes(Ctx& c, const bf16* A, int64_t lda, const bf16* W, int64_t ldw, int64_t M, int64_t N, int64_t K,
+                    Epi epi, void* C, int64_t ldc, const LseEpi* lse = nullptr);
 // Mixed-mode GEMM for any M (decode-sized M goes to gemm_decode_mixed).
 void gemm_mixed(Ctx& c, const float* A, int64_t lda, const bf16* W, int64_t ldw, int64_t M, int64_t N, int64_t K,
                 Epi epi, void* C, int64_t ldc, const LseEpi* lse = nullptr);
@@ -132,8 +136,9 @@ bool attention_prefill_tc(Ctx& c, const bf16* qkv, const int64_t* seq_offsets, i
                           int64_t DH, int64_t M_total, bf16* out, bool force = false);
 // K5a in mixed mode: fp32 q/k/v in, fp32 out, tensor-core products on the
 // two-term bf16 split (three MMAs per product).
+// planes (nullable): write the output as hi | lo bf16 planes [M, 2d] instead of `out`.
 void attention_prefill_split(Ctx& c, const float* qkv, const int64_t* seq_offsets, int64_t B, int64_t max_len,
-                             int64_t H, int64_t DH, float* out);
+                             int64_t H, int64_t DH, float* out, bf16* planes = nullptr);
 
 // K5b: one decode step: append this step's K/V (row b of qkv at position
 // pos[b]) to the paged pool, then attend over positions 0..pos[b].

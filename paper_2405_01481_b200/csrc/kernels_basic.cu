@@ -415,14 +415,16 @@ __global__ void __launch_bounds__(256) layernorm_wide_kernel(const float* __rest
 // Mixed decode: LayerNorm of a row (fp32, two-pass statistics in fp64) written as
 // two bf16 planes, y[r, j] = hi, y[r, d + j] = lo (the consumer GEMM TMAs both).
 __global__ void layernorm_split_kernel(const float* __restrict__ x, int64_t d, const float* __restrict__ g,
-                                       const float* __restrict__ b, bf16* __restrict__ y) {
+                                       const float* __restrict__ b, bf16* __restrict__ y,
+                                       const int32_t* __restrict__ gather) {
   PDL_ENTRY();
   __shared__ double red[32];
   const int64_t r = blockIdx.x;
+  const int64_t src = gather ? gather[r] : r;
   const int nw = (blockDim.x + 31) >> 5, w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int j = threadIdx.x * 4;
   const bool act = j < d;
-  const float4 v = act ? *reinterpret_cast<const float4*>(x + r * d + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+  const float4 v = act ? *reinterpret_cast<const float4*>(x + src * d + j) : make_float4(0.f, 0.f, 0.f, 0.f);
   double s = warp_sum_d(double(v.x) + v.y + v.z + v.w);
   if (lane == 0) red[w] = s;
   __syncthreads();
@@ -451,12 +453,13 @@ __global__ void layernorm_split_kernel(const float* __restrict__ x, int64_t d, c
   *reinterpret_cast<uint2*>(y + r * 2 * d + d + j) = *reinterpret_cast<const uint2*>(lo);
 }
 
-void launch_layernorm_split(Ctx& c, const float* x, int64_t rows, int64_t d, const float* g, const float* b, bf16* y) {
+void launch_layernorm_split(Ctx& c, const float* x, int64_t rows, int64_t d, const float* g, const float* b, bf16* y,
+                            const int32_t* gather) {
   if (rows <= 0) return;
   if (d % 4 || d > 4096) throw ContractError("layernorm (split planes): d % 4 == 0 and d <= 4096 required");
   const int th = int((d / 4 + 31) / 32 * 32);
   c.launch("layernorm", double(rows) * d * 8, 0, [&] {
-    launch_kernel(c, layernorm_split_kernel, dim3(rows), dim3(th), 0, 1, x, d, g, b, y);
+    launch_kernel(c, layernorm_split_kernel, dim3(rows), dim3(th), 0, 1, x, d, g, b, y, gather);
   });
 }
 

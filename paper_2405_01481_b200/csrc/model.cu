@@ -292,6 +292,26 @@ static float* forward_layers_t(Model& m, const Packed& p, const KvTarget* kv) {
 }
 
 // Mixed mode: bf16 weights, fp32 activations / KV, split-bf16 tensor-core GEMMs.
+// Mixed-mode prefill / scoring GEMMs: the in-kernel fp32 -> hi|lo split
+// (gemm_mixed.cu) measured faster than plane operands written by the producers
+// (C2 scoring: 32.2 vs 36.5 ms of GEMM time per step, + 2.3 ms of split
+// LayerNorms); PPOEXP_PREFILL_PLANES=1 selects the planes.  The LM head takes the
+// planes (LSE epilogue: 5.9 -> 4.7 ms) unless PPOEXP_MIXED_PLANES=0.
+static bool mixed_prefill_planes() {
+  static const bool on = [] {
+    const char* e = getenv("PPOEXP_PREFILL_PLANES");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+static bool mixed_head_planes() {
+  static const bool on = [] {
+    const char* e = getenv("PPOEXP_MIXED_PLANES");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 static float* forward_layers_mixed(Model& m, const Packed& p, const KvTarget* kv) {
   Ctx& c = *m.ctx;
   const int64_t M = p.M, d = m.d(), f = m.cfg.d_ff, H = m.cfg.n_heads, DH = m.dh();
@@ -302,6 +322,28 @@ static float* forward_layers_mixed(Model& m, const Packed& p, const KvTarget* kv
   float* up = static_cast<float*>(c.workspace("fwd.up", M * f * 4));
   launch_embed<bf16>(c, p.tokens_d, p.positions_d, M, d, static_cast<const bf16*>(m.tok),
                      static_cast<const bf16*>(m.pos), x);
+  if (mixed_prefill_planes() && d <= 4096) {
+    // activations as hi | lo bf16 planes [M, 2K] written by their producers (split
+    // LayerNorm, attention output, GELU epilogue) and TMA'd by the GEMMs: no
+    // fp32 -> bf16 conversion inside the GEMM main loops
+    bf16* hp = reinterpret_cast<bf16*>(h);
+    bf16* ap = reinterpret_cast<bf16*>(att);
+    bf16* upp = reinterpret_cast<bf16*>(up);
+    for (int64_t l = 0; l < m.cfg.n_layers; ++l) {
+      const Layer& ly = m.layers[l];
+      launch_layernorm_split(c, x, M, d, ly.ln1w, ly.ln1b, hp);
+      gemm_tc_planes(c, hp, 2 * d, static_cast<const bf16*>(ly.wqkv), d, M, 3 * d, d, Epi::kStoreF32, qkv, 3 * d);
+      if (kv)
+        launch_kv_scatter<float>(c, qkv, M, d, p.seq_of_row_d, p.positions_d, kv->block_table, int(l), kv->geom,
+                                 static_cast<float*>(kv->pool));
+      attention_prefill_split(c, qkv, p.offsets_d, p.B, p.max_len, H, DH, nullptr, ap);
+      gemm_tc_planes(c, ap, 2 * d, static_cast<const bf16*>(ly.wo), d, M, d, d, Epi::kAddResidual, x, d);
+      launch_layernorm_split(c, x, M, d, ly.ln2w, ly.ln2b, hp);
+      gemm_tc_planes(c, hp, 2 * d, static_cast<const bf16*>(ly.wup), d, M, f, d, Epi::kGeluSplit, upp, 2 * f);
+      gemm_tc_planes(c, upp, 2 * f, static_cast<const bf16*>(ly.wdown), f, M, d, f, Epi::kAddResidual, x, d);
+    }
+    return x;
+  }
   for (int64_t l = 0; l < m.cfg.n_layers; ++l) {
     const Layer& ly = m.layers[l];
     launch_layernorm<float>(c, x, M, d, ly.ln1w, ly.ln1b, h, nullptr, nullptr, nullptr);
@@ -360,7 +402,11 @@ static void score_logprobs_fused(Model& m, const float* x, const int32_t* gather
     e.tgt_logit = tl;
     e.part = part;
     e.ldp = ldp;
-    if (mx) {
+    if (mx && mixed_head_planes() && d <= 4096) {
+      launch_layernorm_split(c, x, n, d, m.lnfw, m.lnfb, static_cast<bf16*>(hf), gather + r0);
+      gemm_tc_planes(c, static_cast<bf16*>(hf), 2 * d, static_cast<const bf16*>(m.tok), d, n, V, d, Epi::kLse, nullptr,
+                     0, &e);
+    } else if (mx) {
       launch_layernorm<float>(c, x, n, d, m.lnfw, m.lnfb, static_cast<float*>(hf), gather + r0, nullptr, nullptr);
       gemm_mixed(c, static_cast<float*>(hf), d, static_cast<const bf16*>(m.tok), d, n, V, d, Epi::kLse, nullptr, 0, &e);
     } else {

@@ -176,3 +176,45 @@ def test_attention_prefill_vs_torch(ctx, DH, H, lens, path):
         o += T
     err = (out.float() - ref).abs()
     assert err.max().item() < 2e-2, f"max abs err {err.max().item():.3e}"
+
+
+@pytest.mark.parametrize("M,N,K", [(300, 2304, 768), (2048, 768, 3072), (129, 3072, 768), (64, 768, 768),
+                                   (1000, 1000, 256)])
+@pytest.mark.parametrize("epi", [2, 3, 6])
+def test_gemm_planes_vs_torch(ctx, M, N, K, epi):
+    """Mixed mode with the activation as hi | lo bf16 planes (TMA'd, two MMAs per
+    k-step; M <= 128 takes the decode kernel): fp32-grade against fp64 products."""
+    import torch
+    from paper_2405_01481_b200 import ppoexp as px
+    f = px.lib().ppoexp_testing_gemm_planes
+    f.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_int32, C.c_void_p,
+                  C.c_int64]
+    f.restype = C.c_int32
+    g = torch.Generator(device="cuda").manual_seed(M + N + K + epi)
+    A = torch.randn(M, K, generator=g, device="cuda")
+    hi = A.to(torch.bfloat16)
+    lo = (A - hi.float()).to(torch.bfloat16)
+    planes = torch.cat([hi, lo], dim=1).contiguous()
+    W = (torch.randn(N, K, generator=g, device="cuda") * 0.05).to(torch.bfloat16)
+    ref = (hi.double() + lo.double()) @ W.double().T
+    if epi == 6:
+        Cm = torch.zeros(M, 2 * N, dtype=torch.bfloat16, device="cuda")
+        ldc = 2 * N
+    else:
+        Cm = torch.randn(M, N, generator=g, device="cuda") if epi == 2 else torch.zeros(M, N, device="cuda")
+        ldc = N
+    base = Cm.double().clone()
+    torch.cuda.synchronize()
+    px._check(f(ctx.h, planes.data_ptr(), W.data_ptr(), M, N, K, epi, Cm.data_ptr(), ldc))
+    mag = (hi.double().abs() + lo.double().abs()) @ W.double().abs().T
+    if epi == 6:
+        ref = torch.nn.functional.gelu(ref, approximate="tanh")
+        got = Cm[:, :N].double() + Cm[:, N:].double()
+        mag = mag * 1.2
+    else:
+        got = Cm.double()
+        if epi == 2:
+            ref = ref + base
+    err = (got - ref).abs()
+    bound = 2.0 ** -16 * mag + 2e-7 * (1 + ref.abs())
+    assert (err <= bound).all(), f"max abs err {err.max().item():.3e}, max err/bound {(err / bound).max().item():.3f}"
