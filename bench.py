@@ -297,6 +297,43 @@ def cupti_breakdown(step_fn):
     return out
 
 
+def k9_roofline(ctx, rows, V, dev, launches=10):
+    """The standalone K9 log-softmax + gather kernel (logprob_shaping.cu) streaming
+    an fp32 logits matrix of the scoring shape from HBM (the F32 path and
+    PPOEXP_SCORING=logits; the default scoring path never writes logits), timed
+    with CUDA events on the library stream: algorithmic bytes = rows * V * 4 + rows * 20."""
+    import ctypes as C
+    import torch
+    from paper_2405_01481_b200 import ppoexp as px
+    f = px.lib().ppoexp_testing_lm_head_logprobs
+    f.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_void_p,
+                  C.c_void_p, C.c_int32]
+    f.restype = C.c_int32
+    ld = (V + 63) // 64 * 64
+    g = torch.Generator(device=dev).manual_seed(5)
+    L = torch.randn(rows, ld, generator=g, device=dev)
+    tgt = torch.randint(0, V, (rows,), generator=g, device=dev, dtype=torch.int32)
+    out = torch.zeros(rows, dtype=torch.float64, device=dev)
+    torch.cuda.synchronize()
+    px._check(f(ctx.h, L.data_ptr(), None, rows, V, 0, ld, tgt.data_ptr(), out.data_ptr(), 2))  # warm
+    ctx.profile_filter(["logprob_gather"])
+    ctx.profile(True)
+    for _ in range(launches):
+        px._check(f(ctx.h, L.data_ptr(), None, rows, V, 0, ld, tgt.data_ptr(), out.data_ptr(), 2))
+    q = ctx.profile_query("logprob_gather")
+    ctx.profile(False)
+    ctx.profile_filter(None)
+    del L, tgt, out
+    torch.cuda.empty_cache()
+    per_launch_ms = q["ms"] / max(1, q["launches"])
+    bytes_ = rows * V * 4.0 + rows * 20.0
+    return {"kernel": "logprob_gather (K9)", "bound": "hbm", "achieved": bytes_ / per_launch_ms / 1e6,
+            "unit": "GB/s", "per_launch_us": per_launch_ms * 1e3, "rows": rows, "vocab": V,
+            "algorithmic_bytes_per_launch": bytes_,
+            "timing": "CUDA events on the library stream around each of 10 launches over an fp32 [rows, V] logits "
+                      "matrix (3.3 GB at C2: larger than L2), after the timed region"}
+
+
 def decode_bytes(cfg_t, B, act_bytes=2):
     """Algorithmic HBM bytes of one decode step averaged over the generation
     (SURVEY.md §8d): bf16 weights of every layer + the tied LM head, plus the
@@ -538,6 +575,18 @@ def bench_mode(args, dtype, primary):
                 ach = db["decode_attention"] / db["decode_attention_launches"] / (a_["us"] / a_["launches"]) / 1e3
                 line["roofline_decode_attention"] = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
                                                      "frac": ach / hbm}
+        if primary and args.profile_classes:
+            try:
+                k9 = k9_roofline(ctx, B * N, V, dev)
+                k9["peak"] = hbm
+                k9["frac"] = k9["achieved"] / hbm
+                k9["peak_note"] = ("peak = MEASURED_PEAKS.json copy bandwidth (read + write traffic); this kernel "
+                                   "only reads, and a pure read stream can run above the copy figure (B200 HBM3e "
+                                   "spec 8 TB/s: frac_of_spec below)")
+                k9["frac_of_spec"] = k9["achieved"] / 8000.0
+                line["roofline_logprob_gather"] = k9
+            except Exception as e:  # the measurement is informative only
+                _dbg("k9 failed", e)
         if not args.no_cpu_baseline and world == 1 and primary:
             try:
                 threads = host_threads()
