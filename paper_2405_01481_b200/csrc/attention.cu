@@ -10,9 +10,15 @@
 //    src/model.cpp:305-308), then attends over positions 0..pos
 //    (src/model.cpp:313-333): scale by 1/sqrt(dh) before the max, exp(s-max),
 //    normalise, weighted V sum.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <cfloat>
 #include <cstdio>
 #include <cstdlib>
+#include <map>
+#include <mutex>
+#include <tuple>
 
 #include "kernels.hpp"
 
@@ -108,14 +114,23 @@ __device__ __forceinline__ void cp_async16_dec(void* dst, const void* src) {
                : "memory");
 }
 
+__device__ __forceinline__ uint32_t dec_su32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
 // NS: K/V tile stages per warp, TT: tokens per tile.  (NS, TT) = (2, 16) keeps the
 // (1, 32) footprint (32 KB per CTA for dh 64 bf16: 6 CTAs/SM) but double-buffers.
+// Rows of a multiple of 128 bytes arrive by TMA: the pool is a 2-D tensor
+// [rows, DH] (one row = one (layer, page, K|V, head, slot)), boxes of 128 bytes x
+// TT rows with the 128B swizzle, one elected lane per warp issuing them against
+// a per-warp mbarrier; other row sizes use cp.async.
 template <class T, int DH, int NS, int TT>
 __global__ void __launch_bounds__(128, 6) attn_decode_kernel(const T* __restrict__ qkv, const int32_t* __restrict__ pos,
                                                           const int32_t* __restrict__ done,
                                                           const int32_t* __restrict__ block_table, int layer,
                                                           KvGeom g, T* __restrict__ kv, T* __restrict__ out,
-                                                          unsigned long long* dbg, bf16* __restrict__ split_out) {
+                                                          unsigned long long* dbg, bf16* __restrict__ split_out,
+                                                          const __grid_constant__ CUtensorMap tmkv) {
   // debug (PPOEXP_ATTN_TRACE): CTA (0, 0) thread 0 stage clocks
   auto stamp = [&](int k) {
     if (dbg && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) dbg[k] = clock64();
@@ -133,14 +148,17 @@ __global__ void __launch_bounds__(128, 6) attn_decode_kernel(const T* __restrict
   // XOR-swizzled by (row & 7): conflict-free for lane-per-token K reads and
   // per-row V reads, and 32 KB of tiles per CTA (6 CTAs/SM: one wave of 768).
   // Other row sizes keep a 16-byte pad.
+  constexpr bool TMAK = ROWB % 128 == 0;      // TMA-fed tiles: dense [box][TT][128 B], 128B swizzle
   constexpr bool SWZ = ROWB == 128;
-  constexpr int LDB = SWZ ? ROWB : ROWB + 16;  // smem row stride (bytes)
+  constexpr int LDB = (SWZ || TMAK) ? ROWB : ROWB + 16;  // smem bytes per row (per tile: TT * LDB)
+  constexpr int NBOX = ROWB / 128;
   constexpr int CPR = ROWB / 16;              // 16-byte chunks per row
   constexpr int EPT = DH;                     // lane-per-token: whole row
   constexpr int DPL = DH >= 32 ? DH / 32 : 1; // dims per lane (P·V)
   constexpr int DLANES = DH / DPL;
   constexpr bool HALF = TT == 16 && sizeof(T) == 4 && CPR % 2 == 0;  // fp32 KV: 16-token tiles, half rows per lane
-  extern __shared__ __align__(16) uint8_t smem_dec[];
+  extern __shared__ __align__(1024) uint8_t smem_dec[];
+  __shared__ __align__(8) uint64_t tbar[NW][NS];  // TMA completion per warp and stage
   __shared__ float sm_m[NW], sm_l[NW];
   __shared__ float sm_acc[NW][DH];
   __shared__ __align__(16) float sm_q[DH];  // the query (lane-uniform reads: broadcast)
@@ -155,11 +173,52 @@ __global__ void __launch_bounds__(128, 6) attn_decode_kernel(const T* __restrict
     return kv + ((((int64_t)layer * g.n_pages + page) * 2 + which) * g.H + h) * PS * DH + (t % PS) * DH;
   };
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
-  // per-warp tiles: [stage][K|V][TT rows][LDB bytes]
-  uint8_t* wsm = smem_dec + size_t(w) * NS * 2 * TT * LDB;
+  // per-warp tiles: [stage][K|V][TT rows][LDB bytes] (TMA: 1024-byte aligned swizzle atoms)
+  uint8_t* sbase = smem_dec;
+  if constexpr (TMAK)
+    sbase = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_dec) + 1023) & ~uintptr_t(1023));
+  uint8_t* wsm = sbase + size_t(w) * NS * 2 * TT * LDB;
   auto tile_ptr = [&](int buf, int which) { return wsm + (buf * 2 + which) * TT * LDB; };
-  auto chunk = [](int r, int c) { return r * LDB + ((SWZ ? (c ^ (r & 7)) : c) << 4); };
+  auto chunk = [](int r, int c) {
+    if constexpr (TMAK) return (c >> 3) * (TT * 128) + r * 128 + (((c & 7) ^ (r & 7)) << 4);
+    return r * LDB + ((SWZ ? (c ^ (r & 7)) : c) << 4);
+  };
+  if constexpr (TMAK) {
+    if (lane == 0) {
+      for (int s = 0; s < NS; ++s)
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(dec_su32(&tbar[w][s])));
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+  }
+  uint32_t tphase = 0;  // bit s: parity of the next completion of stage s
   auto issue = [&](int64_t t0, int buf) {
+    if constexpr (TMAK) {
+      if (lane == 0) {
+        const int64_t page = bt[t0 / PS];
+        const int64_t rk = ((((int64_t)layer * g.n_pages + page) * 2 + 0) * g.H + h) * PS + (t0 % PS);
+        const int64_t rv = rk + g.H * PS;  // the V rows of the same page / head
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(dec_su32(&tbar[w][buf])),
+                     "r"(2 * TT * ROWB)
+                     : "memory");
+#pragma unroll
+        for (int bx = 0; bx < NBOX; ++bx) {
+          asm volatile(
+              "cp.async.bulk.tensor.2d.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+                  dec_su32(tile_ptr(buf, 0) + bx * TT * 128)),
+              "l"(reinterpret_cast<uint64_t>(&tmkv)), "r"(dec_su32(&tbar[w][buf])), "r"(bx * (128 / int(sizeof(T)))),
+              "r"(int(rk))
+              : "memory");
+          asm volatile(
+              "cp.async.bulk.tensor.2d.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+                  dec_su32(tile_ptr(buf, 1) + bx * TT * 128)),
+              "l"(reinterpret_cast<uint64_t>(&tmkv)), "r"(dec_su32(&tbar[w][buf])), "r"(bx * (128 / int(sizeof(T)))),
+              "r"(int(rv))
+              : "memory");
+        }
+      }
+      return;
+    }
     const int64_t n = (ctx - t0) < TT ? (ctx - t0) : TT;
     const T* k0 = base(t0, 0);  // contiguous within the page
     const T* v0 = base(t0, 1);
@@ -197,6 +256,8 @@ __global__ void __launch_bounds__(128, 6) attn_decode_kernel(const T* __restrict
     base(p, 1)[i] = row[2 * d + h * DH + i];
   }
   for (int i = tid; i < DH; i += 128) sm_q[i] = to_f(row[h * DH + i]);
+  // the appended row is read back by TMA (the async proxy) below
+  if constexpr (TMAK) asm volatile("fence.proxy.async.global;" ::: "memory");
   __syncthreads();  // the appended row and the query are visible to the whole CTA
   stamp(3);
   bool nxt_issued = early1;          // tile it+1 already committed
@@ -209,7 +270,19 @@ __global__ void __launch_bounds__(128, 6) attn_decode_kernel(const T* __restrict
   for (; t0 < ctx; t0 += int64_t(NW) * TT, ++it) {
     const int64_t tn = t0 + int64_t(NW) * TT;
     const int buf = NS == 2 ? (it & 1) : 0;
-    if (NS == 2) {
+    if constexpr (TMAK) {
+      if (NS == 2 && !nxt_issued && tn < ctx) {
+        issue(tn, buf ^ 1);
+        nxt_issued = true;
+      }
+      const uint32_t par = (tphase >> buf) & 1u;
+      asm volatile(
+          "{\n\t.reg .pred P1;\nTW_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t@!P1 bra TW_%=;\n\t}" ::"r"(
+              dec_su32(&tbar[w][buf])),
+          "r"(par)
+          : "memory");
+      tphase ^= 1u << buf;
+    } else if (NS == 2) {
       if (!nxt_issued && tn < ctx) {
         issue(tn, buf ^ 1);
         nxt_issued = true;
@@ -328,13 +401,50 @@ void prefill_impl(Ctx& c, const T* qkv, const int64_t* seq_offsets, int64_t B, i
   c.launch("attention_prefill", 0, flops, [&] { launch_kernel(c, k, dim3(grid), dim3(64 * TPQ), smem, 1, qkv, seq_offsets, H, out); });
 }
 
+// 2-D view of the paged KV pool for TMA: rows of DH elements, boxes of 128 bytes
+// x TT rows, 128B swizzle (cached per pool / shape).
+template <class T>
+CUtensorMap kv_map(const T* kv, const KvGeom& g, int tt) {
+  static std::mutex mu;
+  static std::map<std::tuple<const void*, int64_t, int64_t, int>, CUtensorMap> cache;
+  const int64_t rows = g.n_layers * g.n_pages * 2 * g.H * g.page_size;
+  std::lock_guard<std::mutex> lk(mu);
+  const auto key = std::make_tuple(static_cast<const void*>(kv), rows, g.DH, tt);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }();
+  if (!fn) throw Error(6, "cuda: cuTensorMapEncodeTiled unavailable");
+  if (rows >= (int64_t(1) << 31)) throw ContractError("decode attention: KV pool above 2^31 rows");
+  CUtensorMap m;
+  const cuuint64_t dims[2] = {cuuint64_t(g.DH), cuuint64_t(rows)};
+  const cuuint64_t strides[1] = {cuuint64_t(g.DH * sizeof(T))};
+  const cuuint32_t box[2] = {cuuint32_t(128 / sizeof(T)), cuuint32_t(tt)};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = fn(&m, sizeof(T) == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                        const_cast<T*>(kv), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Error(6, "cuda: cuTensorMapEncodeTiled (KV pool) failed (" + std::to_string(int(r)) + ")");
+  cache.emplace(key, m);
+  return m;
+}
+
 template <class T, int DH, int NS, int TT>
 void decode_launch(Ctx& c, const T* qkv, int64_t B, const int32_t* pos, const int32_t* done,
                    const int32_t* block_table, int layer, const KvGeom& g, T* kv, T* out, double bytes,
                    bf16* split_out) {
   auto k = attn_decode_kernel<T, DH, NS, TT>;
-  const size_t row = DH * sizeof(T) == 128 ? 128 : DH * sizeof(T) + 16;  // kernel's LDB
-  const size_t smem = size_t(4) * NS * 2 * TT * row;                     // 4 warps x NS x (K, V) x TT rows
+  constexpr bool tmak = (DH * sizeof(T)) % 128 == 0;
+  const size_t row = tmak ? DH * sizeof(T) : (DH * sizeof(T) == 128 ? 128 : DH * sizeof(T) + 16);  // kernel's LDB
+  const size_t smem = size_t(4) * NS * 2 * TT * row + (tmak ? 1024 : 0);  // 4 warps x NS x (K, V) x TT rows
+  CUtensorMap tm{};
+  if (tmak) tm = kv_map(kv, g, TT);
   static bool attr = false;
   if (!attr) {
     PPOEXP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
@@ -351,7 +461,7 @@ void decode_launch(Ctx& c, const T* qkv, int64_t B, const int32_t* pos, const in
   if (getenv("PPOEXP_ATTN_TRACE"))  // debug: stamps of the last launch
     dbg = static_cast<unsigned long long*>(c.workspace("attn.trace", 16 * 8));
   c.launch("decode_attention", bytes, 0, [&] { launch_kernel(c, k, grid, dim3(128), smem, 1, qkv, pos, done,
-                                                              block_table, layer, g, kv, out, dbg, split_out); });
+                                                              block_table, layer, g, kv, out, dbg, split_out, tm); });
 }
 
 template <class T, int DH>
