@@ -23,7 +23,26 @@ namespace {
 constexpr int kUnitsPerGraph = 8;
 }
 
-Engine::Engine(Model* model, const ppoexp_engine_options* o) : m(model), c(model->ctx) {
+namespace {
+// Issue work of one lane: its stream and workspace namespace for the scope.
+struct LaneScope {
+  Ctx* c;
+  cudaStream_t s0;
+  std::string p0;
+  LaneScope(Ctx* cc, const Engine& e) : c(cc), s0(cc->stream), p0(cc->ws_prefix) {
+    if (e.lane_stream) {
+      c->stream = e.lane_stream;
+      c->ws_prefix = e.lane_prefix;
+    }
+  }
+  ~LaneScope() {
+    c->stream = s0;
+    c->ws_prefix = p0;
+  }
+};
+}  // namespace
+
+Engine::Engine(Model* model, const ppoexp_engine_options* o, Engine* owner_) : m(model), c(model->ctx), owner(owner_) {
   if (o) opts = *o;
   if (opts.max_batch <= 0) opts.max_batch = 256;
   if (opts.page_size <= 0) opts.page_size = 64;
@@ -41,7 +60,13 @@ Engine::Engine(Model* model, const ppoexp_engine_options* o) : m(model), c(model
   if (m->mixed() && opts.max_batch > 256)
     throw ContractError("engine: mixed mode decodes at most 256 sequences per step (max_batch <= 256)");
   const size_t ts = m->asize();  // activation / KV element
-  kv.ensure(size_t(geom.n_layers) * geom.n_pages * 2 * geom.H * geom.page_size * geom.DH * ts);
+  if (owner) {
+    geom.n_pages = owner->geom.n_pages;  // lanes decode into the owner's pool
+    kvp = owner->kvp;
+  } else {
+    kv.ensure(size_t(geom.n_layers) * geom.n_pages * 2 * geom.H * geom.page_size * geom.DH * ts);
+    kvp = kv.ptr;
+  }
   const int64_t mb = opts.max_batch, d = cfg.d_model, f = cfg.d_ff;
   auto al = [](size_t x) { return (x + 255) / 256 * 256; };
   size_t sbytes = 0;
@@ -112,11 +137,32 @@ Engine::Engine(Model* model, const ppoexp_engine_options* o) : m(model), c(model
   PPOEXP_CUDA(cudaEventCreateWithFlags(&poll_ev[1], cudaEventDisableTiming));
   PPOEXP_CUDA(cudaEventCreate(&t0));
   PPOEXP_CUDA(cudaEventCreate(&t1));
+  PPOEXP_CUDA(cudaEventCreateWithFlags(&lane_ev, cudaEventDisableTiming));
+  if (owner) {
+    PPOEXP_CUDA(cudaStreamCreateWithFlags(&lane_stream, cudaStreamNonBlocking));
+  } else if (m->dtype != PPOEXP_F32) {
+    // two decode lanes by default for the tensor-core modes (PPOEXP_LANES=1 disables)
+    const char* le = getenv("PPOEXP_LANES");
+    n_lanes = le ? std::max(1, std::min(2, atoi(le))) : 2;
+    if (const char* lm = getenv("PPOEXP_LANE_MIN_B")) lane_min_b = std::max<int64_t>(2, atoll(lm));
+    if (n_lanes == 2 && opts.max_batch >= lane_min_b) {
+      ppoexp_engine_options lo = opts;
+      lo.max_batch = ceil_div(opts.max_batch, 2);
+      for (int i = 0; i < 2; ++i) {
+        lanes[i] = std::make_unique<Engine>(m, &lo, this);
+        lanes[i]->lane_prefix = "lane" + std::to_string(i) + ".";
+      }
+    } else {
+      n_lanes = 1;
+    }
+  }
 }
 
 Engine::~Engine() {
   DeviceGuard g(c->device, true);
-  cudaStreamSynchronize(c->stream);
+  lanes[0].reset();
+  lanes[1].reset();
+  cudaStreamSynchronize(lane_stream ? lane_stream : c->stream);
   for (auto& [k, gs] : graphs)
     for (int j = 0; j < 2; ++j) {
       if (gs.exec[j]) cudaGraphExecDestroy(gs.exec[j]);
@@ -130,6 +176,8 @@ Engine::~Engine() {
   cudaEventDestroy(poll_ev[1]);
   cudaEventDestroy(t0);
   cudaEventDestroy(t1);
+  cudaEventDestroy(lane_ev);
+  if (lane_stream) cudaStreamDestroy(lane_stream);
 }
 
 SamplerState Engine::sampler_state() const {
@@ -181,7 +229,7 @@ void Engine::decode_unit(int64_t B, int64_t unit) {
         const LnIn l1{x, d, st(2 * l), ly.ln1w, ly.ln1b, int(d)};
         gemm_decode_fused(cc, nullptr, d, static_cast<const T*>(ly.wqkv), d, B, 3 * d, d, Epi::kStore, q3, 3 * d, &l1,
                           nullptr);
-        launch_attention_decode<T>(cc, q3, B, pos, done, block_table, int(l), geom, static_cast<T*>(kv.ptr), at, 0.0);
+        launch_attention_decode<T>(cc, q3, B, pos, done, block_table, int(l), geom, static_cast<T*>(kvp), at, 0.0);
         const RowStats so2{st(2 * l + 1), stat_ovf};
         gemm_decode_fused(cc, at, d, static_cast<const T*>(ly.wo), d, B, d, d, Epi::kAddResidual, x, d, nullptr, &so2);
         const LnIn l2{x, d, st(2 * l + 1), ly.ln2w, ly.ln2b, int(d)};
@@ -208,7 +256,7 @@ void Engine::decode_unit(int64_t B, int64_t unit) {
     const Layer& ly = m->layers[l];
     if (l > 0 || !fused_head) launch_layernorm<T>(cc, x, B, d, ly.ln1w, ly.ln1b, hh, nullptr, nullptr, nullptr);
     gemm<T>(cc, hh, d, static_cast<const T*>(ly.wqkv), d, B, 3 * d, d, Epi::kStore, q3, 3 * d);
-    launch_attention_decode<T>(cc, q3, B, pos, done, block_table, int(l), geom, static_cast<T*>(kv.ptr), at, 0.0);
+    launch_attention_decode<T>(cc, q3, B, pos, done, block_table, int(l), geom, static_cast<T*>(kvp), at, 0.0);
     gemm<T>(cc, at, d, static_cast<const T*>(ly.wo), d, B, d, d, Epi::kAddResidual, x, d);
     launch_layernorm<T>(cc, x, B, d, ly.ln2w, ly.ln2b, hh, nullptr, nullptr, nullptr);
     gemm<T>(cc, hh, d, static_cast<const T*>(ly.wup), d, B, f, d, Epi::kGelu, uu, f);
@@ -244,7 +292,7 @@ void Engine::decode_unit_mixed(int64_t B, int64_t unit) {
       launch_layernorm_split(cc, x, B, d, ly.ln1w, ly.ln1b, hp);
       gemm_decode_planes(cc, hp, 2 * d, static_cast<const bf16*>(ly.wqkv), d, B, 3 * d, d, Epi::kStoreF32, q3, 3 * d,
                          nullptr);
-      launch_attention_decode<float>(cc, q3, B, pos, done, block_table, int(l), geom, static_cast<float*>(kv.ptr), at,
+      launch_attention_decode<float>(cc, q3, B, pos, done, block_table, int(l), geom, static_cast<float*>(kvp), at,
                                      0.0, ap);
       gemm_decode_planes(cc, ap, 2 * d, static_cast<const bf16*>(ly.wo), d, B, d, d, Epi::kAddResidual, x, d, nullptr);
       launch_layernorm_split(cc, x, B, d, ly.ln2w, ly.ln2b, hp);
@@ -276,7 +324,7 @@ void Engine::decode_unit_mixed(int64_t B, int64_t unit) {
     if (mixed_oplanes) {  // O / down operands as bf16 planes from the attention / GELU epilogues
       bf16* ap = static_cast<bf16*>(att);
       bf16* upp = static_cast<bf16*>(up);
-      launch_attention_decode<float>(cc, q3, B, pos, done, block_table, int(l), geom, static_cast<float*>(kv.ptr), at,
+      launch_attention_decode<float>(cc, q3, B, pos, done, block_table, int(l), geom, static_cast<float*>(kvp), at,
                                      0.0, ap);
       gemm_decode_planes(cc, ap, 2 * d, static_cast<const bf16*>(ly.wo), d, B, d, d, Epi::kAddResidual, x, d, &so2);
       gemm_decode_mixed(cc, nullptr, d, static_cast<const bf16*>(ly.wup), d, B, f, d, Epi::kGeluSplit, upp, 2 * f, &l2,
@@ -285,7 +333,7 @@ void Engine::decode_unit_mixed(int64_t B, int64_t unit) {
                          l + 1 < L ? &so1 : nullptr);
       continue;
     }
-    launch_attention_decode<float>(cc, q3, B, pos, done, block_table, int(l), geom, static_cast<float*>(kv.ptr), at,
+    launch_attention_decode<float>(cc, q3, B, pos, done, block_table, int(l), geom, static_cast<float*>(kvp), at,
                                    0.0);
     gemm_decode_mixed(cc, at, d, static_cast<const bf16*>(ly.wo), d, B, d, d, Epi::kAddResidual, x, d, nullptr, &so2);
     gemm_decode_mixed(cc, nullptr, d, static_cast<const bf16*>(ly.wup), d, B, f, d, Epi::kGeluF32, uu, f, &l2, nullptr);
@@ -307,13 +355,14 @@ void Engine::run_unit(int64_t B, int64_t unit) {
     decode_unit<bf16>(B, unit);
 }
 
-Engine::GraphSet& Engine::graph_for(int64_t B) {
+Engine::GraphSet& Engine::graph_for(int64_t B, int units) {
   std::string sig;
   if (c->profiling) {
     sig = "prof:";
     for (const auto& k : c->profile_filter) sig += k + ",";
   }
-  auto it = graphs.find(B);
+  const int64_t key = B * 16 + units;
+  auto it = graphs.find(key);
   if (it != graphs.end() && it->second.prof_sig == sig) return it->second;
   if (it != graphs.end()) {
     for (int j = 0; j < 2; ++j) {
@@ -325,10 +374,10 @@ Engine::GraphSet& Engine::graph_for(int64_t B) {
     }
     graphs.erase(it);
   }
-  GraphSet& gs = graphs[B];
+  GraphSet& gs = graphs[key];
   gs.profiled = c->profiling;
   gs.prof_sig = sig;
-  gs.units = kUnitsPerGraph;
+  gs.units = units;
   for (int j = 0; j < 2; ++j) {
     cudaGraph_t graph;
     PPOEXP_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
@@ -458,10 +507,66 @@ void Engine::generate(int64_t B, const int32_t* prompts, const int64_t* offsets,
   c->harvest();
 }
 
+int64_t Engine::chunk_pages(int64_t B, const std::vector<int64_t>& off_all, int64_t b0,
+                            const std::vector<int64_t>& mx_all) const {
+  const int64_t S = m->cfg.max_seq_len, PS = geom.page_size;
+  int64_t pages = 0;
+  for (int64_t b = 0; b < B; ++b) {
+    const int64_t P = off_all[b0 + b + 1] - off_all[b0 + b];
+    pages += ceil_div(P + std::min<int64_t>(mx_all[b0 + b], S - std::min<int64_t>(P, S)), PS);
+  }
+  return pages;
+}
+
 void Engine::run_chunk(int64_t B, const int32_t* prompts, const std::vector<int64_t>& off_all, int64_t b0,
                        const std::vector<int64_t>& mx_all, const ppoexp_sampling* sp_all,
                        const std::vector<uint64_t>& seeds_all, int64_t out_stride, int32_t* out_tokens,
                        double* out_logprobs, int64_t* out_lengths, int where, int where_out, int where_tokens) {
+  (void)where;
+  if (n_lanes < 2 || B < lane_min_b) {
+    Run run;
+    chunk_begin(run, B, prompts, off_all, b0, mx_all, sp_all, seeds_all, out_stride, out_tokens, out_logprobs,
+                out_lengths, where_out, where_tokens, 0);
+    while (run.active) {
+      chunk_launch(run);
+      chunk_poll(run);
+    }
+    chunk_finish(run);
+    return;
+  }
+  // two lanes: the first half of the chunk on lane 0, the rest on lane 1, each
+  // on its own stream after the work already queued on the context stream
+  const int64_t h0 = (B + 1) / 2;
+  const int64_t p0 = lanes[0]->chunk_pages(h0, off_all, b0, mx_all);
+  if (p0 + lanes[1]->chunk_pages(B - h0, off_all, b0 + h0, mx_all) > geom.n_pages)
+    throw ContractError("engine: KV pool too small for the batch; raise max_total_tokens");
+  PPOEXP_CUDA(cudaEventRecord(lane_ev, c->stream));
+  for (auto& ln : lanes) PPOEXP_CUDA(cudaStreamWaitEvent(ln->lane_stream, lane_ev, 0));
+  Run r0, r1;
+  lanes[0]->chunk_begin(r0, h0, prompts, off_all, b0, mx_all, sp_all, seeds_all, out_stride, out_tokens, out_logprobs,
+                        out_lengths, where_out, where_tokens, 0);
+  lanes[1]->chunk_begin(r1, B - h0, prompts, off_all, b0 + h0, mx_all, sp_all, seeds_all, out_stride, out_tokens,
+                        out_logprobs, out_lengths, where_out, where_tokens, p0);
+  while (r0.active || r1.active) {
+    lanes[0]->chunk_launch(r0);
+    lanes[1]->chunk_launch(r1);
+    lanes[0]->chunk_poll(r0);
+    lanes[1]->chunk_poll(r1);
+  }
+  lanes[0]->chunk_finish(r0);
+  lanes[1]->chunk_finish(r1);
+  for (auto& ln : lanes) {
+    PPOEXP_CUDA(cudaEventRecord(ln->lane_ev, ln->lane_stream));
+    PPOEXP_CUDA(cudaStreamWaitEvent(c->stream, ln->lane_ev, 0));
+  }
+}
+
+void Engine::chunk_begin(Run& run, int64_t B, const int32_t* prompts, const std::vector<int64_t>& off_all, int64_t b0,
+                         const std::vector<int64_t>& mx_all, const ppoexp_sampling* sp_all,
+                         const std::vector<uint64_t>& seeds_all, int64_t out_stride, int32_t* out_tokens,
+                         double* out_logprobs, int64_t* out_lengths, int where_out, int where_tokens,
+                         int64_t page_base) {
+  LaneScope ls(c, *this);
   Ctx& cc = *c;
   const auto& cfg = m->cfg;
   const int64_t S = cfg.max_seq_len, PS = geom.page_size, d = m->d();
@@ -473,12 +578,12 @@ void Engine::run_chunk(int64_t B, const int32_t* prompts, const std::vector<int6
     max_budget = std::max(max_budget, bud[b]);
     pages += ceil_div(P[b] + bud[b], PS);
   }
-  if (pages > geom.n_pages)
+  if (page_base + pages > geom.n_pages)
     throw ContractError("engine: KV pool too small (" + std::to_string(pages) + " pages needed, " +
                         std::to_string(geom.n_pages) + " available); raise max_total_tokens");
   // block tables: contiguous page runs per sequence
   std::vector<int32_t> bt(B * geom.max_pages_per_seq, 0);
-  int64_t next_page = 0;
+  int64_t next_page = page_base;
   for (int64_t b = 0; b < B; ++b) {
     const int64_t np = ceil_div(P[b] + bud[b], PS);
     for (int64_t k = 0; k < np; ++k) bt[b * geom.max_pages_per_seq + k] = int32_t(next_page++);
@@ -538,7 +643,7 @@ void Engine::run_chunk(int64_t B, const int32_t* prompts, const std::vector<int6
   copy_in(cc, pk.tokens_d, prompts + off_all[b0], M * 4, where_tokens);
   pack_metadata(cc, pk, "gen");  // synchronises: the pinned staging above is free again
   // prefill → last-position logits → first sample
-  KvTarget kt{block_table, geom, kv.ptr};
+  KvTarget kt{block_table, geom, kvp};
   float* xr = forward_layers(*m, pk, &kt);
   if (m->mixed()) {
     launch_layernorm<float>(cc, xr, B, d, m->lnfw, m->lnfb, static_cast<float*>(h), last_rows, nullptr, nullptr);
@@ -557,51 +662,82 @@ void Engine::run_chunk(int64_t B, const int32_t* prompts, const std::vector<int6
   // decode: units 1 .. max_budget-1
   cur_P = P;
   cur_len = bud;  // upper bound until the true lengths are known
-  const int64_t units = max_budget - 1;
-  std::vector<std::pair<int, int64_t>> pending;  // (graph slot, unit0) awaiting harvest
-  if (units > 0) {
+  run = Run{};
+  run.B = B;
+  run.b0 = b0;
+  run.units = max_budget - 1;
+  run.out_stride = out_stride;
+  run.out_tokens = out_tokens;
+  run.out_logprobs = out_logprobs;
+  run.out_lengths = out_lengths;
+  run.where_out = where_out;
+  if (run.units > 0) {
+    run.R = ceil_div(run.units, int64_t(kUnitsPerGraph));
     if (opts.use_graphs) {
-      GraphSet& gs = graph_for(B);
-      const int64_t R = ceil_div(units, gs.units);
-      int64_t r = 0;
-      bool stop = false;
-      for (; r < R && !stop; ++r) {
-        const int j = int(r & 1);
-        PPOEXP_CUDA(cudaGraphLaunch(gs.exec[j], cc.stream));
-        cc.launches += gs.nodes;
-        PPOEXP_CUDA(cudaMemcpyAsync(host_flags + j, n_active, 4, cudaMemcpyDeviceToHost, cc.stream));
-        PPOEXP_CUDA(cudaEventRecord(poll_ev[j], cc.stream));
-        pending.push_back({j, 1 + r * gs.units});
-        if (r >= 1) {
-          PPOEXP_CUDA(cudaEventSynchronize(poll_ev[1 - j]));
-          if (cc.profiling) {
-            // events of replay r-1 must be read before that graph runs again
-            auto [sj, u0] = pending.front();
-            pending.erase(pending.begin());
-            prof_replays.push_back({gs.events[sj], u0, gs.units});
-            snapshot_events(prof_replays.back());
-          }
-          if (host_flags[1 - j] == 0) stop = true;
-        }
-      }
-      PPOEXP_CUDA(cudaStreamSynchronize(cc.stream));
-      if (cc.profiling) {
-        for (auto& [sj, u0] : pending) {
-          prof_replays.push_back({gs.events[sj], u0, gs.units});
-          snapshot_events(prof_replays.back());
-        }
-      }
-    } else {
-      for (int64_t u = 1; u <= units; ++u) {
-        run_unit(B, u);
-        if (u % kUnitsPerGraph == 0) {
-          PPOEXP_CUDA(cudaMemcpyAsync(host_flags, n_active, 4, cudaMemcpyDeviceToHost, cc.stream));
-          PPOEXP_CUDA(cudaStreamSynchronize(cc.stream));
-          if (host_flags[0] == 0) break;
-        }
-      }
+      run.gs = &graph_for(B, kUnitsPerGraph);
+      // the last replay runs exactly the remaining units (no decode steps past the budget)
+      const int rem = int(run.units % kUnitsPerGraph);
+      run.tail = rem ? &graph_for(B, rem) : run.gs;
+    }
+    run.active = true;
+  }
+}
+
+void Engine::chunk_launch(Run& run) {
+  if (!run.active) return;
+  LaneScope ls(c, *this);
+  Ctx& cc = *c;
+  const int j = int(run.r & 1);
+  if (run.gs) {
+    GraphSet* g = run.r + 1 == run.R ? run.tail : run.gs;
+    PPOEXP_CUDA(cudaGraphLaunch(g->exec[j], cc.stream));
+    cc.launches += g->nodes;
+    run.pending.push_back({g, j, 1 + run.r * kUnitsPerGraph});
+  } else {
+    for (int64_t u = 1 + run.r * kUnitsPerGraph; u <= std::min(run.units, (run.r + 1) * kUnitsPerGraph); ++u)
+      run_unit(run.B, u);
+  }
+  PPOEXP_CUDA(cudaMemcpyAsync(host_flags + j, n_active, 4, cudaMemcpyDeviceToHost, cc.stream));
+  PPOEXP_CUDA(cudaEventRecord(poll_ev[j], cc.stream));
+}
+
+void Engine::chunk_poll(Run& run) {
+  if (!run.active) return;
+  LaneScope ls(c, *this);
+  // the host stays one replay behind: replay r is queued while r-1's counter is read
+  if (run.r >= 1) {
+    const int k = int((run.r - 1) & 1);
+    PPOEXP_CUDA(cudaEventSynchronize(poll_ev[k]));
+    if (c->profiling && run.gs) {
+      // events of replay r-1 must be read before that graph runs again
+      auto [g, sj, u0] = run.pending.front();
+      run.pending.erase(run.pending.begin());
+      prof_replays.push_back({g->events[sj], u0, g->units});
+      snapshot_events(prof_replays.back());
+    }
+    if (host_flags[k] == 0) run.stop = true;
+  }
+  ++run.r;
+  run.active = run.r < run.R && !run.stop;
+}
+
+void Engine::chunk_finish(Run& run) {
+  LaneScope ls(c, *this);
+  Ctx& cc = *c;
+  const int64_t B = run.B, b0 = run.b0, S = m->cfg.max_seq_len, out_stride = run.out_stride;
+  int32_t* out_tokens = run.out_tokens;
+  double* out_logprobs = run.out_logprobs;
+  int64_t* out_lengths = run.out_lengths;
+  const int where_out = run.where_out;
+  std::vector<int64_t>& lens_all = owner ? owner->last_lengths : last_lengths;
+  PPOEXP_CUDA(cudaStreamSynchronize(cc.stream));
+  if (cc.profiling && run.gs) {
+    for (auto& [g, sj, u0] : run.pending) {
+      prof_replays.push_back({g->events[sj], u0, g->units});
+      snapshot_events(prof_replays.back());
     }
   }
+  run.pending.clear();
   // outputs
   std::vector<int32_t> ng(B);
   PPOEXP_CUDA(cudaMemcpyAsync(ng.data(), n_gen, B * 4, cudaMemcpyDeviceToHost, cc.stream));
@@ -615,7 +751,7 @@ void Engine::run_chunk(int64_t B, const int32_t* prompts, const std::vector<int6
   }
   for (int64_t b = 0; b < B; ++b) {
     cur_len[b] = ng[b];
-    last_lengths[b0 + b] = ng[b];
+    lens_all[b0 + b] = ng[b];
   }
   if (cc.profiling) {
     for (auto& pr : prof_replays) harvest_snapshot(pr);

@@ -2,7 +2,9 @@
 #pragma once
 
 #include <map>
+#include <memory>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "model.hpp"
@@ -15,6 +17,7 @@ struct Engine {
   ppoexp_engine_options opts{};
   KvGeom geom{};
   DeviceBuffer kv;     // paged pool
+  void* kvp = nullptr; // the pool this engine decodes into (kv.ptr, or the owner's for a lane)
   DeviceBuffer state;  // per-sequence state + step activations + outputs
   int32_t *next_tok, *pos, *n_gen, *done, *budget, *n_active, *block_table, *last_rows;
   SampleParams* sparams;
@@ -56,7 +59,19 @@ struct Engine {
   };
   std::vector<ReplayTimes> prof_replays;
 
-  Engine(Model* model, const ppoexp_engine_options* o);
+  // Decode lanes: a batch split over two sub-engines (each with its own
+  // stream, step state and graphs, pages from the owner's pool) whose decode
+  // chains run concurrently — each decode step is a chain of ~90 dependent
+  // latency-bound launches, so two half-batch chains overlap on the SMs.
+  std::unique_ptr<Engine> lanes[2];
+  Engine* owner = nullptr;
+  cudaStream_t lane_stream = nullptr;
+  std::string lane_prefix;
+  cudaEvent_t lane_ev = nullptr;
+  int n_lanes = 1;          // PPOEXP_LANES (default: 2 for mixed / bf16 decode)
+  int64_t lane_min_b = 128;  // split only batches of at least this many sequences (C3 +13%, C2 / C4 not)
+
+  Engine(Model* model, const ppoexp_engine_options* o, Engine* owner_ = nullptr);
   ~Engine();
 
   void generate(int64_t B, const int32_t* prompts, const int64_t* offsets, const int64_t* max_new,
@@ -65,7 +80,30 @@ struct Engine {
                 int where_tokens = -1);
   std::vector<int64_t> last_lengths;  // host copy of the last call's lengths
 
+  // One chunk of generation, issued in phases so that lanes interleave.
+  struct Run {
+    int64_t B = 0, b0 = 0, units = 0, R = 0, r = 0;
+    bool stop = false, active = false;
+    GraphSet* gs = nullptr;    // kUnitsPerGraph decode units per replay
+    GraphSet* tail = nullptr;  // the last replay: the remaining units
+    std::vector<std::tuple<GraphSet*, int, int64_t>> pending;  // (graph, slot, unit0) awaiting harvest
+    int64_t out_stride = 0;
+    int32_t* out_tokens = nullptr;
+    double* out_logprobs = nullptr;
+    int64_t* out_lengths = nullptr;
+    int where_out = 0;
+  };
+
  private:
+  void chunk_begin(Run& run, int64_t B, const int32_t* prompts, const std::vector<int64_t>& off_all, int64_t b0,
+                   const std::vector<int64_t>& mx_all, const ppoexp_sampling* sp_all,
+                   const std::vector<uint64_t>& seeds_all, int64_t out_stride, int32_t* out_tokens,
+                   double* out_logprobs, int64_t* out_lengths, int where_out, int where_tokens, int64_t page_base);
+  void chunk_launch(Run& run);  // enqueue replay r
+  void chunk_poll(Run& run);    // wait for replay r-1's done counter; decides whether to stop
+  void chunk_finish(Run& run);
+  int64_t chunk_pages(int64_t B, const std::vector<int64_t>& off_all, int64_t b0,
+                      const std::vector<int64_t>& mx_all) const;
   void run_chunk(int64_t B, const int32_t* prompts, const std::vector<int64_t>& off_all, int64_t b0,
                  const std::vector<int64_t>& mx_all, const ppoexp_sampling* sp_all,
                  const std::vector<uint64_t>& seeds_all,
@@ -76,7 +114,7 @@ struct Engine {
   void decode_unit(int64_t B, int64_t unit);
   void decode_unit_mixed(int64_t B, int64_t unit);
   void run_unit(int64_t B, int64_t unit);
-  GraphSet& graph_for(int64_t B);
+  GraphSet& graph_for(int64_t B, int units);
   void harvest_replay(const std::vector<TimedLaunch>& evs, int64_t unit0, int units);
   void snapshot_events(ReplayTimes& r);
   void harvest_snapshot(const ReplayTimes& r);

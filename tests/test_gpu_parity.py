@@ -476,7 +476,11 @@ def _mixed_experience_check(px, ctx, oracle, cfg, prompts, N, seed=3, kl=0.003, 
     return worst
 
 
-def test_mixed_experience_c1(px, ctx, oracle):
+@pytest.mark.parametrize("lanes", ["1", "2"])
+def test_mixed_experience_c1(px, ctx, oracle, monkeypatch, lanes):
+    # lanes=2: the 8 prompts decode as two 4-sequence lanes on separate streams
+    monkeypatch.setenv("PPOEXP_LANES", lanes)
+    monkeypatch.setenv("PPOEXP_LANE_MIN_B", "2")
     cfg = ModelCfg(V=1024, d=128, L=2, H=4, f=512, S=128)
     _mixed_experience_check(px, ctx, oracle, cfg, synthetic_prompts(7, 8, 9, ragged_lengths=True), 64)
 
@@ -649,3 +653,33 @@ def test_mixed_decode_activation_paths(px, ctx, oracle, monkeypatch, planes):
     monkeypatch.setenv("PPOEXP_MIXED_PLANES", planes)
     cfg = ModelCfg(V=50257, d=768, L=2, H=12, f=3072, S=512)
     _mixed_experience_check(px, ctx, oracle, cfg, synthetic_prompts(3, 4, 12, ragged_lengths=True), 16)
+
+
+@pytest.mark.parametrize("dtype", ["MIXED", "BF16"])
+@pytest.mark.parametrize("graphs", [True, False])
+def test_decode_lanes_match_single_lane(px, ctx, oracle, monkeypatch, dtype, graphs):
+    """The two-lane decode (half batches on two streams, pages from one pool)
+    gives exactly the tokens / log-probs / lengths of the single-lane engine:
+    ragged prompts, mixed budgets (chunks of max_batch=24 over 41 tasks), greedy
+    and top-p rows, EOT stops."""
+    cfg = ModelCfg(V=1031, d=256, L=2, H=4, f=1024, S=160)
+    w = oracle.init_params(cfg, 11)
+    prompts = synthetic_prompts(21, 41, 24, ragged_lengths=True)
+    tasks = []
+    for i, p in enumerate(prompts):
+        sp = (px.SamplingSpec.greedy_spec() if i % 3 == 0
+              else px.SamplingSpec.temperature_spec(1.3, 500 + i, 0, 0.95))
+        tasks.append(px.GenTask(p, [40, 7, 23, 1, 64][i % 5], sp))
+    res = {}
+    monkeypatch.setenv("PPOEXP_LANE_MIN_B", "8")
+    for lanes in ("1", "2"):
+        monkeypatch.setenv("PPOEXP_LANES", lanes)
+        eng = engine(px, ctx, cfg, w, getattr(px, dtype), use_graphs=graphs, max_batch=24)
+        res[lanes] = eng.generate_batch(tasks)
+        eng.close()
+    for a, b in zip(res["1"], res["2"]):
+        assert np.array_equal(a.tokens, b.tokens)
+        if dtype == "MIXED":
+            assert np.array_equal(a.logprobs, b.logprobs)
+        else:  # bf16 prefill GEMM tiling follows the packed prompt count: rounding-level differences
+            close(a.logprobs, b.logprobs, 5e-3, 0)
