@@ -376,6 +376,30 @@ CUtensorMap make_map(const void* ptr, int64_t rows, int64_t cols, int64_t ld, in
   return m;
 }
 
+// General 2-D tensor map (128B swizzle) over [rows, cols] elements of `esz`
+// bytes (2: bf16, 4: fp32) with row stride ld elements, box {box_cols, box_rows}.
+CUtensorMap make_map_2d(const void* ptr, int esz, int64_t rows, int64_t cols, int64_t ld, int box_cols, int box_rows) {
+  static std::mutex mu;
+  static std::map<std::tuple<const void*, int, int64_t, int64_t, int64_t, int, int>, CUtensorMap> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  const auto key = std::make_tuple(ptr, esz, rows, cols, ld, box_cols, box_rows);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  CUtensorMap m;
+  const cuuint64_t dims[2] = {cuuint64_t(cols), cuuint64_t(rows)};
+  const cuuint64_t strides[1] = {cuuint64_t(ld * esz)};
+  const cuuint32_t box[2] = {cuuint32_t(box_cols), cuuint32_t(box_rows)};
+  const cuuint32_t estr[2] = {1, 1};
+  auto fn = encode_fn();
+  if (!fn) throw Error(6, "cuda: cuTensorMapEncodeTiled unavailable");
+  const CUresult r = fn(&m, esz == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                        const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Error(6, "cuda: cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
+  cache.emplace(key, m);
+  return m;
+}
+
 namespace {
 
 template <int BN, int EPI, bool SPLIT = false>
@@ -440,6 +464,8 @@ bool gemm_tc_bf16(Ctx& c, const bf16* A, int64_t lda, const bf16* B, int64_t ldb
   if (M <= 0 || N <= 0 || K <= 0) return true;
   // decode-sized M: swap-AB + cluster split-K kernel (gemm_decode.cu)
   if (gemm_decode_bf16(c, A, lda, B, ldb, M, N, K, epi, C, ldc)) return true;
+  if (gemm_pp_enabled() && !(reinterpret_cast<uintptr_t>(C) & 15) && epi != Epi::kLse)
+    return gemm_persist(c, A, lda, B, ldb, M, N, K, epi, C, ldc, false, nullptr), true;
   const int64_t num_m = ceil_div(M, BM);
   static const int bn_env = [] {
     const char* e = getenv("PPOEXP_TC_BN");
@@ -466,9 +492,12 @@ void gemm_tc_planes(Ctx& c, const bf16* A, int64_t lda, const bf16* W, int64_t l
     throw ContractError("gemm (planes): 16-byte aligned rows, K % 8 and a [M, 2K] activation required");
   if (epi == Epi::kLse) {
     if (!lse || lse->ldp < lse_tiles(N)) throw ContractError("gemm (planes): LSE outputs missing");
+    if (gemm_pp_enabled()) return gemm_persist(c, A, lda, W, ldw, M, N, K, epi, nullptr, 0, true, lse);
     return launch_tc<256, int(Epi::kLse), true>(c, A, lda, W, ldw, M, N, K, nullptr, 0, *lse);
   }
   if (M <= 128) return gemm_decode_planes(c, A, lda, W, ldw, M, N, K, epi, C, ldc, nullptr);
+  if (gemm_pp_enabled() && !(reinterpret_cast<uintptr_t>(C) & 15) && ldc % 8 == 0)
+    return gemm_persist(c, A, lda, W, ldw, M, N, K, epi, C, ldc, true, nullptr);
   static const int bn = [] {  // 256: one CTA per SM, three 64 KB stages; 128: two CTAs per SM
     const char* e = getenv("PPOEXP_PLANES_BN");
     return e ? atoi(e) : 256;
@@ -496,6 +525,7 @@ bool gemm_tc_lse(Ctx& c, const bf16* A, int64_t lda, const bf16* B, int64_t ldb,
   if ((lda * 2) % 16 || (ldb * 2) % 16 || K % 8) return false;
   if (e.ldp < lse_tiles(N)) throw ContractError("gemm_tc_lse: partial row stride too small");
   if (M <= 0 || N <= 0 || K <= 0) return true;
+  if (gemm_pp_enabled()) return gemm_persist(c, A, lda, B, ldb, M, N, K, Epi::kLse, nullptr, 0, false, &e), true;
   launch_tc<256, int(Epi::kLse)>(c, A, lda, B, ldb, M, N, K, nullptr, 0, e);
   return true;
 }

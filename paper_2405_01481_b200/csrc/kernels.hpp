@@ -109,6 +109,12 @@ void gemm_decode_planes(Ctx& c, const bf16* X, int64_t ldx, const bf16* W, int64
 void launch_layernorm_split(Ctx& c, const float* x, int64_t rows, int64_t d, const float* g, const float* b, bf16* y,
                             const int32_t* gather = nullptr);
 // Mixed-mode GEMM over a [M, 2K] hi|lo bf16 plane activation (tcgen05, both planes TMA'd).
+// Persistent tcgen05 GEMM (gemm_persist.cu): one CTA per SM over 128 x 256
+// tiles, double-buffered TMEM accumulators, TMA-store epilogues; A bf16
+// [M, K] or hi | lo planes [M, 2K] (split).  PPOEXP_GEMM_PERSIST=0 disables.
+bool gemm_pp_enabled();
+void gemm_persist(Ctx& c, const bf16* A, int64_t lda, const bf16* W, int64_t ldw, int64_t M, int64_t N, int64_t K,
+                  Epi epi, void* C, int64_t ldc, bool split, const LseEpi* lse);
 void gemm_tc_planes(Ctx& c, const bf16* A, int64_t lda, const bf16* W, int64_t ldw, int64_t M, int64_t N, int64_t K,
                     Epi epi, void* C, int64_t ldc, const LseEpi* lse = nullptr);
 // Mixed-mode GEMM for any M (decode-sized M goes to gemm_decode_mixed).

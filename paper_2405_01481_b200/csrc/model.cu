@@ -298,9 +298,12 @@ static float* forward_layers_t(Model& m, const Packed& p, const KvTarget* kv) {
 // LayerNorms); PPOEXP_PREFILL_PLANES=1 selects the planes.  The LM head takes the
 // planes (LSE epilogue: 5.9 -> 4.7 ms) unless PPOEXP_MIXED_PLANES=0.
 static bool mixed_prefill_planes() {
+  // default with the persistent planes GEMM (gemm_persist.cu: 2x the in-kernel
+  // split's throughput at the C2 scoring shapes); PPOEXP_PREFILL_PLANES=0 keeps
+  // fp32 activations split inside gemm_mixed
   static const bool on = [] {
     const char* e = getenv("PPOEXP_PREFILL_PLANES");
-    return e && e[0] == '1';
+    return e ? e[0] == '1' : gemm_pp_enabled();
   }();
   return on;
 }

