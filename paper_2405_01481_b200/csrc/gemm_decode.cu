@@ -421,13 +421,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           if constexpr (EPI == int(Epi::kStore)) {
             static_cast<bf16*>(Cv)[o] = __float2bfloat16_rn(a);
           } else if constexpr (EPI == int(Epi::kGelu)) {
-            static_cast<bf16*>(Cv)[o] = __float2bfloat16_rn(gelu_tanh(a));
+            static_cast<bf16*>(Cv)[o] = __float2bfloat16_rn(gelu_fast(a));
           } else if constexpr (EPI == int(Epi::kAddResidual)) {
             static_cast<float*>(Cv)[o] += a;
           } else if constexpr (EPI == int(Epi::kGeluF32)) {
-            static_cast<float*>(Cv)[o] = gelu_tanh(a);
+            static_cast<float*>(Cv)[o] = gelu_fast(a);
           } else if constexpr (EPI == int(Epi::kGeluSplit)) {
-            const float gv = gelu_tanh(a);
+            const float gv = gelu_fast(a);
             const bf16 hi = __float2bfloat16_rn(gv);
             static_cast<bf16*>(Cv)[o] = hi;
             static_cast<bf16*>(Cv)[o + N] = __float2bfloat16_rn(gv - __bfloat162float(hi));
@@ -599,7 +599,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if constexpr (EPI == int(Epi::kStore)) {
           static_cast<bf16*>(Cv)[o] = __float2bfloat16_rn(a);
         } else if constexpr (EPI == int(Epi::kGelu)) {
-          static_cast<bf16*>(Cv)[o] = __float2bfloat16_rn(gelu_tanh(a));
+          static_cast<bf16*>(Cv)[o] = __float2bfloat16_rn(gelu_fast(a));
         } else if constexpr (EPI == int(Epi::kAddResidual)) {
           float* xp = static_cast<float*>(Cv) + o;
           const int64_t o4 = int64_t(bcol) * ldc + n0 + fl;
@@ -611,9 +611,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           ps += double(nv);
           pq += double(nv) * double(nv);
         } else if constexpr (EPI == int(Epi::kGeluF32)) {
-          static_cast<float*>(Cv)[o] = gelu_tanh(a);
+          static_cast<float*>(Cv)[o] = gelu_fast(a);
         } else if constexpr (EPI == int(Epi::kGeluSplit)) {
-          const float gv = gelu_tanh(a);
+          const float gv = gelu_fast(a);
           const bf16 hi = __float2bfloat16_rn(gv);
           static_cast<bf16*>(Cv)[o] = hi;
           static_cast<bf16*>(Cv)[o + N] = __float2bfloat16_rn(gv - __bfloat162float(hi));

@@ -268,7 +268,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               o.z += x.z;
               o.w += x.w;
             } else if constexpr (EPI == int(Epi::kGeluF32)) {
-              o = make_float4(gelu_tanh(o.x), gelu_tanh(o.y), gelu_tanh(o.z), gelu_tanh(o.w));
+              o = make_float4(gelu_fast(o.x), gelu_fast(o.y), gelu_fast(o.z), gelu_fast(o.w));
             }
             *reinterpret_cast<float4*>(dst + j) = o;
           }
@@ -280,7 +280,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               if constexpr (EPI == int(Epi::kAddResidual))
                 dst[e] += a;
               else if constexpr (EPI == int(Epi::kGeluF32))
-                dst[e] = gelu_tanh(a);
+                dst[e] = gelu_fast(a);
               else
                 dst[e] = a;
             }

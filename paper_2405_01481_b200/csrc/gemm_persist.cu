@@ -276,7 +276,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           if constexpr (EPI == int(Epi::kGeluF32)) {
 #pragma unroll
-            for (int e = 0; e < 32; ++e) v[e] = __float_as_uint(gelu_tanh(__uint_as_float(v[e])));
+            for (int e = 0; e < 32; ++e) v[e] = __float_as_uint(gelu_fast(__uint_as_float(v[e])));
           }
           uint8_t* box = box0 + (nbox & 1) * 4096;
           if (lane == 0) bulk_wait_read<1>();  // the store issued from this box two boxes ago has read it
@@ -325,7 +325,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int e = 0; e < 8; ++e) {
               const int k = 8 * j + e;
               float x = __uint_as_float(k < 32 ? v[k] : (second ? w[k - 32] : 0u));
-              if constexpr (EPI == int(Epi::kGelu) || EPI == int(Epi::kGeluSplit)) x = gelu_tanh(x);
+              if constexpr (EPI == int(Epi::kGelu) || EPI == int(Epi::kGeluSplit)) x = gelu_fast(x);
               g[e] = x;
             }
             uint32_t h[4];

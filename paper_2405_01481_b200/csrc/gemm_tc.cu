@@ -261,13 +261,13 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll
         for (int e = 0; e < 32; e += 2) {
           if (col + e + 1 < N || full_cols) {
-            const float g0 = gelu_tanh(__uint_as_float(v[e])), g1 = gelu_tanh(__uint_as_float(v[e + 1]));
+            const float g0 = gelu_fast(__uint_as_float(v[e])), g1 = gelu_fast(__uint_as_float(v[e + 1]));
             const __nv_bfloat162 h = __floats2bfloat162_rn(g0, g1);
             const float2 hf = __bfloat1622float2(h);
             *reinterpret_cast<__nv_bfloat162*>(dst + e) = h;
             *reinterpret_cast<__nv_bfloat162*>(dst + N + e) = __floats2bfloat162_rn(g0 - hf.x, g1 - hf.y);
           } else if (col + e < N) {
-            const float g0 = gelu_tanh(__uint_as_float(v[e]));
+            const float g0 = gelu_fast(__uint_as_float(v[e]));
             const bf16 h = __float2bfloat16_rn(g0);
             dst[e] = h;
             dst[N + e] = __float2bfloat16_rn(g0 - __bfloat162float(h));
@@ -282,7 +282,7 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll
             for (int e = 0; e < 8; ++e) {
               float f = __uint_as_float(v[j + e]);
-              if constexpr (EPI == int(Epi::kGelu)) f = gelu_tanh(f);
+              if constexpr (EPI == int(Epi::kGelu)) f = gelu_fast(f);
               o.v[e] = __float2bfloat16_rn(f);
             }
             *reinterpret_cast<uint4*>(dst + j) = o.u;
@@ -292,7 +292,7 @@ __global__ void __launch_bounds__(kThreads, 2)
           for (int e = 0; e < 32; ++e) {
             if (col + e < N) {
               float f = __uint_as_float(v[e]);
-              if constexpr (EPI == int(Epi::kGelu)) f = gelu_tanh(f);
+              if constexpr (EPI == int(Epi::kGelu)) f = gelu_fast(f);
               dst[e] = __float2bfloat16_rn(f);
             }
           }

@@ -18,17 +18,18 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-fi
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
     --cache-control none -s 1500 -c 900 --csv --log-file $O/launches_decode.csv $DEC > $O/ncu1.log 2>&1
 # 3. scoring-phase kernels with DRAM bytes
+SCO="python tools/profile_score.py --reps 2"
+$SCO > $O/score_only_plain.log 2>&1
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
-    -k regex:"gemm_mixed|attn_prefill_split|layernorm|lse_combine" -s 100 -c 300 --csv \
-    --log-file $O/launches_scoring.csv $SCORE > $O/ncu2.log 2>&1
+    -k regex:"gemm_pp|attn_prefill|layernorm|lse_combine|embed|logprob" -s 100 -c 100 --csv --log-file $O/launches_scoring.csv $SCO > $O/ncu2.log 2>&1
 # 4. full captures of the top kernels
 ncu --set full --import-source on --clock-control none -k regex:gemm_decode_kernel -s 202 -c 1 -o $R/full_gemm_decode_a $DEC > $O/ncu3.log 2>&1
 ncu --set full --import-source on --clock-control none -k regex:gemm_decode_kernel -s 201 -c 1 -o $R/full_gemm_decode_b $DEC > $O/ncu4.log 2>&1
 ncu --set full --import-source on --clock-control none -k regex:attn_decode -s 100 -c 1 -o $R/full_attn_decode $DEC > $O/ncu5.log 2>&1
 ncu --set full --import-source on --clock-control none -k regex:sampler -s 30 -c 1 -o $R/full_sampler $DEC > $O/ncu6.log 2>&1
-ncu --set full --import-source on --clock-control none -k regex:"gemm_mixed_kernel" -s 40 -c 1 -o $R/full_gemm_mixed $SCORE > $O/ncu7.log 2>&1
+ncu --set full --import-source on --clock-control none -k regex:"gemm_pp_kernel" -s 60 -c 1 -o $R/full_gemm_pp $SCO > $O/ncu7.log 2>&1
 ncu --set full --import-source on --clock-control none -k regex:"attn_prefill_split" -s 10 -c 1 -o $R/full_attn_prefill_split $SCORE > $O/ncu8.log 2>&1
-ncu --set full --import-source on --clock-control none -k regex:"gemm_tc_kernel" -s 30 -c 1 -o $R/full_gemm_tc_planes $SCORE > $O/ncu9.log 2>&1
+ncu --set full --import-source on --clock-control none -k regex:"layernorm_split" -s 30 -c 1 -o $R/full_ln_split $SCO > $O/ncu9.log 2>&1
 # bf16 scoring: tcgen05 flash attention (C2 shape) and the C5-shape launch
 BSCORE="python tools/profile_decode.py --new 24 --dtype bf16 --score 1"
 $BSCORE > $O/bscore_plain.log 2>&1
