@@ -453,10 +453,65 @@ __global__ void layernorm_split_kernel(const float* __restrict__ x, int64_t d, c
   *reinterpret_cast<uint2*>(y + r * 2 * d + d + j) = *reinterpret_cast<const uint2*>(lo);
 }
 
+// Many rows (prefill / scoring): a warp per row, the row's NV float4 per lane
+// loaded up front, shuffle-only fp64 reductions (the same two-pass statistics).
+template <int NV>
+__global__ void __launch_bounds__(256) layernorm_split_warp_kernel(const float* __restrict__ x, int64_t rows, int64_t d,
+                                                                   const float* __restrict__ g,
+                                                                   const float* __restrict__ b, bf16* __restrict__ y,
+                                                                   const int32_t* __restrict__ gather) {
+  PDL_ENTRY();
+  const int lane = threadIdx.x & 31;
+  const int64_t r = int64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (r >= rows) return;
+  const int64_t src = gather ? gather[r] : r;
+  const float4* xr = reinterpret_cast<const float4*>(x + src * d);
+  float4 v[NV];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) v[k] = __ldcs(xr + lane + 32 * k);  // read once: streaming
+  double s = 0.0;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) s += double(v[k].x) + v[k].y + v[k].z + v[k].w;
+  const double mu = warp_sum_d(s) / double(d);
+  double q = 0.0;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    const double c0 = v[k].x - mu, c1 = v[k].y - mu, c2 = v[k].z - mu, c3 = v[k].w - mu;
+    q += c0 * c0 + c1 * c1 + c2 * c2 + c3 * c3;
+  }
+  const double is = 1.0 / sqrt(warp_sum_d(q) / double(d) + 1e-5);
+  bf16* yr = y + r * 2 * d;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    const int j = 4 * (lane + 32 * k);
+    const float4 gg = __ldg(reinterpret_cast<const float4*>(g + j)), bb = __ldg(reinterpret_cast<const float4*>(b + j));
+    const float o[4] = {float(gg.x * ((v[k].x - mu) * is) + bb.x), float(gg.y * ((v[k].y - mu) * is) + bb.y),
+                        float(gg.z * ((v[k].z - mu) * is) + bb.z), float(gg.w * ((v[k].w - mu) * is) + bb.w)};
+    bf16 hi[4], lo[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      hi[e] = __float2bfloat16_rn(o[e]);
+      lo[e] = __float2bfloat16_rn(o[e] - __bfloat162float(hi[e]));
+    }
+    *reinterpret_cast<uint2*>(yr + j) = *reinterpret_cast<const uint2*>(hi);
+    *reinterpret_cast<uint2*>(yr + d + j) = *reinterpret_cast<const uint2*>(lo);
+  }
+}
+
 void launch_layernorm_split(Ctx& c, const float* x, int64_t rows, int64_t d, const float* g, const float* b, bf16* y,
                             const int32_t* gather) {
   if (rows <= 0) return;
   if (d % 4 || d > 4096) throw ContractError("layernorm (split planes): d % 4 == 0 and d <= 4096 required");
+  if (rows >= 1024 && (d == 768 || d == 1024 || d == 2048)) {
+    auto k = d == 768    ? layernorm_split_warp_kernel<6>
+             : d == 1024 ? layernorm_split_warp_kernel<8>
+                         : layernorm_split_warp_kernel<16>;
+    const int wpb = 8;
+    c.launch("layernorm", double(rows) * d * 8, 0, [&] {
+      launch_kernel(c, k, dim3(unsigned(ceil_div(rows, wpb))), dim3(32 * wpb), 0, 1, x, rows, d, g, b, y, gather);
+    });
+    return;
+  }
   const int th = int((d / 4 + 31) / 32 * 32);
   c.launch("layernorm", double(rows) * d * 8, 0, [&] {
     launch_kernel(c, layernorm_split_kernel, dim3(rows), dim3(th), 0, 1, x, d, g, b, y, gather);

@@ -544,6 +544,21 @@ def test_mixed_response_logprob_sums(px, ctx, oracle):
     close(np.concatenate(px.sequence_logprobs(m, seqs)), np.concatenate(lps))
 
 
+@pytest.mark.parametrize("d,H", [(768, 12), (1024, 8), (2048, 16)])
+def test_mixed_scoring_many_rows(px, ctx, oracle, d, H):
+    """Scoring batches of >= 1024 packed rows take the warp-per-row split
+    LayerNorm and the persistent planes GEMM (every epilogue: fp32 store,
+    residual reduce-add, GELU planes, LSE): log-probs at the bar against the
+    oracle (small vocab keeps the fp64 oracle fast)."""
+    cfg = ModelCfg(V=1031, d=d, L=2, H=H, f=4 * d, S=256)
+    w = bf16_round(oracle.init_params(cfg, 7 + d))
+    m = px.DeviceModel(ctx, to_px_cfg(cfg), w, px.MIXED)
+    rng = np.random.default_rng(d)
+    seqs = [rng.integers(0, 1031, int(n)).astype(np.int32) for n in rng.integers(60, 140, 14)]
+    assert sum(len(q) for q in seqs) >= 1024
+    close(np.concatenate(px.sequence_logprobs(m, seqs)), np.concatenate(oracle.sequence_logprobs(cfg, w, seqs)))
+
+
 @pytest.mark.parametrize("dtype", ["mixed", "bf16"])
 def test_fused_ln_statistics_with_outliers(px, ctx, oracle, dtype):
     """1e3-magnitude outlier features at d = 4096 (massive activations): the
