@@ -23,7 +23,8 @@ PPOEXP_API ppoexp_status ppoexp_testing_gemm_bf16(ppoexp_ctx ctx, const void* A,
 PPOEXP_API ppoexp_status ppoexp_testing_variant_count(ppoexp_ctx ctx, const char* name, int64_t* out);
 
 /* Causal prefill attention over packed ragged sequences (bf16 qkv [M, 3 d],
- * out [M, d]); path 0 = tcgen05 flash attention, 1 = mma.sync. */
+ * out [M, d]); path 0 = tcgen05 flash attention, 1 = mma.sync, 2 = the mixed-mode
+ * split tcgen05 kernel (qkv as hi | lo planes [M, 6 d], out planes [M, 2 d]; dh 64). */
 PPOEXP_API ppoexp_status ppoexp_testing_attention_prefill(ppoexp_ctx ctx, const void* qkv, const int64_t* offsets,
                                                int64_t B, int64_t max_len, int64_t H, int64_t DH, int64_t M,
                                                void* out, int32_t path);

@@ -1227,8 +1227,9 @@ extern "C" ppoexp_status ppoexp_testing_attention_prefill(ppoexp_ctx ctx, const 
     DeviceGuard g(c.device);
     const auto* q = static_cast<const bf16*>(qkv);
     auto* o = static_cast<bf16*>(out);
-    bool ok = path == 0 ? attention_prefill_tc(c, q, offsets, B, max_len, H, DH, M, o, true)
-                        : attention_prefill_mma(c, q, offsets, B, max_len, H, DH, o);
+    bool ok = path == 0   ? attention_prefill_tc(c, q, offsets, B, max_len, H, DH, M, o, true)
+              : path == 2 ? attention_prefill_tc_split(c, q, offsets, B, max_len, H, DH, M, o)
+                          : attention_prefill_mma(c, q, offsets, B, max_len, H, DH, o);
     if (!ok) throw ContractError("attention path not eligible for this shape");
     c.sync();
   });

@@ -96,20 +96,29 @@ __device__ __forceinline__ void tst32(uint32_t taddr, const uint32_t (&r)[32]) {
       : "memory");
 }
 
-template <int DH>
+// SPLIT (mixed mode): q / k / v arrive as bf16 hi | lo planes of the packed
+// [M, 3d] projection (hi in columns [0, 3d), lo in [3d, 6d)); every operand
+// tile is held as both terms and each product is issued as three MMAs
+// (hi·hi + hi·lo + lo·hi, fp32-grade), P split the same way; the output is
+// written as hi | lo planes [M, 2d] for the O projection.
+template <int DH, bool SPLIT>
 struct FaSmem {
-  static constexpr int kQ = BQ * DH * 2;      // Q: DH/64 boxes of 128 rows x 128 B
-  static constexpr int kKV = BKV * DH * 2;    // one K (or V) tile: DH/64 boxes of 64 rows x 128 B
-  static constexpr int kP = BQ * BKV * 2;     // P tile: 128 rows x 128 B
+  static constexpr int kT = SPLIT ? 2 : 1;
+  static constexpr int kQ1 = BQ * DH * 2;     // one Q term: DH/64 boxes of 128 rows x 128 B
+  static constexpr int kQ = kQ1 * kT;
+  static constexpr int kKV1 = BKV * DH * 2;   // one term of a K (or V) tile: DH/64 boxes of 64 rows x 128 B
+  static constexpr int kKV = kKV1 * kT;
+  static constexpr int kP1 = BQ * BKV * 2;    // one term of the P tile: 128 rows x 128 B
+  static constexpr int kP = kP1 * kT;
   static constexpr int kBytes = kQ + NST * 2 * kKV + 2 * kP + 1024 /*align*/ + 256 /*barriers*/;
   static constexpr int kTmem = 256;           // S0 (64) | S1 (64) | O (DH <= 128)
 };
 
-template <int DH>
+template <int DH, bool SPLIT>
 __global__ void __launch_bounds__(kThr, 1)
     attn_prefill_tc_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tkv,
                            const int64_t* __restrict__ seq_offsets, int H, bf16* __restrict__ out) {
-  using L = FaSmem<DH>;
+  using L = FaSmem<DH, SPLIT>;
   constexpr int NB = DH / 64;  // 64-column boxes per row
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -167,7 +176,10 @@ __global__ void __launch_bounds__(kThr, 1)
   if (warp == 0) {
     if (lane == 0) {
       bar_expect(q_full, L::kQ);
-      for (int c = 0; c < NB; ++c) tma2d(&tq, q_full, sQ + c * (BQ * 128), int(h * DH + c * 64), int(start + q0));
+      for (int c = 0; c < NB; ++c) {
+        tma2d(&tq, q_full, sQ + c * (BQ * 128), int(h * DH + c * 64), int(start + q0));
+        if constexpr (SPLIT) tma2d(&tq, q_full, sQ + L::kQ1 + c * (BQ * 128), int(3 * d + h * DH + c * 64), int(start + q0));
+      }
       for (int j = 0; j < nt; ++j) {
         const int s = j % NST, r = j / NST;
         if (r > 0) bar_wait(&kv_empty[s], (r - 1) & 1);
@@ -176,6 +188,10 @@ __global__ void __launch_bounds__(kThr, 1)
         for (int c = 0; c < NB; ++c) {
           tma2d(&tkv, &kv_full[s], sK(s) + c * (BKV * 128), int(d + h * DH + c * 64), row);
           tma2d(&tkv, &kv_full[s], sV(s) + c * (BKV * 128), int(2 * d + h * DH + c * 64), row);
+          if constexpr (SPLIT) {
+            tma2d(&tkv, &kv_full[s], sK(s) + L::kKV1 + c * (BKV * 128), int(4 * d + h * DH + c * 64), row);
+            tma2d(&tkv, &kv_full[s], sV(s) + L::kKV1 + c * (BKV * 128), int(5 * d + h * DH + c * 64), row);
+          }
         }
       }
     }
@@ -193,6 +209,12 @@ __global__ void __launch_bounds__(kThr, 1)
           const uint64_t a = desc_k(sQ + (kk >> 2) * (BQ * 128)) + 2 * (kk & 3);
           const uint64_t bb = desc_k(sK(s) + (kk >> 2) * (BKV * 128)) + 2 * (kk & 3);
           mma(tmem + bf * 64, a, bb, id_s, kk > 0);
+          if constexpr (SPLIT) {  // + q_hi k_lo + q_lo k_hi
+            const uint64_t al = desc_k(sQ + L::kQ1 + (kk >> 2) * (BQ * 128)) + 2 * (kk & 3);
+            const uint64_t bl = desc_k(sK(s) + L::kKV1 + (kk >> 2) * (BKV * 128)) + 2 * (kk & 3);
+            mma(tmem + bf * 64, a, bl, id_s, 1);
+            mma(tmem + bf * 64, al, bb, id_s, 1);
+          }
         }
         commit(&s_full[bf]);
       };
@@ -208,6 +230,12 @@ __global__ void __launch_bounds__(kThr, 1)
           const uint64_t a = desc_k(sP(bf)) + 2 * kk;
           const uint64_t bb = desc_mn(sV(s)) + ((2048 * kk) >> 4);
           mma(tO, a, bb, id_o, (j | kk) != 0);
+          if constexpr (SPLIT) {  // + p_hi v_lo + p_lo v_hi
+            const uint64_t al = desc_k(sP(bf) + L::kP1) + 2 * kk;
+            const uint64_t bl = desc_mn(sV(s) + L::kKV1) + ((2048 * kk) >> 4);
+            mma(tO, a, bl, id_o, 1);
+            mma(tO, al, bb, id_o, 1);
+          }
         }
         commit(o_done);
         commit(&kv_empty[s]);
@@ -287,13 +315,21 @@ __global__ void __launch_bounds__(kThr, 1)
       uint8_t* prow = sP(bf) + r * 128;
 #pragma unroll
       for (int c8 = 0; c8 < 8; ++c8) {
-        uint32_t w4[4];
+        uint32_t w4[4], l4[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          const __nv_bfloat162 p2 = __floats2bfloat162_rn(sv[c8 * 8 + 2 * e], sv[c8 * 8 + 2 * e + 1]);
+          const float p0 = sv[c8 * 8 + 2 * e], p1 = sv[c8 * 8 + 2 * e + 1];
+          const __nv_bfloat162 p2 = __floats2bfloat162_rn(p0, p1);
           w4[e] = *reinterpret_cast<const uint32_t*>(&p2);
+          if constexpr (SPLIT) {
+            const float2 hf = __bfloat1622float2(p2);
+            const __nv_bfloat162 q2 = __floats2bfloat162_rn(p0 - hf.x, p1 - hf.y);
+            l4[e] = *reinterpret_cast<const uint32_t*>(&q2);
+          }
         }
         *reinterpret_cast<uint4*>(prow + ((c8 ^ (r & 7)) << 4)) = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+        if constexpr (SPLIT)
+          *reinterpret_cast<uint4*>(prow + L::kP1 + ((c8 ^ (r & 7)) << 4)) = make_uint4(l4[0], l4[1], l4[2], l4[3]);
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -309,13 +345,18 @@ __global__ void __launch_bounds__(kThr, 1)
       tld32(tO + lane_off + c, o);
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
       if (qi < len) {
-        bf16* dst = out + (start + qi) * d + h * DH + c;
+        bf16* dst = out + (start + qi) * (SPLIT ? 2 * d : d) + h * DH + c;
 #pragma unroll
         for (int e8 = 0; e8 < 32; e8 += 8) {
-          Vec16<bf16> ov;
+          Vec16<bf16> ov, ol;
 #pragma unroll
-          for (int e = 0; e < 8; ++e) ov.v[e] = __float2bfloat16_rn(__uint_as_float(o[e8 + e]) * inv);
+          for (int e = 0; e < 8; ++e) {
+            const float y = __uint_as_float(o[e8 + e]) * inv;
+            ov.v[e] = __float2bfloat16_rn(y);
+            if constexpr (SPLIT) ol.v[e] = __float2bfloat16_rn(y - __bfloat162float(ov.v[e]));
+          }
           *reinterpret_cast<uint4*>(dst + e8) = ov.u;
+          if constexpr (SPLIT) *reinterpret_cast<uint4*>(dst + d + e8) = ol.u;  // lo plane
         }
       }
     }
@@ -328,23 +369,23 @@ __global__ void __launch_bounds__(kThr, 1)
   }
 }
 
-template <int DH>
+template <int DH, bool SPLIT = false>
 void launch_fa(Ctx& c, const bf16* qkv, const int64_t* seq_offsets, int64_t B, int64_t max_len, int64_t H,
                int64_t M_total, bf16* out) {
-  using L = FaSmem<DH>;
-  const int64_t d = H * DH;
-  const CUtensorMap tq = make_map(qkv, M_total, 3 * d, 3 * d, BQ);
-  const CUtensorMap tkv = make_map(qkv, M_total, 3 * d, 3 * d, BKV);
+  using L = FaSmem<DH, SPLIT>;
+  const int64_t d = H * DH, w = (SPLIT ? 6 : 3) * d;
+  const CUtensorMap tq = make_map(qkv, M_total, w, w, BQ);
+  const CUtensorMap tkv = make_map(qkv, M_total, w, w, BKV);
+  auto k = attn_prefill_tc_kernel<DH, SPLIT>;
   static bool attr = false;
   if (!attr) {
-    PPOEXP_CUDA(cudaFuncSetAttribute(attn_prefill_tc_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     L::kBytes));
+    PPOEXP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kBytes));
     attr = true;
   }
   dim3 grid(unsigned(ceil_div(max_len, BQ)), unsigned(H), unsigned(B));
   const double flops = 2.0 * 2.0 * B * H * double(max_len) * max_len / 2 * DH;
   c.launch("attention_prefill", 0, flops, [&] {
-    launch_kernel(c, attn_prefill_tc_kernel<DH>, grid, dim3(kThr), L::kBytes, 1, tq, tkv, seq_offsets, int(H), out);
+    launch_kernel(c, k, grid, dim3(kThr), L::kBytes, 1, tq, tkv, seq_offsets, int(H), out);
   });
 }
 
@@ -367,6 +408,20 @@ bool attention_prefill_tc(Ctx& c, const bf16* qkv, const int64_t* seq_offsets, i
     case 128: return launch_fa<128>(c, qkv, seq_offsets, B, max_len, H, M_total, out), true;
     default: return false;
   }
+}
+
+// Mixed mode: qkv as hi | lo planes [M, 6d], output planes [M, 2d]; head_dim 64
+// (the split tiles of head_dim 128 would not fit shared memory).  False when
+// not eligible (PPOEXP_ATTN_TC=0 also disables it).
+bool attention_prefill_tc_split(Ctx& c, const bf16* qkv_planes, const int64_t* seq_offsets, int64_t B,
+                                int64_t max_len, int64_t H, int64_t DH, int64_t M_total, bf16* out_planes) {
+  static const int mode = [] {
+    const char* e = getenv("PPOEXP_ATTN_TC");
+    return e ? atoi(e) : 1;
+  }();
+  if (mode == 0 || DH != 64 || M_total <= 0 || (reinterpret_cast<uintptr_t>(qkv_planes) & 15)) return false;
+  launch_fa<64, true>(c, qkv_planes, seq_offsets, B, max_len, H, M_total, out_planes);
+  return true;
 }
 
 }  // namespace ppx

@@ -309,7 +309,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(&acc_empty[acc]);
           }
-          constexpr bool kSplitOut = EPI == int(Epi::kGeluSplit);
+          constexpr bool kSplitOut = EPI == int(Epi::kGeluSplit) || EPI == int(Epi::kStoreSplit);
           uint8_t* box = box0 + (kSplitOut ? 0 : (nbox & 1) * 4096);
           if (lane == 0) {
             if constexpr (kSplitOut)
@@ -386,7 +386,7 @@ void launch_pp(Ctx& c, const bf16* A, int64_t lda, const bf16* W, int64_t ldw, i
     tc = make_map_2d(C, 4, M, N, ldc, 32, 32);
   } else if constexpr (EPI == int(Epi::kStore) || EPI == int(Epi::kGelu)) {
     tc = make_map_2d(C, 2, M, N, ldc, 64, 32);
-  } else if constexpr (EPI == int(Epi::kGeluSplit)) {
+  } else if constexpr (EPI == int(Epi::kGeluSplit) || EPI == int(Epi::kStoreSplit)) {
     tc = make_map_2d(C, 2, M, N, ldc, 64, 32);  // hi plane: columns [0, N)
     tc2 = make_map_2d(static_cast<const bf16*>(C) + N, 2, M, N, ldc, 64, 32);  // lo plane: [N, 2N)
   }
@@ -405,6 +405,7 @@ void launch_pp(Ctx& c, const bf16* A, int64_t lda, const bf16* W, int64_t ldw, i
   if (EPI == int(Epi::kLse)) out_bytes = double(M) * (num_n * 8 + 8);
   if (EPI == int(Epi::kStore) || EPI == int(Epi::kGelu)) out_bytes = double(M) * N * 2;
   if (EPI == int(Epi::kAddResidual)) out_bytes = double(M) * N * 8;
+  if (EPI == int(Epi::kGeluSplit) || EPI == int(Epi::kStoreSplit)) out_bytes = double(M) * N * 4;
   const char* cls = EPI == int(Epi::kLse) ? "lm_head_lse" : (SPLIT ? "gemm_mixed" : "gemm_tc");
   c.launch(cls, a_bytes + 2.0 * N * K + out_bytes, flops, [&] {
     launch_kernel(c, k, dim3(grid), dim3(kThreads), L::kBytes, 1, ta, ta2, tb, tc, tc2, int(M), int(N), int(K),
@@ -434,6 +435,7 @@ void gemm_persist(Ctx& c, const bf16* A, int64_t lda, const bf16* W, int64_t ldw
       case Epi::kStoreF32: return launch_pp<int(Epi::kStoreF32), true>(c, A, lda, W, ldw, M, N, K, C, ldc, le);
       case Epi::kAddResidual: return launch_pp<int(Epi::kAddResidual), true>(c, A, lda, W, ldw, M, N, K, C, ldc, le);
       case Epi::kGeluSplit: return launch_pp<int(Epi::kGeluSplit), true>(c, A, lda, W, ldw, M, N, K, C, ldc, le);
+      case Epi::kStoreSplit: return launch_pp<int(Epi::kStoreSplit), true>(c, A, lda, W, ldw, M, N, K, C, ldc, le);
       case Epi::kGeluF32: return launch_pp<int(Epi::kGeluF32), true>(c, A, lda, W, ldw, M, N, K, C, ldc, le);
       case Epi::kLse: return launch_pp<int(Epi::kLse), true>(c, A, lda, W, ldw, M, N, K, C, ldc, le);
       default: throw ContractError("gemm (persistent planes): unsupported epilogue");

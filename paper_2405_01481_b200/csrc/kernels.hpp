@@ -38,7 +38,7 @@ void launch_layernorm(Ctx& c, const float* x, int64_t rows, int64_t d, const flo
 
 // K3: C[M,N] = A[M,K] · B[N,K]^T with epilogue.
 // kGeluSplit: GELU output written as two bf16 planes (hi at [row, col], lo at [row, N + col]; ldc >= 2N)
-enum class Epi : int { kStore = 0, kGelu = 1, kAddResidual = 2, kStoreF32 = 3, kLse = 4, kGeluF32 = 5, kGeluSplit = 6 };
+enum class Epi : int { kStore = 0, kGelu = 1, kAddResidual = 2, kStoreF32 = 3, kLse = 4, kGeluF32 = 5, kGeluSplit = 6, kStoreSplit = 7 };
 // Epilogue outputs of the fused LM-head + log-sum-exp + gather GEMM (Epi::kLse).
 struct LseEpi {
   const int32_t* target = nullptr;  // [M] target column per row (< 0: none)
@@ -138,6 +138,8 @@ void launch_attention_prefill(Ctx& c, const T* qkv, const int64_t* seq_offsets, 
                               int64_t H, int64_t DH, T* out);
 
 // K5a on tcgen05 (bf16, head_dim 64 / 128): false when not eligible.
+bool attention_prefill_tc_split(Ctx& c, const bf16* qkv_planes, const int64_t* seq_offsets, int64_t B,
+                                int64_t max_len, int64_t H, int64_t DH, int64_t M_total, bf16* out_planes);
 bool attention_prefill_tc(Ctx& c, const bf16* qkv, const int64_t* seq_offsets, int64_t B, int64_t max_len, int64_t H,
                           int64_t DH, int64_t M_total, bf16* out, bool force = false);
 // K5a in mixed mode: fp32 q/k/v in, fp32 out, tensor-core products on the

@@ -315,6 +315,14 @@ static bool mixed_head_planes() {
   return on;
 }
 
+static bool split_attention_tc() {  // PPOEXP_ATTN_SPLIT_TC=0: mma.sync split attention in scoring
+  static const bool on = [] {
+    const char* e = getenv("PPOEXP_ATTN_SPLIT_TC");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 static float* forward_layers_mixed(Model& m, const Packed& p, const KvTarget* kv) {
   Ctx& c = *m.ctx;
   const int64_t M = p.M, d = m.d(), f = m.cfg.d_ff, H = m.cfg.n_heads, DH = m.dh();
@@ -332,14 +340,26 @@ static float* forward_layers_mixed(Model& m, const Packed& p, const KvTarget* kv
     bf16* hp = reinterpret_cast<bf16*>(h);
     bf16* ap = reinterpret_cast<bf16*>(att);
     bf16* upp = reinterpret_cast<bf16*>(up);
+    // the KV-scattering prefill (engine) keeps fp32 q / k / v for the cache
+    const bool qkv_planes = !kv && DH == 64 && M > 128 && gemm_pp_enabled() && split_attention_tc();
     for (int64_t l = 0; l < m.cfg.n_layers; ++l) {
       const Layer& ly = m.layers[l];
       launch_layernorm_split(c, x, M, d, ly.ln1w, ly.ln1b, hp);
-      gemm_tc_planes(c, hp, 2 * d, static_cast<const bf16*>(ly.wqkv), d, M, 3 * d, d, Epi::kStoreF32, qkv, 3 * d);
-      if (kv)
-        launch_kv_scatter<float>(c, qkv, M, d, p.seq_of_row_d, p.positions_d, kv->block_table, int(l), kv->geom,
-                                 static_cast<float*>(kv->pool));
-      attention_prefill_split(c, qkv, p.offsets_d, p.B, p.max_len, H, DH, nullptr, ap);
+      if (qkv_planes) {
+        // scoring: q / k / v as planes [M, 6d] (in the fp32 [M, 3d] buffer) for
+        // the split tcgen05 flash attention, which writes the O operand as planes
+        bf16* qp = reinterpret_cast<bf16*>(qkv);
+        gemm_tc_planes(c, hp, 2 * d, static_cast<const bf16*>(ly.wqkv), d, M, 3 * d, d, Epi::kStoreSplit, qp, 6 * d);
+        if (!attention_prefill_tc_split(c, qp, p.offsets_d, p.B, p.max_len, H, DH, M, ap))
+          throw ContractError("forward (mixed): split tcgen05 attention not eligible (PPOEXP_ATTN_TC=0 needs "
+                              "PPOEXP_ATTN_SPLIT_TC=0)");
+      } else {
+        gemm_tc_planes(c, hp, 2 * d, static_cast<const bf16*>(ly.wqkv), d, M, 3 * d, d, Epi::kStoreF32, qkv, 3 * d);
+        if (kv)
+          launch_kv_scatter<float>(c, qkv, M, d, p.seq_of_row_d, p.positions_d, kv->block_table, int(l), kv->geom,
+                                   static_cast<float*>(kv->pool));
+        attention_prefill_split(c, qkv, p.offsets_d, p.B, p.max_len, H, DH, nullptr, ap);
+      }
       gemm_tc_planes(c, ap, 2 * d, static_cast<const bf16*>(ly.wo), d, M, d, d, Epi::kAddResidual, x, d);
       launch_layernorm_split(c, x, M, d, ly.ln2w, ly.ln2b, hp);
       gemm_tc_planes(c, hp, 2 * d, static_cast<const bf16*>(ly.wup), d, M, f, d, Epi::kGeluSplit, upp, 2 * f);

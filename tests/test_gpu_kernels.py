@@ -178,6 +178,49 @@ def test_attention_prefill_vs_torch(ctx, DH, H, lens, path):
     assert err.max().item() < 2e-2, f"max abs err {err.max().item():.3e}"
 
 
+@pytest.mark.parametrize("H,lens", [(12, [320, 37, 1, 129, 64]), (4, [700]), (2, [128, 128, 255])])
+def test_attention_prefill_split_tc_vs_fp64(ctx, H, lens):
+    """Mixed-mode scoring attention on tcgen05 (q / k / v as hi | lo planes, each
+    product as three MMAs, P split the same way, output planes): fp32-grade
+    against fp64 attention over the reconstructed (hi + lo) operands."""
+    import torch
+    from paper_2405_01481_b200 import ppoexp as px
+    f = px.lib().ppoexp_testing_attention_prefill
+    f.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_int64,
+                  C.c_void_p, C.c_int32]
+    f.restype = C.c_int32
+    DH = 64
+    d = H * DH
+    M = sum(lens)
+    g = torch.Generator(device="cuda").manual_seed(M + H)
+    qkv = torch.randn(M, 3 * d, generator=g, device="cuda") * 1.5
+    hi = qkv.to(torch.bfloat16)
+    lo = (qkv - hi.float()).to(torch.bfloat16)
+    planes = torch.cat([hi, lo], dim=1).contiguous()
+    offs = torch.tensor([0] + list(np.cumsum(lens)), dtype=torch.int64, device="cuda")
+    out = torch.zeros(M, 2 * d, dtype=torch.bfloat16, device="cuda")
+    torch.cuda.synchronize()
+    px._check(f(ctx.h, planes.data_ptr(), offs.data_ptr(), len(lens), max(lens), H, DH, M, out.data_ptr(), 2))
+    got = out[:, :d].double() + out[:, d:].double()
+    x = hi.double() + lo.double()
+    q, k, v = x.split(d, dim=1)
+    ref = torch.empty(M, d, dtype=torch.float64, device="cuda")
+    o = 0
+    for T in lens:
+        qs = q[o:o + T].view(T, H, DH).transpose(0, 1)
+        ks = k[o:o + T].view(T, H, DH).transpose(0, 1)
+        vs = v[o:o + T].view(T, H, DH).transpose(0, 1)
+        s = qs @ ks.transpose(1, 2) / DH ** 0.5
+        s = s.masked_fill(torch.triu(torch.ones(T, T, dtype=torch.bool, device="cuda"), 1), float("-inf"))
+        ref[o:o + T] = (torch.softmax(s, -1) @ vs).transpose(0, 1).reshape(T, d)
+        o += T
+    err = (got - ref).abs()
+    # the omitted lo*lo terms leave ~2^-18 |q||k| per product in the scores
+    # (~5e-5 at |x| ~ 1.5, dh 64), the same as the mma.sync split kernel
+    assert err.max().item() < 2e-4 and err.mean().item() < 1e-5, \
+        f"max abs err {err.max().item():.3e}, mean {err.mean().item():.3e}"
+
+
 @pytest.mark.parametrize("M,N,K", [(300, 2304, 768), (2048, 768, 3072), (129, 3072, 768), (64, 768, 768),
                                    (1000, 1000, 256)])
 @pytest.mark.parametrize("epi", [2, 3, 6])
