@@ -246,7 +246,8 @@ def _dbg(*a):
 KCLASS = [("gemm_decode_kernel", "gemm_decode"), ("attn_decode_kernel", "decode_attention"),
           ("gemm_pp_kernel<4", "lm_head_lse"), ("gemm_pp_kernel<2, true", "gemm_mixed"),
           ("gemm_pp_kernel<3, true", "gemm_mixed"), ("gemm_pp_kernel<5, true", "gemm_mixed"),
-          ("gemm_pp_kernel<6, true", "gemm_mixed"), ("gemm_pp_kernel", "gemm_tc"),
+          ("gemm_pp_kernel<6, true", "gemm_mixed"), ("gemm_pp_kernel<7, true", "gemm_mixed"),
+          ("gemm_pp_kernel", "gemm_tc"),
           ("sampler_kernel", "sampler"), ("gemm_tc_kernel<256, 4", "lm_head_lse"), ("gemm_tc_kernel<128, 3, true", "gemm_mixed"),
           ("gemm_tc_kernel<128, 2, true", "gemm_mixed"), ("gemm_tc_kernel<128, 6, true", "gemm_mixed"),
           ("gemm_tc_kernel<256, 3, true", "gemm_mixed"), ("gemm_tc_kernel<256, 2, true", "gemm_mixed"),
