@@ -100,6 +100,20 @@ struct Vec16 {
 // pdl_trigger() lets the successor grid begin its own prologue early.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+// Small single-wave grids (decode: a CTA per sequence) release their dependent
+// before waiting on their own predecessor, so the next kernel (a decode GEMM)
+// runs its setup and weight prefetch while this one is still queued.  Only
+// safe for a grid that is resident in one wave: early-launched dependents could
+// otherwise hold the SM slots its remaining CTAs need.
+__device__ __forceinline__ void pdl_entry_small_grid() {
+  if (gridDim.x * gridDim.y * gridDim.z <= 256) {
+    pdl_trigger();
+    pdl_wait();
+  } else {
+    pdl_wait();
+    pdl_trigger();
+  }
+}
 #define PDL_ENTRY() \
   do {              \
     pdl_wait();     \

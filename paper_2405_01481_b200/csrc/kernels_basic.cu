@@ -100,7 +100,7 @@ template <class T>
 __global__ void embed_kernel(const int32_t* __restrict__ tokens, const int32_t* __restrict__ positions,
                              int64_t rows, int64_t d, const T* __restrict__ tok, const T* __restrict__ pos,
                              float* __restrict__ x) {
-  PDL_ENTRY();
+  pdl_entry_small_grid();
   const int64_t r = blockIdx.x;
   if (r >= rows) return;
   const int64_t t = tokens[r], p = positions[r];
@@ -417,7 +417,7 @@ __global__ void __launch_bounds__(256) layernorm_wide_kernel(const float* __rest
 __global__ void layernorm_split_kernel(const float* __restrict__ x, int64_t d, const float* __restrict__ g,
                                        const float* __restrict__ b, bf16* __restrict__ y,
                                        const int32_t* __restrict__ gather) {
-  PDL_ENTRY();
+  pdl_entry_small_grid();
   __shared__ double red[32];
   const int64_t r = blockIdx.x;
   const int64_t src = gather ? gather[r] : r;
