@@ -25,7 +25,7 @@ CUtensorMap make_map(const void* ptr, int64_t rows, int64_t cols, int64_t ld, in
 
 namespace {
 
-constexpr int BQ = 128, BKV = 64, NST = 3, kThr = 192;
+constexpr int BQ = 128, BKV = 64, kThr = 192;
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
 __device__ __forceinline__ void bar_init(uint64_t* b, uint32_t n) {
@@ -110,7 +110,13 @@ struct FaSmem {
   static constexpr int kKV = kKV1 * kT;
   static constexpr int kP1 = BQ * BKV * 2;    // one term of the P tile: 128 rows x 128 B
   static constexpr int kP = kP1 * kT;
-  static constexpr int kBytes = kQ + NST * 2 * kKV + 2 * kP + 1024 /*align*/ + 256 /*barriers*/;
+  // the P tile of step j is written only after P_{j-1} V_{j-1} completed (the
+  // softmax waits for it before the O rescale), so one P buffer suffices; the
+  // split head_dim-128 tiles use it (and a 2-stage K / V ring) to fit 227 KB
+  static constexpr bool kBig = SPLIT && DH == 128;
+  static constexpr int kNst = kBig ? 2 : 3;
+  static constexpr int kPB = kBig ? 1 : 2;
+  static constexpr int kBytes = kQ + kNst * 2 * kKV + kPB * kP + 1024 /*align*/ + 256 /*barriers*/;
   static constexpr int kTmem = 256;           // S0 (64) | S1 (64) | O (DH <= 128)
 };
 
@@ -120,13 +126,14 @@ __global__ void __launch_bounds__(kThr, 1)
                            const int64_t* __restrict__ seq_offsets, int H, bf16* __restrict__ out) {
   using L = FaSmem<DH, SPLIT>;
   constexpr int NB = DH / 64;  // 64-column boxes per row
+  constexpr int NST = L::kNst, PB = L::kPB;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = sm;
   auto sK = [&](int s) { return sm + L::kQ + s * 2 * L::kKV; };
   auto sV = [&](int s) { return sm + L::kQ + s * 2 * L::kKV + L::kKV; };
   auto sP = [&](int b) { return sm + L::kQ + NST * 2 * L::kKV + b * L::kP; };
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L::kQ + NST * 2 * L::kKV + 2 * L::kP);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L::kQ + NST * 2 * L::kKV + PB * L::kP);
   uint64_t* q_full = bars;
   uint64_t* kv_full = bars + 1;         // [NST]
   uint64_t* kv_empty = kv_full + NST;   // [NST]
@@ -222,16 +229,16 @@ __global__ void __launch_bounds__(kThr, 1)
       issue_s(0);
       for (int j = 0; j < nt; ++j) {
         if (j + 1 < nt) issue_s(j + 1);
-        const int bf = j & 1, s = j % NST;
-        bar_wait(&p_full[bf], (j >> 1) & 1);
+        const int s = j % NST, pb = j % PB;
+        bar_wait(&p_full[pb], (j / PB) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
         for (int kk = 0; kk < BKV / 16; ++kk) {
-          const uint64_t a = desc_k(sP(bf)) + 2 * kk;
+          const uint64_t a = desc_k(sP(pb)) + 2 * kk;
           const uint64_t bb = desc_mn(sV(s)) + ((2048 * kk) >> 4);
           mma(tO, a, bb, id_o, (j | kk) != 0);
           if constexpr (SPLIT) {  // + p_hi v_lo + p_lo v_hi
-            const uint64_t al = desc_k(sP(bf) + L::kP1) + 2 * kk;
+            const uint64_t al = desc_k(sP(pb) + L::kP1) + 2 * kk;
             const uint64_t bl = desc_mn(sV(s) + L::kKV1) + ((2048 * kk) >> 4);
             mma(tO, a, bl, id_o, 1);
             mma(tO, al, bb, id_o, 1);
@@ -312,7 +319,7 @@ __global__ void __launch_bounds__(kThr, 1)
       }
       m = mn;
       // P_j row (bf16) in the K-major 128B swizzle: row r at r * 128, chunk c ^ (r & 7)
-      uint8_t* prow = sP(bf) + r * 128;
+      uint8_t* prow = sP(j % PB) + r * 128;
 #pragma unroll
       for (int c8 = 0; c8 < 8; ++c8) {
         uint32_t w4[4], l4[4];
@@ -333,7 +340,7 @@ __global__ void __launch_bounds__(kThr, 1)
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-      bar_arrive(&p_full[bf]);
+      bar_arrive(&p_full[j % PB]);
     }
     // ---- epilogue: O / l
     bar_wait(o_done, (nt - 1) & 1);
@@ -410,17 +417,20 @@ bool attention_prefill_tc(Ctx& c, const bf16* qkv, const int64_t* seq_offsets, i
   }
 }
 
-// Mixed mode: qkv as hi | lo planes [M, 6d], output planes [M, 2d]; head_dim 64
-// (the split tiles of head_dim 128 would not fit shared memory).  False when
-// not eligible (PPOEXP_ATTN_TC=0 also disables it).
+// Mixed mode: qkv as hi | lo planes [M, 6d], output planes [M, 2d]; head_dim
+// 64 or 128.  False when not eligible (PPOEXP_ATTN_TC=0 also disables it).
 bool attention_prefill_tc_split(Ctx& c, const bf16* qkv_planes, const int64_t* seq_offsets, int64_t B,
                                 int64_t max_len, int64_t H, int64_t DH, int64_t M_total, bf16* out_planes) {
   static const int mode = [] {
     const char* e = getenv("PPOEXP_ATTN_TC");
     return e ? atoi(e) : 1;
   }();
-  if (mode == 0 || DH != 64 || M_total <= 0 || (reinterpret_cast<uintptr_t>(qkv_planes) & 15)) return false;
-  launch_fa<64, true>(c, qkv_planes, seq_offsets, B, max_len, H, M_total, out_planes);
+  if (mode == 0 || (DH != 64 && DH != 128) || M_total <= 0 || (reinterpret_cast<uintptr_t>(qkv_planes) & 15))
+    return false;
+  if (DH == 64)
+    launch_fa<64, true>(c, qkv_planes, seq_offsets, B, max_len, H, M_total, out_planes);
+  else
+    launch_fa<128, true>(c, qkv_planes, seq_offsets, B, max_len, H, M_total, out_planes);
   return true;
 }
 

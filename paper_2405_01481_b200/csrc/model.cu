@@ -341,7 +341,7 @@ static float* forward_layers_mixed(Model& m, const Packed& p, const KvTarget* kv
     bf16* ap = reinterpret_cast<bf16*>(att);
     bf16* upp = reinterpret_cast<bf16*>(up);
     // the KV-scattering prefill (engine) keeps fp32 q / k / v for the cache
-    const bool qkv_planes = !kv && DH == 64 && M > 128 && gemm_pp_enabled() && split_attention_tc();
+    const bool qkv_planes = !kv && (DH == 64 || DH == 128) && M > 128 && gemm_pp_enabled() && split_attention_tc();
     for (int64_t l = 0; l < m.cfg.n_layers; ++l) {
       const Layer& ly = m.layers[l];
       launch_layernorm_split(c, x, M, d, ly.ln1w, ly.ln1b, hp);

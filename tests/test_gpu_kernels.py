@@ -178,8 +178,9 @@ def test_attention_prefill_vs_torch(ctx, DH, H, lens, path):
     assert err.max().item() < 2e-2, f"max abs err {err.max().item():.3e}"
 
 
-@pytest.mark.parametrize("H,lens", [(12, [320, 37, 1, 129, 64]), (4, [700]), (2, [128, 128, 255])])
-def test_attention_prefill_split_tc_vs_fp64(ctx, H, lens):
+@pytest.mark.parametrize("DH,H,lens", [(64, 12, [320, 37, 1, 129, 64]), (64, 4, [700]), (64, 2, [128, 128, 255]),
+                                       (128, 4, [513, 7, 200]), (128, 2, [1024])])
+def test_attention_prefill_split_tc_vs_fp64(ctx, DH, H, lens):
     """Mixed-mode scoring attention on tcgen05 (q / k / v as hi | lo planes, each
     product as three MMAs, P split the same way, output planes): fp32-grade
     against fp64 attention over the reconstructed (hi + lo) operands."""
@@ -189,7 +190,6 @@ def test_attention_prefill_split_tc_vs_fp64(ctx, H, lens):
     f.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_int64,
                   C.c_void_p, C.c_int32]
     f.restype = C.c_int32
-    DH = 64
     d = H * DH
     M = sum(lens)
     g = torch.Generator(device="cuda").manual_seed(M + H)
@@ -216,8 +216,8 @@ def test_attention_prefill_split_tc_vs_fp64(ctx, H, lens):
         o += T
     err = (got - ref).abs()
     # the omitted lo*lo terms leave ~2^-18 |q||k| per product in the scores
-    # (~5e-5 at |x| ~ 1.5, dh 64), the same as the mma.sync split kernel
-    assert err.max().item() < 2e-4 and err.mean().item() < 1e-5, \
+    # (~5e-5 at |x| ~ 1.5, dh 64; sqrt(2) more at dh 128), as in the mma.sync split kernel
+    assert err.max().item() < 4e-4 and err.mean().item() < 2e-5, \
         f"max abs err {err.max().item():.3e}, mean {err.mean().item():.3e}"
 
 

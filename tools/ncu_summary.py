@@ -57,6 +57,10 @@ def launches(path, out, skip=0.0):
 
 
 def full(rep, out):
+    """rep: a .ncu-rep, or the prefix of its exported pages (<prefix>_details.csv,
+    <prefix>_raw.csv, <prefix>_source.csv: profile_round2.sh exports them on the box)."""
+    if not rep.endswith(".ncu-rep"):
+        return full_csv(rep, out)
     det = subprocess.run(["ncu", "-i", rep, "--page", "details", "--csv"], capture_output=True, text=True).stdout
     r = list(csv.reader(io.StringIO(det)))
     h = r[0]
@@ -105,6 +109,41 @@ def full(rep, out):
             f.write("\n## top stall sites (CUDA source lines)\n\n| share | line | source |\n|---|---|---|\n")
             for smp, fn, ln, src_ in sorted(lines, reverse=True)[:20]:
                 f.write(f"| {100 * smp / tot:.1f}% | {fn}:{ln} | `{src_[:90]}` |\n")
+
+
+def full_csv(prefix, out):
+    r = list(csv.reader(open(prefix + "_details.csv")))
+    h = r[0]
+    mi, vi, ui, si, ki = (h.index(x) for x in ("Metric Name", "Metric Value", "Metric Unit", "Section Name", "Kernel Name"))
+    rr = [x for x in csv.reader(open(prefix + "_raw.csv")) if x]
+    rawv = {k: f"{v} {u}" for k, u, v in zip(rr[0], rr[1], rr[2])} if len(rr) > 2 else {}
+    with open(out, "w") as f:
+        f.write(f"# ncu --set full: `{r[1][ki][:120]}`\n\nexported pages: `{prefix}_{{details,raw,source}}.csv`\n\n"
+                "| section | metric | value | unit |\n|---|---|---|---|\n")
+        for x in r[1:]:
+            if x[si] in ("GPU Speed Of Light Throughput", "Launch Statistics", "Occupancy", "Memory Workload Analysis",
+                         "Compute Workload Analysis"):
+                f.write(f"| {x[si]} | {x[mi]} | {x[vi]} | {x[ui]} |\n")
+        f.write("\n## raw counters\n\n")
+        for k in ("dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__time_duration.sum",
+                  "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+                  "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+                  "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "launch__registers_per_thread"):
+            for key in rawv:
+                if key.startswith(k):
+                    f.write(f"- `{key}` = {rawv[key]}\n")
+        try:
+            s = list(csv.reader(open(prefix + "_source.csv")))
+        except OSError:
+            s = []
+        if len(s) > 2:
+            hh = s[1]
+            sti, ii = hh.index("Warp Stall Sampling (All Samples)"), hh.index("Instructions Executed")
+            rows = [(x[0], x[1], float(x[sti] or 0), float(x[ii] or 0)) for x in s[2:] if len(x) > ii]
+            tot = sum(x[2] for x in rows) or 1
+            f.write("\n## top stall sites (SASS)\n\n| share | executed | instruction |\n|---|---|---|\n")
+            for a, t, smp, n in sorted(rows, key=lambda x: -x[2])[:20]:
+                f.write(f"| {100 * smp / tot:.1f}% | {n:.0f} | `{t.strip()[:90]}` |\n")
 
 
 CLASSES = (("gemm_decode_kernel", "gemm_decode"), ("attn_decode", "decode_attention"), ("sampler", "sampler"),
