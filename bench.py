@@ -80,10 +80,15 @@ class Clocks:
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, gpu):
-        self.gpu, self.p = gpu, None
+    def __init__(self, gpu, enabled=True):
+        # gpu: one index or a comma list (one sampler process for all of a node's ranks:
+        # a poller per rank measurably slowed the multi-rank timed region)
+        self.gpu, self.p, self.enabled = gpu, None, enabled
+        self.lines = []
 
     def __enter__(self):
+        if not self.enabled:
+            return self
         try:
             self.p = subprocess.Popen(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
                                        "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
@@ -444,7 +449,7 @@ def bench_mode(args, dtype, primary):
     launches0 = ctx.launch_count
     gen_ms, step_ms, tokens, seqs = [], [], 0, 0
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with Clocks(local) as clk:
+    with Clocks(",".join(str(i) for i in range(world)) if world > 1 else local, enabled=local == 0) as clk:
         for i in range(args.steps):
             with torch.cuda.stream(stream):
                 flush.zero_()  # L2 flush between timed iterations (outside the events)
@@ -458,6 +463,7 @@ def bench_mode(args, dtype, primary):
             st = out["stats"].cpu().numpy()
             gen_ms.append(float(st[6]))
             step_ms.append(ev0.elapsed_time(ev1))
+            _dbg("rank", rank, "step ms", step_ms[-1], "gen ms", gen_ms[-1])
             tokens += int(out["lengths"].sum().item())
             seqs += B
             _dbg("timed step", i)
