@@ -696,10 +696,12 @@ void launch_dec(Ctx& c, const bf16* X, int64_t ldx, const bf16* W, int64_t ldw, 
     return e ? atoi(e) : -1;
   }();
   // auto: the one-wave rule for wide batches (each CTA re-reads a 256-row
-  // activation: measured best at config 3, batch 256); small batches keep
-  // doubling while the grid is under one CTA per SM — more weight streams in
-  // flight (config 4, batch 64: 6.4k -> 7.5k tok/s; config 2 picks the same S either way)
-  const bool fit = fit_env >= 0 ? fit_env != 0 : NB > 64;
+  // activation: measured best at config 3, batch 256) and for the mixed-mode
+  // planes (twice the activation bytes per k-block: config 4 mixed 5.0k -> 5.5k
+  // tok/s); bf16 small batches keep doubling while the grid is under one CTA
+  // per SM — more weight streams in flight (config 4 bf16, batch 64: 6.4k ->
+  // 7.5k tok/s; config 2 picks the same S either way)
+  const bool fit = fit_env >= 0 ? fit_env != 0 : (NB > 64 || XM == 4);
   while (S < cap && (fit ? tiles * S * 2 <= 148 : tiles * S < 148) && nk >= 2 * S) S *= 2;
   // a slice larger than the weight ring cycles it (warp 0 lane 1 refills); only
   // split further for that while the launch stays one wave (1 CTA/SM at batch > 64)
