@@ -222,7 +222,9 @@ def test_attention_prefill_split_tc_vs_fp64(ctx, DH, H, lens):
 
 
 @pytest.mark.parametrize("M,N,K", [(300, 2304, 768), (2048, 768, 3072), (129, 3072, 768), (64, 768, 768),
-                                   (1000, 1000, 256)])
+                                   (1000, 1000, 256),
+                                   # wide decode-sized launches (config-4 shapes, the multi-wave LM head, ragged M / N)
+                                   (64, 8192, 2048), (48, 6144, 4096), (7, 50257, 768), (64, 4096, 14336)])
 @pytest.mark.parametrize("epi", [2, 3, 6])
 def test_gemm_planes_vs_torch(ctx, M, N, K, epi):
     """Mixed mode with the activation as hi | lo bf16 planes (TMA'd, two MMAs per
