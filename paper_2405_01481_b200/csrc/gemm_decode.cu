@@ -108,7 +108,13 @@ struct DecLayout {
   static constexpr int kSmemMax = 232448 - 2 * NB * 4 - 256;
   static constexpr int kFixed = XST * kX + 1024 /*align*/ + 1024 /*barriers*/;
   static constexpr int kWcap = (kSmemMax - kFixed) / kW;
-  static constexpr int kTmemCols = NB <= 32 ? 32 : (NB <= 64 ? 64 : (NB <= 128 ? 128 : 256));
+  // split activations at NB <= 128: the hi and lo tiles are adjacent rows of one
+  // N = 2 NB operand — ONE MMA per k16 step reads the weight tile once (two
+  // N = NB MMAs read it twice: the smem-bandwidth-bound part of a decode MMA),
+  // the epilogue adds the two accumulator halves
+  static constexpr bool kComb = SPLIT && NB <= 128;
+  static constexpr int kAccCols = kComb ? 2 * NB : NB;
+  static constexpr int kTmemCols = kAccCols <= 32 ? 32 : (kAccCols <= 64 ? 64 : (kAccCols <= 128 ? 128 : 256));
   static int bytes(int wst) {
     const int body = wst * kW > kPart ? wst * kW : kPart;
     return body + XST * kX + 1024 + 1024;
@@ -233,7 +239,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncwarp();  // reconverge before any block-wide barrier
   } else if (warp == 1) {
     if (lane == 0) {
-      constexpr uint32_t idesc = idesc_bf16(BMW, NB);
+      constexpr uint32_t idesc = idesc_bf16(BMW, L::kAccCols);
       for (int it = 0; it < nkl; ++it) {
         const int ws = it % wst, wu = it / wst;
         const int xs = it % XST, xu = it / XST;
@@ -245,7 +251,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint64_t dx = smem_desc_sw128(sX + xs * L::kX);
 #pragma unroll
         for (int k = 0; k < BK / 16; ++k) mma_bf16(tmem, dw + 2 * k, dx + 2 * k, idesc, (it | k) != 0);
-        if constexpr (SPLIT) {  // the low-order activation term into the same accumulator
+        if constexpr (SPLIT && !L::kComb) {  // the low-order activation term into the same accumulator
           const uint64_t dxl = smem_desc_sw128(sX + xs * L::kX + L::kXT);
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) mma_bf16(tmem, dw + 2 * k, dxl + 2 * k, idesc, 1);
@@ -397,6 +403,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int c = 0; c < NB; c += 16) {
       uint32_t v[16];
       tmem_ld16(tmem + (uint32_t(q * 32) << 16) + uint32_t(c), v);
+      if constexpr (L::kComb) {  // + the lo-term half of the accumulator
+        uint32_t vl[16];
+        tmem_ld16(tmem + (uint32_t(q * 32) << 16) + uint32_t(NB + c), vl);
+#pragma unroll
+        for (int e = 0; e < 16; ++e) v[e] = __float_as_uint(__uint_as_float(v[e]) + __uint_as_float(vl[e]));
+      }
       if (S > 1 && push == 2) {
 #pragma unroll
         for (int e = 0; e < 16; ++e)
