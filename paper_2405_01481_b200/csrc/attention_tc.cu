@@ -25,7 +25,7 @@ CUtensorMap make_map(const void* ptr, int64_t rows, int64_t cols, int64_t ld, in
 
 namespace {
 
-constexpr int BQ = 128, BKV = 64, kThr = 192;
+constexpr int BQ = 128, BKV = 64;
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
 __device__ __forceinline__ void bar_init(uint64_t* b, uint32_t n) {
@@ -101,57 +101,66 @@ __device__ __forceinline__ void tst32(uint32_t taddr, const uint32_t (&r)[32]) {
 // tile is held as both terms and each product is issued as three MMAs
 // (hi·hi + hi·lo + lo·hi, fp32-grade), P split the same way; the output is
 // written as hi | lo planes [M, 2d] for the O projection.
-template <int DH, bool SPLIT>
+template <int DH, bool SPLIT, int QT>
 struct FaSmem {
   static constexpr int kT = SPLIT ? 2 : 1;
   static constexpr int kQ1 = BQ * DH * 2;     // one Q term: DH/64 boxes of 128 rows x 128 B
-  static constexpr int kQ = kQ1 * kT;
+  static constexpr int kQ = kQ1 * kT;         // one Q tile (both terms)
   static constexpr int kKV1 = BKV * DH * 2;   // one term of a K (or V) tile: DH/64 boxes of 64 rows x 128 B
   static constexpr int kKV = kKV1 * kT;
   static constexpr int kP1 = BQ * BKV * 2;    // one term of the P tile: 128 rows x 128 B
   static constexpr int kP = kP1 * kT;
   // the P tile of step j is written only after P_{j-1} V_{j-1} completed (the
   // softmax waits for it before the O rescale), so one P buffer suffices; the
-  // split head_dim-128 tiles use it (and a 2-stage K / V ring) to fit 227 KB
+  // split head_dim-128 tiles use it (and a 2-stage K / V ring) to fit 227 KB,
+  // and so do two Q tiles per CTA
   static constexpr bool kBig = SPLIT && DH == 128;
   static constexpr int kNst = kBig ? 2 : 3;
-  static constexpr int kPB = kBig ? 1 : 2;
-  static constexpr int kBytes = kQ + kNst * 2 * kKV + kPB * kP + 1024 /*align*/ + 256 /*barriers*/;
-  static constexpr int kTmem = 256;           // S0 (64) | S1 (64) | O (DH <= 128)
+  static constexpr int kPB = (kBig || QT == 2) ? 1 : 2;
+  static constexpr int kBytes = QT * kQ + kNst * 2 * kKV + QT * kPB * kP + 1024 /*align*/ + 512 /*barriers*/;
+  static constexpr int kTmem = 256 * QT;      // per Q tile: S0 (64) | S1 (64) | O (DH <= 128)
+  static constexpr int kThreads = 64 + 128 * QT;
 };
 
-template <int DH, bool SPLIT>
-__global__ void __launch_bounds__(kThr, 1)
+// QT = 2: two 128-query tiles of the same (sequence, head) share each K / V
+// tile, with one softmax warpgroup per Q tile: while one group computes its
+// exponentials the tensor core runs the other group's S = Q K^T / O += P V,
+// and the SMs' schedulers have two softmax warps each to interleave.
+template <int DH, bool SPLIT, int QT>
+__global__ void __launch_bounds__(FaSmem<DH, SPLIT, QT>::kThreads, 1)
     attn_prefill_tc_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tkv,
                            const int64_t* __restrict__ seq_offsets, int H, bf16* __restrict__ out) {
-  using L = FaSmem<DH, SPLIT>;
+  using L = FaSmem<DH, SPLIT, QT>;
   constexpr int NB = DH / 64;  // 64-column boxes per row
   constexpr int NST = L::kNst, PB = L::kPB;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sQ = sm;
-  auto sK = [&](int s) { return sm + L::kQ + s * 2 * L::kKV; };
-  auto sV = [&](int s) { return sm + L::kQ + s * 2 * L::kKV + L::kKV; };
-  auto sP = [&](int b) { return sm + L::kQ + NST * 2 * L::kKV + b * L::kP; };
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L::kQ + NST * 2 * L::kKV + PB * L::kP);
+  auto sQ = [&](int g) { return sm + g * L::kQ; };
+  auto sK = [&](int s) { return sm + QT * L::kQ + s * 2 * L::kKV; };
+  auto sV = [&](int s) { return sm + QT * L::kQ + s * 2 * L::kKV + L::kKV; };
+  auto sP = [&](int g, int bb) { return sm + QT * L::kQ + NST * 2 * L::kKV + (g * PB + bb) * L::kP; };
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + QT * L::kQ + NST * 2 * L::kKV + QT * PB * L::kP);
   uint64_t* q_full = bars;
   uint64_t* kv_full = bars + 1;         // [NST]
   uint64_t* kv_empty = kv_full + NST;   // [NST]
-  uint64_t* s_full = kv_empty + NST;    // [2]
-  uint64_t* s_free = s_full + 2;        // [2]
-  uint64_t* p_full = s_free + 2;        // [2]
-  uint64_t* o_done = p_full + 2;        // one completion per P V product
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(o_done + 1);
+  // per Q tile g: s_full[2] | s_free[2] | p_full[2] | o_done
+  auto s_full = [&](int g) { return kv_empty + NST + g * 8; };
+  auto s_free = [&](int g) { return kv_empty + NST + g * 8 + 2; };
+  auto p_full = [&](int g) { return kv_empty + NST + g * 8 + 4; };
+  auto o_done = [&](int g) { return kv_empty + NST + g * 8 + 6; };
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(kv_empty + NST + QT * 8);
 
   PDL_ENTRY();
   const int64_t b = blockIdx.z;
   const int h = blockIdx.y;
-  const int64_t q0 = int64_t(blockIdx.x) * BQ;
+  const int64_t q0 = int64_t(blockIdx.x) * BQ * QT;
   const int64_t start = seq_offsets[b], len = seq_offsets[b + 1] - start;
   if (q0 >= len) return;
   const int64_t d = int64_t(H) * DH;
-  const int64_t kend = min(len, q0 + BQ);
-  const int nt = int((kend + BKV - 1) / BKV);
+  const int ntile = (QT == 2 && q0 + BQ < len) ? 2 : 1;  // Q tiles holding queries of this sequence
+  // K / V tiles each Q tile needs (causal): keys < min(len, q0 + (g + 1) BQ)
+  auto nt_of = [&](int g) { return int((min(len, q0 + int64_t(g + 1) * BQ) + BKV - 1) / BKV); };
+  const int nt_all = nt_of(ntile - 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
@@ -160,12 +169,14 @@ __global__ void __launch_bounds__(kThr, 1)
       bar_init(&kv_full[s], 1);
       bar_init(&kv_empty[s], 1);
     }
-    for (int i = 0; i < 2; ++i) {
-      bar_init(&s_full[i], 1);
-      bar_init(&s_free[i], 128);
-      bar_init(&p_full[i], 128);
+    for (int g = 0; g < QT; ++g) {
+      for (int i = 0; i < 2; ++i) {
+        bar_init(&s_full(g)[i], 1);
+        bar_init(&s_free(g)[i], 128);
+        bar_init(&p_full(g)[i], 128);
+      }
+      bar_init(o_done(g), 1);
     }
-    bar_init(o_done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tq)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tkv)) : "memory");
@@ -178,16 +189,20 @@ __global__ void __launch_bounds__(kThr, 1)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tslot;
-  const uint32_t tO = tmem + 128;
+  auto tS = [&](int g) { return tmem + uint32_t(g * 256); };
+  auto tO = [&](int g) { return tmem + uint32_t(g * 256 + 128); };
 
   if (warp == 0) {
     if (lane == 0) {
-      bar_expect(q_full, L::kQ);
-      for (int c = 0; c < NB; ++c) {
-        tma2d(&tq, q_full, sQ + c * (BQ * 128), int(h * DH + c * 64), int(start + q0));
-        if constexpr (SPLIT) tma2d(&tq, q_full, sQ + L::kQ1 + c * (BQ * 128), int(3 * d + h * DH + c * 64), int(start + q0));
-      }
-      for (int j = 0; j < nt; ++j) {
+      bar_expect(q_full, ntile * L::kQ);
+      for (int g = 0; g < ntile; ++g)
+        for (int c = 0; c < NB; ++c) {
+          const int row = int(start + q0 + g * BQ);
+          tma2d(&tq, q_full, sQ(g) + c * (BQ * 128), int(h * DH + c * 64), row);
+          if constexpr (SPLIT)
+            tma2d(&tq, q_full, sQ(g) + L::kQ1 + c * (BQ * 128), int(3 * d + h * DH + c * 64), row);
+        }
+      for (int j = 0; j < nt_all; ++j) {
         const int s = j % NST, r = j / NST;
         if (r > 0) bar_wait(&kv_empty[s], (r - 1) & 1);
         bar_expect(&kv_full[s], 2 * L::kKV);
@@ -206,72 +221,78 @@ __global__ void __launch_bounds__(kThr, 1)
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr uint32_t id_s = idesc(BQ, BKV, false), id_o = idesc(BQ, DH, true);
-      auto issue_s = [&](int j) {
+      auto issue_s = [&](int g, int j) {
         const int s = j % NST, bf = j & 1;
         bar_wait(&kv_full[s], (j / NST) & 1);
-        if (j >= 2) bar_wait(&s_free[bf], ((j >> 1) - 1) & 1);
+        if (j >= 2) bar_wait(&s_free(g)[bf], ((j >> 1) - 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
         for (int kk = 0; kk < DH / 16; ++kk) {
-          const uint64_t a = desc_k(sQ + (kk >> 2) * (BQ * 128)) + 2 * (kk & 3);
+          const uint64_t a = desc_k(sQ(g) + (kk >> 2) * (BQ * 128)) + 2 * (kk & 3);
           const uint64_t bb = desc_k(sK(s) + (kk >> 2) * (BKV * 128)) + 2 * (kk & 3);
-          mma(tmem + bf * 64, a, bb, id_s, kk > 0);
+          mma(tS(g) + bf * 64, a, bb, id_s, kk > 0);
           if constexpr (SPLIT) {  // + q_hi k_lo + q_lo k_hi
-            const uint64_t al = desc_k(sQ + L::kQ1 + (kk >> 2) * (BQ * 128)) + 2 * (kk & 3);
+            const uint64_t al = desc_k(sQ(g) + L::kQ1 + (kk >> 2) * (BQ * 128)) + 2 * (kk & 3);
             const uint64_t bl = desc_k(sK(s) + L::kKV1 + (kk >> 2) * (BKV * 128)) + 2 * (kk & 3);
-            mma(tmem + bf * 64, a, bl, id_s, 1);
-            mma(tmem + bf * 64, al, bb, id_s, 1);
+            mma(tS(g) + bf * 64, a, bl, id_s, 1);
+            mma(tS(g) + bf * 64, al, bb, id_s, 1);
           }
         }
-        commit(&s_full[bf]);
+        commit(&s_full(g)[bf]);
       };
       bar_wait(q_full, 0);
-      issue_s(0);
-      for (int j = 0; j < nt; ++j) {
-        if (j + 1 < nt) issue_s(j + 1);
+      for (int g = 0; g < ntile; ++g) issue_s(g, 0);
+      for (int j = 0; j < nt_all; ++j) {
+        for (int g = 0; g < ntile; ++g)
+          if (j + 1 < nt_of(g)) issue_s(g, j + 1);
         const int s = j % NST, pb = j % PB;
-        bar_wait(&p_full[pb], (j / PB) & 1);
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        for (int g = 0; g < ntile; ++g) {
+          if (j >= nt_of(g)) continue;
+          bar_wait(&p_full(g)[pb], (j / PB) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
-        for (int kk = 0; kk < BKV / 16; ++kk) {
-          const uint64_t a = desc_k(sP(pb)) + 2 * kk;
-          const uint64_t bb = desc_mn(sV(s)) + ((2048 * kk) >> 4);
-          mma(tO, a, bb, id_o, (j | kk) != 0);
-          if constexpr (SPLIT) {  // + p_hi v_lo + p_lo v_hi
-            const uint64_t al = desc_k(sP(pb) + L::kP1) + 2 * kk;
-            const uint64_t bl = desc_mn(sV(s) + L::kKV1) + ((2048 * kk) >> 4);
-            mma(tO, a, bl, id_o, 1);
-            mma(tO, al, bb, id_o, 1);
+          for (int kk = 0; kk < BKV / 16; ++kk) {
+            const uint64_t a = desc_k(sP(g, pb)) + 2 * kk;
+            const uint64_t bb = desc_mn(sV(s)) + ((2048 * kk) >> 4);
+            mma(tO(g), a, bb, id_o, (j | kk) != 0);
+            if constexpr (SPLIT) {  // + p_hi v_lo + p_lo v_hi
+              const uint64_t al = desc_k(sP(g, pb) + L::kP1) + 2 * kk;
+              const uint64_t bl = desc_mn(sV(s) + L::kKV1) + ((2048 * kk) >> 4);
+              mma(tO(g), a, bl, id_o, 1);
+              mma(tO(g), al, bb, id_o, 1);
+            }
           }
+          commit(o_done(g));
         }
-        commit(o_done);
         commit(&kv_empty[s]);
       }
     }
     __syncwarp();
   } else {
-    // ---- softmax: thread r <-> query q0 + r <-> TMEM lane r
+    // ---- softmax: warpgroup g = Q tile g; thread r <-> query q0 + g BQ + r <-> TMEM lane r
+    const int g = (warp - 2) >> 2;
     const int q = warp & 3, r = q * 32 + lane;
     const uint32_t lane_off = uint32_t(q * 32) << 16;
-    const int64_t qi = q0 + r;
+    const int64_t qg = q0 + int64_t(g) * BQ, qi = qg + r;
+    const int nt = g < ntile ? nt_of(g) : 0;
     const float scale = 1.4426950408889634f / sqrtf(float(DH));  // log2 domain
     float m = -FLT_MAX, l = 0.f;
     for (int j = 0; j < nt; ++j) {
       const int bf = j & 1;
-      bar_wait(&s_full[bf], (j >> 1) & 1);
+      bar_wait(&s_full(g)[bf], (j >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       uint32_t sa[32], sb[32];
-      tld32(tmem + lane_off + bf * 64, sa);
-      tld32(tmem + lane_off + bf * 64 + 32, sb);
+      tld32(tS(g) + lane_off + bf * 64, sa);
+      tld32(tS(g) + lane_off + bf * 64 + 32, sb);
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-      bar_arrive(&s_free[bf]);
+      bar_arrive(&s_free(g)[bf]);
       const int k0 = j * BKV;
       float sv[64];
       float mx = -FLT_MAX;
       // masks only on tiles that reach the diagonal or the end of the sequence
       // (block-uniform test): the others are raw scaled scores
-      if (k0 + BKV - 1 <= int(q0) && k0 + BKV <= int(len)) {
+      if (k0 + BKV - 1 <= int(qg) && k0 + BKV <= int(len)) {
 #pragma unroll
         for (int c = 0; c < 64; ++c) {
           sv[c] = __uint_as_float(c < 32 ? sa[c] : sb[c - 32]) * scale;
@@ -302,24 +323,24 @@ __global__ void __launch_bounds__(kThr, 1)
       l = l * corr + rs;
       if (j > 0) {
         // O holds P_{j-1} V_{j-1}: wait for it, then rescale rows whose max moved
-        bar_wait(o_done, (j - 1) & 1);
+        bar_wait(o_done(g), (j - 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         if (grow) {
 #pragma unroll 1
           for (int c = 0; c < DH; c += 32) {
             uint32_t o[32];
-            tld32(tO + lane_off + c, o);
+            tld32(tO(g) + lane_off + c, o);
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
             for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * corr);
-            tst32(tO + lane_off + c, o);
+            tst32(tO(g) + lane_off + c, o);
           }
           asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         }
       }
       m = mn;
       // P_j row (bf16) in the K-major 128B swizzle: row r at r * 128, chunk c ^ (r & 7)
-      uint8_t* prow = sP(j % PB) + r * 128;
+      uint8_t* prow = sP(g, j % PB) + r * 128;
 #pragma unroll
       for (int c8 = 0; c8 < 8; ++c8) {
         uint32_t w4[4], l4[4];
@@ -340,30 +361,32 @@ __global__ void __launch_bounds__(kThr, 1)
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-      bar_arrive(&p_full[j % PB]);
+      bar_arrive(&p_full(g)[j % PB]);
     }
     // ---- epilogue: O / l
-    bar_wait(o_done, (nt - 1) & 1);
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const float inv = 1.0f / l;
+    if (nt > 0) {
+      bar_wait(o_done(g), (nt - 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const float inv = 1.0f / l;
 #pragma unroll 1
-    for (int c = 0; c < DH; c += 32) {
-      uint32_t o[32];
-      tld32(tO + lane_off + c, o);
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      if (qi < len) {
-        bf16* dst = out + (start + qi) * (SPLIT ? 2 * d : d) + h * DH + c;
+      for (int c = 0; c < DH; c += 32) {
+        uint32_t o[32];
+        tld32(tO(g) + lane_off + c, o);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (qi < len) {
+          bf16* dst = out + (start + qi) * (SPLIT ? 2 * d : d) + h * DH + c;
 #pragma unroll
-        for (int e8 = 0; e8 < 32; e8 += 8) {
-          Vec16<bf16> ov, ol;
+          for (int e8 = 0; e8 < 32; e8 += 8) {
+            Vec16<bf16> ov, ol;
 #pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            const float y = __uint_as_float(o[e8 + e]) * inv;
-            ov.v[e] = __float2bfloat16_rn(y);
-            if constexpr (SPLIT) ol.v[e] = __float2bfloat16_rn(y - __bfloat162float(ov.v[e]));
+            for (int e = 0; e < 8; ++e) {
+              const float y = __uint_as_float(o[e8 + e]) * inv;
+              ov.v[e] = __float2bfloat16_rn(y);
+              if constexpr (SPLIT) ol.v[e] = __float2bfloat16_rn(y - __bfloat162float(ov.v[e]));
+            }
+            *reinterpret_cast<uint4*>(dst + e8) = ov.u;
+            if constexpr (SPLIT) *reinterpret_cast<uint4*>(dst + d + e8) = ol.u;  // lo plane
           }
-          *reinterpret_cast<uint4*>(dst + e8) = ov.u;
-          if constexpr (SPLIT) *reinterpret_cast<uint4*>(dst + d + e8) = ol.u;  // lo plane
         }
       }
     }
@@ -376,24 +399,46 @@ __global__ void __launch_bounds__(kThr, 1)
   }
 }
 
-template <int DH, bool SPLIT = false>
-void launch_fa(Ctx& c, const bf16* qkv, const int64_t* seq_offsets, int64_t B, int64_t max_len, int64_t H,
-               int64_t M_total, bf16* out) {
-  using L = FaSmem<DH, SPLIT>;
+// Q tiles per CTA (PPOEXP_ATTN_QT forces 1 or 2).  Measured on B200: two help
+// the mixed-mode split kernel at head_dim 64 (C2 scoring pass 10.05 -> 9.83 ms)
+// but slow the bf16 kernel (C5 shape 0.49 -> 0.59 ms per launch: half the CTAs,
+// a longer causal tail), so bf16 keeps one; the split head_dim-128 tiles would
+// not fit shared memory twice.
+int attn_qt(bool split) {
+  static const int qt = [] {
+    const char* e = getenv("PPOEXP_ATTN_QT");
+    return e ? atoi(e) : 0;
+  }();
+  return qt ? qt : (split ? 2 : 1);
+}
+
+template <int DH, bool SPLIT, int QT>
+void launch_fa_qt(Ctx& c, const bf16* qkv, const int64_t* seq_offsets, int64_t B, int64_t max_len, int64_t H,
+                  int64_t M_total, bf16* out) {
+  using L = FaSmem<DH, SPLIT, QT>;
   const int64_t d = H * DH, w = (SPLIT ? 6 : 3) * d;
   const CUtensorMap tq = make_map(qkv, M_total, w, w, BQ);
   const CUtensorMap tkv = make_map(qkv, M_total, w, w, BKV);
-  auto k = attn_prefill_tc_kernel<DH, SPLIT>;
+  auto k = attn_prefill_tc_kernel<DH, SPLIT, QT>;
   static bool attr = false;
   if (!attr) {
     PPOEXP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kBytes));
     attr = true;
   }
-  dim3 grid(unsigned(ceil_div(max_len, BQ)), unsigned(H), unsigned(B));
+  dim3 grid(unsigned(ceil_div(max_len, BQ * QT)), unsigned(H), unsigned(B));
   const double flops = 2.0 * 2.0 * B * H * double(max_len) * max_len / 2 * DH;
   c.launch("attention_prefill", 0, flops, [&] {
-    launch_kernel(c, k, grid, dim3(kThr), L::kBytes, 1, tq, tkv, seq_offsets, int(H), out);
+    launch_kernel(c, k, grid, dim3(L::kThreads), L::kBytes, 1, tq, tkv, seq_offsets, int(H), out);
   });
+}
+
+template <int DH, bool SPLIT = false>
+void launch_fa(Ctx& c, const bf16* qkv, const int64_t* seq_offsets, int64_t B, int64_t max_len, int64_t H,
+               int64_t M_total, bf16* out) {
+  if constexpr (!(SPLIT && DH == 128)) {
+    if (attn_qt(SPLIT) == 2) return launch_fa_qt<DH, SPLIT, 2>(c, qkv, seq_offsets, B, max_len, H, M_total, out);
+  }
+  launch_fa_qt<DH, SPLIT, 1>(c, qkv, seq_offsets, B, max_len, H, M_total, out);
 }
 
 }  // namespace
