@@ -315,10 +315,11 @@ static bool mixed_head_planes() {
   return on;
 }
 
-static bool split_attention_tc() {  // PPOEXP_ATTN_SPLIT_TC=0: mma.sync split attention in scoring
+static bool split_attention_tc() {  // PPOEXP_ATTN_SPLIT_TC=0 (or PPOEXP_ATTN_TC=0): mma.sync split attention
   static const bool on = [] {
     const char* e = getenv("PPOEXP_ATTN_SPLIT_TC");
-    return !(e && e[0] == '0');
+    const char* t = getenv("PPOEXP_ATTN_TC");
+    return !(e && e[0] == '0') && !(t && t[0] == '0');
   }();
   return on;
 }
@@ -351,8 +352,7 @@ static float* forward_layers_mixed(Model& m, const Packed& p, const KvTarget* kv
         bf16* qp = reinterpret_cast<bf16*>(qkv);
         gemm_tc_planes(c, hp, 2 * d, static_cast<const bf16*>(ly.wqkv), d, M, 3 * d, d, Epi::kStoreSplit, qp, 6 * d);
         if (!attention_prefill_tc_split(c, qp, p.offsets_d, p.B, p.max_len, H, DH, M, ap))
-          throw ContractError("forward (mixed): split tcgen05 attention not eligible (PPOEXP_ATTN_TC=0 needs "
-                              "PPOEXP_ATTN_SPLIT_TC=0)");
+          throw ContractError("forward (mixed): split tcgen05 attention not eligible for this shape");
       } else {
         gemm_tc_planes(c, hp, 2 * d, static_cast<const bf16*>(ly.wqkv), d, M, 3 * d, d, Epi::kStoreF32, qkv, 3 * d);
         if (kv)
