@@ -463,7 +463,7 @@ def bench_mode(args, dtype, primary):
             st = out["stats"].cpu().numpy()
             gen_ms.append(float(st[6]))
             step_ms.append(ev0.elapsed_time(ev1))
-            _dbg("rank", rank, "step ms", step_ms[-1], "gen ms", gen_ms[-1])
+            _dbg("rank", rank, "step ms", step_ms[-1], "gen ms", gen_ms[-1], "launches so far", ctx.launch_count - launches0)
             tokens += int(out["lengths"].sum().item())
             seqs += B
             _dbg("timed step", i)
