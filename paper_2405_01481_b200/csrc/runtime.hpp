@@ -4,6 +4,9 @@
 
 #include <cuda_runtime.h>
 
+#include <cstdio>
+#include <cstdlib>
+
 #include <functional>
 #include <algorithm>
 #include <array>
@@ -123,6 +126,9 @@ struct Ctx {
   void* workspace(const std::string& name, size_t bytes) {
     auto& b = ws[ws_prefix + name];
     if (!b) b = std::make_unique<DeviceBuffer>();
+    if (bytes > b->bytes && b->bytes && getenv("PPOEXP_WS_TRACE"))  // debug: data-dependent regrowth
+      fprintf(stderr, "[ppoexp] workspace %s%s grows %zu -> %zu bytes\n", ws_prefix.c_str(), name.c_str(), b->bytes,
+              bytes);
     b->ensure(bytes);
     return b->ptr;
   }
