@@ -286,10 +286,16 @@ void Engine::decode_unit_mixed(int64_t B, int64_t unit) {
     bf16* hp = static_cast<bf16*>(h);   // [mb, 2d] in the fp32 [mb, d] buffer
     bf16* ap = static_cast<bf16*>(att);
     bf16* upp = static_cast<bf16*>(up);  // [mb, 2f]
-    launch_embed<bf16>(cc, next_tok, pos, B, d, static_cast<const bf16*>(m->tok), static_cast<const bf16*>(m->pos), x);
+    if (L == 0)
+      launch_embed<bf16>(cc, next_tok, pos, B, d, static_cast<const bf16*>(m->tok), static_cast<const bf16*>(m->pos),
+                         x);
     for (int64_t l = 0; l < L; ++l) {
       const Layer& ly = m->layers[l];
-      launch_layernorm_split(cc, x, B, d, ly.ln1w, ly.ln1b, hp);
+      if (l == 0)  // the step's embedding and the first LayerNorm in one launch
+        launch_embed_layernorm_split(cc, next_tok, pos, B, d, static_cast<const bf16*>(m->tok),
+                                     static_cast<const bf16*>(m->pos), x, ly.ln1w, ly.ln1b, hp);
+      else
+        launch_layernorm_split(cc, x, B, d, ly.ln1w, ly.ln1b, hp);
       gemm_decode_planes(cc, hp, 2 * d, static_cast<const bf16*>(ly.wqkv), d, B, 3 * d, d, Epi::kStoreF32, q3, 3 * d,
                          nullptr);
       launch_attention_decode<float>(cc, q3, B, pos, done, block_table, int(l), geom, static_cast<float*>(kvp), at,

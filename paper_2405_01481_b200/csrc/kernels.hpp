@@ -106,6 +106,8 @@ void gemm_decode_mixed(Ctx& c, const float* X, int64_t ldx, const bf16* W, int64
 void gemm_decode_planes(Ctx& c, const bf16* X, int64_t ldx, const bf16* W, int64_t ldw, int64_t M, int64_t N, int64_t K,
                         Epi epi, void* C, int64_t ldc, const RowStats* so);
 // LayerNorm written as two bf16 planes y[r, 0:d) = hi, y[r, d:2d) = lo (mixed decode).
+void launch_embed_layernorm_split(Ctx& c, const int32_t* tokens, const int32_t* positions, int64_t rows, int64_t d,
+                                  const bf16* tok, const bf16* pos, float* x, const float* g, const float* b, bf16* y);
 void launch_layernorm_split(Ctx& c, const float* x, int64_t rows, int64_t d, const float* g, const float* b, bf16* y,
                             const int32_t* gather = nullptr);
 // Mixed-mode GEMM over a [M, 2K] hi|lo bf16 plane activation (tcgen05, both planes TMA'd).

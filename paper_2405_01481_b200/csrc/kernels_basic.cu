@@ -414,9 +414,18 @@ __global__ void __launch_bounds__(256) layernorm_wide_kernel(const float* __rest
 
 // Mixed decode: LayerNorm of a row (fp32, two-pass statistics in fp64) written as
 // two bf16 planes, y[r, j] = hi, y[r, d + j] = lo (the consumer GEMM TMAs both).
+// EmbedIn (decode step start): x[r] = tok_embed[tokens[r]] + pos_embed[positions[r]] is
+// computed here and written out, then normalised — one launch instead of embed + LayerNorm.
+struct EmbedIn {
+  const int32_t* tokens = nullptr;
+  const int32_t* positions = nullptr;
+  const bf16* tok = nullptr;
+  const bf16* pos = nullptr;
+};
+
 __global__ void layernorm_split_kernel(const float* __restrict__ x, int64_t d, const float* __restrict__ g,
                                        const float* __restrict__ b, bf16* __restrict__ y,
-                                       const int32_t* __restrict__ gather) {
+                                       const int32_t* __restrict__ gather, EmbedIn em) {
   pdl_entry_small_grid();
   __shared__ double red[32];
   const int64_t r = blockIdx.x;
@@ -424,7 +433,22 @@ __global__ void layernorm_split_kernel(const float* __restrict__ x, int64_t d, c
   const int nw = (blockDim.x + 31) >> 5, w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int j = threadIdx.x * 4;
   const bool act = j < d;
-  const float4 v = act ? *reinterpret_cast<const float4*>(x + src * d + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+  float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (em.tokens) {
+    if (act) {
+      const int64_t t = em.tokens[r], p = em.positions[r];
+      const uint2 a = *reinterpret_cast<const uint2*>(em.tok + t * d + j);
+      const uint2 c = *reinterpret_cast<const uint2*>(em.pos + p * d + j);
+      const float2 a0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&a.x));
+      const float2 a1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&a.y));
+      const float2 c0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&c.x));
+      const float2 c1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&c.y));
+      v = make_float4(a0.x + c0.x, a0.y + c0.y, a1.x + c1.x, a1.y + c1.y);
+      *reinterpret_cast<float4*>(const_cast<float*>(x) + r * d + j) = v;
+    }
+  } else if (act) {
+    v = *reinterpret_cast<const float4*>(x + src * d + j);
+  }
   double s = warp_sum_d(double(v.x) + v.y + v.z + v.w);
   if (lane == 0) red[w] = s;
   __syncthreads();
@@ -516,7 +540,24 @@ void launch_layernorm_split(Ctx& c, const float* x, int64_t rows, int64_t d, con
   }
   const int th = int((d / 4 + 31) / 32 * 32);
   c.launch("layernorm", double(rows) * d * 8, 0, [&] {
-    launch_kernel(c, layernorm_split_kernel, dim3(rows), dim3(th), 0, 1, x, d, g, b, y, gather);
+    launch_kernel(c, layernorm_split_kernel, dim3(rows), dim3(th), 0, 1, x, d, g, b, y, gather, EmbedIn{});
+  });
+}
+
+// Decode step start (mixed planes): embedding sum written to x and its split
+// LayerNorm planes in one launch (embed_kernel's arithmetic: bf16 -> fp32, one add).
+void launch_embed_layernorm_split(Ctx& c, const int32_t* tokens, const int32_t* positions, int64_t rows, int64_t d,
+                                  const bf16* tok, const bf16* pos, float* x, const float* g, const float* b, bf16* y) {
+  if (rows <= 0) return;
+  if (d % 4 || d > 4096) throw ContractError("embed + layernorm (split planes): d % 4 == 0 and d <= 4096 required");
+  const int th = int((d / 4 + 31) / 32 * 32);
+  EmbedIn em;
+  em.tokens = tokens;
+  em.positions = positions;
+  em.tok = tok;
+  em.pos = pos;
+  c.launch("layernorm", double(rows) * d * 12, 0, [&] {
+    launch_kernel(c, layernorm_split_kernel, dim3(rows), dim3(th), 0, 1, x, d, g, b, y, nullptr, em);
   });
 }
 
