@@ -449,7 +449,8 @@ def bench_mode(args, dtype, primary):
     launches0 = ctx.launch_count
     gen_ms, step_ms, tokens, seqs = [], [], 0, 0
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with Clocks(",".join(str(i) for i in range(world)) if world > 1 else local, enabled=local == 0) as clk:
+    with Clocks(",".join(str(i) for i in range(world)) if world > 1 else local,
+                enabled=local == 0 and not os.environ.get("PPOEXP_BENCH_NO_CLOCKS")) as clk:
         for i in range(args.steps):
             with torch.cuda.stream(stream):
                 flush.zero_()  # L2 flush between timed iterations (outside the events)

@@ -821,12 +821,15 @@ ppoexp_status ppoexp_make_experience(const ppoexp_experience_request* req, int64
     PPOEXP_CUDA(cudaMemsetAsync(val, 0, nBN * 8, c.stream));
     PPOEXP_CUDA(cudaEventRecord(ev[3], c.stream));
     // The policy, reference and critic forwards read the same packed tokens and
-    // write disjoint outputs: the reference and critic run on two auxiliary
-    // streams (own workspaces) concurrently with the policy on the main stream,
-    // so one forward's latency-bound kernels overlap another's GEMMs.
+    // write disjoint outputs: with PPOEXP_SCORE_STREAMS=1 the reference and critic
+    // run on two auxiliary streams (own workspaces) concurrently with the policy.
+    // Default: one stream — the persistent GEMMs and the 192 KB attention CTAs
+    // each fill every SM, so concurrency bought nothing (26–27 ms per C2 step
+    // either way) and occasionally cost a lot (a persistent grid waiting for SMs
+    // held by another stream's kernel: single steps up to +100 ms)
     static const bool concurrent = [] {
       const char* e = getenv("PPOEXP_SCORE_STREAMS");
-      return !(e && e[0] == '0');
+      return e ? e[0] == '1' : !gemm_pp_enabled();
     }();
     // concurrent forwards hold one set of activation workspaces each: fall back
     // to one stream when two more sets would not fit comfortably in free HBM

@@ -12,7 +12,8 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 CASES = [
-    # (env, tests): non-persistent tcgen05 GEMMs; in-kernel fp32 split for the mixed
+    # (env, tests): non-persistent tcgen05 GEMMs (which also restores the concurrent
+    # scoring streams); in-kernel fp32 split for the mixed
     # prefill; mma.sync split attention in mixed scoring; one Q tile per CTA for the
     # split tcgen05 attention, two for the bf16 one
     ({"PPOEXP_GEMM_PERSIST": "0"}, "tests/test_gpu_parity.py::test_mixed_scoring_many_rows"),
@@ -20,6 +21,8 @@ CASES = [
     ({"PPOEXP_ATTN_SPLIT_TC": "0"}, "tests/test_gpu_parity.py::test_mixed_scoring_many_rows"),
     ({"PPOEXP_ATTN_QT": "1"}, "tests/test_gpu_kernels.py::test_attention_prefill_split_tc_vs_fp64"),
     ({"PPOEXP_ATTN_QT": "2"}, "tests/test_gpu_kernels.py::test_attention_prefill_vs_torch"),
+    # policy / reference / critic scoring forwards on three concurrent streams
+    ({"PPOEXP_SCORE_STREAMS": "1"}, "tests/test_gpu_parity.py::test_mixed_experience_c2_full_depth"),
 ]
 
 
