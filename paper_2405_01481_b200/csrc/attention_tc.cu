@@ -3,13 +3,14 @@
 // and the engine's batched prefill; src/model.cpp:230-236 semantics: scores
 // scaled by 1/sqrt(dh) before the max, causal, exp(s - max) / sum).
 //
-// CTA = 128 queries of one (sequence, head), 6 warps:
-//   warp 0    : TMA producer — the Q tile once, then K / V tiles of 64 keys
-//               (128B-swizzled boxes of the packed qkv buffer) into a 3-stage ring;
+// CTA = QT tiles of 128 queries of one (sequence, head), 2 + 4 QT warps:
+//   warp 0    : TMA producer — the Q tile(s) once, then K / V tiles of 64 keys
+//               (128B-swizzled boxes of the packed qkv buffer) into a 2-3-stage ring;
 //   warp 1    : TMEM allocator + MMA issuer — S_j = Q K_j^T into one of two TMEM
 //               score buffers (issued one tile ahead), O += P_j V_j into the TMEM
 //               output accumulator (V is the MN-major B operand, straight from TMA);
-//   warps 2-5 : softmax — thread r owns query row r (TMEM lane r): tcgen05.ld of
+//   warps 2-5 (+ 6-9 for the second Q tile) : softmax — thread r owns query row r
+//               (TMEM lane r of its tile's columns): tcgen05.ld of
 //               the score row, mask, online max / sum in the log2 domain, the
 //               O-row rescale in TMEM when the max moves, P_j (bf16) written in
 //               the UMMA K-major swizzle; epilogue O / l -> global.
